@@ -1,0 +1,152 @@
+"""Pin the CPU oracle (oracle/tpp_oracle.py) to the reference's own outputs.
+
+The fixtures were produced by the unmodified reference (tests/golden/make_golden.py);
+every comparison here is bitwise unless stated.
+"""
+
+import numpy as np
+
+from oracle import tpp_oracle as O
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint8).tobytes()
+
+
+def test_rne_matches_reference(golden):
+    g = golden("dtypes.npz")
+    got = O.fp32_to_bf16_rne(g["fp32_bits"].view(np.float32))
+    assert np.array_equal(got, g["bf16_bits"])
+
+
+def test_bf16_roundtrip_exhaustive():
+    pats = np.arange(1 << 16, dtype=np.uint16)
+    assert np.array_equal(O.fp32_to_bf16_rne(O.bf16_to_fp32(pats)), pats)
+
+
+def test_cfg1_brgemm_bitwise(golden):
+    g = golden("cfg1_brgemm.npz")
+    m = n = k = 64
+    a = [O.load_a(g["a"], i * m * k, m, k, m, "fp32") for i in range(16)]
+    b = [O.load_b(g["b"], i * k * n, k, n, k, "fp32") for i in range(16)]
+    c0 = g["c0"].reshape(n, m).T
+    c = O.brgemm(a, b, c0, beta=1.0)
+    assert bits(c.T.reshape(-1)) == bits(g["c"])
+
+
+def _run_case(g, i):
+    key = f"case{i:03d}"
+    m, n, k, lda, ldb, ldc, cnt, sa, sb, vnni = (int(v) for v in g[key + "_meta"])
+    dt = str(g[key + "_dtype"])
+    beta = float(g[key + "_beta"])
+    abuf, bbuf, c0 = g[key + "_a"], g[key + "_b"], g[key + "_c0"]
+    a = [O.load_a(abuf, j * sa, m, k, lda, dt, vnni=bool(vnni)) for j in range(cnt)]
+    b = [O.load_b(bbuf, j * sb, k, n, ldb, dt) for j in range(cnt)]
+    c0w = c0.reshape(n, ldc).T[:m]
+    c = O.brgemm(a, b, c0w, beta=beta, in_dtype=dt)
+    full = c0.reshape(n, ldc).T.copy()
+    full[:m] = c.astype(full.dtype)
+    return full.T.reshape(-1), g[key + "_c"]
+
+
+def test_brgemm_cases_bitwise(golden):
+    g = golden("brgemm_cases.npz")
+    for i in range(int(g["count"])):
+        got, want = _run_case(g, i)
+        assert bits(got) == bits(want), f"case {i}"
+
+
+def test_gelu_table_fit_matches_reference(golden):
+    g = golden("approx.npz")
+    coeffs, base, range_max = O.GELU_TABLE
+    assert np.array_equal(coeffs.view(np.uint32), g["gelu_coeffs"].view(np.uint32))
+    assert base == int(g["gelu_base"]) and range_max == float(g["gelu_range_max"])
+
+
+def test_gelu_and_grad_bitwise(golden):
+    g = golden("approx.npz")
+    assert bits(O.gelu(g["x"])) == bits(g["gelu"])
+    assert bits(O.gelu_grad(g["x"])) == bits(g["gelu_grad"])
+
+
+def test_exp_taylor_bitwise(golden):
+    g = golden("approx.npz")
+    got = O.exp_taylor(g["xe"])
+    assert bits(got) == bits(g["exp"])
+
+
+def test_eltwise_bitwise(golden):
+    g = golden("eltwise.npz")
+    x = g["x"]
+    m, n = x.shape
+    cm = lambda a: a.T.reshape(-1)  # column-major flat
+    assert bits(cm(O.relu(x))) == bits(g["relu"])
+    assert np.array_equal(O.bool_to_mask(O.relu_mask(x)), g["mask"])
+    mb = O.mask_to_bool(g["mask"], m, n)
+    assert bits(cm(O.relu_inv(g["dy"], mb))) == bits(g["relu_inv"])
+    gel = O.fp32_to_bf16_rne(O.gelu(O.round_bf16(x)))
+    assert np.array_equal(cm(gel), g["gelu_bf16"])
+    assert bits(cm(g["dy"] * O.gelu_grad(x))) == bits(g["gelu_inv"])
+    assert bits(cm(O.binary("add", x, g["bias"]))) == bits(g["add_bias"])
+    assert bits(cm(O.muladd(x, g["y"], g["z"]))) == bits(g["muladd"])
+    assert bits(cm(O.muladd(x, g["y"], g["z"], negate=True))) == bits(g["nmuladd"])
+    assert bits(O.reduce_rows_sum(g["y"])) == bits(g["rsum"])
+    assert bits(O.reduce_rows_sum(g["y"], squared=True)) == bits(g["rsumsq"])
+    assert np.array_equal(O.vnni_pack(g["pats"], 2), g["vnni"])
+    assert np.array_equal(O.vnni_to_vnnit(g["vnni"], 2, 2, 12, 10), g["vnnit"])
+    assert np.array_equal(O.vnni_pack(g["pats_odd"], 2), g["vnni_odd"])
+    assert np.array_equal(O.vnni_unpack(g["vnni_odd"], 2, 5, 7), g["pats_odd"])
+    assert np.array_equal(cm(O.fp32_to_bf16_rne(x)), g["convert_bf16"])
+
+
+def test_layernorm_matches_reference(golden):
+    g = golden("layernorm.npz")
+    for i in range(4):
+        x = g[f"x{i}"]
+        dt = str(g[f"dtype{i}"])
+        xf = O.bf16_to_fp32(x) if dt == "bf16" else x
+        out, mu, var = O.layernorm(xf, g[f"g{i}"], g[f"b{i}"], 1e-5)
+        if dt == "bf16":
+            out = O.fp32_to_bf16_rne(out)
+        assert bits(out) == bits(g[f"out{i}"]), i
+        assert bits(mu.astype(np.float32)) == bits(g[f"mean{i}"])
+        assert bits(var.astype(np.float32)) == bits(g[f"var{i}"])
+
+
+def test_softmax_and_split_sgd(golden):
+    g = golden("softmax_sgd.npz")
+    x = g["x"]
+    want = g["y"]
+    for j in range(6):
+        sl = O.softmax_slice(x[:, j * 40:(j + 1) * 40])
+        assert bits(sl.T.reshape(-1)) == bits(want[j * 40:(j + 1) * 40])
+    x2 = g["x2"]
+    want2 = g["y2"].reshape(99, 5).T
+    for j in range(3):
+        sl = O.softmax_slice(x2[:, j * 33:(j + 1) * 33])
+        assert bits(sl) == bits(np.ascontiguousarray(want2[:, j * 33:(j + 1) * 33]))
+    w = g["w0"]
+    for gi in g["grads"]:
+        w = O.split_sgd_step(w, gi, float(g["lr"]))
+    assert bits(w) == bits(g["w1"])
+
+
+def test_fc_fp32_and_bf16_compositions(golden):
+    g = golden("fc.npz")
+    for i in range(3):
+        act = str(g[f"fp32_{i}_act"])
+        c = O.fc_forward_fp32(g[f"fp32_{i}_a"], g[f"fp32_{i}_b"],
+                              activation=None if act == "none" else act)
+        assert bits(c) == bits(g[f"fp32_{i}_c"]), i
+    for i in range(3):
+        res = g[f"bf16_{i}_res"]
+        out, _, _ = O.fc_forward_bf16(g[f"bf16_{i}_x"], g[f"bf16_{i}_w"], g[f"bf16_{i}_bias"],
+                                      activation=str(g[f"bf16_{i}_act"]),
+                                      residual_bits=res if res.size else None)
+        assert np.array_equal(out, g[f"bf16_{i}_out"]), i
+
+
+def test_conv_offset_composition(golden):
+    g = golden("conv.npz")
+    out, _ = O.conv2d_fwd_bf16(g["x"], g["w"])
+    assert np.array_equal(out, g["out"])
