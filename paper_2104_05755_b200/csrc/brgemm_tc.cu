@@ -1,0 +1,521 @@
+// K2/K3: BF16 BRGEMM on tcgen05 tensor cores with the epilogue TPPs fused.
+//
+// The blocked FC layer (kernels.py:300-329) and the offset-addressed 3x3
+// convolution are both a batch-reduce GEMM
+//     C[token, feat] = sum_i A_i[token, :] . W_i[feat, :]
+// over a sequence of 64-wide reduce blocks i (the reference's k_b channel
+// blocks; for the conv the (r, s, c_b) taps).  One persistent CTA per SM
+// walks output tiles of 128 tokens x BN features:
+//
+//   warp 0  TMA producer: per reduce block, one 5-D TMA box of activations
+//           (128 x 64 bf16) and one of packed weights (BN x 64 bf16) into a
+//           STAGES-deep shared-memory ring (128B swizzle, mbarrier complete_tx)
+//   warp 1  MMA issuer: 4 x tcgen05.mma (M=128, N=BN, K=16) per stage into a
+//           TMEM accumulator; tcgen05.commit frees the stage / signals the tile
+//   warp 2  TMEM allocator (2 x BN columns: the accumulator is double
+//           buffered so the epilogue of tile t overlaps the MMAs of tile t+1)
+//   warps 4-7  epilogue: tcgen05.ld rows of the accumulator, apply
+//           + bias (ops.py:747-782, COL broadcast), ReLU + bitmask / GELU
+//           (ops.py:361-366, approx.py:267-276), + residual, RNE narrowing
+//           (dtypes.py:82-97) — every op a separately rounded FP32 op in the
+//           reference's order — and store to the blocked output layout.
+//
+// The batch-reduce loop accumulates on chip: C is written exactly once.
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace tpp {
+
+using namespace sm100;
+
+namespace tc {
+
+constexpr int BM = 128;          // tokens per tile (UMMA M, TMEM lanes)
+constexpr int BK = 64;           // bf16 per reduce block = one 128B swizzle row
+constexpr int kThreads = 256;    // 8 warps
+constexpr int kEpiWarp0 = 4;
+
+enum FeedMode { FEED_FC = 0, FEED_CONV = 1 };
+
+struct Params {
+  // ---- A feed (tokens) ----
+  int mode;
+  int tokens;          // FC: valid tokens (n_b*bn)
+  int kblocks;         // reduce blocks per tile
+  // FC: A 5-D map {64, kpb, bn, k_b, n_b}
+  int a_kpb, a_bn, a_rows_split;  // a_rows_split: bn >= 128
+  // conv: A 5-D map {64, W, H, C_b, N}; 2 output rows x 64 columns per tile
+  int cv_P, cv_Q, cv_R, cv_S, cv_pad, cv_Cb, cv_tiles_per_img;
+  // ---- B feed (features) ----
+  int b_kpb, b_bm, b_rows_split;  // B 5-D map {64, kpb, bm, k_b, m_b}; split: bm >= BN
+  // ---- tiles ----
+  int tiles_m, tiles_n, feats;
+  // ---- output / epilogue: out[n_b][m_b][bn][bm] ----
+  int o_bn, o_bm, o_mb;
+  int act, flags;
+  const void* bias;
+  const uint16_t* residual;
+  void* out;
+  uint8_t* mask;
+};
+
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  // barriers: full[S], empty[S], tfull[2], tempty[2]; then tmem base + gelu table
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 64 * 4 + 1024;
+};
+
+__device__ __forceinline__ void a_coords(const Params& p, int tm, int j, int c[5]) {
+  if (p.mode == FEED_FC) {
+    c[0] = 0;
+    c[1] = j % p.a_kpb;
+    c[3] = j / p.a_kpb;
+    if (p.a_rows_split) {
+      c[2] = (tm * BM) % p.a_bn;
+      c[4] = (tm * BM) / p.a_bn;
+    } else {
+      c[2] = 0;
+      c[4] = tm * (BM / p.a_bn);
+    }
+  } else {
+    // reduce block j = (r*S + s)*C_b + cb ; tile = (image n, output rows 2*pr, 2*pr+1)
+    const int cb = j % p.cv_Cb;
+    const int tap = j / p.cv_Cb;
+    const int r = tap / p.cv_S, s = tap % p.cv_S;
+    const int n = tm / p.cv_tiles_per_img;
+    const int pr = tm % p.cv_tiles_per_img;
+    c[0] = 0;
+    c[1] = s - p.cv_pad;          // input column of output column 0 (may be < 0: zero fill)
+    c[2] = 2 * pr + r - p.cv_pad; // input row
+    c[3] = cb;
+    c[4] = n;
+  }
+}
+
+__device__ __forceinline__ void b_coords(const Params& p, int tn, int j, int c[5]) {
+  c[0] = 0;
+  c[1] = j % p.b_kpb;
+  c[3] = j / p.b_kpb;
+  const int f0 = tn * p.feats / p.tiles_n;  // = tn * BN
+  if (p.b_rows_split) {
+    c[2] = f0 % p.b_bm;
+    c[4] = f0 / p.b_bm;
+  } else {
+    c[2] = 0;
+    c[4] = f0 / p.b_bm;
+  }
+}
+
+// global token index of accumulator row r of tile tm (or -1 if padding)
+__device__ __forceinline__ int row_token(const Params& p, int tm, int r) {
+  if (p.mode == FEED_FC) {
+    const int t = tm * BM + r;
+    return t < p.tokens ? t : -1;
+  }
+  const int n = tm / p.cv_tiles_per_img;
+  const int pr = tm % p.cv_tiles_per_img;
+  const int oh = 2 * pr + (r >> 6), ow = r & 63;
+  if (oh >= p.cv_P || ow >= p.cv_Q) return -1;
+  return (n * p.cv_P + oh) * p.cv_Q + ow;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                 const __grid_constant__ CUtensorMap map_b, const Params p) {
+  using S = Smem<BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128B-swizzled tiles
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* gelu_tab = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_tiles = p.tiles_m * p.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&map_a);
+    prefetch_tmap(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  if (threadIdx.x >= 64 && threadIdx.x < 128) load_gelu_table(gelu_tab, threadIdx.x - 64, 64);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+        for (int j = 0; j < p.kblocks; ++j, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * S::STAGE_BYTES;
+          uint8_t* sb = sa + S::A_BYTES;
+          mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+          int ca[5], cb[5];
+          a_coords(p, tm, j, ca);
+          b_coords(p, tn, j, cb);
+          tma_load_5d(sa, &map_a, &full[s], ca[0], ca[1], ca[2], ca[3], ca[4]);
+          tma_load_5d(sb, &map_b, &full[s], cb[0], cb[1], cb[2], cb[3], cb[4]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      uint32_t it = 0, tcount = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
+        const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+        mbar_wait(&tempty[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + as * BN;
+        for (int j = 0; j < p.kblocks; ++j, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
+          const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            umma_f16(tmem_d, sw128_kmajor_desc(sa + kk * 32), sw128_kmajor_desc(sb + kk * 32),
+                     idesc, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;
+    uint32_t tcount = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
+      const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+      const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const int t = row_token(p, tm, r);
+      const int nb = t >= 0 ? t / p.o_bn : 0;
+      const int n_in = t >= 0 ? t % p.o_bn : 0;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + ch * 32, v);
+        tmem_ld_wait();
+        const int f0 = tn * BN + ch * 32;
+        if (t < 0 || f0 >= p.feats) continue;
+        const int mb = f0 / p.o_bm, m_in = f0 % p.o_bm;
+        const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+        if (p.flags & TPP_FC_BIAS) {
+          if (p.flags & TPP_FC_BIAS_FP32) {
+            const float4* bp = reinterpret_cast<const float4*>(
+                reinterpret_cast<const float*>(p.bias) + f0);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              float4 b4 = __ldg(bp + i);
+              x[4 * i] = __fadd_rn(x[4 * i], b4.x);
+              x[4 * i + 1] = __fadd_rn(x[4 * i + 1], b4.y);
+              x[4 * i + 2] = __fadd_rn(x[4 * i + 2], b4.z);
+              x[4 * i + 3] = __fadd_rn(x[4 * i + 3], b4.w);
+            }
+          } else {
+            const uint4* bp = reinterpret_cast<const uint4*>(
+                reinterpret_cast<const uint16_t*>(p.bias) + f0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint4 b4 = __ldg(bp + i);
+              const uint32_t w[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], bf16_to_f32((uint16_t)(w[e] & 0xFFFF)));
+                x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], bf16_to_f32((uint16_t)(w[e] >> 16)));
+              }
+            }
+          }
+        }
+        if (p.act == TPP_ACT_RELU) {
+          if (p.flags & TPP_FC_RELU_MASK) {
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) bits |= (x[i] > 0.0f ? 1u : 0u) << i;
+            *reinterpret_cast<uint32_t*>(p.mask + row_off * (p.o_bm / 8) + m_in / 8) = bits;
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = relu_f(x[i]);
+        } else if (p.act == TPP_ACT_GELU) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = gelu_fwd(x[i], gelu_tab);
+        }
+        if (p.flags & TPP_FC_RESIDUAL) {
+          const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 r4 = __ldg(rp + i);
+            const uint32_t w[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], bf16_to_f32((uint16_t)(w[e] & 0xFFFF)));
+              x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], bf16_to_f32((uint16_t)(w[e] >> 16)));
+            }
+          }
+        }
+        if (p.flags & TPP_FC_OUT_FP32) {
+          float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + row_off * p.o_bm + m_in);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            op[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+        } else {
+          uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            op[i] = make_uint4(pack_bf16x2(x[8 * i], x[8 * i + 1]), pack_bf16x2(x[8 * i + 2], x[8 * i + 3]),
+                               pack_bf16x2(x[8 * i + 4], x[8 * i + 5]), pack_bf16x2(x[8 * i + 6], x[8 * i + 7]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, S::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: tensor maps (driver entry point, no -lcuda), launch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 5-D bf16 map, dims innermost first, strides in bytes for dims 1..4
+static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
+                       const uint64_t strides[4], const uint32_t box[5]) {
+  auto enc = get_encode();
+  if (!enc) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  if (reinterpret_cast<uintptr_t>(base) % 16) return fail(TPP_E_TENSOR, "TMA base not 16B aligned");
+  cuuint64_t gd[5];
+  cuuint64_t gs[4];
+  cuuint32_t bd[5], es[5];
+  for (int i = 0; i < 5; ++i) {
+    gd[i] = dims[i];
+    bd[i] = box[i];
+    es[i] = 1;
+  }
+  for (int i = 0; i < 4; ++i) {
+    if (strides[i] % 16) return fail(TPP_E_TENSOR, "TMA stride not a multiple of 16 bytes");
+    gs[i] = strides[i];
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gd, gs, bd,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return TPP_OK;
+}
+
+template <int BN, int STAGES>
+static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+                      cudaStream_t stream) {
+  using S = Smem<BN, STAGES>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
+    attr_set = true;
+  }
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  brgemm_tc_kernel<BN, STAGES><<<grid, kThreads, S::BYTES, stream>>>(ma, mb, p);
+  TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
+  return TPP_OK;
+}
+
+static int launch(int bn_tile, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+                  cudaStream_t s) {
+  switch (bn_tile) {
+    case 64: return launch_cfg<64, 8>(ma, mb, p, s);
+    case 128: return launch_cfg<128, 6>(ma, mb, p, s);
+    case 256: return launch_cfg<256, 4>(ma, mb, p, s);
+    default: return fail(TPP_E_UNSUPPORTED, "tile width must be 64, 128 or 256");
+  }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// FC forward (BF16, tensor cores).  Reference naming (kernels.py:287-297):
+//   weights packed [m_b][k_b][bm][bk] (K-major), input [n_b][k_b][bn][bk],
+//   output [n_b][m_b][bn][bm].
+// ---------------------------------------------------------------------------
+int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
+                  const void* residual, void* out, void* mask, cudaStream_t stream) {
+  using namespace tc;
+  const int m_b = d->m_b, n_b = d->n_b, k_b = d->k_b, bm = d->bm, bn = d->bn, bk = d->bk;
+  TPP_REQUIRE(bk % 64 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bk % 64 == 0");
+  TPP_REQUIRE(bm % 32 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bm % 32 == 0");
+  TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
+              "tensor-core FC needs bn | 128 or 128 | bn");
+  const int feats = m_b * bm;
+  int BN = d->block_n;
+  if (BN == 0) {
+    // enough tiles to cover the SMs, widest tile otherwise
+    const int tiles_m = (n_b * bn + BM - 1) / BM;
+    BN = 256;
+    while (BN > 64 && (feats % BN != 0 || (int64_t)tiles_m * (feats / BN) < num_sms())) BN /= 2;
+  }
+  TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "features must be a multiple of the tile width");
+  TPP_REQUIRE((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0), TPP_E_UNSUPPORTED,
+              "bm and the tile width must nest");
+
+  Params p{};
+  p.mode = FEED_FC;
+  p.tokens = n_b * bn;
+  p.kblocks = k_b * (bk / 64);
+  p.a_kpb = bk / 64;
+  p.a_bn = bn;
+  p.a_rows_split = bn >= BM;
+  p.b_kpb = bk / 64;
+  p.b_bm = bm;
+  p.b_rows_split = bm >= BN;
+  p.tiles_m = (p.tokens + BM - 1) / BM;
+  p.tiles_n = feats / BN;
+  p.feats = feats;
+  p.o_bn = bn;
+  p.o_bm = bm;
+  p.o_mb = m_b;
+  p.act = d->activation;
+  p.flags = d->flags;
+  p.bias = bias;
+  p.residual = reinterpret_cast<const uint16_t*>(residual);
+  p.out = out;
+  p.mask = reinterpret_cast<uint8_t*>(mask);
+
+  CUtensorMap ma, mb;
+  {
+    const uint64_t dims[5] = {64, (uint64_t)(bk / 64), (uint64_t)bn, (uint64_t)k_b, (uint64_t)n_b};
+    const uint64_t str[4] = {128, (uint64_t)bk * 2, (uint64_t)bn * bk * 2, (uint64_t)k_b * bn * bk * 2};
+    const uint32_t box[5] = {64, 1, (uint32_t)(bn >= BM ? BM : bn), 1, (uint32_t)(bn >= BM ? 1 : BM / bn)};
+    int rc = make_map_5d(&ma, x, dims, str, box);
+    if (rc) return rc;
+  }
+  {
+    const uint64_t dims[5] = {64, (uint64_t)(bk / 64), (uint64_t)bm, (uint64_t)k_b, (uint64_t)m_b};
+    const uint64_t str[4] = {128, (uint64_t)bk * 2, (uint64_t)bm * bk * 2, (uint64_t)k_b * bm * bk * 2};
+    const uint32_t box[5] = {64, 1, (uint32_t)(bm >= BN ? BN : bm), 1, (uint32_t)(bm >= BN ? 1 : BN / bm)};
+    int rc = make_map_5d(&mb, w_packed, dims, str, box);
+    if (rc) return rc;
+  }
+  return launch(BN, ma, mb, p, stream);
+}
+
+// ---------------------------------------------------------------------------
+// 3x3 (R x S) stride-1 'same' convolution, bc = bk = 64 per block.
+//   input [N][C_b][H][W][64], weights packed [K_b][R][S][C_b][64 out][64 in],
+//   output [N][K_b][H][W][64].  Tiles: 2 output rows x 64 columns (W <= 64).
+// ---------------------------------------------------------------------------
+int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
+                    const void* w_packed, const void* x, void* out, cudaStream_t stream) {
+  using namespace tc;
+  TPP_REQUIRE(W <= 64, TPP_E_UNSUPPORTED, "tensor-core conv tiles need W <= 64");
+  TPP_REQUIRE(2 * pad == R - 1 && 2 * pad == S - 1, TPP_E_UNSUPPORTED,
+              "tensor-core conv implements 'same' padding");
+  const int P = H, Q = W;
+  const int feats = Kb * 64;
+  const int BN = feats >= 256 && feats % 256 == 0 ? 256 : (feats % 128 == 0 ? 128 : 64);
+  Params p{};
+  p.mode = FEED_CONV;
+  p.kblocks = R * S * Cb;
+  p.cv_P = P;
+  p.cv_Q = Q;
+  p.cv_R = R;
+  p.cv_S = S;
+  p.cv_pad = pad;
+  p.cv_Cb = Cb;
+  p.cv_tiles_per_img = (P + 1) / 2;
+  p.b_kpb = 1;
+  p.b_bm = 64;
+  p.b_rows_split = 64 >= BN;
+  p.tiles_m = N * p.cv_tiles_per_img;
+  p.tiles_n = feats / BN;
+  p.feats = feats;
+  p.o_bn = P * Q;
+  p.o_bm = 64;
+  p.o_mb = Kb;
+  p.act = TPP_ACT_NONE;
+  p.flags = 0;
+  p.out = out;
+
+  CUtensorMap ma, mb;
+  {
+    const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Cb, (uint64_t)N};
+    const uint64_t str[4] = {128, (uint64_t)W * 128, (uint64_t)H * W * 128, (uint64_t)Cb * H * W * 128};
+    const uint32_t box[5] = {64, 64, 2, 1, 1};
+    int rc = make_map_5d(&ma, x, dims, str, box);
+    if (rc) return rc;
+  }
+  {
+    const int J = R * S * Cb;
+    const uint64_t dims[5] = {64, 1, 64, (uint64_t)J, (uint64_t)Kb};
+    const uint64_t str[4] = {128, 128, 64 * 128, (uint64_t)J * 64 * 128};
+    const uint32_t box[5] = {64, 1, 64, 1, (uint32_t)(BN / 64)};
+    int rc = make_map_5d(&mb, w_packed, dims, str, box);
+    if (rc) return rc;
+  }
+  return launch(BN, ma, mb, p, stream);
+}
+
+}  // namespace tpp

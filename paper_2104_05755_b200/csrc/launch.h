@@ -1,0 +1,68 @@
+// Internal launch interfaces shared by the translation units of the library.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tpp_b200.h"
+
+namespace tpp {
+
+struct OrderedParams {
+  int m, n, k, lda, ldb, ldc, vnni, alpha;
+  int64_t count;
+  int mode;  // 0 stride, 1 offset, 2 address
+  const char* a;
+  const char* b;
+  int64_t stride_a, stride_b;
+  const int64_t* a_offs;
+  const int64_t* b_offs;
+  const void* const* a_ptrs;
+  const void* const* b_ptrs;
+  char* c;
+  int64_t inst_a, inst_b, inst_c;
+  int64_t instances;
+  double beta;
+};
+int launch_brgemm_ordered(const OrderedParams& p, int in_dtype, cudaStream_t s);
+
+int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
+                  const void* residual, void* out, void* mask, cudaStream_t stream);
+int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
+                    const void* w_packed, const void* x, void* out, cudaStream_t stream);
+
+struct BlockRemap {
+  int mode;            // 0 identity, 1 conv fwd [Kb][Cb][R][S] -> [Kb][R][S][Cb]
+  int d0, d1, d2, d3;  // src block index = ((i0*d1 + i1)*d2 + i2)*d3 + i3
+};
+int launch_word_transpose_blocks(const void* src, void* dst, int rows, int cols, int64_t nblocks,
+                                 BlockRemap remap, cudaStream_t s);
+int launch_pack_conv_bwd(const void* src, void* dst, int Kb, int Cb, int R, int S, int bc, int bk,
+                         cudaStream_t s);
+// kind: 0 TRANSPOSE, 1 VNNI, 2 VNNI_TO_VNNIT, 3 COPY
+int launch_transform(int kind, int esize, const void* in, int in_ld, void* out, int out_rows,
+                     int out_cols, int out_ld, int alpha, int alpha_out, int lrows, int lcols,
+                     cudaStream_t s);
+
+struct DView {
+  const void* p;
+  int rows, cols, ld, dtype, bcast;
+};
+int launch_unary(int kind, const DView& in, const DView& aux, void* out, int out_dtype, int out_ld,
+                 uint8_t* mask_out, bool f64, cudaStream_t s);
+int launch_nary(int arity, int kind, const DView& a, const DView& b, const DView& c, void* out,
+                int rows, int cols, int out_dtype, int out_ld, bool f64, cudaStream_t s);
+int launch_reduce(const DView& in, int axis, int op, int squared, void* out, int out_dtype,
+                  int out_ld, void* scratch, bool f64, cudaStream_t s);
+
+int launch_layernorm_view(const DView& x, const DView& g, const DView& b, double eps, void* out,
+                          int out_ld, int out_dtype, float* mean_out, float* var_out,
+                          cudaStream_t s);
+int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
+                             const float* gamma, const float* beta, double eps, void* out,
+                             float* mean_out, float* var_out, cudaStream_t s);
+int launch_softmax(int s1, int s2, int s3, const DView& x, float* y, int y_ld, cudaStream_t s);
+int launch_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad, int grad_dtype,
+                     float lr, cudaStream_t s);
+
+}  // namespace tpp

@@ -1,0 +1,250 @@
+// K4 / K9: LayerNorm equation TPP, softmax, split-SGD — bitwise to the reference.
+//
+// LayerNorm (kernels.py:134-176): per row, FP32 sums of x and x*x folded in
+// ascending column order (ops.py:484-522), float64 glue
+//     mu = s/n ; var = ss/n - mu*mu ; rstd = 1/sqrt(var + eps)
+// stored as FP32 scale = rstd, shift = -mu*rstd, then the scaling equation of
+// two cascaded MULADDs  out = B + (shift + x*scale) * G  (ops.py:812-815).
+// The reference order is one sequential chain per row, so one thread owns a
+// row's statistics; what makes it fast on B200 is that the chain reads come
+// from a coalesced access pattern (column-major view: consecutive threads =
+// consecutive rows) or from shared memory (blocked layout), never from
+// scattered HBM.
+
+#include "common.cuh"
+
+namespace tpp {
+
+__device__ __forceinline__ float nload(const DView& v, int i, int j) {
+  const int pi = (v.bcast == TPP_BCAST_ROW || v.bcast == TPP_BCAST_SCALAR) ? 0 : i;
+  const int pj = (v.bcast == TPP_BCAST_COL || v.bcast == TPP_BCAST_SCALAR) ? 0 : j;
+  const int64_t idx = pi + (int64_t)pj * v.ld;
+  if (v.dtype == TPP_BF16) return bf16_to_f32(reinterpret_cast<const uint16_t*>(v.p)[idx]);
+  return reinterpret_cast<const float*>(v.p)[idx];
+}
+
+__device__ __forceinline__ void row_glue(float s, float ss, int n, double eps, float& scale,
+                                         float& shift, double& mu, double& var) {
+  mu = (double)s / (double)n;
+  var = __dsub_rn((double)ss / (double)n, __dmul_rn(mu, mu));
+  const double rstd = 1.0 / sqrt(__dadd_rn(var, eps));
+  scale = (float)rstd;
+  shift = (float)__dmul_rn(-mu, rstd);
+}
+
+// ---- column-major view: one thread per row, coalesced across threads -------
+__global__ void layernorm_view_kernel(DView x, DView g, DView b, double eps, void* out, int out_ld,
+                                      int out_dtype, float* mean_out, float* var_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= x.rows) return;
+  const int n = x.cols;
+  float s = 0.0f, ss = 0.0f;
+  for (int j = 0; j < n; ++j) {
+    const float v = nload(x, i, j);
+    s = __fadd_rn(s, v);
+    ss = __fadd_rn(ss, __fmul_rn(v, v));
+  }
+  float scale, shift;
+  double mu, var;
+  row_glue(s, ss, n, eps, scale, shift, mu, var);
+  if (mean_out) mean_out[i] = (float)mu;
+  if (var_out) var_out[i] = (float)var;
+  for (int j = 0; j < n; ++j) {
+    const float v = nload(x, i, j);
+    const float inner = __fadd_rn(shift, __fmul_rn(v, scale));
+    const float r = __fadd_rn(nload(b, i, j), __fmul_rn(inner, nload(g, i, j)));
+    const int64_t o = i + (int64_t)j * out_ld;
+    if (out_dtype == TPP_BF16) reinterpret_cast<uint16_t*>(out)[o] = f32_to_bf16(r);
+    else reinterpret_cast<float*>(out)[o] = r;
+  }
+}
+
+int launch_layernorm_view(const DView& x, const DView& g, const DView& b, double eps, void* out,
+                          int out_ld, int out_dtype, float* mean_out, float* var_out,
+                          cudaStream_t s) {
+  if (x.rows == 0) return TPP_OK;
+  const int threads = 128;
+  layernorm_view_kernel<<<(x.rows + threads - 1) / threads, threads, 0, s>>>(
+      x, g, b, eps, out, out_ld, out_dtype, mean_out, var_out);
+  TPP_CUDA_LAUNCH_CHECK("layernorm_view_kernel");
+  return TPP_OK;
+}
+
+// ---- blocked activations [n_b][m_b][bn][bm] (tokens x features) -------------
+// CTA = 32 tokens of one token block, all F = m_b*bm features staged in smem
+// (row pitch F+2 elements: conflict-free per-thread row walks).  Phase 1:
+// coalesced HBM -> smem.  Phase 2: thread t walks its token's features
+// ascending (the reference fold).  Phase 3: all threads apply the scaling
+// equation and store coalesced.
+template <typename T>
+__global__ void __launch_bounds__(256)
+layernorm_blocked_kernel(int n_b, int m_b, int bn, int bm, const T* __restrict__ x,
+                         const float* __restrict__ gamma, const float* __restrict__ beta,
+                         double eps, T* __restrict__ out, float* mean_out, float* var_out) {
+  extern __shared__ __align__(16) uint8_t lsm[];
+  const int F = m_b * bm;
+  const int pitch = F + (sizeof(T) == 2 ? 2 : 1);
+  T* rows = reinterpret_cast<T*>(lsm);
+  float* sc = reinterpret_cast<float*>(lsm + (((size_t)32 * pitch * sizeof(T) + 15) & ~(size_t)15));
+  float* sh = sc + 32;
+  const int chunks_per_blk = (bn + 31) / 32;
+  const int nb = blockIdx.x / chunks_per_blk;
+  const int n0 = (blockIdx.x % chunks_per_blk) * 32;
+  const int T_ = min(32, bn - n0);
+  // phase 1
+  for (int mb = 0; mb < m_b; ++mb) {
+    const T* src = x + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
+      const int t = e / bm, m = e % bm;
+      rows[t * pitch + mb * bm + m] = src[e];
+    }
+  }
+  __syncthreads();
+  // phase 2
+  if (threadIdx.x < T_) {
+    const T* r = rows + threadIdx.x * pitch;
+    float s = 0.0f, ss = 0.0f;
+    for (int f = 0; f < F; ++f) {
+      float v;
+      if (sizeof(T) == 2) v = bf16_to_f32(reinterpret_cast<const uint16_t*>(r)[f]);
+      else v = reinterpret_cast<const float*>(r)[f];
+      s = __fadd_rn(s, v);
+      ss = __fadd_rn(ss, __fmul_rn(v, v));
+    }
+    float scale, shift;
+    double mu, var;
+    row_glue(s, ss, F, eps, scale, shift, mu, var);
+    sc[threadIdx.x] = scale;
+    sh[threadIdx.x] = shift;
+    const int64_t tok = (int64_t)nb * bn + n0 + threadIdx.x;
+    if (mean_out) mean_out[tok] = (float)mu;
+    if (var_out) var_out[tok] = (float)var;
+  }
+  __syncthreads();
+  // phase 3
+  for (int mb = 0; mb < m_b; ++mb) {
+    T* dst = out + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
+      const int t = e / bm, m = e % bm;
+      const int f = mb * bm + m;
+      float v;
+      if (sizeof(T) == 2) v = bf16_to_f32(reinterpret_cast<const uint16_t*>(rows)[t * pitch + f]);
+      else v = reinterpret_cast<const float*>(rows)[t * pitch + f];
+      const float inner = __fadd_rn(sh[t], __fmul_rn(v, sc[t]));
+      const float gv = gamma ? gamma[f] : 1.0f;
+      const float bv = beta ? beta[f] : 0.0f;
+      const float res = __fadd_rn(bv, __fmul_rn(inner, gv));
+      if (sizeof(T) == 2) reinterpret_cast<uint16_t*>(dst)[e] = f32_to_bf16(res);
+      else reinterpret_cast<float*>(dst)[e] = res;
+    }
+  }
+}
+
+int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
+                             const float* gamma, const float* beta, double eps, void* out,
+                             float* mean_out, float* var_out, cudaStream_t s) {
+  const int F = m_b * bm;
+  const int es = dtype == TPP_BF16 ? 2 : 4;
+  const int pitch = F + (es == 2 ? 2 : 1);
+  const size_t smem = (((size_t)32 * pitch * es + 15) & ~(size_t)15) + 64 * sizeof(float);
+  TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "layernorm_blocked: feature row too long for smem");
+  const int blocks = n_b * ((bn + 31) / 32);
+  if (blocks == 0) return TPP_OK;
+  cudaError_t e;
+  if (es == 2) {
+    e = cudaFuncSetAttribute(layernorm_blocked_kernel<uint16_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked)");
+    layernorm_blocked_kernel<uint16_t><<<blocks, 256, smem, s>>>(
+        n_b, m_b, bn, bm, (const uint16_t*)x, gamma, beta, eps, (uint16_t*)out, mean_out, var_out);
+  } else {
+    e = cudaFuncSetAttribute(layernorm_blocked_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked)");
+    layernorm_blocked_kernel<float><<<blocks, 256, smem, s>>>(
+        n_b, m_b, bn, bm, (const float*)x, gamma, beta, eps, (float*)out, mean_out, var_out);
+  }
+  TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_kernel");
+  return TPP_OK;
+}
+
+// ---- softmax (kernels.py:84-99), one CTA per s1 x s3 slice -------------------
+__global__ void softmax_kernel(int s1, int s3, DView x, float* y, int y_ld) {
+  extern __shared__ float ssm[];  // per-column sums [s3], then reduction scratch
+  const int j0 = blockIdx.x * s3;
+  // max over the slice (order irrelevant for max; NaN propagates)
+  float mx = -__int_as_float(0x7F800000);
+  bool nan = false;
+  for (int e = threadIdx.x; e < s1 * s3; e += blockDim.x) {
+    const float v = nload(x, e % s1, j0 + e / s1);
+    if (v != v) nan = true;
+    mx = fmaxf(mx, v);
+  }
+  float* red = ssm + s3;
+  red[threadIdx.x] = nan ? __int_as_float(0x7FC00000) : mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = red[0];
+    for (int t = 1; t < blockDim.x; ++t) m = (m != m || red[t] != red[t]) ? __int_as_float(0x7FC00000) : fmaxf(m, red[t]);
+    red[0] = m;
+  }
+  __syncthreads();
+  mx = red[0];
+  // per-column fold over rows ascending (ops.py:519 "per_col")
+  for (int c = threadIdx.x; c < s3; c += blockDim.x) {
+    float acc = 0.0f;
+    for (int i = 0; i < s1; ++i) acc = __fadd_rn(acc, exp_taylor(__fsub_rn(nload(x, i, j0 + c), mx)));
+    ssm[c] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.0f;
+    for (int c = 0; c < s3; ++c) tot = __fadd_rn(tot, ssm[c]);
+    red[1] = __fdiv_rn(1.0f, tot);
+  }
+  __syncthreads();
+  const float rcp = red[1];
+  for (int e = threadIdx.x; e < s1 * s3; e += blockDim.x) {
+    const int i = e % s1, c = e / s1;
+    const float ev = exp_taylor(__fsub_rn(nload(x, i, j0 + c), mx));
+    y[i + (int64_t)(j0 + c) * y_ld] = __fmul_rn(ev, rcp);
+  }
+}
+
+int launch_softmax(int s1, int s2, int s3, const DView& x, float* y, int y_ld, cudaStream_t s) {
+  if (s2 == 0) return TPP_OK;
+  const int threads = 128;
+  const size_t smem = (size_t)(s3 + threads + 2) * sizeof(float);
+  TPP_REQUIRE(smem <= 48 * 1024, TPP_E_UNSUPPORTED, "softmax slice too wide");
+  softmax_kernel<<<s2, threads, smem, s>>>(s1, s3, x, y, y_ld);
+  TPP_CUDA_LAUNCH_CHECK("softmax_kernel");
+  return TPP_OK;
+}
+
+// ---- split-SGD (kernels.py:235-251): pack, W - g*lr, unpack (bitwise FP32 SGD)
+__global__ void split_sgd_kernel(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad,
+                                 int grad_dtype, float lr) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float w = __uint_as_float(((uint32_t)hi[e] << 16) | lo[e]);
+    const float g = grad_dtype == TPP_BF16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(grad)[e])
+                                           : reinterpret_cast<const float*>(grad)[e];
+    const float r = __fsub_rn(w, __fmul_rn(g, lr));
+    const uint32_t u = __float_as_uint(r);
+    hi[e] = (uint16_t)(u >> 16);
+    lo[e] = (uint16_t)(u & 0xFFFF);
+  }
+}
+
+int launch_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad, int grad_dtype,
+                     float lr, cudaStream_t s) {
+  if (n == 0) return TPP_OK;
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  split_sgd_kernel<<<(unsigned)blocks, threads, 0, s>>>(n, hi, lo, grad, grad_dtype, lr);
+  TPP_CUDA_LAUNCH_CHECK("split_sgd_kernel");
+  return TPP_OK;
+}
+
+}  // namespace tpp

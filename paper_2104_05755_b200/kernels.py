@@ -1,0 +1,361 @@
+"""Composite kernels on the GPU — drop-in for kernels.py of the reference
+(/root/reference/pkg/src/tensorprim/kernels.py) on the BRGEMM hot path:
+``fc_forward`` (FcSpec), ``layernorm``, ``softmax``, ``split_sgd_step``;
+plus the B200 layer objects the paper's drivers become on a GPU:
+
+* ``FcLayer`` — blocked BF16 fully-connected layer: weights are re-laid out
+  ONCE from VNNI-2 into UMMA-canonical K-major blocks (the paper formats
+  weights into VNNI once; here into the tensor-core
+  layout), then every forward is one tcgen05 BRGEMM launch with bias, ReLU
+  (+bitmask) / GELU, residual and BF16 RNE narrowing fused into the epilogue.
+* ``layernorm_blocked`` — the LayerNorm equation TPP on the blocked
+  activation layout FC produces, bitwise to the reference.
+* ``Conv2d`` — 3x3 direct convolution as an offset-addressed BRGEMM over the
+  taps, forward and backward-data.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+import math
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .dtypes import DType
+from .ops import UnaryKind
+from .tensor import (Bcast, TensorDesc, TensorError, TensorView, alloc, broadcast)
+
+# ---------------------------------------------------------------------------
+# fully connected (kernels.py:287-329)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class FcSpec:
+    """Blocked FC: A[M_b][K_b][b_k][b_m] x B[N_b][K_b][b_n][b_k] -> C[N_b][M_b][b_n][b_m]."""
+    m_b: int
+    n_b: int
+    k_b: int
+    bm: int
+    bn: int
+    bk: int
+    activation: Optional[UnaryKind] = None
+
+
+_ACT = {None: _lib.ACT_NONE, UnaryKind.RELU: _lib.ACT_RELU, UnaryKind.GELU: _lib.ACT_GELU}
+
+
+def _flat(x) -> torch.Tensor:
+    if isinstance(x, TensorView):
+        return x.primary
+    if isinstance(x, tuple):
+        buf, off = x
+        buf = buf.primary if isinstance(buf, TensorView) else buf
+        return buf[int(off):]
+    return x
+
+
+def _fc_desc(spec: FcSpec, in_dtype: DType, flags: int = 0, block_n: int = 0) -> _lib.FcDescC:
+    return _lib.FcDescC(spec.m_b, spec.n_b, spec.k_b, spec.bm, spec.bn, spec.bk, in_dtype.code,
+                        _ACT[spec.activation], flags, block_n)
+
+
+def fc_forward(spec: FcSpec, a_buf, b_buf, c: TensorView, threads: int = 1, stream=None) -> None:
+    """kernels.py:300-329 — FP32, bitwise the reference: per output block a
+    stride-BRGEMM over K_b in reference order, then the activation.
+    (BF16 layers use :class:`FcLayer`.)"""
+    bm, bn, bk = spec.bm, spec.bn, spec.bk
+    if (c.desc.rows, c.desc.cols) != (bm, spec.n_b * spec.m_b * bn) or c.desc.ld != bm:
+        raise TensorError("C must be a contiguous bm x (N_b*M_b*bn) block container")
+    if spec.activation not in (None, UnaryKind.RELU):
+        raise NotImplementedError("FP32 fc_forward: activation must be None or RELU")
+    a, b = _flat(a_buf), _flat(b_buf)
+    for t, n, what in ((a, spec.m_b * spec.k_b * bk * bm, "A"), (b, spec.n_b * spec.k_b * bn * bk, "B")):
+        if t.dtype != torch.float32:
+            raise TensorError(f"{what} buffer must be FP32")
+        if t.numel() < n:
+            raise TensorError(f"{what} buffer too small: {t.numel()} < {n}")
+    if c.desc.dtype is not DType.FP32:
+        raise TensorError("C must be FP32")
+    c.require_cuda("fc_forward")
+    lib = _lib.load()
+    d = _fc_desc(spec, DType.FP32)
+    _lib.check(lib.tpp_fc_forward(C.byref(d), a.data_ptr(), b.data_ptr(), None, None, c.ptr, None,
+                                  _lib.stream_ptr(stream)), "fc_forward")
+
+
+class FcLayer:
+    """BF16 blocked FC layer on tcgen05 (SURVEY §0.1 naming):
+
+    weights VNNI ``[m_b][k_b][bk/2][bm][2]`` (out-feature blocks x in-channel
+    blocks), input ``[n_b][k_b][bn][bk]``, output ``[n_b][m_b][bn][bm]``,
+    bias ``[m_b*bm]`` (BF16 or FP32).  ``forward`` computes
+    ``out = act(W x + bias) + residual`` with every epilogue op fused and the
+    reference's FP32 op order, narrowed to BF16 with RNE.
+    """
+
+    def __init__(self, m_b: int, k_b: int, bm: int, bk: int, w_vnni: torch.Tensor,
+                 bias: Optional[torch.Tensor] = None, activation: Optional[UnaryKind] = None,
+                 block_n: int = 0, stream=None):
+        if w_vnni.dtype != torch.bfloat16 or not w_vnni.is_cuda:
+            raise TensorError("FcLayer weights must be a CUDA bfloat16 VNNI buffer")
+        if w_vnni.numel() < m_b * k_b * bm * bk:
+            raise TensorError("weight buffer too small")
+        if bias is not None and (bias.numel() < m_b * bm or bias.dtype not in (torch.bfloat16, torch.float32)):
+            raise TensorError("bias must hold m_b*bm BF16/FP32 values")
+        self.m_b, self.k_b, self.bm, self.bk = m_b, k_b, bm, bk
+        self.activation = activation
+        self.bias = bias
+        self.block_n = block_n
+        self.w_packed = torch.empty(m_b * k_b * bm * bk, dtype=torch.bfloat16, device=w_vnni.device)
+        self.repack(w_vnni, stream)
+
+    def repack(self, w_vnni: torch.Tensor, stream=None) -> None:
+        """VNNI -> K-major word transpose (tpp_fc_pack_weights)."""
+        lib = _lib.load()
+        d = _lib.FcDescC(self.m_b, 1, self.k_b, self.bm, 1, self.bk, _lib.BF16, 0, 0, 0)
+        _lib.check(lib.tpp_fc_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_packed.data_ptr(),
+                                           _lib.stream_ptr(stream)), "fc_pack_weights")
+
+    def desc(self, n_b: int, bn: int, flags: int) -> _lib.FcDescC:
+        return _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16,
+                            _ACT[self.activation], flags, self.block_n)
+
+    def forward(self, x: torch.Tensor, n_b: int, bn: int, out: Optional[torch.Tensor] = None,
+                residual: Optional[torch.Tensor] = None, relu_mask: Optional[torch.Tensor] = None,
+                out_fp32: bool = False, stream=None) -> torch.Tensor:
+        if x.dtype != torch.bfloat16 or not x.is_cuda:
+            raise TensorError("FC input must be a CUDA bfloat16 buffer")
+        if x.numel() < n_b * self.k_b * bn * self.bk:
+            raise TensorError("input buffer too small")
+        n_out = n_b * self.m_b * bn * self.bm
+        if out is None:
+            out = torch.empty(n_out, dtype=torch.float32 if out_fp32 else torch.bfloat16, device=x.device)
+        if out.numel() < n_out:
+            raise TensorError("output buffer too small")
+        flags = 0
+        if self.bias is not None:
+            flags |= _lib.FC_BIAS | (_lib.FC_BIAS_FP32 if self.bias.dtype == torch.float32 else 0)
+        if residual is not None:
+            if residual.dtype != torch.bfloat16 or residual.numel() < n_out:
+                raise TensorError("residual must be a BF16 buffer shaped like the output")
+            flags |= _lib.FC_RESIDUAL
+        if relu_mask is not None:
+            if self.activation is not UnaryKind.RELU:
+                raise TensorError("a ReLU bitmask needs RELU activation")
+            if relu_mask.numel() < n_b * self.m_b * bn * ((self.bm + 7) // 8):
+                raise TensorError("bitmask buffer too small")
+            flags |= _lib.FC_RELU_MASK
+        if out_fp32 or out.dtype == torch.float32:
+            flags |= _lib.FC_OUT_FP32
+        lib = _lib.load()
+        d = self.desc(n_b, bn, flags)
+        _lib.check(lib.tpp_fc_forward(
+            C.byref(d), self.w_packed.data_ptr(), x.data_ptr(),
+            self.bias.data_ptr() if self.bias is not None else None,
+            residual.data_ptr() if residual is not None else None, out.data_ptr(),
+            relu_mask.data_ptr() if relu_mask is not None else None,
+            _lib.stream_ptr(stream)), "FcLayer.forward")
+        return out
+
+
+# ---------------------------------------------------------------------------
+# normalisation (kernels.py:106-176)
+# ---------------------------------------------------------------------------
+
+
+def layernorm(x: TensorView, g: TensorView, b: TensorView, eps: float, out: TensorView,
+              mean_out: TensorView | None = None, var_out: TensorView | None = None,
+              stream=None) -> None:
+    """kernels.py:134-176 — per-row layer normalisation of a column-major
+    rows x cols view, bitwise the reference (FP32 ascending sums, float64
+    glue, two cascaded MULADDs)."""
+    rows, cols = x.desc.rows, x.desc.cols
+    if cols < 2:
+        raise TensorError("layernorm needs a feature dimension of at least 2")
+    if eps <= 0:
+        raise TensorError("eps must be positive")
+    for v, name in ((g, "G"), (b, "B")):
+        if (v.desc.rows, v.desc.cols) != (rows, cols):
+            raise TensorError(f"{name} must broadcast to the input shape")
+    for v, name in ((mean_out, "mean"), (var_out, "var")):
+        if v is not None and (v.desc.dtype is not DType.FP32 or v.desc.rows != rows
+                              or v.desc.ld != rows and v.desc.cols > 1):
+            raise TensorError(f"{name} output must be an FP32 rows x 1 view")
+    for v in (x, g, b, out):
+        v.require_cuda("layernorm")
+    lib = _lib.load()
+    _lib.check(lib.tpp_layernorm(x.desc.c(), x.ptr, g.desc.c(), g.ptr, b.desc.c(), b.ptr,
+                                 float(eps), out.desc.c(), out.ptr,
+                                 mean_out.ptr if mean_out is not None else None,
+                                 var_out.ptr if var_out is not None else None,
+                                 _lib.stream_ptr(stream)), "layernorm")
+
+
+def layernorm_blocked(x: torch.Tensor, n_b: int, m_b: int, bn: int, bm: int, eps: float = 1e-5,
+                      gamma: Optional[torch.Tensor] = None, beta: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, mean_out: Optional[torch.Tensor] = None,
+                      var_out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """LayerNorm of every token of a blocked [n_b][m_b][bn][bm] activation
+    over its m_b*bm features (ascending feature order), gamma/beta FP32
+    [m_b*bm] (default 1 / 0, still applied as MULADD so signed zeros match)."""
+    if x.dtype not in (torch.bfloat16, torch.float32) or not x.is_cuda:
+        raise TensorError("x must be a CUDA bf16/fp32 buffer")
+    n = n_b * m_b * bn * bm
+    if x.numel() < n:
+        raise TensorError("x buffer too small")
+    if out is None:
+        out = torch.empty(n, dtype=x.dtype, device=x.device)
+    for t, name in ((gamma, "gamma"), (beta, "beta")):
+        if t is not None and (t.dtype != torch.float32 or t.numel() < m_b * bm):
+            raise TensorError(f"{name} must be FP32 [m_b*bm]")
+    lib = _lib.load()
+    dt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.FP32
+    p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    _lib.check(lib.tpp_layernorm_blocked(n_b, m_b, bn, bm, dt, x.data_ptr(), p(gamma), p(beta),
+                                         float(eps), out.data_ptr(), p(mean_out), p(var_out),
+                                         _lib.stream_ptr(stream)), "layernorm_blocked")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# softmax (kernels.py:49-99)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class SoftmaxSpec:
+    s1: int
+    s2: int
+    s3: int
+
+
+def softmax(spec: SoftmaxSpec, x: TensorView, y: TensorView, strategy=None, stream=None) -> None:
+    """Slice-wise softmax with exp_taylor, bitwise the reference."""
+    if (x.desc.rows, x.desc.cols) != (spec.s1, spec.s2 * spec.s3):
+        raise TensorError("softmax input must be s1 x (s2*s3)")
+    if (y.desc.rows, y.desc.cols) != (x.desc.rows, x.desc.cols):
+        raise TensorError("softmax output shape mismatch")
+    x.require_cuda("softmax")
+    lib = _lib.load()
+    _lib.check(lib.tpp_softmax(spec.s1, spec.s2, spec.s3, x.desc.c(), x.ptr, y.desc.c(), y.ptr,
+                               _lib.stream_ptr(stream)), "softmax")
+
+
+# ---------------------------------------------------------------------------
+# split SGD (kernels.py:235-251)
+# ---------------------------------------------------------------------------
+
+
+def split_sgd_step(weights, grad: TensorView, lr: float, stream=None) -> None:
+    """One SGD step on hi/lo split FP32 weights: bitwise FP32 SGD."""
+    from .tensor import SplitTensor
+    if not isinstance(weights, SplitTensor):
+        raise TensorError("weights must be a SplitTensor")
+    rows, cols = weights.rows, weights.cols
+    if (grad.desc.rows, grad.desc.cols) != (rows, cols):
+        raise TensorError("gradient shape mismatch")
+    for v in (weights.hi, weights.lo, grad):
+        if v.desc.ld != rows or v.desc.bcast is not Bcast.NONE:
+            raise TensorError("split_sgd_step needs contiguous views")
+    if grad.desc.dtype not in (DType.FP32, DType.BF16):
+        raise TensorError("gradient must be FP32 or BF16")
+    grad.require_cuda("split_sgd_step")
+    lib = _lib.load()
+    _lib.check(lib.tpp_split_sgd(rows * cols, weights.hi.ptr, weights.lo.ptr, grad.ptr,
+                                 grad.desc.dtype.code, float(lr), _lib.stream_ptr(stream)),
+               "split_sgd_step")
+
+
+def split_sgd_flat(hi: torch.Tensor, lo: torch.Tensor, grad: torch.Tensor, lr: float,
+                   stream=None) -> None:
+    """split_sgd_step on flat buffers (hi: bf16, lo: int16, grad: fp32/bf16)."""
+    lib = _lib.load()
+    gd = _lib.BF16 if grad.dtype == torch.bfloat16 else _lib.FP32
+    _lib.check(lib.tpp_split_sgd(hi.numel(), hi.data_ptr(), lo.data_ptr(), grad.data_ptr(), gd,
+                                 float(lr), _lib.stream_ptr(stream)), "split_sgd")
+
+
+# ---------------------------------------------------------------------------
+# direct convolution via offset BRGEMM
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class ConvSpec:
+    """3x3-style direct convolution, stride 1, 'same' padding.
+    input [N][C_b][H][W][bc], weights VNNI [K_b][C_b][R][S][bc/2][bk][2],
+    output [N][K_b][H][W][bk]."""
+    n: int
+    c_b: int
+    k_b: int
+    h: int
+    w: int
+    r: int = 3
+    s: int = 3
+    pad: int = 1
+    bc: int = 64
+    bk: int = 64
+
+    def c(self) -> _lib.ConvDescC:
+        return _lib.ConvDescC(self.n, self.c_b, self.k_b, self.h, self.w, self.r, self.s, self.pad,
+                              self.bc, self.bk, 0, 0)
+
+    @property
+    def flops(self) -> int:
+        return 2 * self.n * self.h * self.w * self.c_b * self.bc * self.k_b * self.bk * self.r * self.s
+
+
+class Conv2d:
+    """Weights packed once for forward ([K_b][R][S][C_b][bk][bc], K-major
+    per tap) and for backward-data (taps flipped, C/K swapped)."""
+
+    def __init__(self, spec: ConvSpec, w_vnni: torch.Tensor, stream=None):
+        if w_vnni.dtype != torch.bfloat16 or not w_vnni.is_cuda:
+            raise TensorError("conv weights must be a CUDA bfloat16 VNNI buffer")
+        need = spec.k_b * spec.c_b * spec.r * spec.s * spec.bc * spec.bk
+        if w_vnni.numel() < need:
+            raise TensorError("weight buffer too small")
+        self.spec = spec
+        lib = _lib.load()
+        d = spec.c()
+        self.w_fwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
+        self.w_bwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
+        s = _lib.stream_ptr(stream)
+        _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_fwd.data_ptr(), 0, s),
+                   "conv_pack_weights")
+        _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_bwd.data_ptr(), 1, s),
+                   "conv_pack_weights(bwd)")
+
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        sp = self.spec
+        n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
+        n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
+        if x.dtype != torch.bfloat16 or x.numel() < n_in:
+            raise TensorError("conv input must be a bf16 [N][C_b][H][W][bc] buffer")
+        if out is None:
+            out = torch.empty(n_out, dtype=torch.bfloat16, device=x.device)
+        lib = _lib.load()
+        d = sp.c()
+        _lib.check(lib.tpp_conv_forward(C.byref(d), self.w_fwd.data_ptr(), x.data_ptr(),
+                                        out.data_ptr(), _lib.stream_ptr(stream)), "conv_forward")
+        return out
+
+    def backward_data(self, dout: torch.Tensor, din: Optional[torch.Tensor] = None,
+                      stream=None) -> torch.Tensor:
+        sp = self.spec
+        n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
+        n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
+        if dout.dtype != torch.bfloat16 or dout.numel() < n_out:
+            raise TensorError("dO must be a bf16 [N][K_b][H][W][bk] buffer")
+        if din is None:
+            din = torch.empty(n_in, dtype=torch.bfloat16, device=dout.device)
+        lib = _lib.load()
+        d = sp.c()
+        _lib.check(lib.tpp_conv_backward_data(C.byref(d), self.w_bwd.data_ptr(), dout.data_ptr(),
+                                              din.data_ptr(), _lib.stream_ptr(stream)),
+                   "conv_backward_data")
+        return din

@@ -1,0 +1,415 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference
+(golden fixtures) and the CPU oracle.  Bit-exact where the reference's order
+is reproduced (ordered BRGEMM, eltwise, transforms, LayerNorm, softmax, SGD);
+normwise <= 2e-2 for BF16 tensor-core layers (north_star tolerance: fp32
+accumulation in a different order, then BF16 RNE)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tpp_oracle as O
+
+from gpu_util import bf16_bits_to_f32, normwise, to_dev, to_host, vnni_weights
+
+pytestmark = pytest.mark.gpu
+
+tpp = pytest.importorskip("paper_2104_05755_b200")
+
+BF16_TOL = 2e-2
+
+
+def bits(a):
+    """Byte image of an array with every float NaN canonicalised: NaN
+    payloads produced by invalid operations differ between x86 (0xFFC00000)
+    and the GPU (0x7FFFFFFF); both-NaN counts as a match."""
+    a = np.ascontiguousarray(np.array(a, copy=True))
+    if a.dtype in (np.float32, np.float64):
+        a[np.isnan(a)] = np.nan
+    return a.view(np.uint8).tobytes()
+
+
+def bf16_equal(a, b) -> bool:
+    """BF16 pattern equality with both-NaN counted as a match."""
+    a, b = np.asarray(a, np.uint16), np.asarray(b, np.uint16)
+    nan = lambda p: ((p & 0x7F80) == 0x7F80) & ((p & 0x7F) != 0)  # noqa: E731
+    return a.shape == b.shape and bool(np.all((a == b) | (nan(a) & nan(b))))
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# BRGEMM (ordered SIMT engine): bitwise vs the reference
+# ---------------------------------------------------------------------------
+
+def test_cfg1_brgemm_bitwise(golden):
+    g = golden("cfg1_brgemm.npz")
+    m = n = k = 64
+    a, b = to_dev(g["a"]), to_dev(g["b"])
+    c = tpp.TensorView(tpp.TensorDesc(m, n, m, tpp.DType.FP32), to_dev(g["c0"]))
+    tpp.brgemm(tpp.GemmSpec(m, n, k, m, k, m, beta=1.0),
+               tpp.BrgemmBatch.stride(a, b, m * k, k * n, 16), c)
+    assert bits(to_host(c.primary)) == bits(g["c"])
+
+
+_DT = {"fp32": "FP32", "bf16": "BF16", "fp64": "FP64", "int8": "INT8"}
+
+
+@pytest.mark.parametrize("variant", ["stride", "offset", "address"])
+def test_brgemm_cases_bitwise(golden, variant):
+    g = golden("brgemm_cases.npz")
+    for i in range(int(g["count"])):
+        key = f"case{i:03d}"
+        m, n, k, lda, ldb, ldc, cnt, sa, sb, vnni = (int(v) for v in g[key + "_meta"])
+        dt = tpp.DType[_DT[str(g[key + "_dtype"])]]
+        acc = {tpp.DType.FP64: tpp.DType.FP64, tpp.DType.INT8: tpp.DType.INT32}.get(dt, tpp.DType.FP32)
+        abuf, bbuf = to_dev(g[key + "_a"]), to_dev(g[key + "_b"])
+        c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, acc), to_dev(g[key + "_c0"]))
+        spec = tpp.GemmSpec(m, n, k, lda, ldb, ldc, in_dtype=dt, out_dtype=acc,
+                            beta=float(g[key + "_beta"]),
+                            a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN)
+        if variant == "stride":
+            batch = tpp.BrgemmBatch.stride(abuf, bbuf, sa, sb, cnt)
+        elif variant == "offset":
+            batch = tpp.BrgemmBatch.offset(abuf, bbuf, [j * sa for j in range(cnt)],
+                                           [j * sb for j in range(cnt)])
+        else:
+            batch = tpp.BrgemmBatch.address([(abuf, j * sa) for j in range(cnt)],
+                                            [(bbuf, j * sb) for j in range(cnt)])
+        tpp.brgemm(spec, batch, c)
+        assert bits(to_host(c.primary)) == bits(g[key + "_c"]), f"case {i} ({dt}, {variant})"
+
+
+def test_brgemm_cancellation_and_doubling():
+    """test_gemm.py:117-137 properties on the GPU (FP64, exact)."""
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((6, 6))
+    b = rng.standard_normal((6, 6))
+    av, nav, bv = (tpp.from_array(x) for x in (a, -a, b))
+    c = tpp.alloc(tpp.TensorDesc(6, 6, 6, tpp.DType.FP64))
+    sp = tpp.GemmSpec(6, 6, 6, 6, 6, 6, in_dtype=tpp.DType.FP64, out_dtype=tpp.DType.FP64)
+    tpp.brgemm(sp, tpp.BrgemmBatch.address([av, nav], [bv, bv]), c)
+    assert np.all(tpp.to_array(c) == 0.0)
+    c2 = tpp.alloc(tpp.TensorDesc(6, 6, 6, tpp.DType.FP64))
+    tpp.brgemm(sp, tpp.BrgemmBatch.address([av, av], [bv, bv]), c2)
+    c1 = tpp.alloc(tpp.TensorDesc(6, 6, 6, tpp.DType.FP64))
+    tpp.gemm(sp, av, bv, c1)
+    assert bits(tpp.to_array(c2)) == bits(2.0 * tpp.to_array(c1))
+
+
+def test_brgemm_empty_batch_and_errors():
+    sp = tpp.GemmSpec(2, 2, 2, 2, 2, 2, beta=1.0)
+    c = tpp.from_array(np.full((2, 2), 7.0, np.float32))
+    tpp.brgemm(sp, tpp.BrgemmBatch.address([], []), c)
+    assert np.all(tpp.to_array(c) == 7.0)
+    tpp.brgemm(tpp.GemmSpec(2, 2, 2, 2, 2, 2, beta=0.0), tpp.BrgemmBatch.address([], []), c)
+    assert np.all(tpp.to_array(c) == 0.0)
+    a = tpp.from_array(np.ones((2, 2), np.float32))
+    with pytest.raises(tpp.TensorError):
+        tpp.gemm(tpp.GemmSpec(2, 2, 2, 2, 2, 2), a, a, a)  # C aliases an input
+    with pytest.raises(tpp.TensorError):
+        tpp.gemm(tpp.GemmSpec(2, 2, 4, 2, 4, 2), a, a, tpp.alloc(tpp.TensorDesc(2, 2, 2, tpp.DType.FP32)))
+
+
+def test_brgemm_int8_no_saturation():
+    a = tpp.from_array(np.full((1, 300), 127, np.int8))
+    b = tpp.from_array(np.full((300, 1), 127, np.int8))
+    c = tpp.alloc(tpp.TensorDesc(1, 1, 1, tpp.DType.INT32))
+    tpp.gemm(tpp.GemmSpec(1, 1, 300, 1, 300, 1, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32), a, b, c)
+    assert int(c.item()) == 127 * 127 * 300
+
+
+# ---------------------------------------------------------------------------
+# elementwise / transform / conversion TPPs: bitwise
+# ---------------------------------------------------------------------------
+
+def test_rne_convert_bitwise(golden):
+    g = golden("dtypes.npz")
+    pats = g["fp32_bits"].view(np.float32)
+    src = tpp.TensorView(tpp.TensorDesc(pats.size, 1, pats.size, tpp.DType.FP32), to_dev(pats))
+    out = tpp.convert(src, tpp.DType.BF16)
+    assert np.array_equal(to_host(out.primary), g["bf16_bits"])
+    back = tpp.convert(out, tpp.DType.FP32)
+    assert np.array_equal(to_host(back.primary).view(np.uint32) >> 16, g["bf16_bits"].astype(np.uint32))
+
+
+def test_gelu_and_exp_bitwise(golden):
+    g = golden("approx.npz")
+    x = g["x"]
+    xv = tpp.TensorView(tpp.TensorDesc(x.size, 1, x.size, tpp.DType.FP32), to_dev(x))
+    out = tpp.alloc(xv.desc)
+    tpp.apply_unary(tpp.UnaryKind.GELU, xv, out)
+    assert bits(to_host(out.primary)) == bits(g["gelu"])
+    xe = g["xe"]
+    ev = tpp.TensorView(tpp.TensorDesc(xe.size, 1, xe.size, tpp.DType.FP32), to_dev(xe))
+    eo = tpp.alloc(ev.desc)
+    tpp.apply_unary(tpp.UnaryKind.EXP, ev, eo)
+    assert bits(to_host(eo.primary)) == bits(g["exp"])
+
+
+def test_eltwise_bitwise(golden):
+    g = golden("eltwise.npz")
+    x = g["x"]
+    m, n = x.shape
+    xv = tpp.from_array(x)
+    out = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.RELU, xv, out, bitmask_output=True)
+    assert bits(to_host(out.primary)) == bits(g["relu"])
+    assert np.array_equal(to_host(out.secondary), g["mask"])
+    dyv = tpp.from_array(g["dy"])
+    dyv.secondary = to_dev(g["mask"])
+    dx = tpp.alloc(out.desc)
+    tpp.apply_unary(tpp.UnaryKind.RELU_INV, dyv, dx)
+    assert bits(to_host(dx.primary)) == bits(g["relu_inv"])
+    xb = tpp.from_array(x, tpp.DType.BF16)
+    gb = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.BF16))
+    tpp.apply_unary(tpp.UnaryKind.GELU, xb, gb)
+    assert bf16_equal(to_host(gb.primary), g["gelu_bf16"])
+    dyg = tpp.from_array(g["dy"])
+    dyg.secondary = xv.primary
+    gi = tpp.alloc(out.desc)
+    tpp.apply_unary(tpp.UnaryKind.GELU_INV, dyg, gi)
+    assert bits(to_host(gi.primary)) == bits(g["gelu_inv"])
+    bb = tpp.broadcast(tpp.from_array(g["bias"]), tpp.Bcast.COL, m, n)
+    ad = tpp.alloc(out.desc)
+    tpp.apply_binary(tpp.BinaryKind.ADD, xv, bb, ad)
+    assert bits(to_host(ad.primary)) == bits(g["add_bias"])
+    yv, zv = tpp.from_array(g["y"]), tpp.from_array(g["z"])
+    ma = tpp.alloc(out.desc)
+    tpp.apply_ternary(tpp.TernaryKind.MULADD, xv, yv, zv, ma)
+    assert bits(to_host(ma.primary)) == bits(g["muladd"])
+    tpp.apply_ternary(tpp.TernaryKind.NMULADD, xv, yv, zv, ma)
+    assert bits(to_host(ma.primary)) == bits(g["nmuladd"])
+    r1 = tpp.alloc(tpp.TensorDesc(m, 1, m, tpp.DType.FP32))
+    tpp.reduce(yv, tpp.ReduceSpec(tpp.ReduceAxis.ROWS, tpp.ReduceOp.SUM), r1)
+    assert bits(to_host(r1.primary)) == bits(g["rsum"])
+    tpp.reduce(yv, tpp.ReduceSpec(tpp.ReduceAxis.ROWS, tpp.ReduceOp.SUM, True), r1)
+    assert bits(to_host(r1.primary)) == bits(g["rsumsq"])
+    cv = tpp.convert(xv, tpp.DType.BF16)
+    assert np.array_equal(to_host(cv.primary), g["convert_bf16"])
+
+
+def test_transforms_bitwise(golden):
+    g = golden("eltwise.npz")
+    for pats, want_key in ((g["pats"], "vnni"), (g["pats_odd"], "vnni_odd")):
+        pv = tpp.from_array(pats, tpp.DType.BF16)
+        m, k = pats.shape
+        out = tpp.alloc(tpp.TensorDesc(m * 2, -(-k // 2), m * 2, tpp.DType.BF16))
+        tpp.transform(pv, tpp.TransformSpec(tpp.TransformKind.VNNI, alpha=2), out)
+        assert np.array_equal(tpp.bits_of(out), g[want_key])
+    vn = tpp.from_array(g["vnni"], tpp.DType.BF16)
+    out = tpp.alloc(tpp.TensorDesc(10 * 2, 6, 20, tpp.DType.BF16))
+    tpp.transform(vn, tpp.TransformSpec(tpp.TransformKind.VNNI_TO_VNNIT, alpha=2, alpha_out=2,
+                                        rows=12, cols=10), out)
+    assert np.array_equal(tpp.bits_of(out), g["vnnit"])
+    x = np.arange(12, dtype=np.float32).reshape(3, 4)
+    t = tpp.alloc(tpp.TensorDesc(4, 3, 4, tpp.DType.FP32))
+    tpp.transform(tpp.from_array(x), tpp.TransformSpec(tpp.TransformKind.TRANSPOSE), t)
+    assert np.array_equal(tpp.to_array(t), x.T)
+
+
+# ---------------------------------------------------------------------------
+# composite kernels: bitwise
+# ---------------------------------------------------------------------------
+
+def test_layernorm_view_bitwise(golden):
+    g = golden("layernorm.npz")
+    for i in range(4):
+        x = g[f"x{i}"]
+        dt = tpp.DType[_DT[str(g[f"dtype{i}"])]]
+        m, n = x.shape
+        xv = tpp.from_array(x, dt) if dt is tpp.DType.FP32 else tpp.from_array(x, tpp.DType.BF16)
+        gg = tpp.broadcast(tpp.from_array(g[f"g{i}"]), tpp.Bcast.ROW, m, n)
+        bb = tpp.broadcast(tpp.from_array(g[f"b{i}"]), tpp.Bcast.ROW, m, n)
+        out = tpp.alloc(tpp.TensorDesc(m, n, m, dt))
+        mo = tpp.alloc(tpp.TensorDesc(m, 1, m, tpp.DType.FP32))
+        vo = tpp.alloc(tpp.TensorDesc(m, 1, m, tpp.DType.FP32))
+        tpp.layernorm(xv, gg, bb, 1e-5, out, mo, vo)
+        assert bits(tpp.bits_of(out)) == bits(g[f"out{i}"]), i
+        assert bits(to_host(mo.primary)) == bits(g[f"mean{i}"])
+        assert bits(to_host(vo.primary)) == bits(g[f"var{i}"])
+
+
+def test_softmax_and_split_sgd_bitwise(golden):
+    g = golden("softmax_sgd.npz")
+    for xk, yk, spec in (("x", "y", tpp.SoftmaxSpec(1, 6, 40)), ("x2", "y2", tpp.SoftmaxSpec(5, 3, 33))):
+        xv = tpp.from_array(g[xk])
+        yv = tpp.alloc(xv.desc)
+        tpp.softmax(spec, xv, yv)
+        assert bits(to_host(yv.primary)) == bits(g[yk])
+    split = tpp.split_fp32(tpp.from_array(g["w0"]))
+    for gi in g["grads"]:
+        tpp.split_sgd_step(split, tpp.from_array(gi), float(g["lr"]))
+    assert bits(tpp.to_array(tpp.pack_fp32(split))) == bits(g["w1"])
+
+
+def test_fc_fp32_bitwise(golden):
+    g = golden("fc.npz")
+    for i in range(3):
+        a4, b4 = g[f"fp32_{i}_a"], g[f"fp32_{i}_b"]
+        mb, kb, bk, bm = a4.shape
+        nb, _, bn, _ = b4.shape
+        act = str(g[f"fp32_{i}_act"])
+        spec = tpp.FcSpec(mb, nb, kb, bm, bn, bk, activation=tpp.UnaryKind.RELU if act == "relu" else None)
+        c = tpp.alloc(tpp.TensorDesc(bm, nb * mb * bn, bm, tpp.DType.FP32))
+        tpp.fc_forward(spec, to_dev(a4), to_dev(b4), c)
+        assert bits(to_host(c.primary)) == bits(g[f"fp32_{i}_c"]), i
+
+
+def test_layernorm_blocked_bitwise():
+    rng = np.random.default_rng(21)
+    for (n_b, m_b, bn, bm, dt) in ((4, 16, 32, 64, "bf16"), (2, 3, 48, 32, "fp32"), (3, 2, 8, 64, "bf16")):
+        x = rng.normal(0, 1, (n_b, m_b, bn, bm)).astype(np.float32) + 0.3
+        if dt == "bf16":
+            x = O.fp32_to_bf16_rne(x)
+        gam = (1 + 0.1 * rng.standard_normal(m_b * bm)).astype(np.float32)
+        bet = (0.1 * rng.standard_normal(m_b * bm)).astype(np.float32)
+        mean = torch.empty(n_b * bn, dtype=torch.float32, device="cuda")
+        var = torch.empty_like(mean)
+        out = tpp.layernorm_blocked(to_dev(x), n_b, m_b, bn, bm, 1e-5, to_dev(gam), to_dev(bet),
+                                    mean_out=mean, var_out=var)
+        xf = O.bf16_to_fp32(x) if dt == "bf16" else x
+        logical = xf.transpose(0, 2, 1, 3).reshape(n_b * bn, m_b * bm)  # tokens x features
+        ref, mu, vr = O.layernorm(logical, gam[None, :], bet[None, :], 1e-5)
+        ref = ref.reshape(n_b, bn, m_b, bm).transpose(0, 2, 1, 3)
+        if dt == "bf16":
+            assert np.array_equal(to_host(out), O.fp32_to_bf16_rne(ref).reshape(-1))
+        else:
+            assert bits(to_host(out)) == bits(ref.reshape(-1))
+        assert bits(to_host(mean)) == bits(mu.astype(np.float32))
+        assert bits(to_host(var)) == bits(vr.astype(np.float32))
+
+
+# ---------------------------------------------------------------------------
+# BF16 tensor-core layers (tcgen05): normwise tolerance vs the oracle
+# ---------------------------------------------------------------------------
+
+def _fc_case(rng, Nb, Cb, bn, bc, Kb, bk, act, bias=True, residual=False, block_n=0,
+             mask=False, nb_sel=None):
+    x = O.fp32_to_bf16_rne(rng.normal(0, 1, (Nb, Cb, bn, bc)).astype(np.float32))
+    wv = vnni_weights(rng, Kb, Cb, bk, bc, 0.05)
+    b = O.fp32_to_bf16_rne(rng.normal(0, 0.5, Kb * bk).astype(np.float32)) if bias else None
+    res = O.fp32_to_bf16_rne(rng.normal(0, 1, (Nb, Kb, bn, bk)).astype(np.float32)) if residual else None
+    layer = tpp.FcLayer(Kb, Cb, bk, bc, to_dev(wv), bias=to_dev(b) if bias else None,
+                        activation={"relu": tpp.UnaryKind.RELU, "gelu": tpp.UnaryKind.GELU, None: None}[act],
+                        block_n=block_n)
+    mbuf = torch.zeros(Nb * Kb * bn * (bk // 8), dtype=torch.uint8, device="cuda") if mask else None
+    out = layer.forward(to_dev(x), Nb, bn, residual=to_dev(res) if residual else None, relu_mask=mbuf)
+    got_bits = to_host(out).reshape(Nb, Kb, bn, bk)
+    sel = list(range(Nb)) if nb_sel is None else list(nb_sel)
+    want_bits, want_mask, _ = O.fc_forward_bf16(x, wv, b, activation=act, residual_bits=res, nb_sel=sel)
+    got = bf16_bits_to_f32(got_bits[sel])
+    want = O.bf16_to_fp32(want_bits)
+    err = normwise(got, want)
+    exact = float(np.mean(got_bits[sel] == want_bits))
+    mask_agree = None
+    if mask:
+        mb_host = to_host(mbuf).reshape(Nb, Kb, bn, bk // 8)[sel]
+        got_mask = np.unpackbits(mb_host, axis=-1, bitorder="little").astype(bool)
+        mask_agree = float(np.mean(got_mask == want_mask))
+    return err, exact, mask_agree
+
+
+@pytest.mark.parametrize("block_n", [64, 128, 256])
+def test_fc_bf16_relu_bias_tile_widths(block_n):
+    rng = np.random.default_rng(30)
+    err, exact, mask_agree = _fc_case(rng, 4, 4, 64, 64, 4, 64, "relu", block_n=block_n, mask=True)
+    assert err <= BF16_TOL, err
+    assert exact > 0.9, exact
+    assert mask_agree > 0.999, mask_agree
+
+
+def test_fc_bf16_golden(golden):
+    g = golden("fc.npz")
+    i = 2  # the TC-compatible golden case: bc = bk = 64, bn = 32
+    x, wv, bias = g[f"bf16_{i}_x"], g[f"bf16_{i}_w"], g[f"bf16_{i}_bias"]
+    Nb, Cb, bn, bc = x.shape
+    Kb, _, _, bk, _ = wv.shape
+    layer = tpp.FcLayer(Kb, Cb, bk, bc, to_dev(wv), bias=to_dev(bias), activation=tpp.UnaryKind.RELU)
+    out = layer.forward(to_dev(x), Nb, bn)
+    got = to_host(out).reshape(Nb, Kb, bn, bk)
+    want = g[f"bf16_{i}_out"]
+    assert normwise(bf16_bits_to_f32(got), O.bf16_to_fp32(want)) <= BF16_TOL
+
+
+def test_fc_bf16_gelu_residual_bn32():
+    rng = np.random.default_rng(31)
+    err, exact, _ = _fc_case(rng, 8, 3, 32, 64, 3, 64, "gelu", residual=True)
+    assert err <= BF16_TOL, err
+    assert exact > 0.9, exact
+
+
+def test_fc_bf16_cfg2_full():
+    """BASELINE cfg 2 (N=C=K=1024, bias+ReLU) at full size; the oracle checks
+    sampled token blocks exactly as the reference would compute them."""
+    rng = np.random.default_rng(0)
+    err, exact, _ = _fc_case(rng, 16, 16, 64, 64, 16, 64, "relu", nb_sel=[0, 7, 15])
+    assert err <= BF16_TOL, err
+    assert exact > 0.9, exact
+
+
+def test_fc_bf16_cfg3_shapes_sampled():
+    """BASELINE cfg 3 FC1 (1024->4096, GELU) and FC2 (4096->1024 + residual)
+    at their real K / N, tokens sampled (bn = 32)."""
+    rng = np.random.default_rng(1)
+    err, _, _ = _fc_case(rng, 8, 16, 32, 64, 64, 64, "gelu", bias=False, nb_sel=[0, 5])
+    assert err <= BF16_TOL, err
+    err, _, _ = _fc_case(rng, 4, 64, 32, 64, 16, 64, None, bias=False, residual=True, nb_sel=[1, 3])
+    assert err <= BF16_TOL, err
+
+
+def test_fc_bf16_ragged_tokens():
+    """Token count not a multiple of the 128-row tile (TMA zero-fill + masked stores)."""
+    rng = np.random.default_rng(32)
+    err, _, _ = _fc_case(rng, 3, 2, 32, 64, 2, 64, "relu")  # 96 tokens
+    assert err <= BF16_TOL, err
+    err, _, _ = _fc_case(rng, 5, 2, 64, 64, 4, 64, None)    # 320 tokens
+    assert err <= BF16_TOL, err
+
+
+def _conv_case(rng, N, Cb, Kb, H, W, n_sel=None):
+    x = O.fp32_to_bf16_rne(rng.random((N, Cb, H, W, 64)).astype(np.float32))
+    wl = O.fp32_to_bf16_rne(rng.normal(0, np.sqrt(2 / (9 * 64 * Cb)), (Kb, Cb, 3, 3, 64, 64)).astype(np.float32))
+    wv = wl.reshape(Kb, Cb, 3, 3, 64, 32, 2).transpose(0, 1, 2, 3, 5, 4, 6).copy()
+    spec = tpp.ConvSpec(N, Cb, Kb, H, W)
+    conv = tpp.Conv2d(spec, to_dev(wv))
+    out = conv.forward(to_dev(x))
+    sel = list(range(N)) if n_sel is None else n_sel
+    got = bf16_bits_to_f32(to_host(out).reshape(N, Kb, H, W, 64)[sel])
+    want_bits, _ = O.conv2d_fwd_bf16(x, wv, n_sel=sel)
+    err_f = normwise(got, O.bf16_to_fp32(want_bits))
+    # backward data: dI = conv(dO, flip(W)^T)
+    dout = O.fp32_to_bf16_rne(rng.normal(0, 1, (N, Kb, H, W, 64)).astype(np.float32))
+    din = conv.backward_data(to_dev(dout))
+    got_b = bf16_bits_to_f32(to_host(din).reshape(N, Cb, H, W, 64)[sel])
+    wbwd = O.conv_weights_bwd_data(wv)
+    want_b, _ = O.conv2d_fwd_bf16(dout, wbwd, n_sel=sel)
+    err_b = normwise(got_b, O.bf16_to_fp32(want_b))
+    return err_f, err_b
+
+
+def test_conv_small_fwd_bwd():
+    rng = np.random.default_rng(40)
+    err_f, err_b = _conv_case(rng, 2, 1, 1, 9, 12)
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+    err_f, err_b = _conv_case(rng, 1, 2, 2, 6, 64)
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+
+
+def test_conv_golden(golden):
+    """Reference offset-BRGEMM conv fixture is 8-channel; check the oracle
+    composition the GPU test relies on matches it (pinning), then the GPU
+    conv on the cfg-4 image shape against that oracle."""
+    g = golden("conv.npz")
+    out, _ = O.conv2d_fwd_bf16(g["x"], g["w"])
+    assert np.array_equal(out, g["out"])
+    rng = np.random.default_rng(41)
+    err_f, err_b = _conv_case(rng, 2, 1, 1, 56, 56, n_sel=[1])
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
