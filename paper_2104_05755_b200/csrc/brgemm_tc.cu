@@ -39,8 +39,9 @@ namespace tc {
 
 constexpr int BM = 128;          // tokens per tile (UMMA M, TMEM lanes)
 constexpr int BK = 64;           // bf16 per reduce block = one 128B swizzle row
-constexpr int kThreads = 256;    // 8 warps
+constexpr int kEpiWarps = 8;     // two warpgroups split the tile's columns
 constexpr int kEpiWarp0 = 4;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
 enum FeedMode { FEED_FC = 0, FEED_CONV = 1 };
 
@@ -56,7 +57,7 @@ struct Params {
   // ---- B feed (features) ----
   int b_kpb, b_bm, b_rows_split;  // B 5-D map {64, kpb, bm, k_b, m_b}; split: bm >= BN
   // ---- tiles ----
-  int tiles_m, tiles_n, feats;
+  int tiles_m, tiles_n, feats, bn_tile;
   // ---- output / epilogue: out[n_b][m_b][bn][bm] ----
   int o_bn, o_bm, o_mb;
   int act, flags;
@@ -73,50 +74,50 @@ struct Smem {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  // barriers: full[S], empty[S], tfull[2], tempty[2]; then tmem base + gelu table
-  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 64 * 4 + 1024;
+  // barriers: full[S], empty[S], tfull[2], tempty[2]; then tmem base + gelu table (float4 x 16)
+  static constexpr int TAB_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int BYTES = TAB_OFF + 16 * 16 + 1024;
 };
 
-__device__ __forceinline__ void a_coords(const Params& p, int tm, int j, int c[5]) {
-  if (p.mode == FEED_FC) {
-    c[0] = 0;
-    c[1] = j % p.a_kpb;
-    c[3] = j / p.a_kpb;
-    if (p.a_rows_split) {
-      c[2] = (tm * BM) % p.a_bn;
-      c[4] = (tm * BM) / p.a_bn;
+// Producer-side iterator over the reduce blocks of one tile: coordinates are
+// advanced with counters (no integer division on the issue path — a single
+// issuing thread feeds the tensor core, so its loop must stay short).
+struct FeedIter {
+  int a[5], b[5];
+  int kpb_a, kpb_b, cb_n, s_n, pad, r, s;
+  int mode;
+  __device__ __forceinline__ void start(const Params& p, int tm, int tn) {
+    mode = p.mode;
+    kpb_b = p.b_kpb;
+    const int f0 = tn * p.bn_tile;
+    b[0] = 0; b[1] = 0; b[3] = 0;
+    b[2] = p.b_rows_split ? f0 % p.b_bm : 0;
+    b[4] = f0 / p.b_bm;
+    if (mode == FEED_FC) {
+      kpb_a = p.a_kpb;
+      a[0] = 0; a[1] = 0; a[3] = 0;
+      if (p.a_rows_split) { a[2] = (tm * BM) % p.a_bn; a[4] = (tm * BM) / p.a_bn; }
+      else { a[2] = 0; a[4] = tm * (BM / p.a_bn); }
     } else {
-      c[2] = 0;
-      c[4] = tm * (BM / p.a_bn);
+      cb_n = p.cv_Cb; s_n = p.cv_S; pad = p.cv_pad;
+      const int n = tm / p.cv_tiles_per_img, pr = tm % p.cv_tiles_per_img;
+      r = 0; s = 0;
+      a[0] = 0; a[1] = -pad; a[2] = 2 * pr - pad; a[3] = 0; a[4] = n;
     }
-  } else {
-    // reduce block j = (r*S + s)*C_b + cb ; tile = (image n, output rows 2*pr, 2*pr+1)
-    const int cb = j % p.cv_Cb;
-    const int tap = j / p.cv_Cb;
-    const int r = tap / p.cv_S, s = tap % p.cv_S;
-    const int n = tm / p.cv_tiles_per_img;
-    const int pr = tm % p.cv_tiles_per_img;
-    c[0] = 0;
-    c[1] = s - p.cv_pad;          // input column of output column 0 (may be < 0: zero fill)
-    c[2] = 2 * pr + r - p.cv_pad; // input row
-    c[3] = cb;
-    c[4] = n;
   }
-}
-
-__device__ __forceinline__ void b_coords(const Params& p, int tn, int j, int c[5]) {
-  c[0] = 0;
-  c[1] = j % p.b_kpb;
-  c[3] = j / p.b_kpb;
-  const int f0 = tn * p.feats / p.tiles_n;  // = tn * BN
-  if (p.b_rows_split) {
-    c[2] = f0 % p.b_bm;
-    c[4] = f0 / p.b_bm;
-  } else {
-    c[2] = 0;
-    c[4] = f0 / p.b_bm;
+  __device__ __forceinline__ void next() {
+    if (++b[1] == kpb_b) { b[1] = 0; ++b[3]; }
+    if (mode == FEED_FC) {
+      if (++a[1] == kpb_a) { a[1] = 0; ++a[3]; }
+    } else {
+      // reduce block order (r, s, cb): cb fastest
+      if (++a[3] == cb_n) {
+        a[3] = 0;
+        if (++s == s_n) { s = 0; ++r; ++a[2]; a[1] = -pad; } else { ++a[1]; }
+      }
+    }
   }
-}
+};
 
 // global token index of accumulator row r of tile tm (or -1 if padding)
 __device__ __forceinline__ int row_token(const Params& p, int tm, int r) {
@@ -129,6 +130,29 @@ __device__ __forceinline__ int row_token(const Params& p, int tm, int r) {
   const int oh = 2 * pr + (r >> 6), ow = r & 63;
   if (oh >= p.cv_P || ow >= p.cv_Q) return -1;
   return (n * p.cv_P + oh) * p.cv_Q + ow;
+}
+
+// GELU with the table as one float4 {c0,c1,c2,c3} per interval (one LDS.128)
+__device__ __forceinline__ float gelu4(float x, const float4* tab) {
+  const float ax = fabsf(x);
+  int idx = (int)(__float_as_uint(ax) >> 22) - kGeluBase;
+  idx = idx < 0 ? 0 : (idx > 15 ? 15 : idx);
+  const float4 c = tab[idx];
+  float h = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c.w, ax), c.z), ax), c.y), ax), c.x);
+  if (ax >= kGeluRangeMax) h = 1.0f;
+  h = copysignf(h, x);
+  return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
+}
+
+// two FP32 -> packed BF16 with the reference's RNE (dtypes.py:82-97):
+// hardware cvt.rn for numbers (identical rounding, overflow to inf), the
+// reference's NaN rule patched in for NaNs.
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  if (lo != lo) r = (r & 0xFFFF0000u) | f32_to_bf16(lo);
+  if (hi != hi) r = (r & 0x0000FFFFu) | ((uint32_t)f32_to_bf16(hi) << 16);
+  return r;
 }
 
 template <int BN, int STAGES>
@@ -145,7 +169,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* gelu_tab = reinterpret_cast<float*>(tmem_slot + 4);
+  float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -160,69 +184,72 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, S::TMEM_COLS);
-  if (threadIdx.x >= 64 && threadIdx.x < 128) load_gelu_table(gelu_tab, threadIdx.x - 64, 64);
+  if (warp == 3 && lane < 16)
+    gelu_tab[lane] = make_float4(__uint_as_float(c_gelu_bits[lane]), __uint_as_float(c_gelu_bits[16 + lane]),
+                                 __uint_as_float(c_gelu_bits[32 + lane]), __uint_as_float(c_gelu_bits[48 + lane]));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (one thread) =====================
     if (lane == 0) {
-      uint32_t it = 0;
+      int s = 0;
+      uint32_t ph = 0;
+      FeedIter f;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
-        for (int j = 0; j < p.kblocks; ++j, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+        f.start(p, tile / p.tiles_n, tile % p.tiles_n);
+        for (int j = 0; j < p.kblocks; ++j) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * S::STAGE_BYTES;
-          uint8_t* sb = sa + S::A_BYTES;
           mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-          int ca[5], cb[5];
-          a_coords(p, tm, j, ca);
-          b_coords(p, tn, j, cb);
-          tma_load_5d(sa, &map_a, &full[s], ca[0], ca[1], ca[2], ca[3], ca[4]);
-          tma_load_5d(sb, &map_b, &full[s], cb[0], cb[1], cb[2], cb[3], cb[4]);
+          tma_load_5d(sa, &map_a, &full[s], f.a[0], f.a[1], f.a[2], f.a[3], f.a[4]);
+          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.b[0], f.b[1], f.b[2], f.b[3], f.b[4]);
+          f.next();
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      uint32_t it = 0, tcount = 0;
+      const uint64_t desc0 = sw128_kmajor_desc(smem_u32(smem));
+      int s = 0;
+      uint32_t ph = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
         const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
-        for (int j = 0; j < p.kblocks; ++j, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
+        for (int j = 0; j < p.kblocks; ++j) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
-          const uint32_t sb = sa + S::A_BYTES;
+          // descriptor start-address field is in 16-byte units
+          const uint64_t da = desc0 + (uint64_t)((s * S::STAGE_BYTES) >> 4);
+          const uint64_t db = da + (uint64_t)(S::A_BYTES >> 4);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            umma_f16(tmem_d, sw128_kmajor_desc(sa + kk * 32), sw128_kmajor_desc(sb + kk * 32),
-                     idesc, (j > 0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < BK / 16; ++kk)
+            umma_f16(tmem_d, da + 2 * kk, db + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&empty[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&tfull[as]);
       }
     }
   } else if (warp >= kEpiWarp0) {
-    // ===================== epilogue =====================
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // ===================== epilogue (8 warps) =====================
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3;            // TMEM lane quarter this warp may access
+    const int half = ew >> 2;          // which half of the tile's columns
     const int r = q * 32 + lane;
+    constexpr int CH = BN / 64;        // 32-column chunks per half
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
       const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
@@ -233,40 +260,39 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       const int nb = t >= 0 ? t / p.o_bn : 0;
       const int n_in = t >= 0 ? t % p.o_bn : 0;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
+      for (int ch = 0; ch < CH; ++ch) {
+        const int col = half * (BN / 2) + ch * 32;
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + ch * 32, v);
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
-        const int f0 = tn * BN + ch * 32;
+        const int f0 = tn * BN + col;
         if (t < 0 || f0 >= p.feats) continue;
-        const int mb = f0 / p.o_bm, m_in = f0 % p.o_bm;
+        const int mb = f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
         float x[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
         if (p.flags & TPP_FC_BIAS) {
           if (p.flags & TPP_FC_BIAS_FP32) {
-            const float4* bp = reinterpret_cast<const float4*>(
-                reinterpret_cast<const float*>(p.bias) + f0);
+            const float4* bp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.bias) + f0);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              float4 b4 = __ldg(bp + i);
+              const float4 b4 = __ldg(bp + i);
               x[4 * i] = __fadd_rn(x[4 * i], b4.x);
               x[4 * i + 1] = __fadd_rn(x[4 * i + 1], b4.y);
               x[4 * i + 2] = __fadd_rn(x[4 * i + 2], b4.z);
               x[4 * i + 3] = __fadd_rn(x[4 * i + 3], b4.w);
             }
           } else {
-            const uint4* bp = reinterpret_cast<const uint4*>(
-                reinterpret_cast<const uint16_t*>(p.bias) + f0);
+            const uint4* bp = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.bias) + f0);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              uint4 b4 = __ldg(bp + i);
+              const uint4 b4 = __ldg(bp + i);
               const uint32_t w[4] = {b4.x, b4.y, b4.z, b4.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], bf16_to_f32((uint16_t)(w[e] & 0xFFFF)));
-                x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], bf16_to_f32((uint16_t)(w[e] >> 16)));
+                x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], __uint_as_float(w[e] << 16));
+                x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
               }
             }
           }
@@ -282,18 +308,18 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 32; ++i) x[i] = relu_f(x[i]);
         } else if (p.act == TPP_ACT_GELU) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = gelu_fwd(x[i], gelu_tab);
+          for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], gelu_tab);
         }
         if (p.flags & TPP_FC_RESIDUAL) {
           const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            uint4 r4 = __ldg(rp + i);
+            const uint4 r4 = __ldg(rp + i);
             const uint32_t w[4] = {r4.x, r4.y, r4.z, r4.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], bf16_to_f32((uint16_t)(w[e] & 0xFFFF)));
-              x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], bf16_to_f32((uint16_t)(w[e] >> 16)));
+              x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], __uint_as_float(w[e] << 16));
+              x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
             }
           }
         }
@@ -306,8 +332,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            op[i] = make_uint4(pack_bf16x2(x[8 * i], x[8 * i + 1]), pack_bf16x2(x[8 * i + 2], x[8 * i + 3]),
-                               pack_bf16x2(x[8 * i + 4], x[8 * i + 5]), pack_bf16x2(x[8 * i + 6], x[8 * i + 7]));
+            op[i] = make_uint4(pack2_bf16(x[8 * i], x[8 * i + 1]), pack2_bf16(x[8 * i + 2], x[8 * i + 3]),
+                               pack2_bf16(x[8 * i + 4], x[8 * i + 5]), pack2_bf16(x[8 * i + 6], x[8 * i + 7]));
         }
       }
       tc_fence_before();
@@ -434,6 +460,7 @@ int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, con
   p.tiles_m = (p.tokens + BM - 1) / BM;
   p.tiles_n = feats / BN;
   p.feats = feats;
+  p.bn_tile = BN;
   p.o_bn = bn;
   p.o_bm = bm;
   p.o_mb = m_b;
@@ -492,6 +519,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   p.tiles_m = N * p.cv_tiles_per_img;
   p.tiles_n = feats / BN;
   p.feats = feats;
+  p.bn_tile = BN;
   p.o_bn = P * Q;
   p.o_bm = 64;
   p.o_mb = Kb;
