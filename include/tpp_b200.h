@@ -107,7 +107,7 @@ int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void*
  * BF16 runs tcgen05 with the epilogue TPPs fused into the GEMM tail. */
 enum tpp_act { TPP_ACT_NONE = 0, TPP_ACT_RELU = 1, TPP_ACT_GELU = 2 };
 enum tpp_fc_flags { TPP_FC_BIAS = 1, TPP_FC_RESIDUAL = 2, TPP_FC_RELU_MASK = 4,
-                    TPP_FC_OUT_FP32 = 8, TPP_FC_BIAS_FP32 = 16 };
+                    TPP_FC_OUT_FP32 = 8, TPP_FC_BIAS_FP32 = 16, TPP_FC_RELU_INV = 32 };
 
 typedef struct {
   int32_t m_b, n_b, k_b, bm, bn, bk;
@@ -130,6 +130,29 @@ int tpp_fc_pack_weights(const tpp_fc_desc* d, const void* w_vnni, void* w_packed
 int tpp_fc_forward(const tpp_fc_desc* d, const void* w, const void* x,
                    const void* bias, const void* residual, void* out, void* relu_mask,
                    void* stream);
+
+/* Backward of the blocked FC (BF16, tcgen05), the training-side BRGEMMs of
+ * PAPER.md:700-720 (kernel K8).  `d` describes the
+ * FORWARD layer.  Both read the blocked buffers in place (MN-major UMMA
+ * operands) — no transposed copies.
+ *   backward-data:    din[n_b][k_b][bn][bk] = dout . W, then, with
+ *                     TPP_FC_RELU_INV in d->flags, where(mask_in, ., 0)
+ *                     (ops.py:367-369) with the forward input's ReLU bitmask
+ *                     (layout of din, bytes [n_b][k_b][bn][bk/8]).
+ *   backward-weights: dW[m_b][k_b][bm][bk] (packed weight layout) =
+ *                     sum over tokens dout^T x; FP32 unless d->flags lacks
+ *                     TPP_FC_OUT_FP32 (then BF16). */
+int tpp_fc_backward_data(const tpp_fc_desc* d, const void* w_packed, const void* dout,
+                         const void* relu_mask_in, void* din, void* stream);
+int tpp_fc_backward_weights(const tpp_fc_desc* d, const void* dout, const void* x, void* dw,
+                            void* stream);
+/* Softmax cross-entropy gradient on blocked FP32 logits [n_b][m_b][bn][bm]
+ * (tokens x classes): per token the reference softmax (kernels.py:84-99 with
+ * exp_taylor, approx.py:190-218), then dlogits = (p - onehot(target)) * scale
+ * (BF16, same blocked layout) and loss[t] = -log(p[target]) (FP32). */
+int tpp_softmax_xent_blocked(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, const float* logits,
+                             const int32_t* targets, float scale, void* dlogits, float* loss,
+                             void* stream);
 
 /* ---- direct convolution via offset BRGEMM --------------
  * Input [N][C_b][H][W][bc], weights VNNI [K_b][C_b][R][S][bc/2][bk][2],

@@ -559,3 +559,58 @@ def conv_weights_bwd_data(w_vnni_bits):
                     out[cb, kb, R - 1 - r, S - 1 - s] = (
                         vnni_pack_a(logical.T.copy(), 2).reshape(bk // 2, bc, 2))
     return out
+
+
+# ---------------------------------------------------------------------------
+# blocked MLP training step (BASELINE cfg 5) as a composition of the
+# reference TPPs: brgemm over 64-wide reduce blocks (contraction.py:371),
+# RELU + bitmask / RELU_INV (ops.py:363-369), softmax (kernels.py:84-99),
+# split-SGD (kernels.py:235-251).  Logical row-major matrices; BF16 values
+# are carried as exactly-representable FP32.
+# ---------------------------------------------------------------------------
+
+
+def blocked_matmul(x: np.ndarray, w: np.ndarray, blk: int = 64) -> np.ndarray:
+    """out[t, o] = sum_c x[t, c] * w[o, c] with the BRGEMM order: batch entries
+    are the 64-wide blocks of c (ascending), each a partial from +0 along
+    ascending c (contraction.py:405-425).  x [T, C], w [O, C] -> [T, O] FP32."""
+    x = np.asarray(x, np.float32)
+    w = np.asarray(w, np.float32)
+    t, c = x.shape
+    o = w.shape[0]
+    a_stack = w.reshape(o, c // blk, blk).transpose(1, 0, 2)       # [Cb, O, blk]
+    b_stack = x.reshape(t, c // blk, blk).transpose(1, 2, 0)       # [Cb, blk, T]
+    return brgemm_blocked(a_stack, b_stack).T                       # [T, O]
+
+
+def mlp_train_step(x_bits, weights32, targets, lr: float, global_batch: int):
+    """One step on one shard.  x_bits: [T, d0] uint16; weights32: list of FP32
+    [out, in] masters (the BF16 weight used by the GEMMs is the hi half,
+    i.e. the truncated value, as in split-SGD); returns (new weights, dW list,
+    per-token loss)."""
+    nl = len(weights32)
+    wb = [bf16_to_fp32((np.asarray(w, np.float32).view(np.uint32) >> 16).astype(np.uint16))
+          for w in weights32]
+    h = [bf16_to_fp32(x_bits)]
+    masks = [None]
+    for l in range(nl - 1):
+        z = blocked_matmul(h[l], wb[l])
+        masks.append(z > 0)
+        h.append(round_bf16(relu(z)))
+    logits = blocked_matmul(h[nl - 1], wb[nl - 1])
+    tcount, ncls = logits.shape
+    p = np.stack([softmax_slice(logits[i:i + 1, :])[0] for i in range(tcount)])
+    onehot = np.zeros_like(p)
+    onehot[np.arange(tcount), targets] = 1.0
+    scale = np.float32(1.0 / global_batch)
+    with np.errstate(all="ignore"):
+        g = round_bf16((p - onehot) * scale)
+        loss = -np.log(p[np.arange(tcount), targets])
+    dws = [None] * nl
+    for l in range(nl - 1, -1, -1):
+        dws[l] = blocked_matmul(g.T.copy(), h[l].T.copy())             # [out, in], tokens reduced
+        if l > 0:
+            dh = blocked_matmul(g, wb[l].T.copy())                       # [T, in]
+            g = round_bf16(relu_inv(dh, masks[l]))
+    new = [split_sgd_step(weights32[l], dws[l], lr) for l in range(nl)]
+    return new, dws, loss

@@ -76,9 +76,12 @@ from .kernels import (
     layernorm,
     layernorm_blocked,
     softmax,
+    softmax_xent_blocked,
     split_sgd_flat,
     split_sgd_step,
 )
 from ._lib import TppUnavailableError
+from . import parallel
+from .training import BlockedMLP
 
 __version__ = "0.1.0"

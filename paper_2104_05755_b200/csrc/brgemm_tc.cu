@@ -45,17 +45,25 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
 enum FeedMode { FEED_FC = 0, FEED_CONV = 1 };
 
+// One operand's walk through a 5-D tensor map.  Tile t starts at element
+// t0 = t * rows_per_tile along the tiled axis, split as (t0 % extent) on
+// dimension lo_dim and (t0 / extent) on hi_dim; every reduce block then adds
+// `inc` on inc_dim and, on reaching `wrap`, resets it and carries 1 into
+// carry_dim.  This single form covers the forward (K-major tokens / weights),
+// backward-data (MN-major weights) and backward-weight (MN-major tokens) feeds.
+struct OpFeed {
+  int lo_dim, hi_dim, extent, rows_per_tile;
+  int inc_dim, inc, wrap, carry_dim;
+};
+
 struct Params {
-  // ---- A feed (tokens) ----
   int mode;
-  int tokens;          // FC: valid tokens (n_b*bn)
+  int tokens;          // valid rows of the output (M extent)
   int kblocks;         // reduce blocks per tile
-  // FC: A 5-D map {64, kpb, bn, k_b, n_b}
-  int a_kpb, a_bn, a_rows_split;  // a_rows_split: bn >= 128
+  OpFeed fa, fb;       // FC-mode feeds
+  int a_mn, b_mn;      // operand major-ness (0 K-major, 1 MN-major)
   // conv: A 5-D map {64, W, H, C_b, N}; 2 output rows x 64 columns per tile
   int cv_P, cv_Q, cv_R, cv_S, cv_pad, cv_Cb, cv_tiles_per_img;
-  // ---- B feed (features) ----
-  int b_kpb, b_bm, b_rows_split;  // B 5-D map {64, kpb, bm, k_b, m_b}; split: bm >= BN
   // ---- tiles ----
   int tiles_m, tiles_n, feats, bn_tile;
   // ---- output / epilogue: out[n_b][m_b][bn][bm] ----
@@ -64,7 +72,8 @@ struct Params {
   const void* bias;
   const uint16_t* residual;
   void* out;
-  uint8_t* mask;
+  uint8_t* mask;        // ReLU bitmask written (TPP_FC_RELU_MASK)
+  const uint8_t* mask_in;  // ReLU bitmask applied (RELU_INV, backward-data)
 };
 
 template <int BN, int STAGES>
@@ -79,25 +88,37 @@ struct Smem {
   static constexpr int BYTES = TAB_OFF + 16 * 16 + 1024;
 };
 
+struct OpIter {
+  int c[5];
+  int inc_dim, inc, wrap, carry_dim;
+  __device__ __forceinline__ void start(const OpFeed& f, int tile) {
+    c[0] = c[1] = c[2] = c[3] = c[4] = 0;
+    const int t0 = tile * f.rows_per_tile;
+    c[f.lo_dim] += t0 % f.extent;
+    c[f.hi_dim] += t0 / f.extent;
+    inc_dim = f.inc_dim; inc = f.inc; wrap = f.wrap; carry_dim = f.carry_dim;
+  }
+  __device__ __forceinline__ void next() {
+    c[inc_dim] += inc;
+    if (c[inc_dim] == wrap) { c[inc_dim] = 0; ++c[carry_dim]; }
+  }
+};
+
 // Producer-side iterator over the reduce blocks of one tile: coordinates are
 // advanced with counters (no integer division on the issue path — a single
 // issuing thread feeds the tensor core, so its loop must stay short).
 struct FeedIter {
-  int a[5], b[5];
-  int kpb_a, kpb_b, cb_n, s_n, pad, r, s;
+  OpIter ai, bi;
+  int a[5];
+  int cb_n, s_n, pad, r, s;
   int mode;
+  __device__ __forceinline__ int* A() { return mode == FEED_FC ? ai.c : a; }
+  __device__ __forceinline__ int* B() { return bi.c; }
   __device__ __forceinline__ void start(const Params& p, int tm, int tn) {
     mode = p.mode;
-    kpb_b = p.b_kpb;
-    const int f0 = tn * p.bn_tile;
-    b[0] = 0; b[1] = 0; b[3] = 0;
-    b[2] = p.b_rows_split ? f0 % p.b_bm : 0;
-    b[4] = f0 / p.b_bm;
+    bi.start(p.fb, tn);
     if (mode == FEED_FC) {
-      kpb_a = p.a_kpb;
-      a[0] = 0; a[1] = 0; a[3] = 0;
-      if (p.a_rows_split) { a[2] = (tm * BM) % p.a_bn; a[4] = (tm * BM) / p.a_bn; }
-      else { a[2] = 0; a[4] = tm * (BM / p.a_bn); }
+      ai.start(p.fa, tm);
     } else {
       cb_n = p.cv_Cb; s_n = p.cv_S; pad = p.cv_pad;
       const int n = tm / p.cv_tiles_per_img, pr = tm % p.cv_tiles_per_img;
@@ -106,9 +127,9 @@ struct FeedIter {
     }
   }
   __device__ __forceinline__ void next() {
-    if (++b[1] == kpb_b) { b[1] = 0; ++b[3]; }
+    bi.next();
     if (mode == FEED_FC) {
-      if (++a[1] == kpb_a) { a[1] = 0; ++a[3]; }
+      ai.next();
     } else {
       // reduce block order (r, s, cb): cb fastest
       if (++a[3] == cb_n) {
@@ -209,8 +230,10 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * S::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-          tma_load_5d(sa, &map_a, &full[s], f.a[0], f.a[1], f.a[2], f.a[3], f.a[4]);
-          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.b[0], f.b[1], f.b[2], f.b[3], f.b[4]);
+          const int* ca = f.A();
+          const int* cb = f.B();
+          tma_load_5d(sa, &map_a, &full[s], ca[0], ca[1], ca[2], ca[3], ca[4]);
+          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], cb[0], cb[1], cb[2], cb[3], cb[4]);
           f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -219,8 +242,13 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      const uint64_t desc0 = sw128_kmajor_desc(smem_u32(smem));
+      const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
+      // K-major: a 16-element K step is +32 B; MN-major: +2 K-groups (+2048 B)
+      const uint64_t adesc0 = p.a_mn ? sw128_mnmajor_desc(smem_u32(smem), 8192) : sw128_kmajor_desc(smem_u32(smem));
+      const uint64_t bdesc0 = (p.b_mn ? sw128_mnmajor_desc(smem_u32(smem), 8192) : sw128_kmajor_desc(smem_u32(smem))) +
+                              (uint64_t)(S::A_BYTES >> 4);
+      const uint32_t astep = p.a_mn ? (2048 >> 4) : (32 >> 4);
+      const uint32_t bstep = p.b_mn ? (2048 >> 4) : (32 >> 4);
       int s = 0;
       uint32_t ph = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
@@ -232,11 +260,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait(&full[s], ph);
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
-          const uint64_t da = desc0 + (uint64_t)((s * S::STAGE_BYTES) >> 4);
-          const uint64_t db = da + (uint64_t)(S::A_BYTES >> 4);
+          const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            umma_f16(tmem_d, da + 2 * kk, db + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+            umma_f16(tmem_d, adesc0 + soff + astep * kk, bdesc0 + soff + bstep * kk, idesc,
+                     (j > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -296,6 +324,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               }
             }
           }
+        }
+        if (p.flags & TPP_FC_RELU_INV) {
+          // ops.py:367-369: where(mask, dy, 0) with the forward ReLU bitmask
+          const uint32_t bits = *reinterpret_cast<const uint32_t*>(p.mask_in + row_off * (p.o_bm / 8) + m_in / 8);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[i] = ((bits >> i) & 1u) ? x[i] : 0.0f;
         }
         if (p.act == TPP_ACT_RELU) {
           if (p.flags & TPP_FC_RELU_MASK) {
@@ -423,70 +457,134 @@ static int launch(int bn_tile, const CUtensorMap& ma, const CUtensorMap& mb, con
 }  // namespace tc
 
 // ---------------------------------------------------------------------------
-// FC forward (BF16, tensor cores).  Reference naming (kernels.py:287-297):
+// Blocked FC GEMMs on tensor cores.  Reference naming (kernels.py:287-297):
 //   weights packed [m_b][k_b][bm][bk] (K-major), input [n_b][k_b][bn][bk],
 //   output [n_b][m_b][bn][bm].
+//   forward          out[t, f] = sum_c x[t, c]  W[f, c]      A K-major,  B K-major
+//   backward-data    dx[t, c]  = sum_f dy[t, f] W[f, c]      A K-major,  B MN-major
+//   backward-weights dW[f, c]  = sum_t dy[t, f] x[t, c]      A MN-major, B MN-major
+// All three read the same blocked buffers in place — no transposes.
 // ---------------------------------------------------------------------------
-int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
-                  const void* residual, void* out, void* mask, cudaStream_t stream) {
+namespace {
+
+struct Operand {
+  uint64_t dims[5];
+  uint64_t strides[4];
+  uint32_t box[5];
+  tc::OpFeed feed;
+};
+
+// K-major operand: rows of a blocked [nblk][kblk][rows_b][k_in] tensor
+// (k_in a multiple of 64), tiles of `tile_rows` rows.
+Operand kmajor_operand(int nblk, int kblk, int rows_b, int k_in, int tile_rows) {
+  Operand o{};
+  const uint64_t kb = (uint64_t)k_in * 2;
+  o.dims[0] = 64; o.dims[1] = k_in / 64; o.dims[2] = rows_b; o.dims[3] = kblk; o.dims[4] = nblk;
+  o.strides[0] = 128; o.strides[1] = kb; o.strides[2] = (uint64_t)rows_b * kb;
+  o.strides[3] = (uint64_t)kblk * rows_b * kb;
+  const bool split = rows_b >= tile_rows;
+  o.box[0] = 64; o.box[1] = 1; o.box[2] = split ? tile_rows : rows_b; o.box[3] = 1;
+  o.box[4] = split ? 1 : tile_rows / rows_b;
+  o.feed = {2, 4, rows_b, tile_rows, 1, 1, k_in / 64, 3};
+  return o;
+}
+
+// MN-major operand over a blocked [red_blk][mn_blk][red_in][64] tensor
+// (the MN block is exactly 64 wide = one 128B atom; the reduce index runs
+// over red_in rows then red_blk blocks), tiles of `tile_mn` MN elements.
+Operand mnmajor_operand(int red_blk, int mn_blk, int red_in, int tile_mn) {
+  Operand o{};
+  o.dims[0] = 64; o.dims[1] = red_in; o.dims[2] = mn_blk; o.dims[3] = red_blk; o.dims[4] = 1;
+  o.strides[0] = 128; o.strides[1] = (uint64_t)red_in * 128; o.strides[2] = (uint64_t)mn_blk * red_in * 128;
+  o.strides[3] = (uint64_t)red_blk * mn_blk * red_in * 128;
+  o.box[0] = 64; o.box[1] = 64; o.box[2] = tile_mn / 64; o.box[3] = 1; o.box[4] = 1;
+  o.feed = {0, 2, 64, tile_mn, 1, 64, red_in, 3};
+  return o;
+}
+
+int pick_bn(int feats, int tiles_m, int pref) {
+  if (pref) return pref;
+  int BN = 256;
+  while (BN > 64 && (feats % BN != 0 || (int64_t)tiles_m * (feats / BN) < num_sms())) BN /= 2;
+  return BN;
+}
+
+int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* b_ptr, tc::Params p,
+             int BN, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  int rc = tc::make_map_5d(&ma, a_ptr, A.dims, A.strides, A.box);
+  if (rc) return rc;
+  rc = tc::make_map_5d(&mb, b_ptr, B.dims, B.strides, B.box);
+  if (rc) return rc;
+  p.fa = A.feed;
+  p.fb = B.feed;
+  return tc::launch(BN, ma, mb, p, stream);
+}
+
+}  // namespace
+
+// flavor: 0 forward, 1 backward-data, 2 backward-weights
+int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
+               const void* x_for_dw, const void* bias, const void* residual, void* out,
+               void* mask_out, const void* mask_in, cudaStream_t stream) {
   using namespace tc;
   const int m_b = d->m_b, n_b = d->n_b, k_b = d->k_b, bm = d->bm, bn = d->bn, bk = d->bk;
-  TPP_REQUIRE(bk % 64 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bk % 64 == 0");
-  TPP_REQUIRE(bm % 32 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bm % 32 == 0");
-  TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
-              "tensor-core FC needs bn | 128 or 128 | bn");
-  const int feats = m_b * bm;
-  int BN = d->block_n;
-  if (BN == 0) {
-    // enough tiles to cover the SMs, widest tile otherwise
-    const int tiles_m = (n_b * bn + BM - 1) / BM;
-    BN = 256;
-    while (BN > 64 && (feats % BN != 0 || (int64_t)tiles_m * (feats / BN) < num_sms())) BN /= 2;
-  }
-  TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "features must be a multiple of the tile width");
-  TPP_REQUIRE((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0), TPP_E_UNSUPPORTED,
-              "bm and the tile width must nest");
-
   Params p{};
   p.mode = FEED_FC;
-  p.tokens = n_b * bn;
-  p.kblocks = k_b * (bk / 64);
-  p.a_kpb = bk / 64;
-  p.a_bn = bn;
-  p.a_rows_split = bn >= BM;
-  p.b_kpb = bk / 64;
-  p.b_bm = bm;
-  p.b_rows_split = bm >= BN;
-  p.tiles_m = (p.tokens + BM - 1) / BM;
-  p.tiles_n = feats / BN;
-  p.feats = feats;
-  p.bn_tile = BN;
-  p.o_bn = bn;
-  p.o_bm = bm;
-  p.o_mb = m_b;
   p.act = d->activation;
   p.flags = d->flags;
   p.bias = bias;
   p.residual = reinterpret_cast<const uint16_t*>(residual);
   p.out = out;
-  p.mask = reinterpret_cast<uint8_t*>(mask);
+  p.mask = reinterpret_cast<uint8_t*>(mask_out);
+  p.mask_in = reinterpret_cast<const uint8_t*>(mask_in);
+  TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
+              "tensor-core FC needs bn | 128 or 128 | bn");
+  if (flavor == 0) {
+    TPP_REQUIRE(bk % 64 == 0 && bm % 32 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bk % 64 == 0, bm % 32 == 0");
+    const int feats = m_b * bm, tokens = n_b * bn;
+    const int tiles_m = (tokens + BM - 1) / BM;
+    const int BN = pick_bn(feats, tiles_m, d->block_n);
+    TPP_REQUIRE(feats % BN == 0 && ((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0)),
+                TPP_E_UNSUPPORTED, "features must tile by the tile width");
+    p.tokens = tokens; p.kblocks = k_b * (bk / 64);
+    p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
+    p.o_bn = bn; p.o_bm = bm; p.o_mb = m_b;
+    return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM), kmajor_operand(m_b, k_b, bm, bk, BN), x_or_dy,
+                    w_packed, p, BN, stream);
+  }
+  if (flavor == 1) {
+    // dx[n_b][k_b][bn][bk] = dy[n_b][m_b][bn][bm] . W ; B = W as MN-major over its bk
+    TPP_REQUIRE(bk == 64 && bm % 64 == 0, TPP_E_UNSUPPORTED, "backward-data needs bk == 64, bm % 64 == 0");
+    const int feats = k_b * bk, tokens = n_b * bn;
+    const int tiles_m = (tokens + BM - 1) / BM;
+    const int BN = pick_bn(feats, tiles_m, d->block_n);
+    TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
+    p.tokens = tokens; p.kblocks = m_b * (bm / 64);
+    p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
+    p.o_bn = bn; p.o_bm = bk; p.o_mb = k_b;
+    p.b_mn = 1;
+    return run_gemm(kmajor_operand(n_b, m_b, bn, bm, BM), mnmajor_operand(m_b, k_b, bm, BN), x_or_dy,
+                    w_packed, p, BN, stream);
+  }
+  // flavor 2: dW[m_b][k_b][bm][bk] = sum_t dy[t][f] x[t][c]
+  TPP_REQUIRE(bm == 64 && bk == 64 && bn % 64 == 0, TPP_E_UNSUPPORTED,
+              "backward-weights needs bm == bk == 64 and bn % 64 == 0");
+  const int rows = m_b * bm, feats = k_b * bk;
+  const int tiles_m = (rows + BM - 1) / BM;
+  const int BN = pick_bn(feats, tiles_m, d->block_n);
+  TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
+  p.tokens = rows; p.kblocks = n_b * (bn / 64);
+  p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
+  p.o_bn = bm; p.o_bm = bk; p.o_mb = k_b;
+  p.a_mn = 1; p.b_mn = 1;
+  return run_gemm(mnmajor_operand(n_b, m_b, bn, BM), mnmajor_operand(n_b, k_b, bn, BN), x_or_dy, x_for_dw, p,
+                  BN, stream);
+}
 
-  CUtensorMap ma, mb;
-  {
-    const uint64_t dims[5] = {64, (uint64_t)(bk / 64), (uint64_t)bn, (uint64_t)k_b, (uint64_t)n_b};
-    const uint64_t str[4] = {128, (uint64_t)bk * 2, (uint64_t)bn * bk * 2, (uint64_t)k_b * bn * bk * 2};
-    const uint32_t box[5] = {64, 1, (uint32_t)(bn >= BM ? BM : bn), 1, (uint32_t)(bn >= BM ? 1 : BM / bn)};
-    int rc = make_map_5d(&ma, x, dims, str, box);
-    if (rc) return rc;
-  }
-  {
-    const uint64_t dims[5] = {64, (uint64_t)(bk / 64), (uint64_t)bm, (uint64_t)k_b, (uint64_t)m_b};
-    const uint64_t str[4] = {128, (uint64_t)bk * 2, (uint64_t)bm * bk * 2, (uint64_t)k_b * bm * bk * 2};
-    const uint32_t box[5] = {64, 1, (uint32_t)(bm >= BN ? BN : bm), 1, (uint32_t)(bm >= BN ? 1 : BN / bm)};
-    int rc = make_map_5d(&mb, w_packed, dims, str, box);
-    if (rc) return rc;
-  }
-  return launch(BN, ma, mb, p, stream);
+int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
+                  const void* residual, void* out, void* mask, cudaStream_t stream) {
+  return fc_gemm_tc(0, d, w_packed, x, nullptr, bias, residual, out, mask, nullptr, stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -513,9 +611,6 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   p.cv_pad = pad;
   p.cv_Cb = Cb;
   p.cv_tiles_per_img = (P + 1) / 2;
-  p.b_kpb = 1;
-  p.b_bm = 64;
-  p.b_rows_split = 64 >= BN;
   p.tiles_m = N * p.cv_tiles_per_img;
   p.tiles_n = feats / BN;
   p.feats = feats;
@@ -535,12 +630,11 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     int rc = make_map_5d(&ma, x, dims, str, box);
     if (rc) return rc;
   }
+  // weights: K-major rows [K_b][J = R*S*C_b][64 out][64 in]
+  const Operand wb = kmajor_operand(Kb, R * S * Cb, 64, 64, BN);
+  p.fb = wb.feed;
   {
-    const int J = R * S * Cb;
-    const uint64_t dims[5] = {64, 1, 64, (uint64_t)J, (uint64_t)Kb};
-    const uint64_t str[4] = {128, 128, 64 * 128, (uint64_t)J * 64 * 128};
-    const uint32_t box[5] = {64, 1, 64, 1, (uint32_t)(BN / 64)};
-    int rc = make_map_5d(&mb, w_packed, dims, str, box);
+    int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
   return launch(BN, ma, mb, p, stream);

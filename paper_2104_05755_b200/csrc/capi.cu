@@ -162,6 +162,41 @@ static int check_fc(const tpp_fc_desc* d) {
   return TPP_OK;
 }
 
+int tpp_fc_backward_data(const tpp_fc_desc* d, const void* w_packed, const void* dout,
+                         const void* relu_mask_in, void* din, void* stream) {
+  int rc = check_fc(d);
+  if (rc) return rc;
+  TPP_REQUIRE(d->in_dtype == TPP_BF16, TPP_E_SPEC_DTYPE, "FC backward runs on BF16 operands");
+  TPP_REQUIRE(w_packed && dout && din, TPP_E_TENSOR, "null FC operand");
+  TPP_REQUIRE(!(d->flags & TPP_FC_RELU_INV) || relu_mask_in, TPP_E_TENSOR,
+              "RELU_INV requires a recorded bitmask");
+  TPP_REQUIRE(!(d->flags & (TPP_FC_BIAS | TPP_FC_RESIDUAL | TPP_FC_RELU_MASK)) &&
+                  d->activation == TPP_ACT_NONE,
+              TPP_E_SPEC_FLAG, "backward-data fuses only RELU_INV");
+  return fc_gemm_tc(1, d, w_packed, dout, nullptr, nullptr, nullptr, din, nullptr, relu_mask_in,
+                    as_stream(stream));
+}
+
+int tpp_fc_backward_weights(const tpp_fc_desc* d, const void* dout, const void* x, void* dw,
+                            void* stream) {
+  int rc = check_fc(d);
+  if (rc) return rc;
+  TPP_REQUIRE(d->in_dtype == TPP_BF16, TPP_E_SPEC_DTYPE, "FC backward runs on BF16 operands");
+  TPP_REQUIRE(dout && x && dw, TPP_E_TENSOR, "null FC operand");
+  TPP_REQUIRE(!(d->flags & ~TPP_FC_OUT_FP32) && d->activation == TPP_ACT_NONE, TPP_E_SPEC_FLAG,
+              "backward-weights takes only the FP32-output flag");
+  return fc_gemm_tc(2, d, nullptr, dout, x, nullptr, nullptr, dw, nullptr, nullptr, as_stream(stream));
+}
+
+int tpp_softmax_xent_blocked(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, const float* logits,
+                             const int32_t* targets, float scale, void* dlogits, float* loss,
+                             void* stream) {
+  TPP_REQUIRE(n_b >= 1 && m_b >= 1 && bn >= 1 && bm >= 1, TPP_E_TENSOR, "bad blocking");
+  TPP_REQUIRE(logits && targets && dlogits, TPP_E_TENSOR, "null operand");
+  return launch_softmax_xent_blocked(n_b, m_b, bn, bm, logits, targets, scale, dlogits, loss,
+                                     as_stream(stream));
+}
+
 int64_t tpp_fc_packed_weight_bytes(const tpp_fc_desc* d) {
   if (!d) return -1;
   return (int64_t)d->m_b * d->k_b * d->bm * d->bk * (d->in_dtype == TPP_BF16 ? 2 : 4);

@@ -28,6 +28,12 @@ int launch_brgemm_ordered(const OrderedParams& p, int in_dtype, cudaStream_t s);
 
 int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
                   const void* residual, void* out, void* mask, cudaStream_t stream);
+int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
+               const void* x_for_dw, const void* bias, const void* residual, void* out,
+               void* mask_out, const void* mask_in, cudaStream_t stream);
+int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* logits,
+                                const int32_t* targets, float scale, void* dlogits, float* loss,
+                                cudaStream_t s);
 int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
                     const void* w_packed, const void* x, void* out, cudaStream_t stream);
 

@@ -248,3 +248,82 @@ int launch_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad, in
 }
 
 }  // namespace tpp
+
+namespace tpp {
+
+// ---- softmax cross-entropy gradient on blocked logits ------------------------
+// Per token: the reference softmax of a 1 x F slice (kernels.py:60-99:
+// max-shift, exp_taylor, ascending sum, reciprocal, multiply), then
+// dlogit = (p - onehot) * scale and loss = -log(p[target]).
+__global__ void __launch_bounds__(256)
+softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __restrict__ logits,
+                            const int32_t* __restrict__ targets, float scale,
+                            uint16_t* __restrict__ dlog, float* __restrict__ loss) {
+  extern __shared__ __align__(16) uint8_t xsm[];
+  const int F = m_b * bm;
+  const int pitch = F + 1;
+  float* rows = reinterpret_cast<float*>(xsm);
+  float* rcp = rows + 32 * pitch;
+  const int chunks_per_blk = (bn + 31) / 32;
+  const int nb = blockIdx.x / chunks_per_blk;
+  const int n0 = (blockIdx.x % chunks_per_blk) * 32;
+  const int T_ = min(32, bn - n0);
+  for (int mb = 0; mb < m_b; ++mb) {
+    const float* src = logits + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
+      const int t = e / bm, m = e - t * bm;
+      rows[t * pitch + mb * bm + m] = src[e];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < T_) {
+    float* r = rows + threadIdx.x * pitch;
+    float mx = r[0];
+    for (int f = 1; f < F; ++f) {
+      const float v = r[f];
+      mx = (mx != mx) ? mx : ((v != v) ? v : fmaxf(mx, v));
+    }
+    float tot = 0.0f;
+    for (int f = 0; f < F; ++f) {
+      const float e = exp_taylor(__fsub_rn(r[f], mx));
+      r[f] = e;
+      tot = __fadd_rn(tot, e);
+    }
+    const float rc = __fdiv_rn(1.0f, tot);
+    rcp[threadIdx.x] = rc;
+    const int64_t tok = (int64_t)nb * bn + n0 + threadIdx.x;
+    const int tg = targets[tok];
+    if (loss) loss[tok] = -logf(__fmul_rn(r[tg], rc));
+  }
+  __syncthreads();
+  for (int mb = 0; mb < m_b; ++mb) {
+    uint16_t* dst = dlog + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
+      const int t = e / bm, m = e - t * bm;
+      const int f = mb * bm + m;
+      const float pr = __fmul_rn(rows[t * pitch + f], rcp[t]);
+      const int tg = targets[(int64_t)nb * bn + n0 + t];
+      const float g = __fmul_rn(__fsub_rn(pr, f == tg ? 1.0f : 0.0f), scale);
+      dst[e] = f32_to_bf16(g);
+    }
+  }
+}
+
+int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* logits,
+                                const int32_t* targets, float scale, void* dlogits, float* loss,
+                                cudaStream_t s) {
+  const int F = m_b * bm;
+  const size_t smem = (size_t)32 * (F + 1) * sizeof(float) + 32 * sizeof(float);
+  TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "softmax_xent: class dimension too long for smem");
+  const int blocks = n_b * ((bn + 31) / 32);
+  if (blocks == 0) return TPP_OK;
+  cudaError_t e = cudaFuncSetAttribute(softmax_xent_blocked_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(softmax_xent)");
+  softmax_xent_blocked_kernel<<<blocks, 256, smem, s>>>(n_b, m_b, bn, bm, logits, targets, scale,
+                                                         reinterpret_cast<uint16_t*>(dlogits), loss);
+  TPP_CUDA_LAUNCH_CHECK("softmax_xent_blocked_kernel");
+  return TPP_OK;
+}
+
+}  // namespace tpp

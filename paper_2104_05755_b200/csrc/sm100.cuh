@@ -126,11 +126,28 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor for kind::f16: BF16 x BF16 -> FP32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
+// MN-major, 128-byte swizzle (canonical ((T,8,m),(8,k)):((1,T,LBO),(8T,SBO))):
+// atoms of 8 K-rows x 128 B (64 bf16 along M/N), K-groups of 8 rows SBO =
+// 1024 B apart, successive 64-element M/N atoms LBO bytes apart.  A K-step
+// of 16 rows advances the start address by 2 K-groups (2048 B).
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t saddr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;  // LBO: stride between M/N atoms
+  d |= (uint64_t)(1024u >> 4) << 32;                  // SBO: stride between 8-row K groups
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+// Instruction descriptor for kind::f16: BF16 x BF16 -> FP32; a_mn / b_mn
+// select MN-major operands (bits 15 / 16).
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n, int a_mn = 0, int b_mn = 0) {
   return (1u << 4)                       // D format F32
          | (1u << 7)                     // A format BF16
          | (1u << 10)                    // B format BF16
+         | ((uint32_t)(a_mn & 1) << 15)  // A major
+         | ((uint32_t)(b_mn & 1) << 16)  // B major
          | ((uint32_t)(n >> 3) << 17)    // N / 8
          | ((uint32_t)(m >> 4) << 24);   // M / 16
 }

@@ -97,19 +97,26 @@ class FcLayer:
     reference's FP32 op order, narrowed to BF16 with RNE.
     """
 
-    def __init__(self, m_b: int, k_b: int, bm: int, bk: int, w_vnni: torch.Tensor,
+    def __init__(self, m_b: int, k_b: int, bm: int, bk: int, w_vnni: Optional[torch.Tensor],
                  bias: Optional[torch.Tensor] = None, activation: Optional[UnaryKind] = None,
-                 block_n: int = 0, stream=None):
-        if w_vnni.dtype != torch.bfloat16 or not w_vnni.is_cuda:
-            raise TensorError("FcLayer weights must be a CUDA bfloat16 VNNI buffer")
-        if w_vnni.numel() < m_b * k_b * bm * bk:
-            raise TensorError("weight buffer too small")
+                 block_n: int = 0, stream=None, w_packed: Optional[torch.Tensor] = None):
         if bias is not None and (bias.numel() < m_b * bm or bias.dtype not in (torch.bfloat16, torch.float32)):
             raise TensorError("bias must hold m_b*bm BF16/FP32 values")
         self.m_b, self.k_b, self.bm, self.bk = m_b, k_b, bm, bk
         self.activation = activation
         self.bias = bias
         self.block_n = block_n
+        if w_packed is not None:
+            # weights already in the K-major packed layout [m_b][k_b][bm][bk]
+            # (e.g. the hi halves of split-SGD master weights)
+            if w_packed.dtype != torch.bfloat16 or not w_packed.is_cuda or w_packed.numel() < m_b * k_b * bm * bk:
+                raise TensorError("packed weights must be a CUDA bfloat16 [m_b][k_b][bm][bk] buffer")
+            self.w_packed = w_packed
+            return
+        if w_vnni is None or w_vnni.dtype != torch.bfloat16 or not w_vnni.is_cuda:
+            raise TensorError("FcLayer weights must be a CUDA bfloat16 VNNI buffer")
+        if w_vnni.numel() < m_b * k_b * bm * bk:
+            raise TensorError("weight buffer too small")
         self.w_packed = torch.empty(m_b * k_b * bm * bk, dtype=torch.bfloat16, device=w_vnni.device)
         self.repack(w_vnni, stream)
 
@@ -160,6 +167,65 @@ class FcLayer:
             relu_mask.data_ptr() if relu_mask is not None else None,
             _lib.stream_ptr(stream)), "FcLayer.forward")
         return out
+
+    def backward_data(self, dout: torch.Tensor, n_b: int, bn: int, relu_mask_in: Optional[torch.Tensor] = None,
+                      out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """din = dout . W  ([n_b][k_b][bn][bk], BF16), optionally masked by the
+        forward input's ReLU bitmask (RELU_INV fused in the epilogue)."""
+        if dout.dtype != torch.bfloat16 or dout.numel() < n_b * self.m_b * bn * self.bm:
+            raise TensorError("dout must be a BF16 [n_b][m_b][bn][bm] buffer")
+        n_in = n_b * self.k_b * bn * self.bk
+        if out is None:
+            out = torch.empty(n_in, dtype=torch.bfloat16, device=dout.device)
+        flags = 0
+        if relu_mask_in is not None:
+            if relu_mask_in.numel() < n_b * self.k_b * bn * ((self.bk + 7) // 8):
+                raise TensorError("bitmask buffer too small")
+            flags |= _lib.FC_RELU_INV
+        lib = _lib.load()
+        d = _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16, _lib.ACT_NONE, flags,
+                         self.block_n)
+        _lib.check(lib.tpp_fc_backward_data(
+            C.byref(d), self.w_packed.data_ptr(), dout.data_ptr(),
+            relu_mask_in.data_ptr() if relu_mask_in is not None else None, out.data_ptr(),
+            _lib.stream_ptr(stream)), "FcLayer.backward_data")
+        return out
+
+    def backward_weights(self, dout: torch.Tensor, x: torch.Tensor, n_b: int, bn: int,
+                         out: Optional[torch.Tensor] = None, fp32: bool = True, stream=None) -> torch.Tensor:
+        """dW = sum over tokens of dout^T x, in the packed weight layout
+        [m_b][k_b][bm][bk] (FP32 by default)."""
+        if dout.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
+            raise TensorError("dout and x must be BF16")
+        n_w = self.m_b * self.k_b * self.bm * self.bk
+        if out is None:
+            out = torch.empty(n_w, dtype=torch.float32 if fp32 else torch.bfloat16, device=dout.device)
+        lib = _lib.load()
+        d = _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16, _lib.ACT_NONE,
+                         _lib.FC_OUT_FP32 if out.dtype == torch.float32 else 0, self.block_n)
+        _lib.check(lib.tpp_fc_backward_weights(C.byref(d), dout.data_ptr(), x.data_ptr(), out.data_ptr(),
+                                               _lib.stream_ptr(stream)), "FcLayer.backward_weights")
+        return out
+
+
+def softmax_xent_blocked(logits: torch.Tensor, targets: torch.Tensor, n_b: int, m_b: int, bn: int,
+                         bm: int, scale: float, dlogits: Optional[torch.Tensor] = None,
+                         loss: Optional[torch.Tensor] = None, stream=None):
+    """Softmax cross-entropy gradient on blocked FP32 logits (tokens x
+    classes): the reference softmax per token, dlogits = (p - onehot) * scale
+    as BF16 in the same blocked layout; per-token loss -log p[target]."""
+    if logits.dtype != torch.float32 or targets.dtype != torch.int32:
+        raise TensorError("logits must be FP32 and targets int32")
+    n = n_b * m_b * bn * bm
+    if dlogits is None:
+        dlogits = torch.empty(n, dtype=torch.bfloat16, device=logits.device)
+    if loss is None:
+        loss = torch.empty(n_b * bn, dtype=torch.float32, device=logits.device)
+    lib = _lib.load()
+    _lib.check(lib.tpp_softmax_xent_blocked(n_b, m_b, bn, bm, logits.data_ptr(), targets.data_ptr(),
+                                            float(scale), dlogits.data_ptr(), loss.data_ptr(),
+                                            _lib.stream_ptr(stream)), "softmax_xent_blocked")
+    return dlogits, loss
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,142 @@
+"""Blocked-MLP training on tcgen05 (BASELINE cfg 5): forward, softmax-CE,
+backward-data / backward-weights BRGEMMs and the split-SGD update, data
+parallel over the minibatch with one dW allreduce per layer.
+
+Composition of the reference TPPs (SURVEY §0.2 row "MLP training"):
+  forward    fc_forward + RELU with bitmask        (kernels.py:300-329, ops.py:363-366)
+  loss       softmax per token                     (kernels.py:84-99) -> (p - onehot)/B
+  backward   brgemm for dX and dW, RELU_INV        (contraction.py:371, ops.py:367-369)
+  update     split_sgd_step on hi/lo FP32 masters  (kernels.py:235-251)
+Weights live in the UMMA-canonical packed layout [out/64][in/64][64][64]; the
+hi halves of the split FP32 master ARE the BF16 weights the GEMMs read, so no
+per-step re-layout is needed (the MN-major backward operands read them in
+place).
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+
+from . import kernels as K
+from .ops import UnaryKind
+from .parallel import GradAllreduce, world
+
+BLK = 64
+
+
+def pack_logical_weight(w: torch.Tensor) -> torch.Tensor:
+    """Logical [out, in] -> packed [out/64][in/64][64][64] (row o, col i)."""
+    o, i = w.shape
+    return w.reshape(o // BLK, BLK, i // BLK, BLK).permute(0, 2, 1, 3).contiguous().reshape(-1)
+
+
+def unpack_weight(flat: torch.Tensor, o: int, i: int) -> torch.Tensor:
+    return flat.reshape(o // BLK, i // BLK, BLK, BLK).permute(0, 2, 1, 3).reshape(o, i)
+
+
+def split_master(w32: torch.Tensor):
+    """FP32 -> (hi as bfloat16 bits, lo as int16): tensor.py:292-304 on device."""
+    u = w32.contiguous().view(torch.int32)
+    hi = (u >> 16).to(torch.int16).view(torch.bfloat16)
+    lo = (u & 0xFFFF).to(torch.int16)
+    return hi, lo
+
+
+def pack_master(hi: torch.Tensor, lo: torch.Tensor) -> torch.Tensor:
+    """tensor.py:307-315."""
+    return ((hi.view(torch.int16).to(torch.int32) << 16) | (lo.to(torch.int32) & 0xFFFF)).view(torch.float32)
+
+
+class BlockedMLP:
+    """MLP dims[0] -> dims[1] -> ... -> dims[-1], ReLU between layers, no
+    bias, BF16 activations / weights with FP32 split masters.  Activations are
+    blocked [n_b][d/64][bn][64] (tokens x features)."""
+
+    def __init__(self, dims: Sequence[int], tokens: int, bn: int = 64, lr: float = 0.01,
+                 global_batch: Optional[int] = None, init_std: float = 0.02, seed: int = 0,
+                 device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None):
+        if any(d % BLK for d in dims) or tokens % bn or bn % BLK:
+            raise ValueError("dims must be multiples of 64 and tokens a multiple of bn (itself a multiple of 64)")
+        self.dims = list(dims)
+        self.nl = len(dims) - 1
+        self.tokens, self.bn, self.n_b = tokens, bn, tokens // bn
+        self.lr = lr
+        rank, ws = world()
+        self.global_batch = global_batch or tokens * ws
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.hi, self.lo, self.layers = [], [], []
+        for l in range(self.nl):
+            o, i = dims[l + 1], dims[l]
+            if weights is not None:
+                w32 = weights[l].to(dev, torch.float32)
+            else:
+                w32 = torch.randn(o, i, generator=gen, device=dev) * init_std
+            hi, lo = split_master(pack_logical_weight(w32))
+            self.hi.append(hi)
+            self.lo.append(lo)
+            act = UnaryKind.RELU if l < self.nl - 1 else None
+            self.layers.append(K.FcLayer(o // BLK, i // BLK, BLK, BLK, None, activation=act, w_packed=hi))
+        # activations h[0] = input, h[l] = output of layer l-1 (BF16); masks of h[1..nl-1]
+        self.h = [None] + [torch.empty(tokens * dims[l], dtype=torch.bfloat16, device=dev)
+                           for l in range(1, self.nl)]
+        self.mask = [None] + [torch.empty(tokens * dims[l] // 8, dtype=torch.uint8, device=dev)
+                              for l in range(1, self.nl)]
+        self.logits = torch.empty(tokens * dims[-1], dtype=torch.float32, device=dev)
+        self.g = [torch.empty(tokens * dims[l], dtype=torch.bfloat16, device=dev) for l in range(1, self.nl + 1)]
+        self.dw = [torch.empty(dims[l + 1] * dims[l], dtype=torch.float32, device=dev) for l in range(self.nl)]
+        self.loss = torch.empty(tokens, dtype=torch.float32, device=dev)
+        self.comm = GradAllreduce(group)
+
+    # ------------------------------------------------------------------
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x: BF16 blocked [n_b][d0/64][bn][64]; returns FP32 logits (blocked)."""
+        self.h[0] = x
+        for l, layer in enumerate(self.layers):
+            if l < self.nl - 1:
+                layer.forward(self.h[l], self.n_b, self.bn, out=self.h[l + 1], relu_mask=self.mask[l + 1])
+            else:
+                layer.forward(self.h[l], self.n_b, self.bn, out=self.logits, out_fp32=True)
+        return self.logits
+
+    def backward(self, targets: torch.Tensor) -> None:
+        """Softmax-CE gradient, then per layer dW (allreduce launched at once,
+        overlapping the next dX) and dX with the ReLU mask fused."""
+        nl = self.nl
+        K.softmax_xent_blocked(self.logits, targets, self.n_b, self.dims[-1] // BLK, self.bn, BLK,
+                               1.0 / self.global_batch, dlogits=self.g[nl - 1], loss=self.loss)
+        for l in range(nl - 1, -1, -1):
+            layer = self.layers[l]
+            layer.backward_weights(self.g[l], self.h[l], self.n_b, self.bn, out=self.dw[l])
+            self.comm.push(self.dw[l])
+            if l > 0:
+                layer.backward_data(self.g[l], self.n_b, self.bn, relu_mask_in=self.mask[l],
+                                    out=self.g[l - 1])
+
+    def step(self) -> None:
+        """Wait for the dW allreduce, then split-SGD on every layer."""
+        self.comm.wait()
+        for l in range(self.nl):
+            K.split_sgd_flat(self.hi[l], self.lo[l], self.dw[l], self.lr)
+
+    def train_step(self, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        self.forward(x)
+        self.backward(targets)
+        self.step()
+        return self.loss
+
+    # ------------------------------------------------------------------
+    def master_weight(self, l: int) -> torch.Tensor:
+        """FP32 master weight of layer l as a logical [out, in] matrix."""
+        return unpack_weight(pack_master(self.hi[l], self.lo[l]), self.dims[l + 1], self.dims[l])
+
+    @property
+    def flops_per_step(self) -> int:
+        t = self.tokens
+        fwd = sum(2 * t * self.dims[l] * self.dims[l + 1] for l in range(self.nl))
+        dx = sum(2 * t * self.dims[l] * self.dims[l + 1] for l in range(1, self.nl))
+        return 2 * fwd + dx  # fwd + dW (same as fwd) + dX (layers 2..nl)

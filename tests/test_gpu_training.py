@@ -1,0 +1,110 @@
+"""GPU parity of the training-side BRGEMMs (backward-data with fused RELU_INV,
+backward-weights via MN-major tcgen05 operands), the softmax-CE gradient and
+one full blocked-MLP training step, against the CPU oracle composition of the
+reference TPPs.  BF16 layers: normwise <= 2e-2 (north_star tolerance)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tpp_oracle as O
+
+from gpu_util import bf16_bits_to_f32, normwise, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+tpp = pytest.importorskip("paper_2104_05755_b200")
+from paper_2104_05755_b200 import training as T  # noqa: E402
+
+TOL = 2e-2
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.synchronize()
+
+
+def _blocked(x_logical: np.ndarray, bn: int) -> np.ndarray:
+    """[T, D] -> blocked [T/bn][D/64][bn][64]."""
+    t, d = x_logical.shape
+    return x_logical.reshape(t // bn, bn, d // 64, 64).transpose(0, 2, 1, 3).copy()
+
+
+def _logical(blocked: np.ndarray) -> np.ndarray:
+    nb, db, bn, b = blocked.shape
+    return blocked.transpose(0, 2, 1, 3).reshape(nb * bn, db * b)
+
+
+def _bf16(rng, shape, std):
+    return O.fp32_to_bf16_rne((rng.standard_normal(shape) * std).astype(np.float32))
+
+
+@pytest.mark.parametrize("bn", [64, 32])
+def test_fc_backward_data_relu_inv(bn):
+    rng = np.random.default_rng(50)
+    T_, I_, O_ = 256, 256, 384
+    w = _bf16(rng, (O_, I_), 0.05)                     # logical [out, in]
+    dy = _bf16(rng, (T_, O_), 1.0)
+    mask = rng.random((T_, I_)) > 0.4
+    layer = tpp.FcLayer(O_ // 64, I_ // 64, 64, 64, None,
+                        w_packed=to_dev(T.pack_logical_weight(torch.from_numpy(w.view(np.int16))).numpy().view(np.uint16)))
+    mask_bytes = np.packbits(_blocked(mask.astype(np.uint8), bn), axis=-1, bitorder="little")
+    out = layer.backward_data(to_dev(_blocked(dy, bn)), T_ // bn, bn, relu_mask_in=to_dev(mask_bytes))
+    got = bf16_bits_to_f32(_logical(to_host(out).reshape(T_ // bn, I_ // 64, bn, 64)))
+    ref = O.blocked_matmul(O.bf16_to_fp32(dy), O.bf16_to_fp32(w).T.copy())
+    ref = O.round_bf16(O.relu_inv(ref, mask))
+    assert normwise(got, ref) <= TOL
+    assert np.all(got[~mask] == 0)
+
+
+def test_fc_backward_weights():
+    rng = np.random.default_rng(51)
+    T_, I_, O_ = 512, 192, 256
+    x = _bf16(rng, (T_, I_), 1.0)
+    dy = _bf16(rng, (T_, O_), 1.0)
+    layer = tpp.FcLayer(O_ // 64, I_ // 64, 64, 64, None,
+                        w_packed=torch.zeros(O_ * I_, dtype=torch.bfloat16, device="cuda"))
+    dw = layer.backward_weights(to_dev(_blocked(dy, 64)), to_dev(_blocked(x, 64)), T_ // 64, 64)
+    got = T.unpack_weight(dw.cpu(), O_, I_).numpy()
+    ref = O.blocked_matmul(O.bf16_to_fp32(dy).T.copy(), O.bf16_to_fp32(x).T.copy())
+    assert normwise(got, ref) <= 1e-5  # FP32 output; only the summation order differs
+
+
+def test_softmax_xent_matches_reference_softmax():
+    rng = np.random.default_rng(52)
+    T_, C_ = 128, 256
+    logits = (rng.standard_normal((T_, C_)) * 3).astype(np.float32)
+    tg = rng.integers(0, C_, T_).astype(np.int32)
+    d, loss = tpp.softmax_xent_blocked(to_dev(_blocked(logits, 64)), to_dev(tg), T_ // 64, C_ // 64, 64, 64,
+                                       1.0 / 1000)
+    got = _logical(to_host(d).reshape(T_ // 64, C_ // 64, 64, 64))
+    p = np.stack([O.softmax_slice(logits[i:i + 1])[0] for i in range(T_)])
+    onehot = np.zeros_like(p)
+    onehot[np.arange(T_), tg] = 1
+    want = O.fp32_to_bf16_rne((p - onehot) * np.float32(1e-3))
+    assert np.array_equal(got, want)  # bitwise: same softmax order, same RNE
+    ref_loss = -np.log(p[np.arange(T_), tg])
+    assert np.allclose(to_host(loss), ref_loss, rtol=1e-5, atol=1e-6)
+
+
+def test_mlp_train_step_vs_oracle():
+    rng = np.random.default_rng(53)
+    dims = [128, 256, 256, 128]
+    T_ = 256
+    ws = [(rng.standard_normal((dims[l + 1], dims[l])) * 0.05).astype(np.float32) for l in range(3)]
+    x = _bf16(rng, (T_, dims[0]), 1.0)
+    tg = rng.integers(0, dims[-1], T_).astype(np.int32)
+    mlp = tpp.BlockedMLP(dims, T_, bn=64, lr=0.5, global_batch=T_,
+                         weights=[torch.from_numpy(w) for w in ws])
+    loss = mlp.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
+    torch.cuda.synchronize()
+    new_ref, dws_ref, loss_ref = O.mlp_train_step(x, ws, tg, 0.5, T_)
+    assert np.allclose(to_host(loss), loss_ref, rtol=2e-2, atol=1e-3)
+    for l in range(3):
+        dw = T.unpack_weight(mlp.dw[l].cpu(), dims[l + 1], dims[l]).numpy()
+        assert normwise(dw, dws_ref[l]) <= TOL, l
+        got_w = mlp.master_weight(l).cpu().numpy()
+        assert normwise(got_w - ws[l], new_ref[l] - ws[l]) <= TOL, l
