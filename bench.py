@@ -385,6 +385,23 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
         del xin, yo, dO, dI, conv
     except Exception as e:
         out["cfg4_conv3x3"] = {"error": str(e)[:200]}
+    # ---- cfg 5: 4-layer blocked MLP training step (fwd + CE + bwd + split-SGD), 1 GPU ----
+    try:
+        dims = [1024, 4096, 4096, 4096, 1024]
+        tokens = 8192
+        mlp = tpp.BlockedMLP(dims, tokens, bn=64, lr=0.01, device=dev, seed=7)
+        xin = torch.randn(tokens * 1024, generator=gen, device=dev).to(torch.bfloat16)
+        tg = torch.randint(0, 1024, (tokens,), generator=gen, device=dev, dtype=torch.int32)
+        g = graph_of(torch, [lambda: mlp.train_step(xin, tg)] * 3)
+        ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.5)) / 3
+        tf = mlp.flops_per_step / ms / 1e9
+        out["cfg5_mlp_train_step"] = {"ms": round(ms, 4), "TFLOP/s": round(tf, 1),
+                                      "frac_bf16_sustained": round(tf / 1409.7, 4),
+                                      "flops_per_step": mlp.flops_per_step,
+                                      "loss_mean": round(float(mlp.loss.mean()), 4)}
+        del mlp, xin, tg
+    except Exception as e:
+        out["cfg5_mlp_train_step"] = {"error": str(e)[:200]}
     # ---- cfg 1: FP32 BRGEMM 16 x 64^3, beta = 1, reference order (bitwise) ------
     try:
         m = n = k = 64

@@ -88,19 +88,24 @@ struct Smem {
   static constexpr int BYTES = TAB_OFF + 16 * 16 + 1024;
 };
 
+// Register-resident (all indexing resolved at compile time: a dynamically
+// indexed coordinate array would live in local memory on the issue path).
 struct OpIter {
   int c[5];
-  int inc_dim, inc, wrap, carry_dim;
+  int inc, wrap;
+  int inc_dim, carry_dim;
   __device__ __forceinline__ void start(const OpFeed& f, int tile) {
-    c[0] = c[1] = c[2] = c[3] = c[4] = 0;
     const int t0 = tile * f.rows_per_tile;
-    c[f.lo_dim] += t0 % f.extent;
-    c[f.hi_dim] += t0 / f.extent;
-    inc_dim = f.inc_dim; inc = f.inc; wrap = f.wrap; carry_dim = f.carry_dim;
+    const int lo = t0 % f.extent, hi = t0 / f.extent;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) c[d] = (d == f.lo_dim ? lo : 0) + (d == f.hi_dim ? hi : 0);
+    inc = f.inc; wrap = f.wrap; inc_dim = f.inc_dim; carry_dim = f.carry_dim;
   }
+  // every FC feed steps dimension 1 and carries into dimension 3 (asserted
+  // on the host when the feeds are built)
   __device__ __forceinline__ void next() {
-    c[inc_dim] += inc;
-    if (c[inc_dim] == wrap) { c[inc_dim] = 0; ++c[carry_dim]; }
+    c[1] += inc;
+    if (c[1] == wrap) { c[1] = 0; ++c[3]; }
   }
 };
 
@@ -108,12 +113,9 @@ struct OpIter {
 // advanced with counters (no integer division on the issue path — a single
 // issuing thread feeds the tensor core, so its loop must stay short).
 struct FeedIter {
-  OpIter ai, bi;
-  int a[5];
-  int cb_n, s_n, pad, r, s;
+  OpIter ai, bi;  // conv mode keeps its A coordinates in ai.c as well
+  int cb_n, s_n, pad, s;
   int mode;
-  __device__ __forceinline__ int* A() { return mode == FEED_FC ? ai.c : a; }
-  __device__ __forceinline__ int* B() { return bi.c; }
   __device__ __forceinline__ void start(const Params& p, int tm, int tn) {
     mode = p.mode;
     bi.start(p.fb, tn);
@@ -122,8 +124,8 @@ struct FeedIter {
     } else {
       cb_n = p.cv_Cb; s_n = p.cv_S; pad = p.cv_pad;
       const int n = tm / p.cv_tiles_per_img, pr = tm % p.cv_tiles_per_img;
-      r = 0; s = 0;
-      a[0] = 0; a[1] = -pad; a[2] = 2 * pr - pad; a[3] = 0; a[4] = n;
+      s = 0;
+      ai.c[0] = 0; ai.c[1] = -pad; ai.c[2] = 2 * pr - pad; ai.c[3] = 0; ai.c[4] = n;
     }
   }
   __device__ __forceinline__ void next() {
@@ -132,9 +134,9 @@ struct FeedIter {
       ai.next();
     } else {
       // reduce block order (r, s, cb): cb fastest
-      if (++a[3] == cb_n) {
-        a[3] = 0;
-        if (++s == s_n) { s = 0; ++r; ++a[2]; a[1] = -pad; } else { ++a[1]; }
+      if (++ai.c[3] == cb_n) {
+        ai.c[3] = 0;
+        if (++s == s_n) { s = 0; ++ai.c[2]; ai.c[1] = -pad; } else { ++ai.c[1]; }
       }
     }
   }
@@ -230,10 +232,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * S::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-          const int* ca = f.A();
-          const int* cb = f.B();
-          tma_load_5d(sa, &map_a, &full[s], ca[0], ca[1], ca[2], ca[3], ca[4]);
-          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], cb[0], cb[1], cb[2], cb[3], cb[4]);
+          tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
+          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
           f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -516,6 +516,8 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   if (rc) return rc;
   rc = tc::make_map_5d(&mb, b_ptr, B.dims, B.strides, B.box);
   if (rc) return rc;
+  TPP_REQUIRE(A.feed.inc_dim == 1 && A.feed.carry_dim == 3 && B.feed.inc_dim == 1 && B.feed.carry_dim == 3,
+              TPP_E_UNSUPPORTED, "internal: feed must step dim 1 and carry into dim 3");
   p.fa = A.feed;
   p.fb = B.feed;
   return tc::launch(BN, ma, mb, p, stream);
