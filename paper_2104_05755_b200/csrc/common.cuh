@@ -76,6 +76,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return (uint32_t)f32_to_bf16(lo) | ((uint32_t)f32_to_bf16(hi) << 16);
 }
 
+// Same result as pack_bf16x2, faster: hardware cvt.rn.bf16x2.f32 for numbers
+// (identical RNE incl. overflow to inf and subnormals), the reference's NaN
+// rule patched in for NaNs.
+__device__ __forceinline__ uint32_t pack2_bf16_ref(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  if (lo != lo) r = (r & 0xFFFF0000u) | f32_to_bf16(lo);
+  if (hi != hi) r = (r & 0x0000FFFFu) | ((uint32_t)f32_to_bf16(hi) << 16);
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // GELU minimax erf table (approx.py:144-171, 267-288).  The 64 float32
 // coefficients are the reference's Chebyshev fit (approx.py:127-158),

@@ -140,9 +140,115 @@ layernorm_blocked_kernel(int n_b, int m_b, int bn, int bm, const T* __restrict__
   }
 }
 
+// ---- blocked BF16, bm == 64, bn % 32 == 0: smem-transposed, vectorised ------
+// CTA = 32 tokens of one token block.  (1) all 128 threads stream the 32
+// tokens' 16 x 4 KB feature blocks into smem with coalesced 16-byte loads;
+// (2) warp 0 folds each token's row in the reference's ascending order with
+// LDS.128 (rows padded by 16 B: conflict-free); (3) all threads apply the
+// scaling equation and store coalesced 16-byte chunks.
+__device__ __forceinline__ void fold8(const uint4& v, float& s, float& ss) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float a = __uint_as_float(w[e] << 16), b = __uint_as_float(w[e] & 0xFFFF0000u);
+    s = __fadd_rn(s, a);
+    ss = __fadd_rn(ss, __fmul_rn(a, a));
+    s = __fadd_rn(s, b);
+    ss = __fadd_rn(ss, __fmul_rn(b, b));
+  }
+}
+
+__global__ void __launch_bounds__(256)
+layernorm_blocked_bf16_v(int n_b, int m_b, int bn, const uint4* __restrict__ x,
+                         const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
+                         uint4* __restrict__ out, float* mean_out, float* var_out) {
+  extern __shared__ __align__(16) uint4 lv[];
+  const int F8 = m_b * 8;              // uint4 per token row
+  const int pitch = F8 + 1;            // +16 B: LDS.128 across rows conflict-free
+  float* sc = reinterpret_cast<float*>(lv + 32 * pitch);
+  float* sh = sc + 32;
+  const int chunks = bn / 32;
+  const int nb = blockIdx.x / chunks;
+  const int n0 = (blockIdx.x - nb * chunks) * 32;
+  // (1) block mb of these 32 tokens is 32 x 8 uint4 contiguous
+  const int total = m_b * 256;
+  // 8 independent 16-byte loads in flight per thread before any smem store
+  for (int e0 = 0; e0 < total; e0 += 256 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256 + threadIdx.x;
+      if (e < total) {
+        const int mb = e >> 8, r = e & 255;
+        v[u] = __ldg(x + (((int64_t)nb * m_b + mb) * bn + n0) * 8 + r);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 256 + threadIdx.x;
+      if (e < total) {
+        const int mb = e >> 8, r = e & 255, t = r >> 3, c = r & 7;
+        lv[t * pitch + mb * 8 + c] = v[u];
+      }
+    }
+  }
+  __syncthreads();
+  // (2)
+  if (threadIdx.x < 32) {
+    const uint4* row = lv + threadIdx.x * pitch;
+    float s = 0.0f, ss = 0.0f;
+#pragma unroll 8
+    for (int c = 0; c < F8; ++c) fold8(row[c], s, ss);
+    float scale, shift;
+    double mu, var;
+    row_glue(s, ss, m_b * 64, eps, scale, shift, mu, var);
+    sc[threadIdx.x] = scale;
+    sh[threadIdx.x] = shift;
+    const int64_t tok = (int64_t)nb * bn + n0 + threadIdx.x;
+    if (mean_out) mean_out[tok] = (float)mu;
+    if (var_out) var_out[tok] = (float)var;
+  }
+  __syncthreads();
+  // (3)
+  for (int e = threadIdx.x; e < total; e += 256) {
+    const int mb = e >> 8, r = e & 255, t = r >> 3, c = r & 7;
+    const uint4 v = lv[t * pitch + mb * 8 + c];
+    const float scl = sc[t], shf = sh[t];
+    const int f0 = mb * 64 + c * 8;
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int f = f0 + 2 * q;
+      const float a = __uint_as_float(w[q] << 16), b = __uint_as_float(w[q] & 0xFFFF0000u);
+      const float ga = gamma ? __ldg(gamma + f) : 1.0f, gb = gamma ? __ldg(gamma + f + 1) : 1.0f;
+      const float ba = beta ? __ldg(beta + f) : 0.0f, bb = beta ? __ldg(beta + f + 1) : 0.0f;
+      const float ra = __fadd_rn(ba, __fmul_rn(__fadd_rn(shf, __fmul_rn(a, scl)), ga));
+      const float rb = __fadd_rn(bb, __fmul_rn(__fadd_rn(shf, __fmul_rn(b, scl)), gb));
+      o[q] = pack2_bf16_ref(ra, rb);
+    }
+    out[(((int64_t)nb * m_b + mb) * bn + n0) * 8 + r] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
                              const float* gamma, const float* beta, double eps, void* out,
                              float* mean_out, float* var_out, cudaStream_t s) {
+  if (dtype == TPP_BF16 && bm == 64 && bn % 32 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+    const size_t smem = (size_t)32 * (m_b * 8 + 1) * 16 + 64 * sizeof(float);
+    if (smem <= 227 * 1024) {
+      const int blocks = n_b * (bn / 32);
+      if (blocks == 0) return TPP_OK;
+      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_bf16_v,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_bf16_v)");
+      layernorm_blocked_bf16_v<<<blocks, 256, smem, s>>>(n_b, m_b, bn, (const uint4*)x, gamma, beta, eps,
+                                                         (uint4*)out, mean_out, var_out);
+      TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_bf16_v");
+      return TPP_OK;
+    }
+  }
   const int F = m_b * bm;
   const int es = dtype == TPP_BF16 ? 2 : 4;
   const int pitch = F + (es == 2 ? 2 : 1);
