@@ -238,6 +238,13 @@ int tpp_softmax(int32_t s1, int32_t s2, int32_t s3, const tpp_tensor_desc* x_d,
 int tpp_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad,
                   int32_t grad_dtype, float lr, void* stream);
 
+/* ---- diagnostics ------------------------------------------------------- */
+/* When `dev_buf` (>= 8 uint64, device memory) is non-NULL, subsequent FC
+ * tensor-core launches record %globaltimer phase stamps of CTA 0: start,
+ * prologue done, first stage landed, last MMA issued, accumulator ready,
+ * epilogue done, exit.  NULL disables.  Tools only. */
+int tpp_debug_phase_timestamps(uint64_t* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,7 @@ _SIGS = {
     "tpp_softmax": (C.c_int, [_I32, _I32, _I32, C.POINTER(TensorDescC), _P,
                               C.POINTER(TensorDescC), _P, _P]),
     "tpp_split_sgd": (C.c_int, [_I64, _P, _P, _P, _I32, C.c_float, _P]),
+    "tpp_debug_phase_timestamps": (C.c_int, [_P]),
 }
 
 _lib = None

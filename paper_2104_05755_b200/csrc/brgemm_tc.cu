@@ -47,19 +47,21 @@ enum FeedMode { FEED_FC = 0, FEED_CONV = 1 };
 
 // One operand's walk through a 5-D tensor map.  Tile t starts at element
 // t0 = t * rows_per_tile along the tiled axis, split as (t0 % extent) on
-// dimension lo_dim and (t0 / extent) on hi_dim; every reduce block then adds
-// `inc` on inc_dim and, on reaching `wrap`, resets it and carries 1 into
-// carry_dim.  This single form covers the forward (K-major tokens / weights),
-// backward-data (MN-major weights) and backward-weight (MN-major tokens) feeds.
+// dimension lo_dim and (t0 / extent) on hi_dim.  Each pipeline stage (KPS
+// reduce blocks, ONE TMA box) then advances the reduce coordinate:
+//   step 0: c[1] += inc, wrapping at `wrap` with a carry into c[3]
+//   step 1: c[4] += inc          step 2: c[3] += inc
 struct OpFeed {
   int lo_dim, hi_dim, extent, rows_per_tile;
-  int inc_dim, inc, wrap, carry_dim;
+  int step, inc, wrap;
+  int sub_bytes;   // smem distance between consecutive reduce blocks of a stage
+  int lbo;         // MN-major: distance between 64-wide M/N atoms
 };
 
 struct Params {
   int mode;
   int tokens;          // valid rows of the output (M extent)
-  int kblocks;         // reduce blocks per tile
+  int kblocks;         // reduce blocks per tile (multiple of KPS)
   OpFeed fa, fb;       // FC-mode feeds
   int a_mn, b_mn;      // operand major-ness (0 K-major, 1 MN-major)
   // conv: A 5-D map {64, W, H, C_b, N}; 2 output rows x 64 columns per tile
@@ -74,44 +76,51 @@ struct Params {
   void* out;
   uint8_t* mask;        // ReLU bitmask written (TPP_FC_RELU_MASK)
   const uint8_t* mask_in;  // ReLU bitmask applied (RELU_INV, backward-data)
+  unsigned long long* dbg;  // optional phase timestamps (CTA 0), tools only
+  int tma_store;            // BF16 output through smem staging + TMA (map_c)
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KPS>
 struct Smem {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int A_BYTES = KPS * BM * BK * 2;
+  static constexpr int B_BYTES = KPS * BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   // barriers: full[S], empty[S], tfull[2], tempty[2]; then tmem base + gelu table (float4 x 16)
   static constexpr int TAB_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int BYTES = TAB_OFF + 16 * 16 + 1024;
+  static constexpr int BIAS_OFF = TAB_OFF + 16 * 16;                      // float [2][256]
+  static constexpr int STG_OFF = (BIAS_OFF + 2 * 256 * 4 + 1023) & ~1023;  // 8 warps x 2 KB
+  static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 + 1024;
 };
 
 // Register-resident (all indexing resolved at compile time: a dynamically
 // indexed coordinate array would live in local memory on the issue path).
 struct OpIter {
   int c[5];
-  int inc, wrap;
-  int inc_dim, carry_dim;
+  int step, inc, wrap;
   __device__ __forceinline__ void start(const OpFeed& f, int tile) {
     const int t0 = tile * f.rows_per_tile;
     const int lo = t0 % f.extent, hi = t0 / f.extent;
 #pragma unroll
     for (int d = 0; d < 5; ++d) c[d] = (d == f.lo_dim ? lo : 0) + (d == f.hi_dim ? hi : 0);
-    inc = f.inc; wrap = f.wrap; inc_dim = f.inc_dim; carry_dim = f.carry_dim;
+    step = f.step; inc = f.inc; wrap = f.wrap;
   }
-  // every FC feed steps dimension 1 and carries into dimension 3 (asserted
-  // on the host when the feeds are built)
   __device__ __forceinline__ void next() {
-    c[1] += inc;
-    if (c[1] == wrap) { c[1] = 0; ++c[3]; }
+    if (step == 0) {
+      c[1] += inc;
+      if (c[1] == wrap) { c[1] = 0; ++c[3]; }
+    } else if (step == 1) {
+      c[4] += inc;
+    } else {
+      c[3] += inc;
+    }
   }
 };
 
-// Producer-side iterator over the reduce blocks of one tile: coordinates are
-// advanced with counters (no integer division on the issue path — a single
-// issuing thread feeds the tensor core, so its loop must stay short).
+// Producer-side iterator over the stages of one tile: coordinates advance by
+// counters (no integer division on the issue path — a single issuing thread
+// feeds the tensor core, so its loop must stay short).
 struct FeedIter {
   OpIter ai, bi;  // conv mode keeps its A coordinates in ai.c as well
   int cb_n, s_n, pad, s;
@@ -155,6 +164,12 @@ __device__ __forceinline__ int row_token(const Params& p, int tm, int r) {
   return (n * p.cv_P + oh) * p.cv_Q + ow;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // GELU with the table as one float4 {c0,c1,c2,c3} per interval (one LDS.128)
 __device__ __forceinline__ float gelu4(float x, const float4* tab) {
   const float ax = fabsf(x);
@@ -167,22 +182,12 @@ __device__ __forceinline__ float gelu4(float x, const float4* tab) {
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
 }
 
-// two FP32 -> packed BF16 with the reference's RNE (dtypes.py:82-97):
-// hardware cvt.rn for numbers (identical rounding, overflow to inf), the
-// reference's NaN rule patched in for NaNs.
-__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  if (lo != lo) r = (r & 0xFFFF0000u) | f32_to_bf16(lo);
-  if (hi != hi) r = (r & 0x0000FFFFu) | ((uint32_t)f32_to_bf16(hi) << 16);
-  return r;
-}
-
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KPS>
 __global__ void __launch_bounds__(kThreads, 1)
 brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
-                 const __grid_constant__ CUtensorMap map_b, const Params p) {
-  using S = Smem<BN, STAGES>;
+                 const __grid_constant__ CUtensorMap map_b,
+                 const __grid_constant__ CUtensorMap map_c, const Params p) {
+  using S = Smem<BN, STAGES, KPS>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -194,9 +199,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[0] = gtimer();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.tiles_m * p.tiles_n;
+  const int nstages = p.kblocks / KPS;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
@@ -219,6 +226,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[1] = gtimer();
+  // Programmatic dependent launch: let the next kernel in the stream be
+  // scheduled now (its prologue overlaps our tail), and do not touch global
+  // memory before the previous kernel's results are visible.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ===================== TMA producer (one thread) =====================
@@ -228,7 +241,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       FeedIter f;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         f.start(p, tile / p.tiles_n, tile % p.tiles_n);
-        for (int j = 0; j < p.kblocks; ++j) {
+        for (int j = 0; j < nstages; ++j) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * S::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
@@ -244,11 +257,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
       // K-major: a 16-element K step is +32 B; MN-major: +2 K-groups (+2048 B)
-      const uint64_t adesc0 = p.a_mn ? sw128_mnmajor_desc(smem_u32(smem), 8192) : sw128_kmajor_desc(smem_u32(smem));
-      const uint64_t bdesc0 = (p.b_mn ? sw128_mnmajor_desc(smem_u32(smem), 8192) : sw128_kmajor_desc(smem_u32(smem))) +
+      const uint64_t adesc0 = p.a_mn ? sw128_mnmajor_desc(smem_u32(smem), p.fa.lbo) : sw128_kmajor_desc(smem_u32(smem));
+      const uint64_t bdesc0 = (p.b_mn ? sw128_mnmajor_desc(smem_u32(smem), p.fb.lbo) : sw128_kmajor_desc(smem_u32(smem))) +
                               (uint64_t)(S::A_BYTES >> 4);
       const uint32_t astep = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint32_t bstep = p.b_mn ? (2048 >> 4) : (32 >> 4);
+      const uint32_t asub = (uint32_t)p.fa.sub_bytes >> 4, bsub = (uint32_t)p.fb.sub_bytes >> 4;
       int s = 0;
       uint32_t ph = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
@@ -256,19 +270,24 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
-        for (int j = 0; j < p.kblocks; ++j) {
+        for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
+          if (p.dbg && blockIdx.x == 0 && tcount == 0 && j == 0) p.dbg[2] = gtimer();
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            umma_f16(tmem_d, adesc0 + soff + astep * kk, bdesc0 + soff + bstep * kk, idesc,
-                     (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kb = 0; kb < KPS; ++kb) {
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk)
+              umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bdesc0 + soff + bsub * kb + bstep * kk,
+                       idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+          }
           umma_commit(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&tfull[as]);
+        if (p.dbg && blockIdx.x == 0 && tcount == 0) p.dbg[3] = gtimer();
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -278,61 +297,60 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const int half = ew >> 2;          // which half of the tile's columns
     const int r = q * 32 + lane;
     constexpr int CH = BN / 64;        // 32-column chunks per half
+    float* bias_s = reinterpret_cast<float*>(smem + S::BIAS_OFF);
+    uint8_t* stg = smem + S::STG_OFF + ew * 2048;  // 32 rows x 64 B, 64B-swizzled
     uint32_t tcount = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
       const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+      float* bs = bias_s + as * 256;
+      if (p.flags & TPP_FC_BIAS) {
+        // stage this tile's bias (COL broadcast) in smem while the MMAs run
+        for (int i = ew * 32 + lane; i < BN; i += kEpiWarps * 32) {
+          const int f = tn * BN + i;
+          float v = 0.0f;
+          if (f < p.feats)
+            v = (p.flags & TPP_FC_BIAS_FP32) ? reinterpret_cast<const float*>(p.bias)[f]
+                                             : bf16_to_f32(reinterpret_cast<const uint16_t*>(p.bias)[f]);
+          bs[i] = v;
+        }
+        named_bar_sync(1, kEpiWarps * 32);
+      }
       mbar_wait(&tfull[as], aph);
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[4] = gtimer();
       tc_fence_after();
       const int t = row_token(p, tm, r);
       const int nb = t >= 0 ? t / p.o_bn : 0;
       const int n_in = t >= 0 ? t % p.o_bn : 0;
+      // TMA store: the warp's 32 rows are 32 consecutive tokens of one token block
+      const int t0 = tm * BM + q * 32;
+      const bool warp_rows = p.tma_store && t0 < p.tokens;
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int col = half * (BN / 2) + ch * 32;
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0 && ch == 0) p.dbg[7] = gtimer();
         const int f0 = tn * BN + col;
-        if (t < 0 || f0 >= p.feats) continue;
+        if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
         const int mb = f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
         float x[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
         if (p.flags & TPP_FC_BIAS) {
-          if (p.flags & TPP_FC_BIAS_FP32) {
-            const float4* bp = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p.bias) + f0);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const float4 b4 = __ldg(bp + i);
-              x[4 * i] = __fadd_rn(x[4 * i], b4.x);
-              x[4 * i + 1] = __fadd_rn(x[4 * i + 1], b4.y);
-              x[4 * i + 2] = __fadd_rn(x[4 * i + 2], b4.z);
-              x[4 * i + 3] = __fadd_rn(x[4 * i + 3], b4.w);
-            }
-          } else {
-            const uint4* bp = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.bias) + f0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 b4 = __ldg(bp + i);
-              const uint32_t w[4] = {b4.x, b4.y, b4.z, b4.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                x[8 * i + 2 * e] = __fadd_rn(x[8 * i + 2 * e], __uint_as_float(w[e] << 16));
-                x[8 * i + 2 * e + 1] = __fadd_rn(x[8 * i + 2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
-              }
-            }
-          }
+          for (int i = 0; i < 32; ++i) x[i] = __fadd_rn(x[i], bs[col + i]);
         }
-        if (p.flags & TPP_FC_RELU_INV) {
+        if ((p.flags & TPP_FC_RELU_INV) && t >= 0) {
           // ops.py:367-369: where(mask, dy, 0) with the forward ReLU bitmask
           const uint32_t bits = *reinterpret_cast<const uint32_t*>(p.mask_in + row_off * (p.o_bm / 8) + m_in / 8);
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = ((bits >> i) & 1u) ? x[i] : 0.0f;
         }
         if (p.act == TPP_ACT_RELU) {
-          if (p.flags & TPP_FC_RELU_MASK) {
+          if ((p.flags & TPP_FC_RELU_MASK) && t >= 0) {
             uint32_t bits = 0;
 #pragma unroll
             for (int i = 0; i < 32; ++i) bits |= (x[i] > 0.0f ? 1u : 0u) << i;
@@ -344,7 +362,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], gelu_tab);
         }
-        if (p.flags & TPP_FC_RESIDUAL) {
+        if ((p.flags & TPP_FC_RESIDUAL) && t >= 0) {
           const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -362,18 +380,39 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             op[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
+        } else if (p.tma_store) {
+          uint4 val[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            val[i] = make_uint4(pack2_bf16_ref(x[8 * i], x[8 * i + 1]), pack2_bf16_ref(x[8 * i + 2], x[8 * i + 3]),
+                                pack2_bf16_ref(x[8 * i + 4], x[8 * i + 5]), pack2_bf16_ref(x[8 * i + 6], x[8 * i + 7]));
+          if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging rows
+          __syncwarp();
+          // row `lane`, 16-byte chunk c lands at chunk c ^ ((lane >> 1) & 3) (SWIZZLE_64B)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = val[c];
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0 && warp_rows) {
+            tma_store_5d(&map_c, stg, m_in, 0, t0 % p.o_bn, mb, t0 / p.o_bn);
+            bulk_commit();
+          }
         } else {
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            op[i] = make_uint4(pack2_bf16(x[8 * i], x[8 * i + 1]), pack2_bf16(x[8 * i + 2], x[8 * i + 3]),
-                               pack2_bf16(x[8 * i + 4], x[8 * i + 5]), pack2_bf16(x[8 * i + 6], x[8 * i + 7]));
+            op[i] = make_uint4(pack2_bf16_ref(x[8 * i], x[8 * i + 1]), pack2_bf16_ref(x[8 * i + 2], x[8 * i + 3]),
+                               pack2_bf16_ref(x[8 * i + 4], x[8 * i + 5]), pack2_bf16_ref(x[8 * i + 6], x[8 * i + 7]));
         }
       }
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[8] = gtimer();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[5] = gtimer();
     }
+    if (lane == 0 && p.tma_store) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -382,6 +421,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     tc_fence_after();
     tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 64) p.dbg[6] = gtimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -403,7 +443,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 5-D bf16 map, dims innermost first, strides in bytes for dims 1..4
 static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
-                       const uint64_t strides[4], const uint32_t box[5]) {
+                       const uint64_t strides[4], const uint32_t box[5],
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode();
   if (!enc) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail(TPP_E_TENSOR, "TMA base not 16B aligned");
@@ -420,38 +461,63 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
     gs[i] = strides[i];
   }
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gd, gs, bd,
-                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return TPP_OK;
 }
 
-template <int BN, int STAGES>
-static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
-                      cudaStream_t stream) {
-  using S = Smem<BN, STAGES>;
+template <int BN, int STAGES, int KPS>
+static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                      const Params& p, cudaStream_t stream) {
+  using S = Smem<BN, STAGES, KPS>;
+  static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES, KPS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
     attr_set = true;
   }
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  brgemm_tc_kernel<BN, STAGES><<<grid, kThreads, S::BYTES, stream>>>(ma, mb, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, brgemm_tc_kernel<BN, STAGES, KPS>, ma, mb, mc, p);
+  if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
   return TPP_OK;
 }
 
-static int launch(int bn_tile, const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
-                  cudaStream_t s) {
-  switch (bn_tile) {
-    case 64: return launch_cfg<64, 8>(ma, mb, p, s);
-    case 128: return launch_cfg<128, 6>(ma, mb, p, s);
-    case 256: return launch_cfg<256, 4>(ma, mb, p, s);
-    default: return fail(TPP_E_UNSUPPORTED, "tile width must be 64, 128 or 256");
+// (tile width, reduce blocks per stage) -> instantiation; stages fill ~192 KB
+static int launch(int bn_tile, int kps, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                  const Params& p, cudaStream_t s) {
+  if (kps == 1) {
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 8, 1>(ma, mb, mc, p, s);
+      case 128: return launch_cfg<128, 6, 1>(ma, mb, mc, p, s);
+      case 256: return launch_cfg<256, 4, 1>(ma, mb, mc, p, s);
+    }
+  } else if (kps == 2) {
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 4, 2>(ma, mb, mc, p, s);
+      case 128: return launch_cfg<128, 3, 2>(ma, mb, mc, p, s);
+      case 256: return launch_cfg<256, 2, 2>(ma, mb, mc, p, s);
+    }
+  } else if (kps == 4) {
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 2, 4>(ma, mb, mc, p, s);
+    }
   }
+  return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
 }
 
 }  // namespace tc
@@ -463,7 +529,11 @@ static int launch(int bn_tile, const CUtensorMap& ma, const CUtensorMap& mb, con
 //   forward          out[t, f] = sum_c x[t, c]  W[f, c]      A K-major,  B K-major
 //   backward-data    dx[t, c]  = sum_f dy[t, f] W[f, c]      A K-major,  B MN-major
 //   backward-weights dW[f, c]  = sum_t dy[t, f] x[t, c]      A MN-major, B MN-major
-// All three read the same blocked buffers in place — no transposes.
+// All three read the same blocked buffers in place — no transposes.  A
+// pipeline stage carries KPS consecutive 64-wide reduce blocks in ONE TMA box
+// per operand (the tensor-map dimension order puts the reduce-block index
+// outermost in the box), so the single producer thread issues 2 TMA loads per
+// KPS x 64 reduce elements.
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -474,31 +544,49 @@ struct Operand {
   tc::OpFeed feed;
 };
 
-// K-major operand: rows of a blocked [nblk][kblk][rows_b][k_in] tensor
-// (k_in a multiple of 64), tiles of `tile_rows` rows.
-Operand kmajor_operand(int nblk, int kblk, int rows_b, int k_in, int tile_rows) {
+// K-major operand: rows of a blocked [nblk][kblk][rows_b][k_in] tensor, tiles
+// of `tile_rows` rows, `kps` reduce blocks per stage (kps > 1 needs k_in == 64).
+Operand kmajor_operand(int nblk, int kblk, int rows_b, int k_in, int tile_rows, int kps) {
   Operand o{};
   const uint64_t kb = (uint64_t)k_in * 2;
-  o.dims[0] = 64; o.dims[1] = k_in / 64; o.dims[2] = rows_b; o.dims[3] = kblk; o.dims[4] = nblk;
-  o.strides[0] = 128; o.strides[1] = kb; o.strides[2] = (uint64_t)rows_b * kb;
-  o.strides[3] = (uint64_t)kblk * rows_b * kb;
   const bool split = rows_b >= tile_rows;
-  o.box[0] = 64; o.box[1] = 1; o.box[2] = split ? tile_rows : rows_b; o.box[3] = 1;
-  o.box[4] = split ? 1 : tile_rows / rows_b;
-  o.feed = {2, 4, rows_b, tile_rows, 1, 1, k_in / 64, 3};
+  const uint32_t box_rows = split ? tile_rows : rows_b, box_n = split ? 1 : tile_rows / rows_b;
+  if (kps == 1) {
+    o.dims[0] = 64; o.dims[1] = k_in / 64; o.dims[2] = rows_b; o.dims[3] = kblk; o.dims[4] = nblk;
+    o.strides[0] = 128; o.strides[1] = kb; o.strides[2] = (uint64_t)rows_b * kb;
+    o.strides[3] = (uint64_t)kblk * rows_b * kb;
+    o.box[0] = 64; o.box[1] = 1; o.box[2] = box_rows; o.box[3] = 1; o.box[4] = box_n;
+    o.feed = {2, 4, rows_b, tile_rows, 0, 1, k_in / 64, 0, 0};
+  } else {
+    // dims {c, 1, row, nblk, kblk}: the reduce block is the outermost box dim,
+    // so one box = kps consecutive [tile_rows][64] K-major sub-tiles
+    o.dims[0] = 64; o.dims[1] = 1; o.dims[2] = rows_b; o.dims[3] = nblk; o.dims[4] = kblk;
+    o.strides[0] = 128; o.strides[1] = 128; o.strides[2] = (uint64_t)kblk * rows_b * 128;
+    o.strides[3] = (uint64_t)rows_b * 128;
+    o.box[0] = 64; o.box[1] = 1; o.box[2] = box_rows; o.box[3] = box_n; o.box[4] = kps;
+    o.feed = {2, 3, rows_b, tile_rows, 1, kps, 0, tile_rows * 128, 0};
+  }
   return o;
 }
 
-// MN-major operand over a blocked [red_blk][mn_blk][red_in][64] tensor
-// (the MN block is exactly 64 wide = one 128B atom; the reduce index runs
-// over red_in rows then red_blk blocks), tiles of `tile_mn` MN elements.
-Operand mnmajor_operand(int red_blk, int mn_blk, int red_in, int tile_mn) {
+// MN-major operand over a blocked [red_blk][mn_blk][red_in][64] tensor (the
+// MN block is exactly 64 wide = one 128B atom), tiles of `tile_mn` MN elements.
+Operand mnmajor_operand(int red_blk, int mn_blk, int red_in, int tile_mn, int kps) {
   Operand o{};
   o.dims[0] = 64; o.dims[1] = red_in; o.dims[2] = mn_blk; o.dims[3] = red_blk; o.dims[4] = 1;
   o.strides[0] = 128; o.strides[1] = (uint64_t)red_in * 128; o.strides[2] = (uint64_t)mn_blk * red_in * 128;
   o.strides[3] = (uint64_t)red_blk * mn_blk * red_in * 128;
-  o.box[0] = 64; o.box[1] = 64; o.box[2] = tile_mn / 64; o.box[3] = 1; o.box[4] = 1;
-  o.feed = {0, 2, 64, tile_mn, 1, 64, red_in, 3};
+  o.box[0] = 64; o.box[2] = tile_mn / 64; o.box[4] = 1;
+  if (red_in % (64 * kps) == 0) {
+    // kps x 64 reduce rows inside one red block: smem [mn_local][64*kps][64]
+    o.box[1] = 64 * kps; o.box[3] = 1;
+    o.feed = {0, 2, 64, tile_mn, 0, 64 * kps, red_in, 64 * 128, 64 * kps * 128};
+  } else {
+    // red_in == 64: kps red blocks per box: smem [red_local][mn_local][64][64]
+    o.box[1] = 64; o.box[3] = kps;
+    o.feed = {0, 2, 64, tile_mn, kps == 1 ? 0 : 2, kps == 1 ? 64 : kps, red_in, (tile_mn / 64) * 64 * 128,
+              64 * 128};
+  }
   return o;
 }
 
@@ -509,23 +597,55 @@ int pick_bn(int feats, int tiles_m, int pref) {
   return BN;
 }
 
+// reduce blocks per stage: as many as the smem budget of the tile allows
+int pick_kps(int BN, int kblocks, bool kmajor_ok) {
+  if (!kmajor_ok) return 1;
+  static const int forced = [] {
+    const char* e = getenv("TPP_KPS");  // tuning experiments only
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1 || forced == 2 || forced == 4) {
+    if (kblocks % forced == 0 && !(forced == 4 && BN != 64)) return forced;
+  }
+  // wide tiles are MMA-bound per stage already; keep their deeper pipeline
+  if (BN == 256) return 1;
+  if (BN == 64 && kblocks % 4 == 0) return 4;
+  if (kblocks % 2 == 0) return 2;
+  return 1;
+}
+
 int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* b_ptr, tc::Params p,
-             int BN, cudaStream_t stream) {
-  CUtensorMap ma, mb;
+             int BN, int kps, cudaStream_t stream) {
+  CUtensorMap ma, mb, mc;
   int rc = tc::make_map_5d(&ma, a_ptr, A.dims, A.strides, A.box);
   if (rc) return rc;
   rc = tc::make_map_5d(&mb, b_ptr, B.dims, B.strides, B.box);
   if (rc) return rc;
-  TPP_REQUIRE(A.feed.inc_dim == 1 && A.feed.carry_dim == 3 && B.feed.inc_dim == 1 && B.feed.carry_dim == 3,
-              TPP_E_UNSUPPORTED, "internal: feed must step dim 1 and carry into dim 3");
+  // BF16 outputs leave through smem staging + TMA stores: output tensor
+  // [ntb][o_mb][o_bn][o_bm], box = 32 tokens x 32 features, 64B swizzle
+  p.tma_store = !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
+                reinterpret_cast<uintptr_t>(p.out) % 16 == 0;
+  mc = ma;
+  if (p.tma_store) {
+    const uint64_t rowb = (uint64_t)p.o_bm * 2;
+    const uint64_t dims[5] = {(uint64_t)p.o_bm, 1, (uint64_t)p.o_bn, (uint64_t)p.o_mb,
+                              (uint64_t)((p.tokens + p.o_bn - 1) / p.o_bn)};
+    const uint64_t str[4] = {rowb, rowb, (uint64_t)p.o_bn * rowb, (uint64_t)p.o_mb * p.o_bn * rowb};
+    const uint32_t box[5] = {32, 1, 32, 1, 1};
+    rc = tc::make_map_5d(&mc, p.out, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   p.fa = A.feed;
   p.fb = B.feed;
-  return tc::launch(BN, ma, mb, p, stream);
+  return tc::launch(BN, kps, ma, mb, mc, p, stream);
 }
 
 }  // namespace
 
 // flavor: 0 forward, 1 backward-data, 2 backward-weights
+static unsigned long long* g_dbg_ts = nullptr;
+void set_debug_timestamps(unsigned long long* p) { g_dbg_ts = p; }
+
 int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
                const void* x_for_dw, const void* bias, const void* residual, void* out,
                void* mask_out, const void* mask_in, cudaStream_t stream) {
@@ -540,6 +660,7 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   p.out = out;
   p.mask = reinterpret_cast<uint8_t*>(mask_out);
   p.mask_in = reinterpret_cast<const uint8_t*>(mask_in);
+  p.dbg = g_dbg_ts;
   TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
               "tensor-core FC needs bn | 128 or 128 | bn");
   if (flavor == 0) {
@@ -549,11 +670,13 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     const int BN = pick_bn(feats, tiles_m, d->block_n);
     TPP_REQUIRE(feats % BN == 0 && ((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0)),
                 TPP_E_UNSUPPORTED, "features must tile by the tile width");
-    p.tokens = tokens; p.kblocks = k_b * (bk / 64);
+    const int kblocks = k_b * (bk / 64);
+    const int kps = pick_kps(BN, kblocks, bk == 64);
+    p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
     p.o_bn = bn; p.o_bm = bm; p.o_mb = m_b;
-    return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM), kmajor_operand(m_b, k_b, bm, bk, BN), x_or_dy,
-                    w_packed, p, BN, stream);
+    return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM, kps), kmajor_operand(m_b, k_b, bm, bk, BN, kps), x_or_dy,
+                    w_packed, p, BN, kps, stream);
   }
   if (flavor == 1) {
     // dx[n_b][k_b][bn][bk] = dy[n_b][m_b][bn][bm] . W ; B = W as MN-major over its bk
@@ -562,12 +685,14 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     const int tiles_m = (tokens + BM - 1) / BM;
     const int BN = pick_bn(feats, tiles_m, d->block_n);
     TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
-    p.tokens = tokens; p.kblocks = m_b * (bm / 64);
+    const int kblocks = m_b * (bm / 64);
+    const int kps = pick_kps(BN, kblocks, bm == 64);
+    p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
     p.o_bn = bn; p.o_bm = bk; p.o_mb = k_b;
     p.b_mn = 1;
-    return run_gemm(kmajor_operand(n_b, m_b, bn, bm, BM), mnmajor_operand(m_b, k_b, bm, BN), x_or_dy,
-                    w_packed, p, BN, stream);
+    return run_gemm(kmajor_operand(n_b, m_b, bn, bm, BM, kps), mnmajor_operand(m_b, k_b, bm, BN, kps), x_or_dy,
+                    w_packed, p, BN, kps, stream);
   }
   // flavor 2: dW[m_b][k_b][bm][bk] = sum_t dy[t][f] x[t][c]
   TPP_REQUIRE(bm == 64 && bk == 64 && bn % 64 == 0, TPP_E_UNSUPPORTED,
@@ -576,12 +701,15 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   const int tiles_m = (rows + BM - 1) / BM;
   const int BN = pick_bn(feats, tiles_m, d->block_n);
   TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
-  p.tokens = rows; p.kblocks = n_b * (bn / 64);
+  const int kblocks = n_b * (bn / 64);
+  int kps = pick_kps(BN, kblocks, true);
+  while (kps > 1 && bn != 64 && bn % (64 * kps) != 0) kps /= 2;  // a box must not skip token rows
+  p.tokens = rows; p.kblocks = kblocks;
   p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
   p.o_bn = bm; p.o_bm = bk; p.o_mb = k_b;
   p.a_mn = 1; p.b_mn = 1;
-  return run_gemm(mnmajor_operand(n_b, m_b, bn, BM), mnmajor_operand(n_b, k_b, bn, BN), x_or_dy, x_for_dw, p,
-                  BN, stream);
+  return run_gemm(mnmajor_operand(n_b, m_b, bn, BM, kps), mnmajor_operand(n_b, k_b, bn, BN, kps), x_or_dy, x_for_dw,
+                  p, BN, kps, stream);
 }
 
 int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
@@ -633,13 +761,14 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     if (rc) return rc;
   }
   // weights: K-major rows [K_b][J = R*S*C_b][64 out][64 in]
-  const Operand wb = kmajor_operand(Kb, R * S * Cb, 64, 64, BN);
+  const Operand wb = kmajor_operand(Kb, R * S * Cb, 64, 64, BN, 1);
   p.fb = wb.feed;
   {
     int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
-  return launch(BN, ma, mb, p, stream);
+  p.tma_store = 0;
+  return launch(BN, 1, ma, mb, ma, p, stream);
 }
 
 }  // namespace tpp

@@ -75,6 +75,11 @@ using namespace tpp;
 extern "C" {
 
 const char* tpp_last_error(void) { return g_last_error.c_str(); }
+
+int tpp_debug_phase_timestamps(uint64_t* dev_buf) {
+  set_debug_timestamps(reinterpret_cast<unsigned long long*>(dev_buf));
+  return TPP_OK;
+}
 int tpp_version(void) { return 1; }
 int tpp_device_sm_count(void) {
   int dev = 0, n = 0;

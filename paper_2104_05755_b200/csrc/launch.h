@@ -31,6 +31,7 @@ int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, con
 int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
                const void* x_for_dw, const void* bias, const void* residual, void* out,
                void* mask_out, const void* mask_in, cudaStream_t stream);
+void set_debug_timestamps(unsigned long long* p);
 int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* logits,
                                 const int32_t* targets, float scale, void* dlogits, float* loss,
                                 cudaStream_t s);

@@ -160,7 +160,7 @@ __device__ __forceinline__ void fold8(const uint4& v, float& s, float& ss) {
 
 __global__ void __launch_bounds__(256)
 layernorm_blocked_bf16_v(int n_b, int m_b, int bn, const uint4* __restrict__ x,
-                         const float* __restrict__ gamma, const float* __restrict__ beta, double eps,
+                         const float4* __restrict__ gamma, const float4* __restrict__ beta, double eps,
                          uint4* __restrict__ out, float* mean_out, float* var_out) {
   extern __shared__ __align__(16) uint4 lv[];
   const int F8 = m_b * 8;              // uint4 per token row
@@ -170,64 +170,68 @@ layernorm_blocked_bf16_v(int n_b, int m_b, int bn, const uint4* __restrict__ x,
   const int chunks = bn / 32;
   const int nb = blockIdx.x / chunks;
   const int n0 = (blockIdx.x - nb * chunks) * 32;
-  // (1) block mb of these 32 tokens is 32 x 8 uint4 contiguous
-  const int total = m_b * 256;
-  // 8 independent 16-byte loads in flight per thread before any smem store
-  for (int e0 = 0; e0 < total; e0 += 256 * 8) {
+  // block mb of these 32 tokens is 32 x 8 uint4 contiguous: one uint4 per thread
+  const int tid = threadIdx.x, t = tid >> 3, c = tid & 7;
+  const uint4* src = x + ((int64_t)nb * m_b * bn + n0) * 8 + tid;
+  uint4* dst = out + ((int64_t)nb * m_b * bn + n0) * 8 + tid;
+  const int64_t bstep = (int64_t)bn * 8;
+  uint4* mine = lv + t * pitch + c;
+  // (1) 8 independent loads in flight per thread
+  for (int mb0 = 0; mb0 < m_b; mb0 += 8) {
     uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 256 + threadIdx.x;
-      if (e < total) {
-        const int mb = e >> 8, r = e & 255;
-        v[u] = __ldg(x + (((int64_t)nb * m_b + mb) * bn + n0) * 8 + r);
-      }
-    }
+    for (int u = 0; u < 8; ++u)
+      if (mb0 + u < m_b) v[u] = __ldg(src + (mb0 + u) * bstep);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * 256 + threadIdx.x;
-      if (e < total) {
-        const int mb = e >> 8, r = e & 255, t = r >> 3, c = r & 7;
-        lv[t * pitch + mb * 8 + c] = v[u];
-      }
-    }
+    for (int u = 0; u < 8; ++u)
+      if (mb0 + u < m_b) mine[(mb0 + u) * 8] = v[u];
   }
   __syncthreads();
-  // (2)
-  if (threadIdx.x < 32) {
-    const uint4* row = lv + threadIdx.x * pitch;
+  // (2) the reference fold, one thread per token
+  if (tid < 32) {
+    const uint4* row = lv + tid * pitch;
     float s = 0.0f, ss = 0.0f;
 #pragma unroll 8
-    for (int c = 0; c < F8; ++c) fold8(row[c], s, ss);
+    for (int k = 0; k < F8; ++k) fold8(row[k], s, ss);
     float scale, shift;
     double mu, var;
     row_glue(s, ss, m_b * 64, eps, scale, shift, mu, var);
-    sc[threadIdx.x] = scale;
-    sh[threadIdx.x] = shift;
-    const int64_t tok = (int64_t)nb * bn + n0 + threadIdx.x;
+    sc[tid] = scale;
+    sh[tid] = shift;
+    const int64_t tok = (int64_t)nb * bn + n0 + tid;
     if (mean_out) mean_out[tok] = (float)mu;
     if (var_out) var_out[tok] = (float)var;
   }
   __syncthreads();
-  // (3)
-  for (int e = threadIdx.x; e < total; e += 256) {
-    const int mb = e >> 8, r = e & 255, t = r >> 3, c = r & 7;
-    const uint4 v = lv[t * pitch + mb * 8 + c];
-    const float scl = sc[t], shf = sh[t];
-    const int f0 = mb * 64 + c * 8;
+  // (3) out = B + (shift + x*scale)*G, 8 features per thread per block
+  const float scl = sc[t], shf = sh[t];
+  for (int mb = 0; mb < m_b; ++mb) {
+    const uint4 v = mine[mb * 8];
+    float g[8], b[8];
+    if (gamma) {
+      const float4 g0 = __ldg(gamma + mb * 16 + c * 2), g1 = __ldg(gamma + mb * 16 + c * 2 + 1);
+      g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g[i] = 1.0f;
+    }
+    if (beta) {
+      const float4 b0 = __ldg(beta + mb * 16 + c * 2), b1 = __ldg(beta + mb * 16 + c * 2 + 1);
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) b[i] = 0.0f;
+    }
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     uint32_t o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int f = f0 + 2 * q;
-      const float a = __uint_as_float(w[q] << 16), b = __uint_as_float(w[q] & 0xFFFF0000u);
-      const float ga = gamma ? __ldg(gamma + f) : 1.0f, gb = gamma ? __ldg(gamma + f + 1) : 1.0f;
-      const float ba = beta ? __ldg(beta + f) : 0.0f, bb = beta ? __ldg(beta + f + 1) : 0.0f;
-      const float ra = __fadd_rn(ba, __fmul_rn(__fadd_rn(shf, __fmul_rn(a, scl)), ga));
-      const float rb = __fadd_rn(bb, __fmul_rn(__fadd_rn(shf, __fmul_rn(b, scl)), gb));
-      o[q] = pack2_bf16_ref(ra, rb);
+      const float a0 = __uint_as_float(w[q] << 16), a1 = __uint_as_float(w[q] & 0xFFFF0000u);
+      const float r0 = __fadd_rn(b[2 * q], __fmul_rn(__fadd_rn(shf, __fmul_rn(a0, scl)), g[2 * q]));
+      const float r1 = __fadd_rn(b[2 * q + 1], __fmul_rn(__fadd_rn(shf, __fmul_rn(a1, scl)), g[2 * q + 1]));
+      o[q] = pack2_bf16_ref(r0, r1);
     }
-    out[(((int64_t)nb * m_b + mb) * bn + n0) * 8 + r] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[mb * bstep] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -235,7 +239,8 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
                              const float* gamma, const float* beta, double eps, void* out,
                              float* mean_out, float* var_out, cudaStream_t s) {
   if (dtype == TPP_BF16 && bm == 64 && bn % 32 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
-      reinterpret_cast<uintptr_t>(out) % 16 == 0) {
+      reinterpret_cast<uintptr_t>(out) % 16 == 0 && reinterpret_cast<uintptr_t>(gamma) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(beta) % 16 == 0) {
     const size_t smem = (size_t)32 * (m_b * 8 + 1) * 16 + 64 * sizeof(float);
     if (smem <= 227 * 1024) {
       const int blocks = n_b * (bn / 32);
@@ -243,7 +248,8 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
       cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_bf16_v,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_bf16_v)");
-      layernorm_blocked_bf16_v<<<blocks, 256, smem, s>>>(n_b, m_b, bn, (const uint4*)x, gamma, beta, eps,
+      layernorm_blocked_bf16_v<<<blocks, 256, smem, s>>>(n_b, m_b, bn, (const uint4*)x, (const float4*)gamma,
+                                                         (const float4*)beta, eps,
                                                          (uint4*)out, mean_out, var_out);
       TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_bf16_v");
       return TPP_OK;
