@@ -80,15 +80,20 @@ struct Params {
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
 };
 
-template <int BN, int STAGES, int KPS>
+// RES = 1: the B operand (conv weights, J = R*S*C_b tap blocks of BN x 64)
+// stays resident in smem for the whole kernel; stages then carry only A.
+constexpr int kResMaxBytes = 72 * 1024;
+
+template <int BN, int STAGES, int KPS, int RES = 0>
 struct Smem {
   static constexpr int A_BYTES = KPS * BM * BK * 2;
-  static constexpr int B_BYTES = KPS * BN * BK * 2;
+  static constexpr int B_BYTES = RES ? 0 : KPS * BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  // barriers: full[S], empty[S], tfull[2], tempty[2]; then tmem base + gelu table (float4 x 16)
-  static constexpr int TAB_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int RES_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = RES_OFF + (RES ? kResMaxBytes : 0);
+  // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base + gelu table (float4 x 16)
+  static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
   static constexpr int BIAS_OFF = TAB_OFF + 16 * 16;                      // float [2][256]
   static constexpr int STG_OFF = (BIAS_OFF + 2 * 256 * 4 + 1023) & ~1023;  // 8 warps x 2 KB
   static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 + 1024;
@@ -182,12 +187,12 @@ __device__ __forceinline__ float gelu4(float x, const float4* tab) {
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
 }
 
-template <int BN, int STAGES, int KPS>
+template <int BN, int STAGES, int KPS, int RES>
 __global__ void __launch_bounds__(kThreads, 1)
 brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                  const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const Params p) {
-  using S = Smem<BN, STAGES, KPS>;
+  using S = Smem<BN, STAGES, KPS, RES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -196,7 +201,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[0] = gtimer();
@@ -216,6 +222,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);
     }
+    mbar_init(bres, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, S::TMEM_COLS);
@@ -233,20 +240,39 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == 0) {
-    // ===================== TMA producer (one thread) =====================
+  if (warp == 0 || (RES && warp == 3)) {
+    // ===================== TMA producer(s) =====================
+    // RES kernels run two issuing threads (warps 0 and 3) on alternate
+    // stages: one thread's TMA issue rate cannot keep up with 128-cycle MMAs.
+    constexpr int NPROD = RES ? 2 : 1;
+    const int pid = warp == 0 ? 0 : 1;
     if (lane == 0) {
+      if (RES && pid == 0) {
+        // resident weights: every tap block once, on the bres barrier
+        const int J = p.kblocks;
+        mbar_arrive_expect_tx(bres, J * BN * BK * 2);
+        OpIter w;
+        w.start(p.fb, 0);
+        for (int j = 0; j < J; ++j) {
+          tma_load_5d(smem + S::RES_OFF + j * BN * BK * 2, &map_b, bres, w.c[0], w.c[1], w.c[2], w.c[3], w.c[4]);
+          w.next();
+        }
+      }
       int s = 0;
       uint32_t ph = 0;
+      uint32_t it = 0;
       FeedIter f;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         f.start(p, tile / p.tiles_n, tile % p.tiles_n);
-        for (int j = 0; j < nstages; ++j) {
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* sa = smem + s * S::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-          tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
-          tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
+        for (int j = 0; j < nstages; ++j, ++it) {
+          if (NPROD == 1 || (int)(it % NPROD) == pid) {
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* sa = smem + s * S::STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+            tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
+            if (!RES)
+              tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
+          }
           f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -263,6 +289,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       const uint32_t astep = p.a_mn ? (2048 >> 4) : (32 >> 4);
       const uint32_t bstep = p.b_mn ? (2048 >> 4) : (32 >> 4);
       const uint32_t asub = (uint32_t)p.fa.sub_bytes >> 4, bsub = (uint32_t)p.fb.sub_bytes >> 4;
+      // resident B: tap block j at RES_OFF + j * BN*128 (relative to bdesc0's A_BYTES = 0 base)
+      const uint64_t bres0 = sw128_kmajor_desc(smem_u32(smem + S::RES_OFF));
+      if (RES) mbar_wait(bres, 0);
       int s = 0;
       uint32_t ph = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
@@ -278,9 +307,10 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
 #pragma unroll
           for (int kb = 0; kb < KPS; ++kb) {
+            const uint64_t bd = RES ? bres0 + (uint64_t)((j * BN * BK * 2) >> 4) : bdesc0 + soff + bsub * kb;
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk)
-              umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bdesc0 + soff + bsub * kb + bstep * kk,
+              umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
                        idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&empty[s]);
@@ -467,14 +497,14 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
   return TPP_OK;
 }
 
-template <int BN, int STAGES, int KPS>
+template <int BN, int STAGES, int KPS, int RES = 0>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       const Params& p, cudaStream_t stream) {
-  using S = Smem<BN, STAGES, KPS>;
+  using S = Smem<BN, STAGES, KPS, RES>;
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES, KPS>,
+    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES, KPS, RES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
     attr_set = true;
@@ -491,7 +521,7 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, brgemm_tc_kernel<BN, STAGES, KPS>, ma, mb, mc, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, brgemm_tc_kernel<BN, STAGES, KPS, RES>, ma, mb, mc, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
   return TPP_OK;
@@ -515,6 +545,11 @@ static int launch(int bn_tile, int kps, const CUtensorMap& ma, const CUtensorMap
   } else if (kps == 4) {
     switch (bn_tile) {
       case 64: return launch_cfg<64, 2, 4>(ma, mb, mc, p, s);
+    }
+  } else if (kps == -1) {
+    // B resident (conv weights), A-only stages, two producers
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 8, 1, 1>(ma, mb, mc, p, s);
     }
   }
   return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
@@ -768,7 +803,8 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     if (rc) return rc;
   }
   p.tma_store = 0;
-  return launch(BN, 1, ma, mb, ma, p, stream);
+  const bool res = BN == 64 && p.tiles_n == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
+  return launch(BN, res ? -1 : 1, ma, mb, ma, p, stream);
 }
 
 }  // namespace tpp
