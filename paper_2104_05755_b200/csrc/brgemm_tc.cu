@@ -22,6 +22,7 @@
 //
 // The batch-reduce loop accumulates on chip: C is written exactly once.
 
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -77,16 +78,21 @@ struct Params {
   uint8_t* mask;        // ReLU bitmask written (TPP_FC_RELU_MASK)
   const uint8_t* mask_in;  // ReLU bitmask applied (RELU_INV, backward-data)
   unsigned long long* dbg;  // optional phase timestamps (CTA 0), tools only
+  int dbg_tile;
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
 };
 
 // RES = 1: the B operand (conv weights, J = R*S*C_b tap blocks of BN x 64)
 // stays resident in smem for the whole kernel; stages then carry only A.
+// RES = 2 (conv, halo): additionally each stage is ONE input halo of
+// kHaloRows input rows x 64 pixels (all R*S taps of one channel block read
+// it through row-shifted descriptors), instead of one A box per tap.
 constexpr int kResMaxBytes = 72 * 1024;
+constexpr int kHaloRows = 4;   // 2 output rows + R - 1 (R <= 3)
 
 template <int BN, int STAGES, int KPS, int RES = 0>
 struct Smem {
-  static constexpr int A_BYTES = KPS * BM * BK * 2;
+  static constexpr int A_BYTES = RES == 2 ? kHaloRows * 64 * BK * 2 : KPS * BM * BK * 2;
   static constexpr int B_BYTES = RES ? 0 : KPS * BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
@@ -209,7 +215,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_tiles = p.tiles_m * p.tiles_n;
-  const int nstages = p.kblocks / KPS;
+  // stages per tile; halo conv: one per channel block
+  const int nstages = RES == 2 ? p.cv_Cb : p.kblocks / KPS;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
@@ -240,11 +247,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == 0 || (RES && warp == 3)) {
+  if (warp == 0 || (RES == 1 && warp == 3)) {
     // ===================== TMA producer(s) =====================
     // RES kernels run two issuing threads (warps 0 and 3) on alternate
     // stages: one thread's TMA issue rate cannot keep up with 128-cycle MMAs.
-    constexpr int NPROD = RES ? 2 : 1;
+    constexpr int NPROD = RES == 1 ? 2 : 1;
     const int pid = warp == 0 ? 0 : 1;
     if (lane == 0) {
       if (RES && pid == 0) {
@@ -269,11 +276,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* sa = smem + s * S::STAGE_BYTES;
             mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-            tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
+            // halo conv: the input box at (cb = j) covering all taps
+            tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
             if (!RES)
               tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
           }
-          f.next();
+          if (RES != 2) f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -301,23 +309,39 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t tmem_d = tmem_base + as * BN;
         for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
-          if (p.dbg && blockIdx.x == 0 && tcount == 0 && j == 0) p.dbg[2] = gtimer();
+          if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile && j == 0) p.dbg[2] = gtimer();
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
+          if (RES == 2) {
+            // tap (r, s) of channel block j: A rows start at halo row r*64 + s
+            // (the 128B swizzle is address-based, so a row-shifted start is a
+            // valid K-major view); weights block (r*S + s)*C_b + j is resident
+            for (int rr = 0; rr < p.cv_R; ++rr) {
+              for (int ss = 0; ss < p.cv_S; ++ss) {
+                const uint64_t ad = adesc0 + soff + (uint64_t)(((rr * 64 + ss) * 128) >> 4);
+                const uint64_t bd = bres0 + (uint64_t)((((rr * p.cv_S + ss) * p.cv_Cb + j) * BN * BK * 2) >> 4);
 #pragma unroll
-          for (int kb = 0; kb < KPS; ++kb) {
-            const uint64_t bd = RES ? bres0 + (uint64_t)((j * BN * BK * 2) >> 4) : bdesc0 + soff + bsub * kb;
+                for (int kk = 0; kk < BK / 16; ++kk)
+                  umma_f16(tmem_d, ad + astep * kk, bd + bstep * kk, idesc,
+                           (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+          } else {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk)
-              umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
-                       idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+            for (int kb = 0; kb < KPS; ++kb) {
+              const uint64_t bd = RES ? bres0 + (uint64_t)((j * BN * BK * 2) >> 4) : bdesc0 + soff + bsub * kb;
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk)
+                umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
+                         idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&tfull[as]);
-        if (p.dbg && blockIdx.x == 0 && tcount == 0) p.dbg[3] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile) p.dbg[3] = gtimer();
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -347,21 +371,32 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         named_bar_sync(1, kEpiWarps * 32);
       }
       mbar_wait(&tfull[as], aph);
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[4] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[4] = gtimer();
       tc_fence_after();
       const int t = row_token(p, tm, r);
       const int nb = t >= 0 ? t / p.o_bn : 0;
       const int n_in = t >= 0 ? t % p.o_bn : 0;
-      // TMA store: the warp's 32 rows are 32 consecutive tokens of one token block
-      const int t0 = tm * BM + q * 32;
-      const bool warp_rows = p.tma_store && t0 < p.tokens;
+      // TMA store box of this warp: 32 rows x 32 features.  FC: 32 consecutive
+      // tokens of one token block; conv: 32 pixels of one output row.
+      int sc1, sc2, sc4;
+      bool warp_rows;
+      if (p.mode == FEED_FC) {
+        const int t0 = tm * BM + q * 32;
+        sc1 = 0; sc2 = t0 % p.o_bn; sc4 = t0 / p.o_bn;
+        warp_rows = p.tma_store && t0 < p.tokens;
+      } else {
+        const int img = tm / p.cv_tiles_per_img;
+        sc2 = 2 * (tm - img * p.cv_tiles_per_img) + (q >> 1);
+        sc1 = (q & 1) * 32; sc4 = img;
+        warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
+      }
 #pragma unroll 1
       for (int ch = 0; ch < CH; ++ch) {
         const int col = half * (BN / 2) + ch * 32;
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0 && ch == 0) p.dbg[7] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0) p.dbg[7] = gtimer();
         const int f0 = tn * BN + col;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
         const int mb = f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
@@ -411,11 +446,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 8; ++i)
             op[i] = make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]);
         } else if (p.tma_store) {
+          uint32_t w[16];
+          pack_bf16_ref_n<16>(x, w);
           uint4 val[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            val[i] = make_uint4(pack2_bf16_ref(x[8 * i], x[8 * i + 1]), pack2_bf16_ref(x[8 * i + 2], x[8 * i + 3]),
-                                pack2_bf16_ref(x[8 * i + 4], x[8 * i + 5]), pack2_bf16_ref(x[8 * i + 6], x[8 * i + 7]));
+          for (int i = 0; i < 4; ++i) val[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
           if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging rows
           __syncwarp();
           // row `lane`, 16-byte chunk c lands at chunk c ^ ((lane >> 1) & 3) (SWIZZLE_64B)
@@ -425,22 +460,22 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           fence_async_smem();
           __syncwarp();
           if (lane == 0 && warp_rows) {
-            tma_store_5d(&map_c, stg, m_in, 0, t0 % p.o_bn, mb, t0 / p.o_bn);
+            tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
             bulk_commit();
           }
         } else {
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
+          uint32_t w[16];
+          pack_bf16_ref_n<16>(x, w);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            op[i] = make_uint4(pack2_bf16_ref(x[8 * i], x[8 * i + 1]), pack2_bf16_ref(x[8 * i + 2], x[8 * i + 3]),
-                               pack2_bf16_ref(x[8 * i + 4], x[8 * i + 5]), pack2_bf16_ref(x[8 * i + 6], x[8 * i + 7]));
+          for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[8] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[8] = gtimer();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 0) p.dbg[5] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[5] = gtimer();
     }
     if (lane == 0 && p.tma_store) bulk_wait_all();
   }
@@ -550,6 +585,11 @@ static int launch(int bn_tile, int kps, const CUtensorMap& ma, const CUtensorMap
     // B resident (conv weights), A-only stages, two producers
     switch (bn_tile) {
       case 64: return launch_cfg<64, 8, 1, 1>(ma, mb, mc, p, s);
+    }
+  } else if (kps == -2) {
+    // B resident + one input halo per channel block (conv)
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 4, 1, 2>(ma, mb, mc, p, s);
     }
   }
   return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
@@ -696,6 +736,7 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   p.mask = reinterpret_cast<uint8_t*>(mask_out);
   p.mask_in = reinterpret_cast<const uint8_t*>(mask_in);
   p.dbg = g_dbg_ts;
+  p.dbg_tile = (g_dbg_ts && getenv("TPP_DBG_TILE")) ? atoi(getenv("TPP_DBG_TILE")) : 0;
   TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
               "tensor-core FC needs bn | 128 or 128 | bn");
   if (flavor == 0) {
@@ -787,12 +828,25 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   p.flags = 0;
   p.out = out;
 
-  CUtensorMap ma, mb;
+  const bool res = BN == 64 && p.tiles_n == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
+  // halo: one box of (2 + R - 1) input rows x 64 pixels per channel block
+  const bool halo = res && 2 + R - 1 <= tc::kHaloRows && W + S - 1 <= 64;
+  CUtensorMap ma, mb, mc;
   {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Cb, (uint64_t)N};
     const uint64_t str[4] = {128, (uint64_t)W * 128, (uint64_t)H * W * 128, (uint64_t)Cb * H * W * 128};
-    const uint32_t box[5] = {64, 64, 2, 1, 1};
+    const uint32_t box[5] = {64, 64, halo ? (uint32_t)tc::kHaloRows : 2u, 1, 1};
     int rc = make_map_5d(&ma, x, dims, str, box);
+    if (rc) return rc;
+  }
+  // output [N][K_b][H][W][64] through TMA stores: box 32 channels x 32 pixels
+  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  mc = ma;
+  if (p.tma_store) {
+    const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Kb, (uint64_t)N};
+    const uint64_t str[4] = {128, (uint64_t)W * 128, (uint64_t)H * W * 128, (uint64_t)Kb * H * W * 128};
+    const uint32_t box[5] = {32, 32, 1, 1, 1};
+    int rc = make_map_5d(&mc, out, dims, str, box, CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
   // weights: K-major rows [K_b][J = R*S*C_b][64 out][64 in]
@@ -802,9 +856,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
-  p.tma_store = 0;
-  const bool res = BN == 64 && p.tiles_n == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
-  return launch(BN, res ? -1 : 1, ma, mb, ma, p, stream);
+  return launch(BN, halo ? -2 : (res ? -1 : 1), ma, mb, mc, p, stream);
 }
 
 }  // namespace tpp

@@ -62,29 +62,51 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t b) {
 // fp32 -> bf16 RNE; NaN truncated with the quiet bit forced when the
 // surviving payload would be empty (dtypes.py:92-97).  CUDA's own
 // __float2bfloat16_rn canonicalises NaNs, so this is hand-written.
+// Written with selects only: a per-element branch costs ~20 cycles of
+// branch resolution on sm_100, more than the arithmetic.
 __device__ __forceinline__ uint16_t f32_to_bf16(float v) {
-  uint32_t u = __float_as_uint(v);
-  if ((u & 0x7FFFFFFFu) > 0x7F800000u) {  // NaN
-    uint16_t t = (uint16_t)(u >> 16);
-    return (t & 0x7F) == 0 ? (uint16_t)(t | 0x40) : t;
-  }
-  uint32_t lsb = (u >> 16) & 1u;
-  return (uint16_t)((u + 0x7FFFu + lsb) >> 16);
+  const uint32_t u = __float_as_uint(v);
+  const uint32_t t = u >> 16;
+  const uint32_t nan_bits = (t & 0x7Fu) == 0 ? (t | 0x40u) : t;
+  const uint32_t rne = (u + 0x7FFFu + (t & 1u)) >> 16;
+  return (uint16_t)((u & 0x7FFFFFFFu) > 0x7F800000u ? nan_bits : rne);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return (uint32_t)f32_to_bf16(lo) | ((uint32_t)f32_to_bf16(hi) << 16);
 }
 
-// Same result as pack_bf16x2, faster: hardware cvt.rn.bf16x2.f32 for numbers
-// (identical RNE incl. overflow to inf and subnormals), the reference's NaN
-// rule patched in for NaNs.
-__device__ __forceinline__ uint32_t pack2_bf16_ref(float lo, float hi) {
+// hardware cvt.rn.bf16x2.f32: identical RNE (incl. overflow to inf and
+// subnormals) for numbers; NaNs come out canonical (0x7FFF)
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
-  if (lo != lo) r = (r & 0xFFFF0000u) | f32_to_bf16(lo);
-  if (hi != hi) r = (r & 0x0000FFFFu) | ((uint32_t)f32_to_bf16(hi) << 16);
   return r;
+}
+
+// Same result as pack_bf16x2, faster: the hardware convert, with the
+// reference's NaN rule selected in for NaNs (branch-free).
+__device__ __forceinline__ uint32_t pack2_bf16_ref(float lo, float hi) {
+  const uint32_t r = cvt_bf16x2(lo, hi);
+  const uint32_t lo_nan = (r & 0xFFFF0000u) | f32_to_bf16(lo);
+  const uint32_t hi_nan = (r & 0x0000FFFFu) | ((uint32_t)f32_to_bf16(hi) << 16);
+  return lo != lo ? (hi != hi ? pack_bf16x2(lo, hi) : lo_nan) : (hi != hi ? hi_nan : r);
+}
+
+// N pairs x[2i], x[2i+1] -> out[i]: hardware converts plus ONE (rarely taken)
+// branch for the reference NaN rule, for the unrolled epilogues.
+template <int N>
+__device__ __forceinline__ void pack_bf16_ref_n(const float* x, uint32_t* out) {
+  bool nan = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    out[i] = cvt_bf16x2(x[2 * i], x[2 * i + 1]);
+    nan |= (x[2 * i] != x[2 * i]) | (x[2 * i + 1] != x[2 * i + 1]);
+  }
+  if (nan) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = pack_bf16x2(x[2 * i], x[2 * i + 1]);
+  }
 }
 
 // ---------------------------------------------------------------------------
