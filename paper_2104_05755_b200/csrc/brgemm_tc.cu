@@ -40,7 +40,8 @@ namespace tc {
 
 constexpr int BM = 128;          // tokens per tile (UMMA M, TMEM lanes)
 constexpr int BK = 64;           // bf16 per reduce block = one 128B swizzle row
-constexpr int kEpiWarps = 8;     // two warpgroups split the tile's columns
+constexpr int kEpiGroups = 3;    // epilogue warps per TMEM lane quarter (split the columns)
+constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
@@ -79,6 +80,7 @@ struct Params {
   const uint8_t* mask_in;  // ReLU bitmask applied (RELU_INV, backward-data)
   unsigned long long* dbg;  // optional phase timestamps (CTA 0), tools only
   int dbg_tile;
+  int dbg_mode;  // experiments: bit0 skip epilogue math, bit1 skip MMAs
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
 };
 
@@ -90,10 +92,15 @@ struct Params {
 constexpr int kResMaxBytes = 72 * 1024;
 constexpr int kHaloRows = 4;   // 2 output rows + R - 1 (R <= 3)
 
-template <int BN, int STAGES, int KPS, int RES = 0>
+// CG = 2: CTA pair (cluster of 2, tcgen05 cta_group::2).  The pair computes a
+// 256 x BN tile: each CTA stages its own 128 rows of A and HALF of the B rows
+// (BN/2), the leader issues M=256 MMAs that read both CTAs' smem and write
+// each CTA's TMEM.  Per-SM operand traffic (TMA ingest and the tensor core's
+// smem reads) drops by a quarter (BN=256: 48 KB -> 32 KB per 64-deep block).
+template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1>
 struct Smem {
   static constexpr int A_BYTES = RES == 2 ? kHaloRows * 64 * BK * 2 : KPS * BM * BK * 2;
-  static constexpr int B_BYTES = RES ? 0 : KPS * BN * BK * 2;
+  static constexpr int B_BYTES = RES ? 0 : KPS * (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int RES_OFF = STAGES * STAGE_BYTES;
@@ -181,24 +188,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-// GELU with the table as one float4 {c0,c1,c2,c3} per interval (one LDS.128)
-__device__ __forceinline__ float gelu4(float x, const float4* tab) {
-  const float ax = fabsf(x);
-  int idx = (int)(__float_as_uint(ax) >> 22) - kGeluBase;
-  idx = idx < 0 ? 0 : (idx > 15 ? 15 : idx);
-  const float4 c = tab[idx];
+__device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(saddr));
+  return v;
+}
+
+// GELU with the table as one float4 {c0,c1,c2,c3} per interval: one
+// ld.shared.v4 at tab_s (shared address) + 16 * clamp(exp-code - 244, 0, 15);
+// ~18 instructions per element (the epilogue's issue budget).
+__device__ __forceinline__ float gelu4(float x, uint32_t tab_s) {
+  const uint32_t xb = __float_as_uint(x);
+  const uint32_t ab = xb & 0x7FFFFFFFu;
+  const float ax = __uint_as_float(ab);
+  const uint32_t e = min(max(ab >> 22, (uint32_t)kGeluBase), (uint32_t)kGeluBase + 15u);
+  const float4 c = lds_f4(tab_s + ((e - kGeluBase) << 4));
   float h = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c.w, ax), c.z), ax), c.y), ax), c.x);
-  if (ax >= kGeluRangeMax) h = 1.0f;
-  h = copysignf(h, x);
+  h = ax >= kGeluRangeMax ? 1.0f : h;
+  h = __uint_as_float((__float_as_uint(h) & 0x7FFFFFFFu) | (xb & 0x80000000u));  // copysign(h, x)
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
 }
 
-template <int BN, int STAGES, int KPS, int RES>
+template <int BN, int STAGES, int KPS, int RES, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                  const __grid_constant__ CUtensorMap map_b,
                  const __grid_constant__ CUtensorMap map_c, const Params p) {
-  using S = Smem<BN, STAGES, KPS, RES>;
+  using S = Smem<BN, STAGES, KPS, RES, CG>;
+  constexpr bool PAIR = CG == 2;
+  static_assert(!PAIR || RES == 0, "CTA pairs stream both operands");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -214,7 +232,13 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[0] = gtimer();
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int num_tiles = p.tiles_m * p.tiles_n;
+  // pair mode: work items are 256-row pair tiles, one per cluster; this CTA
+  // owns row tile 2*tm + rank and B rows [rank*BN/2, (rank+1)*BN/2) of the tile
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int cl_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_cl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int num_tiles = (PAIR ? (p.tiles_m + 1) >> 1 : p.tiles_m) * p.tiles_n;
   // stages per tile; halo conv: one per channel block
   const int nstages = RES == 2 ? p.cv_Cb : p.kblocks / KPS;
 
@@ -227,17 +251,21 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], kEpiWarps * CG);
     }
     mbar_init(bres, 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  if (warp == 2) {
+    if (PAIR) tmem_alloc_pair(tmem_slot, S::TMEM_COLS);
+    else tmem_alloc(tmem_slot, S::TMEM_COLS);
+  }
   if (warp == 3 && lane < 16)
     gelu_tab[lane] = make_float4(__uint_as_float(c_gelu_bits[lane]), __uint_as_float(c_gelu_bits[16 + lane]),
                                  __uint_as_float(c_gelu_bits[32 + lane]), __uint_as_float(c_gelu_bits[48 + lane]));
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // the peer signals the leader's barriers
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[1] = gtimer();
@@ -269,17 +297,28 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       uint32_t ph = 0;
       uint32_t it = 0;
       FeedIter f;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        f.start(p, tile / p.tiles_n, tile % p.tiles_n);
+      // pair: completion bytes of both CTAs count on the leader's full[s]
+      const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
+      for (int tile = cl_id; tile < num_tiles; tile += n_cl) {
+        const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+        if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
+        else f.start(p, tm, tn);
         for (int j = 0; j < nstages; ++j, ++it) {
           if (NPROD == 1 || (int)(it % NPROD) == pid) {
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* sa = smem + s * S::STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-            // halo conv: the input box at (cb = j) covering all taps
-            tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
-            if (!RES)
-              tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
+            if (PAIR) {
+              if (leader) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
+              tma_load_5d_pair(sa, &map_a, full_cl + 8 * s, f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
+              tma_load_5d_pair(sa + S::A_BYTES, &map_b, full_cl + 8 * s, f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3],
+                               f.bi.c[4]);
+            } else {
+              mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+              // halo conv: the input box at (cb = j) covering all taps
+              tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
+              if (!RES)
+                tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
+            }
           }
           if (RES != 2) f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -287,9 +326,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(BM, BN, p.a_mn, p.b_mn);
+    // ===================== MMA issuer (one thread; pair: the leader's) =====================
+    if (lane == 0 && leader) {
+      const uint32_t idesc = idesc_bf16_f32(BM * CG, BN, p.a_mn, p.b_mn);
       // K-major: a 16-element K step is +32 B; MN-major: +2 K-groups (+2048 B)
       const uint64_t adesc0 = p.a_mn ? sw128_mnmajor_desc(smem_u32(smem), p.fa.lbo) : sw128_kmajor_desc(smem_u32(smem));
       const uint64_t bdesc0 = (p.b_mn ? sw128_mnmajor_desc(smem_u32(smem), p.fb.lbo) : sw128_kmajor_desc(smem_u32(smem))) +
@@ -302,7 +341,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (RES) mbar_wait(bres, 0);
       int s = 0;
       uint32_t ph = 0, tcount = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
+      for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
         const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         tc_fence_after();
@@ -310,6 +349,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
           if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile && j == 0) p.dbg[2] = gtimer();
+          if (p.dbg && blockIdx.x == 0 && tcount < 32 && j == 0) p.dbg[16 + 4 * tcount] = gtimer();
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
@@ -332,30 +372,39 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int kb = 0; kb < KPS; ++kb) {
               const uint64_t bd = RES ? bres0 + (uint64_t)((j * BN * BK * 2) >> 4) : bdesc0 + soff + bsub * kb;
 #pragma unroll
-              for (int kk = 0; kk < BK / 16; ++kk)
-                umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
-                         idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                if (p.dbg_mode & 2) continue;
+                if (PAIR)
+                  umma_f16_pair(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk, idesc,
+                                (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                else
+                  umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
+                           idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+              }
             }
           }
-          umma_commit(&empty[s]);
+          if (PAIR) umma_commit_pair(&empty[s], 3);
+          else umma_commit(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        umma_commit(&tfull[as]);
+        if (PAIR) umma_commit_pair(&tfull[as], 3);
+        else umma_commit(&tfull[as]);
         if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile) p.dbg[3] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && tcount < 32) p.dbg[17 + 4 * tcount] = gtimer();
       }
     }
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (8 warps) =====================
     const int ew = warp - kEpiWarp0;
     const int q = warp & 3;            // TMEM lane quarter this warp may access
-    const int half = ew >> 2;          // which half of the tile's columns
+    const int grp = ew >> 2;           // 32-column chunks grp, grp + kEpiGroups, ...
     const int r = q * 32 + lane;
-    constexpr int CH = BN / 64;        // 32-column chunks per half
     float* bias_s = reinterpret_cast<float*>(smem + S::BIAS_OFF);
     uint8_t* stg = smem + S::STG_OFF + ew * 2048;  // 32 rows x 64 B, 64B-swizzled
     uint32_t tcount = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tcount) {
-      const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+    for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
+      const int tn = tile % p.tiles_n;
+      const int tm = PAIR ? 2 * (tile / p.tiles_n) + (int)rank : tile / p.tiles_n;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       float* bs = bias_s + as * 256;
       if (p.flags & TPP_FC_BIAS) {
@@ -372,6 +421,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
       mbar_wait(&tfull[as], aph);
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[4] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[18 + 4 * tcount] = gtimer();
       tc_fence_after();
       const int t = row_token(p, tm, r);
       const int nb = t >= 0 ? t / p.o_bn : 0;
@@ -391,13 +441,15 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
       }
 #pragma unroll 1
-      for (int ch = 0; ch < CH; ++ch) {
-        const int col = half * (BN / 2) + ch * 32;
+      for (int ch = 0; grp + ch * kEpiGroups < BN / 32; ++ch) {
+        const int col = (grp + ch * kEpiGroups) * 32;
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0) p.dbg[7] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 0] = gtimer();
         const int f0 = tn * BN + col;
+        if (p.dbg_mode & 1) continue;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
         const int mb = f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
@@ -406,7 +458,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
         if (p.flags & TPP_FC_BIAS) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = __fadd_rn(x[i], bs[col + i]);
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b4 = lds_f4(smem_u32(bs + col + i));
+            x[i] = __fadd_rn(x[i], b4.x); x[i + 1] = __fadd_rn(x[i + 1], b4.y);
+            x[i + 2] = __fadd_rn(x[i + 2], b4.z); x[i + 3] = __fadd_rn(x[i + 3], b4.w);
+          }
         }
         if ((p.flags & TPP_FC_RELU_INV) && t >= 0) {
           // ops.py:367-369: where(mask, dy, 0) with the forward ReLU bitmask
@@ -425,8 +481,21 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 32; ++i) x[i] = relu_f(x[i]);
         } else if (p.act == TPP_ACT_GELU) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], gelu_tab);
+          if (!(p.dbg_mode & 4))
+            for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], smem_u32(gelu_tab));
+          if (p.dbg_mode & 4) {  // experiment: same arithmetic, one fixed interval (no table loads)
+            const float4 c = lds_f4(smem_u32(gelu_tab) + 16 * 7);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float ax = fabsf(x[i]);
+              float h = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c.w, ax), c.z), ax), c.y), ax), c.x);
+              h = ax >= kGeluRangeMax ? 1.0f : h;
+              h = copysignf(h, x[i]);
+              x[i] = __fmul_rn(__fmul_rn(0.5f, x[i]), __fadd_rn(1.0f, h));
+            }
+          }
         }
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 1] = gtimer();
         if ((p.flags & TPP_FC_RESIDUAL) && t >= 0) {
           const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
 #pragma unroll
@@ -448,6 +517,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         } else if (p.tma_store) {
           uint32_t w[16];
           pack_bf16_ref_n<16>(x, w);
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 2] = gtimer();
           uint4 val[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) val[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
@@ -462,6 +532,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           if (lane == 0 && warp_rows) {
             tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
             bulk_commit();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 3] = gtimer();
           }
         } else {
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
@@ -474,17 +545,23 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[8] = gtimer();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[as]);
+      if (lane == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+        else mbar_arrive(&tempty[as]);
+      }
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[5] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[19 + 4 * tcount] = gtimer();
     }
     if (lane == 0 && p.tma_store) bulk_wait_all();
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // neither CTA leaves while the pair still uses its smem / TMEM
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::TMEM_COLS);
+    if (PAIR) tmem_dealloc_pair(tmem_base, S::TMEM_COLS);
+    else tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 64) p.dbg[6] = gtimer();
 }
@@ -532,39 +609,76 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
   return TPP_OK;
 }
 
-template <int BN, int STAGES, int KPS, int RES = 0>
+template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       const Params& p, cudaStream_t stream) {
-  using S = Smem<BN, STAGES, KPS, RES>;
+  using S = Smem<BN, STAGES, KPS, RES, CG>;
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(brgemm_tc_kernel<BN, STAGES, KPS, RES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+  auto kern = brgemm_tc_kernel<BN, STAGES, KPS, RES, CG>;
+  static int max_clusters = -1;
+  if (max_clusters < 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
-    attr_set = true;
+    max_clusters = num_sms() / CG;
+    if (CG > 1) {
+      // co-resident pairs (SM pairs of one TPC) — a persistent grid must not exceed it
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(num_sms());
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = S::BYTES;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = CG; ca[0].val.clusterDim.y = 1; ca[0].val.clusterDim.z = 1;
+      q.attrs = ca;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0 && n < max_clusters) max_clusters = n;
+      cudaGetLastError();
+    }
   }
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * p.tiles_n;
+  const int grid = CG * (units < max_clusters ? units : max_clusters);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = S::BYTES;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, brgemm_tc_kernel<BN, STAGES, KPS, RES>, ma, mb, mc, p);
+  cfg.numAttrs = CG > 1 ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
   return TPP_OK;
 }
 
-// (tile width, reduce blocks per stage) -> instantiation; stages fill ~192 KB
-static int launch(int bn_tile, int kps, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+// (tile width, reduce blocks per stage, CTAs per MMA) -> instantiation; stages fill ~192 KB
+static int launch(int bn_tile, int kps, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                   const Params& p, cudaStream_t s) {
+  if (cg == 2) {
+    if (kps == 1) {
+      switch (bn_tile) {
+        case 64: return launch_cfg<64, 8, 1, 0, 2>(ma, mb, mc, p, s);
+        case 128: return launch_cfg<128, 8, 1, 0, 2>(ma, mb, mc, p, s);
+        case 256: return launch_cfg<256, 6, 1, 0, 2>(ma, mb, mc, p, s);
+      }
+    } else if (kps == 2) {
+      switch (bn_tile) {
+        case 64: return launch_cfg<64, 4, 2, 0, 2>(ma, mb, mc, p, s);
+        case 128: return launch_cfg<128, 4, 2, 0, 2>(ma, mb, mc, p, s);
+        case 256: return launch_cfg<256, 3, 2, 0, 2>(ma, mb, mc, p, s);
+      }
+    } else if (kps == 4) {
+      switch (bn_tile) {
+        case 64: return launch_cfg<64, 2, 4, 0, 2>(ma, mb, mc, p, s);
+      }
+    }
+    return fail(TPP_E_UNSUPPORTED, "no CTA-pair kernel instantiation for this tile width / stage depth");
+  }
   if (kps == 1) {
     switch (bn_tile) {
       case 64: return launch_cfg<64, 8, 1>(ma, mb, mc, p, s);
@@ -584,12 +698,12 @@ static int launch(int bn_tile, int kps, const CUtensorMap& ma, const CUtensorMap
   } else if (kps == -1) {
     // B resident (conv weights), A-only stages, two producers
     switch (bn_tile) {
-      case 64: return launch_cfg<64, 8, 1, 1>(ma, mb, mc, p, s);
+      case 64: return launch_cfg<64, 7, 1, 1>(ma, mb, mc, p, s);
     }
   } else if (kps == -2) {
     // B resident + one input halo per channel block (conv)
     switch (bn_tile) {
-      case 64: return launch_cfg<64, 4, 1, 2>(ma, mb, mc, p, s);
+      case 64: return launch_cfg<64, 3, 1, 2>(ma, mb, mc, p, s);
     }
   }
   return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
@@ -673,7 +787,7 @@ int pick_bn(int feats, int tiles_m, int pref) {
 }
 
 // reduce blocks per stage: as many as the smem budget of the tile allows
-int pick_kps(int BN, int kblocks, bool kmajor_ok) {
+int pick_kps(int BN, int kblocks, bool kmajor_ok, int cg) {
   if (!kmajor_ok) return 1;
   static const int forced = [] {
     const char* e = getenv("TPP_KPS");  // tuning experiments only
@@ -682,15 +796,30 @@ int pick_kps(int BN, int kblocks, bool kmajor_ok) {
   if (forced == 1 || forced == 2 || forced == 4) {
     if (kblocks % forced == 0 && !(forced == 4 && BN != 64)) return forced;
   }
-  // wide tiles are MMA-bound per stage already; keep their deeper pipeline
-  if (BN == 256) return 1;
+  // 1-CTA wide tiles: keep the deeper pipeline (48 KB per block already);
+  // pairs: 32 KB per block, two per TMA box halve the producer's issue count
+  if (BN == 256) return (cg == 2 && kblocks % 2 == 0) ? 2 : 1;
   if (BN == 64 && kblocks % 4 == 0) return 4;
   if (kblocks % 2 == 0) return 2;
   return 1;
 }
 
+// CTAs per MMA: pairs (cta_group::2) when there are row tiles to pair up and
+// each CTA's half of B is a whole swizzle atom for the operand's major-ness
+int pick_cg(int BN, int tiles_m, int tiles_n, bool b_mn) {
+  static const int forced = [] {
+    const char* e = getenv("TPP_CG");  // tuning experiments only
+    return e ? atoi(e) : 0;
+  }();
+  const bool ok = tiles_m >= 2 && (b_mn ? (BN / 2) % 64 == 0 : (BN / 2) % 32 == 0);
+  if (forced == 1 || !ok) return 1;
+  if (forced == 2) return 2;
+  // wide tiles with at least a full wave of pairs: halve per-SM operand traffic
+  return (BN == 256 && (int64_t)((tiles_m + 1) / 2) * tiles_n >= num_sms() / 2) ? 2 : 1;
+}
+
 int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* b_ptr, tc::Params p,
-             int BN, int kps, cudaStream_t stream) {
+             int BN, int kps, int cg, cudaStream_t stream) {
   CUtensorMap ma, mb, mc;
   int rc = tc::make_map_5d(&ma, a_ptr, A.dims, A.strides, A.box);
   if (rc) return rc;
@@ -712,7 +841,7 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   }
   p.fa = A.feed;
   p.fb = B.feed;
-  return tc::launch(BN, kps, ma, mb, mc, p, stream);
+  return tc::launch(BN, kps, cg, ma, mb, mc, p, stream);
 }
 
 }  // namespace
@@ -737,6 +866,7 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   p.mask_in = reinterpret_cast<const uint8_t*>(mask_in);
   p.dbg = g_dbg_ts;
   p.dbg_tile = (g_dbg_ts && getenv("TPP_DBG_TILE")) ? atoi(getenv("TPP_DBG_TILE")) : 0;
+  p.dbg_mode = getenv("TPP_DBG_MODE") ? atoi(getenv("TPP_DBG_MODE")) : 0;
   TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
               "tensor-core FC needs bn | 128 or 128 | bn");
   if (flavor == 0) {
@@ -747,12 +877,13 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     TPP_REQUIRE(feats % BN == 0 && ((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0)),
                 TPP_E_UNSUPPORTED, "features must tile by the tile width");
     const int kblocks = k_b * (bk / 64);
-    const int kps = pick_kps(BN, kblocks, bk == 64);
+    const int cg = pick_cg(BN, tiles_m, feats / BN, false);
+    const int kps = pick_kps(BN, kblocks, bk == 64, cg);
     p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
     p.o_bn = bn; p.o_bm = bm; p.o_mb = m_b;
-    return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM, kps), kmajor_operand(m_b, k_b, bm, bk, BN, kps), x_or_dy,
-                    w_packed, p, BN, kps, stream);
+    return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM, kps), kmajor_operand(m_b, k_b, bm, bk, BN / cg, kps),
+                    x_or_dy, w_packed, p, BN, kps, cg, stream);
   }
   if (flavor == 1) {
     // dx[n_b][k_b][bn][bk] = dy[n_b][m_b][bn][bm] . W ; B = W as MN-major over its bk
@@ -762,13 +893,14 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     const int BN = pick_bn(feats, tiles_m, d->block_n);
     TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
     const int kblocks = m_b * (bm / 64);
-    const int kps = pick_kps(BN, kblocks, bm == 64);
+    const int cg = pick_cg(BN, tiles_m, feats / BN, true);
+    const int kps = pick_kps(BN, kblocks, bm == 64, cg);
     p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
     p.o_bn = bn; p.o_bm = bk; p.o_mb = k_b;
     p.b_mn = 1;
-    return run_gemm(kmajor_operand(n_b, m_b, bn, bm, BM, kps), mnmajor_operand(m_b, k_b, bm, BN, kps), x_or_dy,
-                    w_packed, p, BN, kps, stream);
+    return run_gemm(kmajor_operand(n_b, m_b, bn, bm, BM, kps), mnmajor_operand(m_b, k_b, bm, BN / cg, kps), x_or_dy,
+                    w_packed, p, BN, kps, cg, stream);
   }
   // flavor 2: dW[m_b][k_b][bm][bk] = sum_t dy[t][f] x[t][c]
   TPP_REQUIRE(bm == 64 && bk == 64 && bn % 64 == 0, TPP_E_UNSUPPORTED,
@@ -778,14 +910,15 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   const int BN = pick_bn(feats, tiles_m, d->block_n);
   TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
   const int kblocks = n_b * (bn / 64);
-  int kps = pick_kps(BN, kblocks, true);
+  const int cg = pick_cg(BN, tiles_m, feats / BN, true);
+  int kps = pick_kps(BN, kblocks, true, cg);
   while (kps > 1 && bn != 64 && bn % (64 * kps) != 0) kps /= 2;  // a box must not skip token rows
   p.tokens = rows; p.kblocks = kblocks;
   p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
   p.o_bn = bm; p.o_bm = bk; p.o_mb = k_b;
   p.a_mn = 1; p.b_mn = 1;
-  return run_gemm(mnmajor_operand(n_b, m_b, bn, BM, kps), mnmajor_operand(n_b, k_b, bn, BN, kps), x_or_dy, x_for_dw,
-                  p, BN, kps, stream);
+  return run_gemm(mnmajor_operand(n_b, m_b, bn, BM, kps), mnmajor_operand(n_b, k_b, bn, BN / cg, kps), x_or_dy,
+                  x_for_dw, p, BN, kps, cg, stream);
 }
 
 int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, const void* bias,
@@ -809,6 +942,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   const int BN = feats >= 256 && feats % 256 == 0 ? 256 : (feats % 128 == 0 ? 128 : 64);
   Params p{};
   p.mode = FEED_CONV;
+  p.dbg = g_dbg_ts;
   p.kblocks = R * S * Cb;
   p.cv_P = P;
   p.cv_Q = Q;
@@ -856,7 +990,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
-  return launch(BN, halo ? -2 : (res ? -1 : 1), ma, mb, mc, p, stream);
+  return launch(BN, halo ? -2 : (res ? -1 : 1), 1, ma, mb, mc, p, stream);
 }
 
 }  // namespace tpp
