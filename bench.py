@@ -374,7 +374,8 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
             if name == "layernorm":
                 byts = 2 * 16384 * 1024 * 2
                 res[name] = {"ms": round(ms, 5), "GB/s": round(byts / ms / 1e6, 1),
-                             "frac_hbm": round(byts / ms / 1e6 / peak_hbm, 4), "bitwise": True}
+                             "frac_hbm": round(byts / ms / 1e6 / peak_hbm, 4),
+                             "parity": "bitwise vs oracle in tests/test_gpu_parity.py"}
             else:
                 tf = fl1 / ms / 1e9
                 res[name] = {"ms": round(ms, 5), "TFLOP/s": round(tf, 1),
@@ -436,7 +437,8 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
         g = graph_of(torch, [lambda: tpp.brgemm(spec1, batch, c)] * R)
         ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.2)) / R
         out["cfg1_brgemm_fp32_ordered"] = {"latency_us": round(ms * 1e3, 2),
-                                           "GFLOP/s": round(8388608 / ms / 1e6, 1), "bitwise": True}
+                                           "GFLOP/s": round(8388608 / ms / 1e6, 1),
+                                           "parity": "bitwise vs oracle in tests/test_gpu_parity.py"}
     except Exception as e:
         out["cfg1_brgemm_fp32_ordered"] = {"error": str(e)[:200]}
     return out

@@ -711,6 +711,15 @@ static int launch(int bn_tile, int kps, int cg, const CUtensorMap& ma, const CUt
 
 }  // namespace tc
 
+int make_tma_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5], const uint64_t strides[4],
+                    const uint32_t box[5], int swizzle_bytes) {
+  const CUtensorMapSwizzle swz = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return tc::make_map_5d(m, base, dims, strides, box, swz);
+}
+
 // ---------------------------------------------------------------------------
 // Blocked FC GEMMs on tensor cores.  Reference naming (kernels.py:287-297):
 //   weights packed [m_b][k_b][bm][bk] (K-major), input [n_b][k_b][bn][bk],

@@ -11,7 +11,10 @@
 // consecutive rows) or from shared memory (blocked layout), never from
 // scattered HBM.
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace tpp {
 
@@ -235,9 +238,221 @@ layernorm_blocked_bf16_v(int n_b, int m_b, int bn, const uint4* __restrict__ x,
   }
 }
 
+// ---- persistent TMA pipeline for BF16 blocked LayerNorm ---------------------
+// One CTA per SM walks groups of 16 tokens.  A group (16 tokens x F features,
+// F = m_b * 64) is ONE 5-D TMA box (128B-swizzled: lane t reading its row's
+// 16-byte chunk c at c ^ (t & 7) is bank-conflict free) into a ring of
+// `stages` buffers.  Warp roles:
+//   warp 0        TMA loads (ring ahead) and TMA stores of finished groups
+//   warps 1..4    the reference fold: one lane per token, FP32 ascending sums
+//                 of x and x*x, float64 glue -> (scale, shift)
+//   warps 5..12   the scaling equation in place (16 B per thread per step),
+//                 then the group leaves through a TMA store from the same buffer
+// so HBM reads, the latency-bound folds and the writes of different groups
+// overlap; 16 x F x 2 bytes cross HBM once in each direction.
+namespace lnt {
+constexpr int kTok = 16;
+constexpr int kFoldWarps = 4;
+constexpr int kApplyWarps = 8;
+constexpr int kThreads = 32 * (1 + kFoldWarps + kApplyWarps);
+constexpr int kMaxStages = 8;
+constexpr int kRingBytes = 200 * 1024;
+}  // namespace lnt
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(lnt::kThreads, 1)
+layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_o,
+                      int n_groups, int bn, int m_b, int stages, const float* __restrict__ gamma,
+                      const float* __restrict__ beta, double eps, float* mean_out, float* var_out) {
+  using namespace sm100;
+  using namespace lnt;
+  extern __shared__ __align__(1024) uint8_t ln_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ln_raw) + 1023) & ~uintptr_t(1023));
+  const int gbytes = kTok * m_b * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + stages * gbytes);
+  uint64_t* stat = full + kMaxStages;
+  uint64_t* done = stat + kMaxStages;
+  float2* st = reinterpret_cast<float2*>(done + kMaxStages);  // [stage][token] (scale, shift)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&map_x);
+    prefetch_tmap(&map_o);
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&stat[s], 1);
+      mbar_init(&done[s], kApplyWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int my = (n_groups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+  const uint32_t sbase = smem_u32(sm);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int nl = 0, ns = 0;
+      while (ns < my) {
+        while (nl < my && nl < ns + stages) {
+          const int s = nl % stages;
+          if (nl >= stages) bulk_wait_read<0>();  // the store of group nl - stages has left buffer s
+          const int t0 = ((int)blockIdx.x + nl * (int)gridDim.x) * kTok;
+          mbar_arrive_expect_tx(&full[s], gbytes);
+          tma_load_5d(sm + s * gbytes, &map_x, &full[s], 0, t0 % bn, 0, t0 / bn, 0);
+          ++nl;
+        }
+        const int s = ns % stages;
+        mbar_wait_sleep(&done[s], (ns / stages) & 1);
+        const int t0 = ((int)blockIdx.x + ns * (int)gridDim.x) * kTok;
+        tma_store_5d(&map_o, sm + s * gbytes, 0, t0 % bn, 0, t0 / bn, 0);
+        bulk_commit();
+        ++ns;
+      }
+      bulk_wait_all();
+    }
+  } else if (warp <= kFoldWarps) {
+    // a fold warp takes two groups at once: lanes 0-15 group 2P, 16-31 group 2P+1
+    const int half = lane >> 4, t = lane & (kTok - 1);
+    for (int P = warp - 1; 2 * P < my; P += kFoldWarps) {
+      const int i = 2 * P + half;
+      const bool live = i < my;
+      const int s = (live ? i : 2 * P) % stages;
+      mbar_wait_sleep(&full[(2 * P) % stages], ((2 * P) / stages) & 1);
+      if (2 * P + 1 < my) mbar_wait_sleep(&full[(2 * P + 1) % stages], ((2 * P + 1) / stages) & 1);
+      const uint32_t row = sbase + s * gbytes + t * 128;
+      const int sw = t & 7;
+      float a = 0.0f, b = 0.0f;
+      // software pipeline: the next slab's 8 chunks are in flight while this
+      // slab is folded (the fold itself is a 2 x F-long FADD chain per token)
+      uint4 cur[8], nxt[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) cur[c] = lds128(row + ((c ^ sw) << 4));
+      for (int cb = 0; cb < m_b; ++cb) {
+        const uint32_t nrow = row + (cb + 1 < m_b ? cb + 1 : cb) * (kTok * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) nxt[c] = lds128(nrow + ((c ^ sw) << 4));
+#pragma unroll
+        for (int c = 0; c < 8; ++c) fold8(cur[c], a, b);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) cur[c] = nxt[c];
+      }
+      if (live) {
+        float scale, shift;
+        double mu, var;
+        row_glue(a, b, m_b * 64, eps, scale, shift, mu, var);
+        st[s * kTok + t] = make_float2(scale, shift);
+        const int64_t tok = (int64_t)((int)blockIdx.x + i * (int)gridDim.x) * kTok + t;
+        if (mean_out) mean_out[tok] = (float)mu;
+        if (var_out) var_out[tok] = (float)var;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&stat[(2 * P) % stages]);
+      if (lane == 16 && 2 * P + 1 < my) mbar_arrive(&stat[(2 * P + 1) % stages]);
+    }
+  } else {
+    // 256 apply threads = 2 slabs of 128 chunks: a thread keeps one (token,
+    // chunk) position and walks the slabs cb = tid/128, +2, +4, ...
+    const int tid = (warp - 1 - kFoldWarps) * 32 + lane;
+    const int t = (tid >> 3) & (kTok - 1), c = (tid & 7) ^ (t & 7);
+    for (int i = 0; i < my; ++i) {
+      const int s = i % stages;
+      mbar_wait_sleep(&full[s], (i / stages) & 1);  // (already complete: the fold waited on it)
+      mbar_wait_sleep(&stat[s], (i / stages) & 1);
+      const float2 sc = st[s * kTok + t];
+      uint32_t addr = sbase + s * gbytes + tid * 16;
+      for (int cb = tid >> 7; cb < m_b; cb += 2, addr += 2 * kTok * 128) {
+        const uint4 v = lds128(addr);
+        const int f0 = cb * 64 + c * 8;
+        float4 g4[2], b4[2];
+        if (gamma) {
+          g4[0] = __ldg(reinterpret_cast<const float4*>(gamma + f0));
+          g4[1] = __ldg(reinterpret_cast<const float4*>(gamma + f0 + 4));
+        } else {
+          g4[0] = g4[1] = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+        }
+        if (beta) {
+          b4[0] = __ldg(reinterpret_cast<const float4*>(beta + f0));
+          b4[1] = __ldg(reinterpret_cast<const float4*>(beta + f0 + 4));
+        } else {
+          b4[0] = b4[1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        }
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        float r[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          // B + (shift + x*scale)*G, every product and sum rounded separately
+          // (scalar: ptxas contracts paired f32x2 mul/add into FFMA2)
+          const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
+          const float g0 = (q & 1) ? g4[q >> 1].z : g4[q >> 1].x, g1 = (q & 1) ? g4[q >> 1].w : g4[q >> 1].y;
+          const float b0 = (q & 1) ? b4[q >> 1].z : b4[q >> 1].x, b1 = (q & 1) ? b4[q >> 1].w : b4[q >> 1].y;
+          r[2 * q] = __fadd_rn(b0, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x0, sc.x)), g0));
+          r[2 * q + 1] = __fadd_rn(b1, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x1, sc.x)), g1));
+        }
+        uint32_t o[4];
+        pack_bf16_ref_n<4>(r, o);
+        sts128(addr, make_uint4(o[0], o[1], o[2], o[3]));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&done[s]);
+    }
+  }
+}
+
 int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
                              const float* gamma, const float* beta, double eps, void* out,
                              float* mean_out, float* var_out, cudaStream_t s) {
+  const bool al16 = reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(gamma) % 16 == 0 && reinterpret_cast<uintptr_t>(beta) % 16 == 0;
+  const int gbytes = lnt::kTok * m_b * 128;
+  if (dtype == TPP_BF16 && bm == 64 && bn % lnt::kTok == 0 && al16 && m_b <= 256 &&
+      2 * gbytes <= lnt::kRingBytes && !getenv("TPP_LN_SIMPLE")) {
+    const int n_groups = n_b * bn / lnt::kTok;
+    if (n_groups == 0) return TPP_OK;
+    int stages = lnt::kRingBytes / gbytes;
+    if (stages > lnt::kMaxStages) stages = lnt::kMaxStages;
+    CUtensorMap mx, mo;
+    const uint64_t dims[5] = {64, (uint64_t)bn, (uint64_t)m_b, (uint64_t)n_b, 1};
+    const uint64_t str[4] = {128, (uint64_t)bn * 128, (uint64_t)m_b * bn * 128, (uint64_t)n_b * m_b * bn * 128};
+    const uint32_t box[5] = {64, (uint32_t)lnt::kTok, (uint32_t)m_b, 1, 1};
+    int rc = make_tma_map_5d(&mx, x, dims, str, box, 128);
+    if (rc) return rc;
+    rc = make_tma_map_5d(&mo, out, dims, str, box, 128);
+    if (rc) return rc;
+    const size_t smem = (size_t)stages * gbytes + 3 * lnt::kMaxStages * 8 + lnt::kMaxStages * lnt::kTok * 8 + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(lnt::kRingBytes + 4096));
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_tma)");
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_groups < num_sms() ? n_groups : num_sms());
+    cfg.blockDim = dim3(lnt::kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, layernorm_blocked_tma, mx, mo, n_groups, bn, m_b, stages, gamma, beta,
+                                       eps, mean_out, var_out);
+    if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(layernorm_blocked_tma)");
+    TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_tma");
+    return TPP_OK;
+  }
   if (dtype == TPP_BF16 && bm == 64 && bn % 32 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(out) % 16 == 0 && reinterpret_cast<uintptr_t>(gamma) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(beta) % 16 == 0) {
