@@ -858,6 +858,7 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
 // flavor: 0 forward, 1 backward-data, 2 backward-weights
 static unsigned long long* g_dbg_ts = nullptr;
 void set_debug_timestamps(unsigned long long* p) { g_dbg_ts = p; }
+unsigned long long* debug_timestamps() { return g_dbg_ts; }
 
 int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
                const void* x_for_dw, const void* bias, const void* residual, void* out,

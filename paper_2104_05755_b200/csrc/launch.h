@@ -33,6 +33,7 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
                const void* x_for_dw, const void* bias, const void* residual, void* out,
                void* mask_out, const void* mask_in, cudaStream_t stream);
 void set_debug_timestamps(unsigned long long* p);
+unsigned long long* debug_timestamps();
 // bf16 5-D TMA map (dims innermost first, byte strides of dims 1..4)
 int make_tma_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5], const uint64_t strides[4],
                     const uint32_t box[5], int swizzle_bytes);

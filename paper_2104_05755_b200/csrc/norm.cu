@@ -250,15 +250,23 @@ layernorm_blocked_bf16_v(int n_b, int m_b, int bn, const uint4* __restrict__ x,
 //                 then the group leaves through a TMA store from the same buffer
 // so HBM reads, the latency-bound folds and the writes of different groups
 // overlap; 16 x F x 2 bytes cross HBM once in each direction.
+// waits sleep on the barrier (spin = 1: plain try_wait loop, for profiling tools)
+#define LN_WAIT(bar, par) ((spin & 1) ? mbar_wait((bar), (par)) : mbar_wait_sleep((bar), (par)))
 namespace lnt {
 constexpr int kTok = 16;
 constexpr int kFoldWarps = 4;
-constexpr int kApplyWarps = 8;
+constexpr int kApplyWarps = 16;
+constexpr int kApplySlabs = kApplyWarps * 32 / (kTok * 8);  // slabs covered per pass
 constexpr int kThreads = 32 * (1 + kFoldWarps + kApplyWarps);
 constexpr int kMaxStages = 8;
-constexpr int kRingBytes = 200 * 1024;
+constexpr int kRingBytes = 224 * 1024;  // 7 groups of 16 x 1024 bf16: a CTA's whole share of cfg 3
 }  // namespace lnt
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -272,7 +280,8 @@ __device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
 __global__ void __launch_bounds__(lnt::kThreads, 1)
 layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_o,
                       int n_groups, int bn, int m_b, int stages, const float* __restrict__ gamma,
-                      const float* __restrict__ beta, double eps, float* mean_out, float* var_out) {
+                      const float* __restrict__ beta, double eps, float* mean_out, float* var_out, int spin,
+                      unsigned long long* dbg) {
   using namespace sm100;
   using namespace lnt;
   extern __shared__ __align__(1024) uint8_t ln_raw[];
@@ -282,11 +291,16 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
   uint64_t* stat = full + kMaxStages;
   uint64_t* done = stat + kMaxStages;
   float2* st = reinterpret_cast<float2*>(done + kMaxStages);  // [stage][token] (scale, shift)
+  // seq[s] = group whose load was last issued into buffer s: a fold warp may
+  // run ahead of buffer reuse, and an mbarrier parity wait cannot tell phase
+  // u from phase u-2, so it first waits for its group's load to be issued
+  volatile int* seq = reinterpret_cast<volatile int*>(st + kMaxStages * kTok);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     prefetch_tmap(&map_x);
     prefetch_tmap(&map_o);
     for (int s = 0; s < stages; ++s) {
+      seq[s] = -1;
       mbar_init(&full[s], 1);
       mbar_init(&stat[s], 1);
       mbar_init(&done[s], kApplyWarps);
@@ -298,6 +312,8 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int my = (n_groups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const uint32_t sbase = smem_u32(sm);
+  if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[0] = globaltimer_ns();
+  if (dbg && threadIdx.x == 0) dbg[200 + 2 * blockIdx.x] = globaltimer_ns();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -307,18 +323,22 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
           const int s = nl % stages;
           if (nl >= stages) bulk_wait_read<0>();  // the store of group nl - stages has left buffer s
           const int t0 = ((int)blockIdx.x + nl * (int)gridDim.x) * kTok;
+          seq[s] = nl;
           mbar_arrive_expect_tx(&full[s], gbytes);
           tma_load_5d(sm + s * gbytes, &map_x, &full[s], 0, t0 % bn, 0, t0 / bn, 0);
+          if (dbg && blockIdx.x == 0 && (nl) < 16) dbg[8 + 5 * (nl) + 0] = globaltimer_ns();
           ++nl;
         }
         const int s = ns % stages;
-        mbar_wait_sleep(&done[s], (ns / stages) & 1);
+        LN_WAIT(&done[s], (ns / stages) & 1);
         const int t0 = ((int)blockIdx.x + ns * (int)gridDim.x) * kTok;
         tma_store_5d(&map_o, sm + s * gbytes, 0, t0 % bn, 0, t0 / bn, 0);
         bulk_commit();
+        if (dbg && blockIdx.x == 0 && (ns) < 16) dbg[8 + 5 * (ns) + 4] = globaltimer_ns();
         ++ns;
       }
       bulk_wait_all();
+      if (dbg) dbg[201 + 2 * blockIdx.x] = globaltimer_ns();
     }
   } else if (warp <= kFoldWarps) {
     // a fold warp takes two groups at once: lanes 0-15 group 2P, 16-31 group 2P+1
@@ -327,8 +347,11 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
       const int i = 2 * P + half;
       const bool live = i < my;
       const int s = (live ? i : 2 * P) % stages;
-      mbar_wait_sleep(&full[(2 * P) % stages], ((2 * P) / stages) & 1);
-      if (2 * P + 1 < my) mbar_wait_sleep(&full[(2 * P + 1) % stages], ((2 * P + 1) / stages) & 1);
+      for (int g = 2 * P; g < 2 * P + 2 && g < my; ++g) {
+        while (seq[g % stages] != g) __nanosleep(64);
+        LN_WAIT(&full[g % stages], (g / stages) & 1);
+      }
+      if (lane == 0) { if (dbg && blockIdx.x == 0 && (2 * P) < 16) dbg[8 + 5 * (2 * P) + 1] = globaltimer_ns(); }
       const uint32_t row = sbase + s * gbytes + t * 128;
       const int sw = t & 7;
       float a = 0.0f, b = 0.0f;
@@ -356,38 +379,46 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
         if (var_out) var_out[tok] = (float)var;
       }
       __syncwarp();
+      if (lane == 0) { if (dbg && blockIdx.x == 0 && (2 * P) < 16) dbg[8 + 5 * (2 * P) + 2] = globaltimer_ns(); }
       if (lane == 0) mbar_arrive(&stat[(2 * P) % stages]);
       if (lane == 16 && 2 * P + 1 < my) mbar_arrive(&stat[(2 * P + 1) % stages]);
     }
   } else {
-    // 256 apply threads = 2 slabs of 128 chunks: a thread keeps one (token,
-    // chunk) position and walks the slabs cb = tid/128, +2, +4, ...
+    // kApplyWarps*32 apply threads = kApplySlabs slabs of 128 chunks: a thread
+    // keeps one (token, chunk) position and walks the slabs tid/128 + k*kApplySlabs
     const int tid = (warp - 1 - kFoldWarps) * 32 + lane;
     const int t = (tid >> 3) & (kTok - 1), c = (tid & 7) ^ (t & 7);
     for (int i = 0; i < my; ++i) {
       const int s = i % stages;
-      mbar_wait_sleep(&full[s], (i / stages) & 1);  // (already complete: the fold waited on it)
-      mbar_wait_sleep(&stat[s], (i / stages) & 1);
+      LN_WAIT(&full[s], (i / stages) & 1);  // (already complete: the fold waited on it)
+      LN_WAIT(&stat[s], (i / stages) & 1);
       const float2 sc = st[s * kTok + t];
       uint32_t addr = sbase + s * gbytes + tid * 16;
-      for (int cb = tid >> 7; cb < m_b; cb += 2, addr += 2 * kTok * 128) {
-        const uint4 v = lds128(addr);
-        const int f0 = cb * 64 + c * 8;
+      // 4 chunks per step (slabs cb, cb+2, cb+4, cb+6): their shared-memory
+      // loads are in flight together
+      for (int cb0 = tid >> 7; cb0 < m_b; cb0 += 4 * kApplySlabs, addr += 4 * kApplySlabs * kTok * 128) {
+       uint4 vv[4];
+#pragma unroll
+       for (int u = 0; u < 4; ++u)
+         vv[u] = cb0 + kApplySlabs * u < m_b ? lds128(addr + u * kApplySlabs * kTok * 128) : make_uint4(0, 0, 0, 0);
+       float r[32];
+#pragma unroll
+       for (int u = 0; u < 4; ++u) {
+        const int f0 = (cb0 + kApplySlabs * u) * 64 + c * 8;
         float4 g4[2], b4[2];
-        if (gamma) {
+        if (gamma && cb0 + kApplySlabs * u < m_b) {
           g4[0] = __ldg(reinterpret_cast<const float4*>(gamma + f0));
           g4[1] = __ldg(reinterpret_cast<const float4*>(gamma + f0 + 4));
         } else {
           g4[0] = g4[1] = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
         }
-        if (beta) {
+        if (beta && cb0 + kApplySlabs * u < m_b) {
           b4[0] = __ldg(reinterpret_cast<const float4*>(beta + f0));
           b4[1] = __ldg(reinterpret_cast<const float4*>(beta + f0 + 4));
         } else {
           b4[0] = b4[1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         }
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-        float r[8];
+        const uint32_t w[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           // B + (shift + x*scale)*G, every product and sum rounded separately
@@ -395,16 +426,22 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
           const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
           const float g0 = (q & 1) ? g4[q >> 1].z : g4[q >> 1].x, g1 = (q & 1) ? g4[q >> 1].w : g4[q >> 1].y;
           const float b0 = (q & 1) ? b4[q >> 1].z : b4[q >> 1].x, b1 = (q & 1) ? b4[q >> 1].w : b4[q >> 1].y;
-          r[2 * q] = __fadd_rn(b0, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x0, sc.x)), g0));
-          r[2 * q + 1] = __fadd_rn(b1, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x1, sc.x)), g1));
+          r[8 * u + 2 * q] = __fadd_rn(b0, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x0, sc.x)), g0));
+          r[8 * u + 2 * q + 1] = __fadd_rn(b1, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x1, sc.x)), g1));
         }
-        uint32_t o[4];
-        pack_bf16_ref_n<4>(r, o);
-        sts128(addr, make_uint4(o[0], o[1], o[2], o[3]));
+       }
+       // one NaN check for the 32 results, then the 4 stores
+       uint32_t o[16];
+       pack_bf16_ref_n<16>(r, o);
+#pragma unroll
+       for (int u = 0; u < 4; ++u)
+         if (cb0 + kApplySlabs * u < m_b)
+           sts128(addr + u * kApplySlabs * kTok * 128, make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]));
       }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&done[s]);
+      if (lane == 0 && warp == 1 + kFoldWarps) { if (dbg && blockIdx.x == 0 && (i) < 16) dbg[8 + 5 * (i) + 3] = globaltimer_ns(); }
     }
   }
 }
@@ -429,11 +466,12 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     if (rc) return rc;
     rc = make_tma_map_5d(&mo, out, dims, str, box, 128);
     if (rc) return rc;
-    const size_t smem = (size_t)stages * gbytes + 3 * lnt::kMaxStages * 8 + lnt::kMaxStages * lnt::kTok * 8 + 1024;
+    const size_t smem = (size_t)stages * gbytes + 3 * lnt::kMaxStages * 8 + lnt::kMaxStages * lnt::kTok * 8 +
+                        lnt::kMaxStages * 4 + 1024;
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(lnt::kRingBytes + 4096));
+                                           (int)(lnt::kRingBytes + 3 * 1024));
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_tma)");
       attr = true;
     }
@@ -448,7 +486,8 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, layernorm_blocked_tma, mx, mo, n_groups, bn, m_b, stages, gamma, beta,
-                                       eps, mean_out, var_out);
+                                       eps, mean_out, var_out, getenv("TPP_LN_SPIN") ? atoi(getenv("TPP_LN_SPIN")) : 0,
+                                       debug_timestamps());
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(layernorm_blocked_tma)");
     TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_tma");
     return TPP_OK;
