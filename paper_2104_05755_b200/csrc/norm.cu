@@ -256,7 +256,9 @@ namespace lnt {
 constexpr int kTok = 16;
 constexpr int kFoldWarps = 4;
 constexpr int kApplyWarps = 16;
-constexpr int kApplySlabs = kApplyWarps * 32 / (kTok * 8);  // slabs covered per pass
+constexpr int kApplyTeams = 4;    // teams apply different groups concurrently
+constexpr int kTeamWarps = kApplyWarps / kApplyTeams;
+constexpr int kApplySlabs = kTeamWarps * 32 / (kTok * 8);  // slabs a team covers per pass
 constexpr int kThreads = 32 * (1 + kFoldWarps + kApplyWarps);
 constexpr int kMaxStages = 8;
 constexpr int kRingBytes = 224 * 1024;  // 7 groups of 16 x 1024 bf16: a CTA's whole share of cfg 3
@@ -303,13 +305,15 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
       seq[s] = -1;
       mbar_init(&full[s], 1);
       mbar_init(&stat[s], 1);
-      mbar_init(&done[s], kApplyWarps);
+      mbar_init(&done[s], kTeamWarps);
     }
     fence_mbar_init();
   }
   __syncthreads();
+  const unsigned long long t_resident = dbg ? globaltimer_ns() : 0;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (dbg && threadIdx.x == 0) dbg[500 + blockIdx.x % 64] = t_resident;
   const int my = (n_groups - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
   const uint32_t sbase = smem_u32(sm);
   if (dbg && blockIdx.x == 0 && threadIdx.x == 0) dbg[0] = globaltimer_ns();
@@ -384,11 +388,14 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
       if (lane == 16 && 2 * P + 1 < my) mbar_arrive(&stat[(2 * P + 1) % stages]);
     }
   } else {
-    // kApplyWarps*32 apply threads = kApplySlabs slabs of 128 chunks: a thread
-    // keeps one (token, chunk) position and walks the slabs tid/128 + k*kApplySlabs
-    const int tid = (warp - 1 - kFoldWarps) * 32 + lane;
+    // team = kTeamWarps warps = kApplySlabs slabs of 128 chunks: a thread keeps
+    // one (token, chunk) position and walks the slabs tid/128 + k*kApplySlabs;
+    // team j takes groups j, j + kApplyTeams, ... so per-group waits overlap
+    const int aw = warp - 1 - kFoldWarps;
+    const int team = aw / kTeamWarps;
+    const int tid = (aw % kTeamWarps) * 32 + lane;
     const int t = (tid >> 3) & (kTok - 1), c = (tid & 7) ^ (t & 7);
-    for (int i = 0; i < my; ++i) {
+    for (int i = team; i < my; i += kApplyTeams) {
       const int s = i % stages;
       LN_WAIT(&full[s], (i / stages) & 1);  // (already complete: the fold waited on it)
       LN_WAIT(&stat[s], (i / stages) & 1);
@@ -441,7 +448,7 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&done[s]);
-      if (lane == 0 && warp == 1 + kFoldWarps) { if (dbg && blockIdx.x == 0 && (i) < 16) dbg[8 + 5 * (i) + 3] = globaltimer_ns(); }
+      if (lane == 0 && aw % kTeamWarps == 0) { if (dbg && blockIdx.x == 0 && (i) < 16) dbg[8 + 5 * (i) + 3] = globaltimer_ns(); }
     }
   }
 }

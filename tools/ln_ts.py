@@ -32,3 +32,5 @@ for it in range(2):
     import statistics as S
     print(f"  CTA start min/med/max {min(st):.2f}/{S.median(st):.2f}/{max(st):.2f}  end min/med/max {min(en):.2f}/{S.median(en):.2f}/{max(en):.2f}")
     print("  latest CTAs:", sorted(range(148), key=lambda b: -en[b])[:8], [round(en[b], 2) for b in sorted(range(148), key=lambda b: -en[b])[:8]])
+    res = [(t[500 + b] - t[0]) / 1e3 for b in range(64)]
+    print(f"  CTA resident (before griddepcontrol.wait) min/med/max {min(res):.2f}/{S.median(res):.2f}/{max(res):.2f}")
