@@ -13,6 +13,9 @@
 // TN accumulation chains are independent, which is the ILP this kernel has
 // (the per-element chain itself is inherently serial — that is the order).
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace tpp {
@@ -121,8 +124,175 @@ brgemm_ordered_kernel(OrderedParams p) {
   }
 }
 
+// Shared-memory variant: a CTA owns a TM x TN tile of C (one element per
+// thread) and stages the tile's A rows and B columns of a chunk of batch
+// entries in shared memory, so the serial per-element chain reads operands
+// at shared-memory latency instead of waiting on L2 every step.  Same order,
+// same bits as brgemm_ordered_kernel.
+constexpr int kOTM = 16, kOTN = 8;  // 128 threads
+
+template <typename TIn>
+__device__ __forceinline__ const TIn* batch_a(const OrderedParams& p, int64_t inst, int64_t i) {
+  if (p.mode == 0) return reinterpret_cast<const TIn*>(p.a) + inst * p.inst_a + i * p.stride_a;
+  if (p.mode == 1) return reinterpret_cast<const TIn*>(p.a) + p.a_offs[i];
+  return reinterpret_cast<const TIn*>(p.a_ptrs[i]);
+}
+template <typename TIn>
+__device__ __forceinline__ const TIn* batch_b(const OrderedParams& p, int64_t inst, int64_t i) {
+  if (p.mode == 0) return reinterpret_cast<const TIn*>(p.b) + inst * p.inst_b + i * p.stride_b;
+  if (p.mode == 1) return reinterpret_cast<const TIn*>(p.b) + p.b_offs[i];
+  return reinterpret_cast<const TIn*>(p.b_ptrs[i]);
+}
+
+template <typename TIn>
+__device__ __forceinline__ void stage_elem(TIn* dst, const TIn* src) {
+  if constexpr (sizeof(TIn) == 4 || sizeof(TIn) == 8) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "n"((int)sizeof(TIn))
+                 : "memory");
+  } else {
+    *dst = __ldg(src);
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// KC: compile-time reduce length (64 = the paper's blocks; 0 = runtime p.k).
+// fast: FP32, plain layouts, 16-byte aligned rows/columns, full tile ->
+// 16-byte cp.async staging.
+template <typename TIn, typename TAcc, int KC>
+__global__ void __launch_bounds__(kOTM * kOTN)
+brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long* dbg) {
+  using A = Arith<TAcc>;
+  using W = Widen<TIn, TAcc>;
+  const int K = KC ? KC : p.k;
+  extern __shared__ __align__(16) unsigned char osm[];
+  TIn* As = reinterpret_cast<TIn*>(osm);            // [nb][K][kOTM]  (rows contiguous)
+  TIn* Bs = As + (size_t)nb * K * kOTM;             // [nb][kOTN][K]  (columns contiguous)
+  const int tiles_m = (p.m + kOTM - 1) / kOTM;
+  const int m0 = (blockIdx.x % tiles_m) * kOTM, n0 = (blockIdx.x / tiles_m) * kOTN;
+  const int tid = threadIdx.x, r = tid % kOTM, cidx = tid / kOTM;
+  const int mi = m0 + r, ni = n0 + cidx;
+  const bool live = mi < p.m && ni < p.n;
+  constexpr int nthr = kOTM * kOTN;
+  auto gt = [] { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
+  if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[0] = gt();
+  for (int64_t inst = blockIdx.y; inst < p.instances; inst += gridDim.y) {
+    TAcc* c = reinterpret_cast<TAcc*>(p.c) + inst * p.inst_c;
+    TAcc acc = TAcc(0);
+    if (live) {
+      if (p.beta == 0.0) acc = TAcc(0);
+      else if (p.beta == 1.0) acc = c[mi + (int64_t)ni * p.ldc];
+      else acc = A::mul(c[mi + (int64_t)ni * p.ldc], A::beta(p.beta));
+    }
+    for (int64_t i0 = 0; i0 < p.count; i0 += nb) {
+      const int cnt = (int)min((int64_t)nb, p.count - i0);
+      __syncthreads();  // previous chunk fully consumed
+      // stage the chunk's A rows [m0, m0+kOTM) and B columns [n0, n0+kOTN)
+      for (int bi = 0; bi < cnt; ++bi) {
+        const TIn* ab = batch_a<TIn>(p, inst, i0 + bi);
+        const TIn* bb = batch_b<TIn>(p, inst, i0 + bi);
+        TIn* as = As + (size_t)bi * K * kOTM;
+        TIn* bs = Bs + (size_t)bi * K * kOTN;
+        if (fast) {
+          // 16-byte copies: A row segments (4 per k), B column segments (K/4 per column)
+          for (int j = tid; j < K * (kOTM / 4); j += nthr) {
+            const int kk = j / (kOTM / 4), q = j % (kOTM / 4);
+            cp_async16(as + kk * kOTM + q * 4, ab + m0 + q * 4 + (int64_t)kk * p.lda);
+          }
+          for (int j = tid; j < kOTN * (K / 4); j += nthr) {
+            const int cc = j / (K / 4), q = j % (K / 4);
+            cp_async16(bs + cc * K + q * 4, bb + q * 4 + (int64_t)(n0 + cc) * p.ldb);
+          }
+        } else {
+          const int rr = tid % kOTM, m = m0 + rr;
+#pragma unroll 4
+          for (int kk = tid / kOTM; kk < K; kk += nthr / kOTM) {
+            TIn* dst = as + kk * kOTM + rr;
+            if (m < p.m) {
+              const TIn* src = p.vnni ? ab + (int64_t)(kk / p.alpha) * p.m * p.alpha + (int64_t)m * p.alpha + (kk % p.alpha)
+                                      : ab + m + (int64_t)kk * p.lda;
+              stage_elem(dst, src);
+            } else {
+              *dst = TIn(0);
+            }
+          }
+#pragma unroll 4
+          for (int e = tid; e < kOTN * K; e += nthr) {
+            const int cc = e / K, kk = e - cc * K, n = n0 + cc;
+            TIn* dst = bs + cc * K + kk;
+            if (n < p.n) stage_elem(dst, bb + kk + (int64_t)n * p.ldb);
+            else *dst = TIn(0);
+          }
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[1] = gt();
+      for (int bi = 0; bi < cnt; ++bi) {
+        const TIn* a = As + (size_t)bi * K * kOTM + r;
+        const TIn* b = Bs + (size_t)bi * K * kOTN + cidx * K;
+        TAcc part = TAcc(0);
+        if (KC) {
+          // the whole 64-long chain unrolled: every operand load is issued
+          // ahead of the dependent adds
+          TAcc av[KC > 0 ? KC : 1], bv[KC > 0 ? KC : 1];
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) { av[kk] = W::w(a[kk * kOTM]); bv[kk] = W::w(b[kk]); }
+#pragma unroll
+          for (int kk = 0; kk < KC; ++kk) part = A::add(part, A::mul(av[kk], bv[kk]));
+        } else {
+#pragma unroll 8
+          for (int kk = 0; kk < K; ++kk) part = A::add(part, A::mul(W::w(a[kk * kOTM]), W::w(b[kk])));
+        }
+        acc = A::add(acc, part);
+      }
+    }
+    if (live) c[mi + (int64_t)ni * p.ldc] = acc;
+    if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[2] = gt();
+  }
+}
+
+template <typename TIn, typename TAcc, int KC>
+static int launch_smem_kc(const OrderedParams& p, cudaStream_t s, int nb, int fast, size_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(brgemm_ordered_smem_kernel<TIn, TAcc, KC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_ordered_smem)");
+    attr = true;
+  }
+  const int tiles = ((p.m + kOTM - 1) / kOTM) * ((p.n + kOTN - 1) / kOTN);
+  dim3 grid((unsigned)tiles, (unsigned)(p.instances < 65535 ? p.instances : 65535));
+  brgemm_ordered_smem_kernel<TIn, TAcc, KC><<<grid, kOTM * kOTN, smem, s>>>(p, nb, fast, debug_timestamps());
+  TPP_CUDA_LAUNCH_CHECK("brgemm_ordered_smem_kernel");
+  return TPP_OK;
+}
+
+template <typename TIn, typename TAcc>
+static int launch_smem_t(const OrderedParams& p, cudaStream_t s, int nb, size_t smem) {
+  // 16-byte staging: FP32 plain layouts, whole tiles, every row / column
+  // segment 16-byte aligned (stride batches only: offsets live on the device)
+  const bool fast = sizeof(TIn) == 4 && std::is_same<TIn, TAcc>::value && !p.vnni && p.mode == 0 &&
+                    p.m % kOTM == 0 && p.n % kOTN == 0 && p.k % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 &&
+                    p.stride_a % 4 == 0 && p.stride_b % 4 == 0 && p.inst_a % 4 == 0 && p.inst_b % 4 == 0 &&
+                    reinterpret_cast<uintptr_t>(p.a) % 16 == 0 && reinterpret_cast<uintptr_t>(p.b) % 16 == 0;
+  if (p.k == 64) return launch_smem_kc<TIn, TAcc, 64>(p, s, nb, fast ? 1 : 0, smem);
+  return launch_smem_kc<TIn, TAcc, 0>(p, s, nb, fast ? 1 : 0, smem);
+}
+
 template <typename TIn, typename TAcc>
 static int launch_t(const OrderedParams& p, cudaStream_t s) {
+  // staged variant: chunks of up to nb batch entries (<= 96 KB of operands)
+  if (p.k > 0 && p.count > 0 && !getenv("TPP_ORDERED_GLOBAL")) {
+    const size_t per = (size_t)p.k * (kOTM + kOTN) * sizeof(TIn);
+    int64_t nb = (int64_t)(96 * 1024) / (int64_t)per;
+    if (nb > p.count) nb = p.count;
+    if (nb >= 1) return launch_smem_t<TIn, TAcc>(p, s, (int)nb, (size_t)nb * per);
+  }
   constexpr int TN = 4;
   const int ncg = (p.n + TN - 1) / TN;
   const int64_t elems = (int64_t)p.m * ncg;

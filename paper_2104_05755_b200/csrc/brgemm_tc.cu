@@ -40,7 +40,7 @@ namespace tc {
 
 constexpr int BM = 128;          // tokens per tile (UMMA M, TMEM lanes)
 constexpr int BK = 64;           // bf16 per reduce block = one 128B swizzle row
-constexpr int kEpiGroups = 3;    // epilogue warps per TMEM lane quarter (split the columns)
+constexpr int kEpiGroups = 2;    // epilogue warps per TMEM lane quarter (split the columns)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
