@@ -481,19 +481,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 32; ++i) x[i] = relu_f(x[i]);
         } else if (p.act == TPP_ACT_GELU) {
 #pragma unroll
-          if (!(p.dbg_mode & 4))
-            for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], smem_u32(gelu_tab));
-          if (p.dbg_mode & 4) {  // experiment: same arithmetic, one fixed interval (no table loads)
-            const float4 c = lds_f4(smem_u32(gelu_tab) + 16 * 7);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float ax = fabsf(x[i]);
-              float h = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c.w, ax), c.z), ax), c.y), ax), c.x);
-              h = ax >= kGeluRangeMax ? 1.0f : h;
-              h = copysignf(h, x[i]);
-              x[i] = __fmul_rn(__fmul_rn(0.5f, x[i]), __fadd_rn(1.0f, h));
-            }
-          }
+          for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], smem_u32(gelu_tab));
         }
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 1] = gtimer();
         if ((p.flags & TPP_FC_RESIDUAL) && t >= 0) {
@@ -836,7 +824,8 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   if (rc) return rc;
   // BF16 outputs leave through smem staging + TMA stores: output tensor
   // [ntb][o_mb][o_bn][o_bm], box = 32 tokens x 32 features, 64B swizzle
-  p.tma_store = !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
+  static const bool no_tma_store = getenv("TPP_NO_TMA_STORE") != nullptr;  // experiments
+  p.tma_store = !no_tma_store && !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
                 reinterpret_cast<uintptr_t>(p.out) % 16 == 0;
   mc = ma;
   if (p.tma_store) {
