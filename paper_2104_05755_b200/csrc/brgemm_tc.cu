@@ -108,8 +108,12 @@ struct Smem {
   // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base + gelu table (float4 x 16)
   static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
   static constexpr int BIAS_OFF = TAB_OFF + 16 * 16;                      // float [2][256]
-  static constexpr int STG_OFF = (BIAS_OFF + 2 * 256 * 4 + 1023) & ~1023;  // 8 warps x 2 KB
-  static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 + 1024;
+  // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
+  // when the smem budget allows (a chunk's store need not have left the
+  // buffer before the next chunk is staged)
+  static constexpr int STG_OFF = (BIAS_OFF + 2 * 256 * 4 + 1023) & ~1023;
+  static constexpr int STG_BUFS = STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1;
+  static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 * STG_BUFS + 1024;
 };
 
 // Register-resident (all indexing resolved at compile time: a dynamically
@@ -327,7 +331,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread; pair: the leader's) =====================
-    if (lane == 0 && leader) {
+    if (leader) {  // the whole warp runs the loop (uniform descriptors); one lane issues
       const uint32_t idesc = idesc_bf16_f32(BM * CG, BN, p.a_mn, p.b_mn);
       // K-major: a 16-element K step is +32 B; MN-major: +2 K-groups (+2048 B)
       const uint64_t adesc0 = p.a_mn ? sw128_mnmajor_desc(smem_u32(smem), p.fa.lbo) : sw128_kmajor_desc(smem_u32(smem));
@@ -348,8 +352,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t tmem_d = tmem_base + as * BN;
         for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
-          if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile && j == 0) p.dbg[2] = gtimer();
-          if (p.dbg && blockIdx.x == 0 && tcount < 32 && j == 0) p.dbg[16 + 4 * tcount] = gtimer();
+          if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0) p.dbg[2] = gtimer();
+          if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount < 32 && j == 0) p.dbg[16 + 4 * tcount] = gtimer();
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
@@ -357,14 +361,30 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             // tap (r, s) of channel block j: A rows start at halo row r*64 + s
             // (the 128B swizzle is address-based, so a row-shifted start is a
             // valid K-major view); weights block (r*S + s)*C_b + j is resident
-            for (int rr = 0; rr < p.cv_R; ++rr) {
-              for (int ss = 0; ss < p.cv_S; ++ss) {
-                const uint64_t ad = adesc0 + soff + (uint64_t)(((rr * 64 + ss) * 128) >> 4);
-                const uint64_t bd = bres0 + (uint64_t)((((rr * p.cv_S + ss) * p.cv_Cb + j) * BN * BK * 2) >> 4);
+            const uint64_t a0 = adesc0 + soff;
+            const uint64_t b0 = bres0 + (uint64_t)((j * BN * BK * 2) >> 4);
+            const uint64_t btap = (uint64_t)((p.cv_Cb * BN * BK * 2) >> 4);
+            if (p.cv_R == 3 && p.cv_S == 3) {
+              // 3x3: every descriptor offset is an immediate (the single
+              // issuing thread must keep pace with 48-cycle N=64 MMAs)
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap) {
+                const uint64_t ad = a0 + (uint64_t)((((tap / 3) * 64 + tap % 3) * 128) >> 4);
+                const uint64_t bd = b0 + btap * tap;
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
-                  umma_f16(tmem_d, ad + astep * kk, bd + bstep * kk, idesc,
-                           (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+                  if (!(p.dbg_mode & 2))
+                    umma_f16_warp(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (j > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+              }
+            } else {
+              for (int rr = 0; rr < p.cv_R; ++rr) {
+                for (int ss = 0; ss < p.cv_S; ++ss) {
+                  const uint64_t ad = a0 + (uint64_t)(((rr * 64 + ss) * 128) >> 4);
+                  const uint64_t bd = b0 + btap * (rr * p.cv_S + ss);
+#pragma unroll
+                  for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_f16_warp(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+                }
               }
             }
           } else {
@@ -375,22 +395,22 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               for (int kk = 0; kk < BK / 16; ++kk) {
                 if (p.dbg_mode & 2) continue;
                 if (PAIR)
-                  umma_f16_pair(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk, idesc,
+                  umma_f16_pair_warp(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk, idesc,
                                 (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
                 else
-                  umma_f16(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
+                  umma_f16_warp(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
                            idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
               }
             }
           }
-          if (PAIR) umma_commit_pair(&empty[s], 3);
-          else umma_commit(&empty[s]);
+          if (PAIR) umma_commit_pair_warp(&empty[s], 3);
+          else umma_commit_warp(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
-        if (PAIR) umma_commit_pair(&tfull[as], 3);
-        else umma_commit(&tfull[as]);
-        if (p.dbg && blockIdx.x == 0 && tcount == p.dbg_tile) p.dbg[3] = gtimer();
-        if (p.dbg && blockIdx.x == 0 && tcount < 32) p.dbg[17 + 4 * tcount] = gtimer();
+        if (PAIR) umma_commit_pair_warp(&tfull[as], 3);
+        else umma_commit_warp(&tfull[as]);
+        if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile) p.dbg[3] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount < 32) p.dbg[17 + 4 * tcount] = gtimer();
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -400,7 +420,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const int grp = ew >> 2;           // 32-column chunks grp, grp + kEpiGroups, ...
     const int r = q * 32 + lane;
     float* bias_s = reinterpret_cast<float*>(smem + S::BIAS_OFF);
-    uint8_t* stg = smem + S::STG_OFF + ew * 2048;  // 32 rows x 64 B, 64B-swizzled
+    uint8_t* stg0 = smem + S::STG_OFF + ew * 2048 * S::STG_BUFS;  // 32 rows x 64 B, 64B-swizzled
+    uint32_t nstore = 0;
     uint32_t tcount = 0;
     for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
       const int tn = tile % p.tiles_n;
@@ -423,9 +444,19 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[4] = gtimer();
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[18 + 4 * tcount] = gtimer();
       tc_fence_after();
-      const int t = row_token(p, tm, r);
-      const int nb = t >= 0 ? t / p.o_bn : 0;
-      const int n_in = t >= 0 ? t % p.o_bn : 0;
+      // first chunk's TMEM load goes out before any index arithmetic
+      const int nch = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
+      uint32_t v[32];
+      if (nch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + grp * 32, v);
+      // token coordinates only for the paths that address rows themselves
+      const bool need_rows = !p.tma_store || (p.flags & (TPP_FC_RELU_INV | TPP_FC_RESIDUAL | TPP_FC_OUT_FP32)) ||
+                             (p.act == TPP_ACT_RELU && (p.flags & TPP_FC_RELU_MASK));
+      int t = 0, nb = 0, n_in = 0;
+      if (need_rows) {
+        t = row_token(p, tm, r);
+        nb = t >= 0 ? t / p.o_bn : 0;
+        n_in = t >= 0 ? t % p.o_bn : 0;
+      }
       // TMA store box of this warp: 32 rows x 32 features.  FC: 32 consecutive
       // tokens of one token block; conv: 32 pixels of one output row.
       int sc1, sc2, sc4;
@@ -440,18 +471,30 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         sc1 = (q & 1) * 32; sc4 = img;
         warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
       }
+      // release this warp's share of the accumulator as soon as its last
+      // chunk is in registers, so the next tile's MMAs can start while the
+      // math and stores of this one proceed
+      auto release = [&] {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
+          else mbar_arrive(&tempty[as]);
+        }
+      };
+      if (nch <= 0) release();
 #pragma unroll 1
-      for (int ch = 0; grp + ch * kEpiGroups < BN / 32; ++ch) {
+      for (int ch = 0; ch < nch; ++ch) {
         const int col = (grp + ch * kEpiGroups) * 32;
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
+        if (ch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
+        if (ch == nch - 1) release();
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0) p.dbg[7] = gtimer();
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 0] = gtimer();
         const int f0 = tn * BN + col;
         if (p.dbg_mode & 1) continue;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
-        const int mb = f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
+        const int mb = p.o_bm == 64 ? f0 >> 6 : f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
         float x[32];
 #pragma unroll
@@ -509,7 +552,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           uint4 val[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) val[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-          if (lane == 0) bulk_wait_read<0>();  // the previous store has read the staging rows
+          uint8_t* stg = stg0 + (nstore % S::STG_BUFS) * 2048;
+          if (lane == 0) {  // the store that last used this buffer has read it
+            if (S::STG_BUFS == 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
           __syncwarp();
           // row `lane`, 16-byte chunk c lands at chunk c ^ ((lane >> 1) & 3) (SWIZZLE_64B)
 #pragma unroll
@@ -517,8 +564,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = val[c];
           fence_async_smem();
           __syncwarp();
-          if (lane == 0 && warp_rows) {
-            tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
+          ++nstore;
+          if (lane == 0) {
+            // every chunk commits a bulk group (possibly empty) so that the
+            // per-buffer wait_group counts stay aligned with nstore
+            if (warp_rows) tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
             bulk_commit();
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 3] = gtimer();
           }
@@ -531,12 +581,6 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
       }
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[8] = gtimer();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[as]), 0));
-        else mbar_arrive(&tempty[as]);
-      }
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[5] = gtimer();
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[19 + 4 * tcount] = gtimer();
     }
@@ -942,6 +986,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   Params p{};
   p.mode = FEED_CONV;
   p.dbg = g_dbg_ts;
+  p.dbg_mode = getenv("TPP_DBG_MODE") ? atoi(getenv("TPP_DBG_MODE")) : 0;
   p.kblocks = R * S * Cb;
   p.cv_P = P;
   p.cv_Q = Q;
