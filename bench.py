@@ -231,16 +231,18 @@ def run_ours(args, rank, world, dist):
     for e in ev_comp + ev_out:
         e.record(comp)
 
-    def e2e_step(i):
+    def e2e_step(i, comp):
         """Pipelined serving step: H2D of step i overlaps compute of i-1 and
         D2H of i-2 (double-buffered device and host buffers, 3 streams)."""
         b = i % 2
         with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_comp[b])          # x_dev[b] no longer read
+            if i >= 2:
+                s_in.wait_event(ev_comp[b])      # x_dev[b] no longer read
             x_dev[b].copy_(x_host, non_blocking=True)
             ev_in[b].record(s_in)
         comp.wait_event(ev_in[b])
-        comp.wait_event(ev_out[b])               # out_dev[b] already copied out
+        if i >= 2:
+            comp.wait_event(ev_out[b])           # out_dev[b] already copied out
         layer0.forward(x_dev[b], NB, BN, out=out_dev[b], stream=comp)
         ev_comp[b].record(comp)
         with torch.cuda.stream(s_out):
@@ -248,8 +250,26 @@ def run_ours(args, rank, world, dist):
             out_host[b].copy_(out_dev[b], non_blocking=True)
             ev_out[b].record(s_out)
 
+    # the K-step serving loop is captured once as a CUDA graph (copies, the
+    # layer's kernel and the cross-stream events), then replayed: per step the
+    # timed region still moves the step's input H2D and its output D2H
+    def e2e_graph():
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            cap = torch.cuda.current_stream()
+            s_in.wait_stream(cap)
+            s_out.wait_stream(cap)
+            for i in range(K):
+                e2e_step(i, cap)
+            cap.wait_stream(s_in)
+            cap.wait_stream(s_out)
+        return gr
+
     for i in range(max(W, 3)):
-        e2e_step(i)
+        e2e_step(i, comp)
+    torch.cuda.synchronize()
+    g_e2e = e2e_graph()
+    g_e2e.replay()
     torch.cuda.synchronize()
     e2e_times = []
     for _ in range(5):
@@ -259,12 +279,7 @@ def run_ours(args, rank, world, dist):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(comp)
-        s_in.wait_stream(comp)
-        s_out.wait_stream(comp)
-        for i in range(K):
-            e2e_step(i)
-        comp.wait_stream(s_out)
-        comp.wait_stream(s_in)
+        g_e2e.replay()
         e1.record(comp)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -273,6 +288,8 @@ def run_ours(args, rank, world, dist):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         e2e_times.append(ms)
+    if os.environ.get("TPP_BENCH_DEBUG"):
+        print("e2e region ms:", e2e_times, file=sys.stderr)
     e2e_ms_step = statistics.median(e2e_times) / K
     e2e_value = FLOPS_CFG2 * world / (e2e_ms_step * 1e-3) / 1e12
 
@@ -331,7 +348,7 @@ def run_ours(args, rank, world, dist):
                 "h2d_bytes_per_step": n_in * 2,
                 "d2h_bytes_per_step": n_out * 2,
                 "ms_per_step": round(e2e_ms_step, 6),
-                "api": "FcLayer.forward with a pinned H2D of the input and a D2H of the output every step; copies pipelined against compute on separate streams (double-buffered)",
+                "api": "FcLayer.forward with a pinned H2D of the input and a D2H of the output every step; copies pipelined against compute on separate streams (double-buffered), the K-step serving loop captured once as a CUDA graph and replayed",
             },
             "gpu_launches": K,
             "clocks": clocks,
