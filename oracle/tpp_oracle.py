@@ -614,3 +614,23 @@ def mlp_train_step(x_bits, weights32, targets, lr: float, global_batch: int):
             g = round_bf16(relu_inv(dh, masks[l]))
     new = [split_sgd_step(weights32[l], dws[l], lr) for l in range(nl)]
     return new, dws, loss
+
+
+def dilated_conv1d(x, wt, c: int, k: int, s: int, d: int, q: int) -> np.ndarray:
+    """1-D dilated convolution forward (kernels.py:350-378): the reference
+    runs, per output block, an address-based BRGEMM over the S taps with
+    A_s = W^T block s (K x C) and B_s = input columns at pos + s*d (C x bq);
+    per output element that is acc = +0; for s: part = +0; for c ascending:
+    part += W[s*C + c, k] * x[c, q + s*d]; acc += part (contraction.py:300-315).
+    x: [C, W] FP32; wt: [C*S, K] FP32; returns [K, Q] FP32.
+    Vectorised over (k, q); every product and sum rounded as FP32."""
+    x = np.asarray(x, np.float32)
+    wt = np.asarray(wt, np.float32)
+    acc = np.zeros((k, q), np.float32)
+    for ss in range(s):
+        part = np.zeros((k, q), np.float32)
+        for cc in range(c):
+            prod = (wt[ss * c + cc, :][:, None] * x[cc, ss * d: ss * d + q][None, :]).astype(np.float32)
+            part = (part + prod).astype(np.float32)
+        acc = (acc + part).astype(np.float32)
+    return acc

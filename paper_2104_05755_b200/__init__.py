@@ -69,6 +69,8 @@ from .contraction import (
 from .kernels import (
     Conv2d,
     ConvSpec,
+    DilatedConvSpec,
+    dilated_conv1d_forward,
     FcLayer,
     FcSpec,
     SoftmaxSpec,

@@ -425,3 +425,49 @@ class Conv2d:
                                               din.data_ptr(), _lib.stream_ptr(stream)),
                    "conv_backward_data")
         return din
+
+
+# ---------------------------------------------------------------------------
+# 1-D dilated convolution (kernels.py:336-378): the address-based BRGEMM user
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class DilatedConvSpec:
+    """kernels.py:336-348."""
+    in_channels: int     # C
+    out_channels: int    # K
+    width: int           # W (input positions)
+    out_width: int       # Q (output positions)
+    taps: int            # S (filter size)
+    dilation: int        # d
+    block_q: int = 8     # output-position block (the reference's loop; results do not depend on it)
+
+    def __post_init__(self):
+        if self.out_width + (self.taps - 1) * self.dilation > self.width:
+            raise TensorError("output width exceeds the dilated receptive field")
+
+
+def dilated_conv1d_forward(spec: DilatedConvSpec, inp: TensorView, weights: TensorView,
+                           out: TensorView, stream=None) -> None:
+    """kernels.py:350-378.  ``inp`` is C x W (one column per position),
+    ``weights`` (C*S) x K with row s*C + c holding tap s of channel c, ``out``
+    K x Q.  The weights are transposed once (TRANSPOSE TPP), then the whole
+    output is ONE batch-reduce over the S taps: A_s = W^T columns [s*C, s*C+C),
+    B_s = the input columns starting at s*d.  Per output element that is the
+    reference's order (taps outer, channels inner, no FMA), so the result is
+    bitwise the reference's for every block_q — on the ordered BRGEMM kernel."""
+    from .contraction import BrgemmBatch, GemmSpec, brgemm
+    from .ops import TransformKind, TransformSpec, transform
+    c_ch, k_ch, s_taps, d = spec.in_channels, spec.out_channels, spec.taps, spec.dilation
+    if (inp.desc.rows, inp.desc.cols) != (c_ch, spec.width):
+        raise TensorError("input must be C x W")
+    if (weights.desc.rows, weights.desc.cols) != (c_ch * s_taps, k_ch):
+        raise TensorError("weights must be (C*S) x K")
+    if (out.desc.rows, out.desc.cols) != (k_ch, spec.out_width):
+        raise TensorError("output must be K x Q")
+    wt = alloc(TensorDesc(k_ch, c_ch * s_taps, k_ch, weights.desc.dtype), device=weights.primary.device)
+    transform(weights, TransformSpec(TransformKind.TRANSPOSE), wt, stream=stream)
+    gspec = GemmSpec(m=k_ch, n=spec.out_width, k=c_ch, lda=k_ch, ldb=inp.desc.ld, ldc=out.desc.ld,
+                     in_dtype=wt.desc.dtype, out_dtype=out.desc.dtype, beta=0.0)
+    batch = BrgemmBatch.stride(wt.primary, inp.primary, c_ch * k_ch, d * inp.desc.ld, s_taps)
+    brgemm(gspec, batch, out, stream=stream)

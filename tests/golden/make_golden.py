@@ -356,6 +356,25 @@ def gen_conv():
     save("conv.npz", x=x, w=wv, out=out)
 
 
+def gen_dilated():
+    """1-D dilated conv (kernels.py:336-378) through the reference's own
+    address-based BRGEMM driver: the reference test's shape and a wider
+    ATACworks-like slice (C = K = 15, S = 51, d = 8)."""
+    out = {}
+    for name, (c, k, s, d, w, q, seed) in {"small": (3, 2, 5, 2, 28, 20, 15),
+                                            "atac": (15, 15, 51, 8, 800, 400, 16)}.items():
+        rng = np.random.default_rng(seed)
+        x = rng.standard_normal((c, w)).astype(np.float32)
+        wt = rng.standard_normal((c * s, k)).astype(np.float32)
+        o = tp.alloc(tp.TensorDesc(k, q, k, tp.DType.FP32))
+        tp.dilated_conv1d_forward(tp.DilatedConvSpec(c, k, w, q, s, d), tp.from_array(x), tp.from_array(wt), o)
+        out[f"{name}_x"] = x
+        out[f"{name}_w"] = wt
+        out[f"{name}_out"] = tp.to_array(o).astype(np.float32)
+        out[f"{name}_shape"] = np.array([c, k, s, d, w, q], dtype=np.int64)
+    save("dilated.npz", **out)
+
+
 if __name__ == "__main__":
     gen_dtypes()
     gen_cfg1()
@@ -366,3 +385,4 @@ if __name__ == "__main__":
     gen_softmax_sgd()
     gen_fc()
     gen_conv()
+    gen_dilated()

@@ -416,3 +416,37 @@ def test_conv_golden(golden):
     rng = np.random.default_rng(41)
     err_f, err_b = _conv_case(rng, 2, 1, 1, 56, 56, n_sel=[1])
     assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+
+
+# ---------------------------------------------------------------------------
+# 1-D dilated conv (kernels.py:336-378): stride BRGEMM over taps, bitwise
+# ---------------------------------------------------------------------------
+
+def test_dilated_conv1d_bitwise(golden):
+    g = golden("dilated.npz")
+    for name in ("small", "atac"):
+        c, k, s, d, w, q = (int(v) for v in g[f"{name}_shape"])
+        x = tpp.from_array(g[f"{name}_x"], device="cuda")
+        wt = tpp.from_array(g[f"{name}_w"], device="cuda")
+        out = tpp.alloc(tpp.TensorDesc(k, q, k, tpp.DType.FP32), device="cuda")
+        tpp.dilated_conv1d_forward(tpp.DilatedConvSpec(c, k, w, q, s, d), x, wt, out)
+        assert bits(tpp.to_array(out)) == bits(g[f"{name}_out"]), name
+
+
+def test_dilated_conv1d_impulse_and_guard():
+    """test_kernels.py:395-409 and 423-425: an impulse reproduces the taps."""
+    c_, k_, s_, d_, q_ = 1, 2, 3, 2, 6
+    w_ = q_ + (s_ - 1) * d_
+    x = np.zeros((c_, w_), dtype=np.float32)
+    x[0, 4] = 1.0
+    wt = np.arange(s_ * c_ * k_, dtype=np.float32).reshape(s_ * c_, k_) + 1
+    out = tpp.alloc(tpp.TensorDesc(k_, q_, k_, tpp.DType.FP32), device="cuda")
+    tpp.dilated_conv1d_forward(tpp.DilatedConvSpec(c_, k_, w_, q_, s_, d_), tpp.from_array(x, device="cuda"),
+                               tpp.from_array(wt, device="cuda"), out)
+    o = tpp.to_array(out)
+    for k2 in range(k_):
+        for qq in range(q_):
+            hits = [wt[s2, k2] for s2 in range(s_) if qq + s2 * d_ == 4]
+            assert o[k2, qq] == (hits[0] if hits else 0.0)
+    with pytest.raises(tpp.TensorError):
+        tpp.DilatedConvSpec(1, 1, 10, 9, 3, 2)

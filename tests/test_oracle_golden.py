@@ -150,3 +150,12 @@ def test_conv_offset_composition(golden):
     g = golden("conv.npz")
     out, _ = O.conv2d_fwd_bf16(g["x"], g["w"])
     assert np.array_equal(out, g["out"])
+
+
+def test_dilated_conv1d(golden):
+    """The address-BRGEMM dilated conv of the reference, bitwise (kernels.py:350-378)."""
+    g = golden("dilated.npz")
+    for name in ("small", "atac"):
+        c, k, s, d, w, q = (int(v) for v in g[f"{name}_shape"])
+        out = O.dilated_conv1d(g[f"{name}_x"], g[f"{name}_w"], c, k, s, d, q)
+        assert bits(out) == bits(g[f"{name}_out"]), name
