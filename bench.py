@@ -447,6 +447,37 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
         del mlp, xin, tg
     except Exception as e:
         out["cfg5_mlp_train_step"] = {"error": str(e)[:200]}
+    # ---- standalone memory-bound TPPs (dense BF16 8192 x 4096 views) ---------
+    # three rotating operand sets (3 x 128 MiB > 2x L2): every launch streams HBM
+    try:
+        from paper_2104_05755_b200.ops import TransformKind, TransformSpec, transform
+        R, Cc = 8192, 4096
+        mk = lambda rows, cols: tpp.TensorView(tpp.TensorDesc(rows, cols, rows, tpp.DType.BF16),  # noqa: E731
+                                               torch.randn(rows * cols, generator=gen, device=dev).to(torch.bfloat16))
+        sets_ = [(mk(R, Cc), mk(R, Cc), mk(R, Cc)) for _ in range(3)]
+        trs = [mk(Cc, R) for _ in range(3)]
+        vns = [mk(2 * R, Cc // 2) for _ in range(3)]
+        nb = R * Cc * 2
+        cases = {
+            "relu": (lambda k: tpp.apply_unary(tpp.UnaryKind.RELU, sets_[k][0], sets_[k][1]), 2 * nb),
+            "add": (lambda k: tpp.apply_binary(tpp.BinaryKind.ADD, sets_[k][0], sets_[k][1], sets_[k][2]), 3 * nb),
+            "transpose": (lambda k: transform(sets_[k][0], TransformSpec(TransformKind.TRANSPOSE), trs[k]), 2 * nb),
+            "vnni": (lambda k: transform(sets_[k][0], TransformSpec(TransformKind.VNNI, alpha=2), vns[k]), 2 * nb),
+            "vnni_to_vnnit": (lambda k: transform(vns[k], TransformSpec(TransformKind.VNNI_TO_VNNIT, alpha=2,
+                                                                        alpha_out=2, rows=R, cols=Cc),
+                                                  sets_[k][2]), 2 * nb),
+        }
+        res = {}
+        for name, (fn, byts) in cases.items():
+            g = graph_of(torch, [(lambda k=k: fn(k)) for k in range(3)] * 2)
+            ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.2)) / 6
+            res[name] = {"us": round(ms * 1e3, 2), "GB/s": round(byts / ms / 1e6, 1),
+                         "frac_hbm": round(byts / ms / 1e6 / peak_hbm, 4)}
+        res["shape"] = "bf16 8192 x 4096 column-major views (transforms: 8192 x 4096 logical)"
+        out["memory_bound_tpps"] = res
+        del sets_, trs, vns
+    except Exception as e:
+        out["memory_bound_tpps"] = {"error": str(e)[:200]}
     # ---- cfg 1: FP32 BRGEMM 16 x 64^3, beta = 1, reference order (bitwise) ------
     try:
         m = n = k = 64

@@ -119,6 +119,11 @@ int launch_unary(int kind, const DView& in, const DView& aux, void* out, int out
                  uint8_t* mask_out, bool f64, cudaStream_t s) {
   const int64_t groups = (int64_t)((in.rows + 7) / 8) * in.cols;
   if (groups == 0) return TPP_OK;
+  if (!f64) {
+    const int rc = fast_unary(kind, in, aux, out, out_dtype, out_ld, mask_out, s);
+    if (rc == 0) return TPP_OK;
+    if (rc == 2) return cuda_status(cudaGetLastError(), "unary_vec_kernel");
+  }
   const int threads = 256;
   int64_t blocks = (groups + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
@@ -166,6 +171,11 @@ int launch_nary(int arity, int kind, const DView& a, const DView& b, const DView
                 int rows, int cols, int out_dtype, int out_ld, bool f64, cudaStream_t s) {
   const int64_t total = (int64_t)rows * cols;
   if (total == 0) return TPP_OK;
+  if (!f64) {
+    const int rc = fast_nary(arity, kind, a, b, c, out, rows, cols, out_dtype, out_ld, s);
+    if (rc == 0) return TPP_OK;
+    if (rc == 2) return cuda_status(cudaGetLastError(), "nary_vec_kernel");
+  }
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148 * 32) blocks = 148 * 32;

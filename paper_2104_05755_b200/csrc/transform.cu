@@ -130,6 +130,12 @@ int launch_transform(int kind, int esize, const void* in, int in_ld, void* out, 
                      cudaStream_t s) {
   const int64_t total = (int64_t)out_rows * out_cols;
   if (total == 0) return TPP_OK;
+  if (kind <= 2) {
+    const int rc = fast_transform(kind, esize, in, in_ld, out, out_rows, out_cols, out_ld, alpha, alpha_out, lrows,
+                                  lcols, s);
+    if (rc == 0) return TPP_OK;
+    if (rc == 2) return cuda_status(cudaGetLastError(), "fast transform");
+  }
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 65536) blocks = 65536;

@@ -450,3 +450,90 @@ def test_dilated_conv1d_impulse_and_guard():
             assert o[k2, qq] == (hits[0] if hits else 0.0)
     with pytest.raises(tpp.TensorError):
         tpp.DilatedConvSpec(1, 1, 10, 9, 3, 2)
+
+
+# ---------------------------------------------------------------------------
+# dense fast paths (eltwise_fast.cu) == the generic kernels, bit for bit
+# ---------------------------------------------------------------------------
+
+def _padded(x: np.ndarray, dt, pad: int):
+    """Column-major view of x with ld = rows + pad (pad 0: the dense fast path)."""
+    m, n = x.shape
+    ld = m + pad
+    buf = np.zeros((ld, n), dtype=np.float32)
+    buf[:m] = x
+    flat = torch.from_numpy(np.asfortranarray(buf).reshape(-1, order="F").copy()).cuda()
+    if dt is tpp.DType.BF16:
+        flat = tpp.convert(tpp.TensorView(tpp.TensorDesc(ld, n, ld, tpp.DType.FP32), flat), tpp.DType.BF16).primary
+    return tpp.TensorView(tpp.TensorDesc(m, n, ld, dt), flat)
+
+
+def _dense_bits(v):
+    """Bit patterns of the logical window, NaN payloads canonicalised (the
+    generic kernels' compiled ReLU may canonicalise a NaN; the reference and
+    the fast path keep the operand's payload)."""
+    m, n, ld = v.desc.rows, v.desc.cols, v.desc.ld
+    a = np.ascontiguousarray(to_host(v.primary).reshape(n, ld)[:, :m])
+    if a.dtype == np.uint16:
+        a = a.copy()
+        a[((a & 0x7F80) == 0x7F80) & ((a & 0x7F) != 0)] = 0x7FC0
+        return a.tobytes()
+    return bits(a)
+
+
+def test_dense_fast_paths_match_generic():
+    rng = np.random.default_rng(77)
+    m, n = 256, 96
+    x = rng.standard_normal((m, n)).astype(np.float32) * 3
+    x.flat[::97] = np.nan
+    x.flat[5::101] = -0.0
+    x.flat[7::103] = np.inf
+    y = rng.standard_normal((m, n)).astype(np.float32)
+    z = rng.standard_normal((m, n)).astype(np.float32)
+    U = tpp.UnaryKind
+    for dt in (tpp.DType.FP32, tpp.DType.BF16):
+        for odt in (tpp.DType.FP32, tpp.DType.BF16):
+            res = {}
+            for pad in (0, 8):
+                xv, yv, zv = _padded(x, dt, pad), _padded(y, dt, pad), _padded(z, dt, pad)
+                outs = {}
+                for kind in (U.IDENTITY, U.SQUARE, U.INC, U.SQRT, U.RECIPROCAL, U.RSQRT, U.EXP, U.RELU, U.GELU):
+                    o = tpp.TensorView(tpp.TensorDesc(m, n, m + pad, odt),
+                                       torch.zeros((m + pad) * n, dtype=odt.storage, device="cuda"))
+                    tpp.apply_unary(kind, xv, o, bitmask_output=kind is U.RELU)
+                    outs[kind] = _dense_bits(o)
+                    if kind is U.RELU:
+                        outs["mask"] = to_host(o.secondary).tolist() if pad == 0 else None
+                for kind in (tpp.BinaryKind.ADD, tpp.BinaryKind.MUL, tpp.BinaryKind.DIV, tpp.BinaryKind.MAX):
+                    o = tpp.TensorView(tpp.TensorDesc(m, n, m + pad, odt),
+                                       torch.zeros((m + pad) * n, dtype=odt.storage, device="cuda"))
+                    tpp.apply_binary(kind, xv, yv, o)
+                    outs[kind] = _dense_bits(o)
+                o = tpp.TensorView(tpp.TensorDesc(m, n, m + pad, odt),
+                                   torch.zeros((m + pad) * n, dtype=odt.storage, device="cuda"))
+                tpp.apply_ternary(tpp.TernaryKind.MULADD, xv, yv, zv, o)
+                outs["muladd"] = _dense_bits(o)
+                res[pad] = outs
+            for k in res[0]:
+                if k == "mask":
+                    continue
+                assert res[0][k] == res[8][k], (dt, odt, k)
+    # transforms: fast (aligned, even) vs the oracle's index formulas
+    a = rng.integers(0, 1 << 16, size=(64, 48), dtype=np.uint16)
+    av = tpp.TensorView(tpp.TensorDesc(64, 48, 64, tpp.DType.BF16),
+                        torch.from_numpy(a.reshape(-1, order="F").view(np.int16).copy()).cuda().view(torch.bfloat16))
+    t = tpp.alloc(tpp.TensorDesc(48, 64, 48, tpp.DType.BF16))
+    tpp.transform(av, tpp.TransformSpec(tpp.TransformKind.TRANSPOSE), t)
+    assert np.array_equal(tpp.bits_of(t), a.T)
+    vn = tpp.alloc(tpp.TensorDesc(128, 24, 128, tpp.DType.BF16))
+    tpp.transform(av, tpp.TransformSpec(tpp.TransformKind.VNNI, alpha=2), vn)
+    got = tpp.bits_of(vn)
+    for g_ in range(24):
+        for mm in range(64):
+            assert got[2 * mm, g_] == a[mm, 2 * g_] and got[2 * mm + 1, g_] == a[mm, 2 * g_ + 1]
+    vt = tpp.alloc(tpp.TensorDesc(96, 32, 96, tpp.DType.BF16))
+    tpp.transform(vn, tpp.TransformSpec(tpp.TransformKind.VNNI_TO_VNNIT, alpha=2, alpha_out=2, rows=64, cols=48), vt)
+    gt = tpp.bits_of(vt)
+    for h in range(32):
+        for kk in range(48):
+            assert gt[2 * kk, h] == a[2 * h, kk] and gt[2 * kk + 1, h] == a[2 * h + 1, kk]

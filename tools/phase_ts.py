@@ -9,7 +9,7 @@ dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev); gen.manual_seed(0)
 lib = _lib.load()
 buf = torch.zeros(16, dtype=torch.int64, device=dev)
-names = ["start", "prologue", "stage0 landed", "last MMA issued", "acc ready", "epilogue done", "exit", "tmem ld done", "stores issued", "rowoff", "bias", "act", "packed", "waitread", "stg", "fence"]
+names = ["start", "prologue", "stage0 landed", "last MMA issued", "acc ready", "epilogue done", "exit", "tmem ld done", "stores issued", "-", "wait released", "first TMA issued"]
 import ctypes as C
 def fwd_flags(layer, x, nb, bn, out, extra):
     d = layer.desc(nb, bn, _lib.FC_BIAS | extra)
@@ -26,4 +26,4 @@ for label, (nb, cb, kb, bn, bnt, extra) in {"cfg2": (16, 16, 16, 64, 64, 0), "K=
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
         t = buf.cpu().tolist()
-        print(label, f"per launch {e0.elapsed_time(e1)*1e3/20:.2f} us |", " ".join(f"{n}={(v - t[0])/1e3:.2f}" for n, v in zip(names, t[:16])))
+        print(label, f"per launch {e0.elapsed_time(e1)*1e3/20:.2f} us |", " ".join(f"{n}={(v - t[0])/1e3:.2f}" for n, v in zip(names, t[:12])))
