@@ -419,15 +419,17 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
         dI = torch.empty_like(xin)
         res = {}
         byts = 2 * 256 * 56 * 56 * 64 * 2 + 9 * 64 * 64 * 2
+        dW = torch.empty(9 * 64 * 64, dtype=torch.float32, device=dev)
         for name, fn in (("fwd", lambda: conv.forward(xin, out=yo)),
-                         ("bwd_data", lambda: conv.backward_data(dO, din=dI))):
+                         ("bwd_data", lambda: conv.backward_data(dO, din=dI)),
+                         ("bwd_weights", lambda: conv.backward_weights(xin, dO, dw=dW))):
             g = graph_of(torch, [fn] * 5)
             ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.3)) / 5
             tf = spec.flops / ms / 1e9
             res[name] = {"ms": round(ms, 5), "TFLOP/s": round(tf, 1), "frac_bf16": round(tf / peak_bf16, 4),
                          "GB/s": round(byts / ms / 1e6, 1), "frac_hbm": round(byts / ms / 1e6 / peak_hbm, 4)}
         out["cfg4_conv3x3"] = res
-        del xin, yo, dO, dI, conv
+        del xin, yo, dO, dI, conv, dW
     except Exception as e:
         out["cfg4_conv3x3"] = {"error": str(e)[:200]}
     # ---- cfg 5: 4-layer blocked MLP training step (fwd + CE + bwd + split-SGD), 1 GPU ----

@@ -172,6 +172,14 @@ int tpp_conv_forward(const tpp_conv_desc* d, const void* w_packed, const void* x
 /* dI[N][C_b][H][W][bc] from dO[N][K_b][P][Q][bk] with bwd-packed weights */
 int tpp_conv_backward_data(const tpp_conv_desc* d, const void* w_packed_bwd,
                            const void* dout, void* din, void* stream);
+/* Backward-weights (no reference kernel — the oracle is the
+ * composition dW[k][c][r][s] = sum_{n,p,q} dO[n][k][p][q] * Xpad[n][c][p+r][q+s]):
+ * dW FP32 [K_b][C_b][R][S][bc][bk] (element (c, k) of a tap at c*bk + k).
+ * `workspace` holds per-CTA partials (tpp_conv_backward_weights_workspace_bytes);
+ * they are summed in a fixed order, so results are deterministic. */
+int64_t tpp_conv_backward_weights_workspace_bytes(const tpp_conv_desc* d);
+int tpp_conv_backward_weights(const tpp_conv_desc* d, const void* x, const void* dout, float* dw,
+                              void* workspace, void* stream);
 
 /* ---- elementwise / reduce / transform TPPs (ops.py) -------------------- */
 /* ops.py:32-64 UnaryKind subset implemented on the GPU */

@@ -634,3 +634,25 @@ def dilated_conv1d(x, wt, c: int, k: int, s: int, d: int, q: int) -> np.ndarray:
             part = (part + prod).astype(np.float32)
         acc = (acc + part).astype(np.float32)
     return acc
+
+
+def conv2d_bwd_weights(x_bits, dout_bits, R: int = 3, S: int = 3, pad: int = 1) -> np.ndarray:
+    """Convolution backward-weights (SURVEY §8(f) 1 — the reference has no
+    kernel for it; this is the composition of its forward, kernels/PAPER.md:655,
+    with the roles of data and output swapped): for every tap,
+        dW[kb][cb][r][s][c][k] = sum_{n, p, q} Xpad[n][cb][p+r][q+s][c] * dO[n][kb][p][q][k]
+    evaluated in float64 (the GPU accumulates in FP32 in its own order; tests
+    compare normwise).  x_bits [N][Cb][H][W][bc], dout_bits [N][Kb][H][W][bk]
+    BF16 patterns; returns float64 [Kb][Cb][R][S][bc][bk]."""
+    x = bf16_to_fp32(np.asarray(x_bits)).astype(np.float64)
+    do = bf16_to_fp32(np.asarray(dout_bits)).astype(np.float64)
+    N, Cb, H, W, bc = x.shape
+    _, Kb, _, _, bk = do.shape
+    xp = np.zeros((N, Cb, H + 2 * pad, W + 2 * pad, bc))
+    xp[:, :, pad:pad + H, pad:pad + W] = x
+    dw = np.zeros((Kb, Cb, R, S, bc, bk))
+    for r in range(R):
+        for s in range(S):
+            xs = xp[:, :, r:r + H, s:s + W, :]                       # [N, Cb, H, W, bc]
+            dw[:, :, r, s] = np.einsum("nchwi,nkhwj->kcij", xs, do, optimize=True)
+    return dw

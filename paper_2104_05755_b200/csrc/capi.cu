@@ -316,6 +316,20 @@ int tpp_conv_backward_data(const tpp_conv_desc* d, const void* w_packed_bwd, con
                          din, as_stream(stream));
 }
 
+int64_t tpp_conv_backward_weights_workspace_bytes(const tpp_conv_desc* d) {
+  if (!d || check_conv(d)) return -1;
+  return conv_dw_workspace_bytes(d->k_b, d->c_b, d->r, d->s);
+}
+
+int tpp_conv_backward_weights(const tpp_conv_desc* d, const void* x, const void* dout, float* dw,
+                              void* workspace, void* stream) {
+  int rc = check_conv(d);
+  if (rc) return rc;
+  TPP_REQUIRE(x && dout && dw && workspace, TPP_E_TENSOR, "conv backward-weights: null buffer");
+  return conv_backward_weights_tc(d->n, d->c_b, d->k_b, d->h, d->w, d->r, d->s, d->pad, x, dout, dw, workspace,
+                                  as_stream(stream));
+}
+
 // ---- eltwise ----------------------------------------------------------------
 static bool valid_view(const tpp_tensor_desc* d) {
   if (!d || d->rows < 1 || d->cols < 1 || d->ld < 1) return false;

@@ -40,6 +40,9 @@ int make_tma_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5], co
 int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* logits,
                                 const int32_t* targets, float scale, void* dlogits, float* loss,
                                 cudaStream_t s);
+int64_t conv_dw_workspace_bytes(int Kb, int Cb, int R, int S);
+int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad, const void* x,
+                             const void* dout, float* dw, void* workspace, cudaStream_t stream);
 int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
                     const void* w_packed, const void* x, void* out, cudaStream_t stream);
 

@@ -426,6 +426,37 @@ class Conv2d:
                    "conv_backward_data")
         return din
 
+    def backward_weights(self, x: torch.Tensor, dout: torch.Tensor, dw: Optional[torch.Tensor] = None,
+                         stream=None) -> torch.Tensor:
+        """dW FP32 [K_b][C_b][R][S][bc][bk] = sum over images and pixels of
+        dO x shifted input.  One tcgen05 pass: every CTA keeps
+        all taps' partial sums in TMEM over its rows; a second kernel adds the
+        per-CTA partials in a fixed order."""
+        sp = self.spec
+        n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
+        n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
+        if x.dtype != torch.bfloat16 or x.numel() < n_in:
+            raise TensorError("conv input must be a bf16 [N][C_b][H][W][bc] buffer")
+        if dout.dtype != torch.bfloat16 or dout.numel() < n_out:
+            raise TensorError("dO must be a bf16 [N][K_b][H][W][bk] buffer")
+        n_w = sp.k_b * sp.c_b * sp.r * sp.s * sp.bc * sp.bk
+        if dw is None:
+            dw = torch.empty(n_w, dtype=torch.float32, device=x.device)
+        elif dw.dtype != torch.float32 or dw.numel() < n_w:
+            raise TensorError("dW must be an FP32 [K_b][C_b][R][S][bc][bk] buffer")
+        lib = _lib.load()
+        d = sp.c()
+        ws = getattr(self, "_dw_ws", None)
+        need = int(lib.tpp_conv_backward_weights_workspace_bytes(C.byref(d)))
+        if need < 0:
+            raise TensorError("invalid conv descriptor for backward-weights")
+        if ws is None or ws.numel() * 4 < need:
+            ws = torch.empty((need + 3) // 4, dtype=torch.float32, device=x.device)
+            self._dw_ws = ws
+        _lib.check(lib.tpp_conv_backward_weights(C.byref(d), x.data_ptr(), dout.data_ptr(), dw.data_ptr(),
+                                                 ws.data_ptr(), _lib.stream_ptr(stream)), "conv_backward_weights")
+        return dw
+
 
 # ---------------------------------------------------------------------------
 # 1-D dilated convolution (kernels.py:336-378): the address-based BRGEMM user

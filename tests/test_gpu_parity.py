@@ -537,3 +537,26 @@ def test_dense_fast_paths_match_generic():
     for h in range(32):
         for kk in range(48):
             assert gt[2 * kk, h] == a[2 * h, kk] and gt[2 * kk + 1, h] == a[2 * h + 1, kk]
+
+
+# ---------------------------------------------------------------------------
+# conv backward-weights: normwise vs the float64 composition
+# ---------------------------------------------------------------------------
+
+def _conv_dw_case(rng, N, Cb, Kb, H, W):
+    spec = tpp.ConvSpec(N, Cb, Kb, H, W)
+    x = O.fp32_to_bf16_rne(rng.uniform(0, 1, (N, Cb, H, W, 64)).astype(np.float32))
+    do = O.fp32_to_bf16_rne(rng.standard_normal((N, Kb, H, W, 64)).astype(np.float32))
+    wv = to_dev(O.fp32_to_bf16_rne(rng.standard_normal(Kb * Cb * 9 * 64 * 64).astype(np.float32) * 0.1))
+    conv = tpp.Conv2d(spec, wv)
+    dw = conv.backward_weights(to_dev(x), to_dev(do))
+    got = to_host(dw).reshape(Kb, Cb, 3, 3, 64, 64).astype(np.float64)
+    want = O.conv2d_bwd_weights(x, do)
+    return normwise(got, want)
+
+
+def test_conv_backward_weights():
+    rng = np.random.default_rng(55)
+    assert _conv_dw_case(rng, 2, 1, 1, 9, 12) <= 1e-5
+    assert _conv_dw_case(rng, 3, 2, 2, 7, 20) <= 1e-5
+    assert _conv_dw_case(rng, 4, 1, 1, 56, 56) <= 1e-5
