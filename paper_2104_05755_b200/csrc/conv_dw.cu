@@ -47,6 +47,9 @@ struct Params {
   float* partial; // [Kb*Cb*Z][taps][64 c][64 k]
 };
 
+// RS3 = 1: a 3x3 filter, every tap-pair descriptor offset an immediate (the
+// single issuing warp must keep pace with 48-cycle N=64 MMAs)
+template <int RS3>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_dw_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_do, const Params p) {
   extern __shared__ __align__(1024) uint8_t raw[];
@@ -107,14 +110,29 @@ conv_dw_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
       tc_fence_after();
       const uint32_t st = smem_u32(smem + s * kStageBytes);
       const uint64_t bdesc = sw128_mnmajor_desc(st + kHaloBytes, 8192);
-      for (int pp = 0; pp < p.pairs; ++pp) {
-        const int t0 = pp * 2 < p.taps - 1 ? pp * 2 : p.taps - 2, t1 = t0 + 1;
-        const int sh0 = (t0 / p.S) * 64 + t0 % p.S, sh1 = (t1 / p.S) * 64 + t1 % p.S;
-        const uint64_t adesc = sw128_mnmajor_desc(st + sh0 * 128, (uint32_t)(sh1 - sh0) * 128);
+      if (RS3) {
+        const uint64_t a0 = sw128_mnmajor_desc(st, 0);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16_warp(tmem_base + pp * 64, adesc + (uint64_t)(kk * (2048 >> 4)), bdesc + (uint64_t)(kk * (2048 >> 4)),
-                        idesc, (row > r0 || kk > 0) ? 1u : 0u);
+        for (int pp = 0; pp < 5; ++pp) {
+          const int t0 = pp < 4 ? 2 * pp : 7, t1 = t0 + 1;
+          const int sh0 = (t0 / 3) * 64 + t0 % 3, sh1 = (t1 / 3) * 64 + t1 % 3;
+          // start address (16-byte units) and LBO field (bits 16..29) as immediates
+          const uint64_t adesc = a0 + (uint64_t)((sh0 * 128) >> 4) + ((uint64_t)(((sh1 - sh0) * 128) >> 4) << 16);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_warp(tmem_base + pp * 64, adesc + (uint64_t)(kk * (2048 >> 4)),
+                          bdesc + (uint64_t)(kk * (2048 >> 4)), idesc, (row > r0 || kk > 0) ? 1u : 0u);
+        }
+      } else {
+        for (int pp = 0; pp < p.pairs; ++pp) {
+          const int t0 = pp * 2 < p.taps - 1 ? pp * 2 : p.taps - 2, t1 = t0 + 1;
+          const int sh0 = (t0 / p.S) * 64 + t0 % p.S, sh1 = (t1 / p.S) * 64 + t1 % p.S;
+          const uint64_t adesc = sw128_mnmajor_desc(st + sh0 * 128, (uint32_t)(sh1 - sh0) * 128);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_warp(tmem_base + pp * 64, adesc + (uint64_t)(kk * (2048 >> 4)),
+                          bdesc + (uint64_t)(kk * (2048 >> 4)), idesc, (row > r0 || kk > 0) ? 1u : 0u);
+        }
       }
       umma_commit_warp(&empty[s]);
       if (++s == kStages) { s = 0; ph ^= 1; }
@@ -221,9 +239,13 @@ int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, 
     if (rc) return rc;
   }
   const int smem = kStages * kStageBytes + (2 * kStages + 1) * 8 + 16 + 1024;
+  const bool rs3 = R == 3 && S == 3;
+  auto kern = rs3 ? conv_dw_kernel<1> : conv_dw_kernel<0>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(conv_dw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(conv_dw_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(conv_dw_kernel)");
     attr = true;
   }
@@ -237,7 +259,7 @@ int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, conv_dw_kernel, mx, md, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, md, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(conv_dw_kernel)");
   TPP_CUDA_LAUNCH_CHECK("conv_dw_kernel");
   const int64_t per4 = (int64_t)p.taps * 64 * 64 / 4, blocks = (int64_t)Kb * Cb;
