@@ -274,10 +274,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   const uint32_t tmem_base = *tmem_slot;
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[1] = gtimer();
   // Programmatic dependent launch: let the next kernel in the stream be
-  // scheduled now (its prologue overlaps our tail), and do not touch global
-  // memory before the previous kernel's results are visible.
+  // scheduled now (its prologue overlaps our tail).  Each role that touches
+  // global memory waits for the previous kernel (griddepcontrol.wait) only
+  // after its parameter-derived setup — kernel parameters are immutable, and
+  // their first (constant-cache-missing) loads are then off the critical path.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  auto pdl_wait_after = [](int dep) { asm volatile("griddepcontrol.wait;" ::"r"(dep) : "memory"); };
 
   if (warp == 0 || (RES == 1 && warp == 3)) {
     // ===================== TMA producer(s) =====================
@@ -286,6 +288,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     constexpr int NPROD = RES == 1 ? 2 : 1;
     const int pid = warp == 0 ? 0 : 1;
     if (lane == 0) {
+      FeedIter f;
+      if (cl_id < num_tiles) {
+        const int tm = cl_id / p.tiles_n, tn = cl_id % p.tiles_n;
+        if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
+        else f.start(p, tm, tn);
+      }
+      pdl_wait_after(f.ai.c[0] + f.ai.c[1] + f.ai.c[2] + f.ai.c[3] + f.ai.c[4] + f.bi.c[0] + f.bi.c[1] + f.bi.c[2] +
+                     f.bi.c[3] + f.bi.c[4] + nstages);
       if (RES && pid == 0) {
         // resident weights: every tap block once, on the bres barrier
         const int J = p.kblocks;
@@ -300,13 +310,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       int s = 0;
       uint32_t ph = 0;
       uint32_t it = 0;
-      FeedIter f;
       // pair: completion bytes of both CTAs count on the leader's full[s]
       const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
       for (int tile = cl_id; tile < num_tiles; tile += n_cl) {
-        const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
-        if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
-        else f.start(p, tm, tn);
+        if (tile != cl_id) {  // the first tile's feed was set up before the wait
+          const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+          if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
+          else f.start(p, tm, tn);
+        }
         for (int j = 0; j < nstages; ++j, ++it) {
           if (NPROD == 1 || (int)(it % NPROD) == pid) {
             mbar_wait(&empty[s], ph ^ 1);
@@ -415,6 +426,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (8 warps) =====================
+    pdl_wait_after(p.flags ^ p.tiles_n ^ p.feats ^ p.o_bn ^ p.o_bm ^ p.o_mb ^ p.act ^ p.tma_store ^ p.mode ^ p.tokens);
     const int ew = warp - kEpiWarp0;
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int grp = ew >> 2;           // 32-column chunks grp, grp + kEpiGroups, ...

@@ -1,0 +1,81 @@
+// Launch-cadence floor: back-to-back launches of an (almost) empty kernel in a
+// CUDA graph, with the tcgen05 GEMM's launch shape (128 CTAs x 384 threads,
+// ~200 KB dynamic smem) and programmatic dependent launch, vs lighter shapes.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/launch_bench.cu -o tools/launch_bench
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define CK(x)                                                                       \
+  do {                                                                              \
+    cudaError_t e_ = (x);                                                           \
+    if (e_ != cudaSuccess) {                                                        \
+      printf("%s failed: %s\n", #x, cudaGetErrorString(e_));                       \
+      return -1.0f;                                                                 \
+    }                                                                               \
+  } while (0)
+
+__global__ void empty_kernel(int* flag, int pdl, int touch) {
+  extern __shared__ int smem[];
+  if (pdl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
+  if (touch && threadIdx.x == 0) smem[0] = blockIdx.x;  // callers pass touch = 0 without dynamic smem
+  if (threadIdx.x == 0 && blockIdx.x == 0 && flag) atomicAdd(flag, touch ? smem[0] + 1 : 1);
+}
+
+static float run(int grid, int threads, int smem, int pdl, int n = 200) {
+  int* flag;
+  CK(cudaMalloc(&flag, 4));
+  CK(cudaFuncSetAttribute(empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < n; ++i) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, empty_kernel, flag, pdl, smem > 0 ? 1 : 0));
+  }
+  CK(cudaStreamEndCapture(s, &g));
+  CK(cudaGraphInstantiate(&ge, g, 0));
+  CK(cudaGraphLaunch(ge, s));
+  CK(cudaStreamSynchronize(s));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0, s);
+    cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(s);
+  cudaFree(flag);
+  return best * 1000.0f / n;
+}
+
+int main() {
+  printf("grid threads smem  pdl : us per launch\n");
+  const int cfgs[][4] = {{128, 384, 200 * 1024, 1}, {128, 384, 200 * 1024, 0}, {128, 384, 0, 1},
+                         {128, 128, 0, 1},          {148, 384, 200 * 1024, 1}, {1, 32, 0, 1}};
+  for (auto& c : cfgs)
+    printf("%4d %6d %6d %3d : %.2f  (%s)\n", c[0], c[1], c[2], c[3], run(c[0], c[1], c[2], c[3]),
+           cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
