@@ -296,6 +296,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
       pdl_wait_after(f.ai.c[0] + f.ai.c[1] + f.ai.c[2] + f.ai.c[3] + f.ai.c[4] + f.bi.c[0] + f.bi.c[1] + f.bi.c[2] +
                      f.bi.c[3] + f.bi.c[4] + nstages);
+      if (p.dbg && blockIdx.x == 0 && pid == 0) p.dbg[10] = gtimer();
       if (RES && pid == 0) {
         // resident weights: every tap block once, on the bres barrier
         const int J = p.kblocks;
@@ -331,6 +332,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
               tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
+              if (p.dbg && blockIdx.x == 0 && it == 0) p.dbg[11] = gtimer();
               if (!RES)
                 tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
             }
