@@ -628,56 +628,140 @@ namespace tpp {
 // Per token: the reference softmax of a 1 x F slice (kernels.py:60-99:
 // max-shift, exp_taylor, ascending sum, reciprocal, multiply), then
 // dlogit = (p - onehot) * scale and loss = -log(p[target]).
+// A CTA stages 16 tokens' logits in smem; the max (order-free), the F
+// exponentials and the outputs are computed by all 256 threads; only the
+// reference's ascending sum is a per-token serial chain (16 lanes).
+constexpr int kXentTok = 16;
+
 __global__ void __launch_bounds__(256)
 softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __restrict__ logits,
                             const int32_t* __restrict__ targets, float scale,
                             uint16_t* __restrict__ dlog, float* __restrict__ loss) {
   extern __shared__ __align__(16) uint8_t xsm[];
   const int F = m_b * bm;
-  const int pitch = F + 1;
+  const int pitch = F + 1;  // odd pitch: per-token row walks are conflict-free
   float* rows = reinterpret_cast<float*>(xsm);
-  float* rcp = rows + 32 * pitch;
-  const int chunks_per_blk = (bn + 31) / 32;
+  float* mxs = rows + kXentTok * pitch;
+  float* rcp = mxs + kXentTok;
+  const int chunks_per_blk = (bn + kXentTok - 1) / kXentTok;
   const int nb = blockIdx.x / chunks_per_blk;
-  const int n0 = (blockIdx.x % chunks_per_blk) * 32;
-  const int T_ = min(32, bn - n0);
-  for (int mb = 0; mb < m_b; ++mb) {
-    const float* src = logits + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
-    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
-      const int t = e / bm, m = e - t * bm;
-      rows[t * pitch + mb * bm + m] = src[e];
+  const int n0 = (blockIdx.x % chunks_per_blk) * kXentTok;
+  const int T_ = min(kXentTok, bn - n0);
+  const int tid = threadIdx.x;
+  if (bm % 4 == 0 && (T_ * bm) % 4 == 0) {
+    // 16-byte loads, 8 in flight per thread (the logits are read once from HBM)
+    const int n4 = T_ * bm / 4, bm4 = bm / 4;
+    for (int base = 0; base < m_b * n4; base += 8 * blockDim.x) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        if (e < m_b * n4) {
+          const int mb = e / n4, r4 = e - mb * n4;
+          v[u] = __ldg(reinterpret_cast<const float4*>(logits + (((int64_t)nb * m_b + mb) * bn + n0) * bm) + r4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        if (e < m_b * n4) {
+          const int mb = e / n4, r4 = e - mb * n4, t = r4 / bm4, m = (r4 - t * bm4) * 4;
+          float* d = rows + t * pitch + mb * bm + m;
+          d[0] = v[u].x; d[1] = v[u].y; d[2] = v[u].z; d[3] = v[u].w;
+        }
+      }
+    }
+  } else {
+    for (int mb = 0; mb < m_b; ++mb) {
+      const float* src = logits + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+      for (int e = tid; e < T_ * bm; e += blockDim.x) {
+        const int t = e / bm, m = e - t * bm;
+        rows[t * pitch + mb * bm + m] = __ldg(src + e);
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x < T_) {
-    float* r = rows + threadIdx.x * pitch;
-    float mx = r[0];
-    for (int f = 1; f < F; ++f) {
-      const float v = r[f];
-      mx = (mx != mx) ? mx : ((v != v) ? v : fmaxf(mx, v));
+  // max over the slice (np.max: NaN if any element is NaN): 16 threads per token
+  {
+    const int t = tid >> 4, k = tid & 15;
+    float mx = -__int_as_float(0x7F800000);
+    bool nan = false;
+    if (t < T_) {
+      const float* r = rows + t * pitch;
+      for (int f = k; f < F; f += 16) {
+        const float v = r[f];
+        nan |= v != v;
+        mx = fmaxf(mx, v);
+      }
     }
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+      nan |= __shfl_xor_sync(0xFFFFFFFFu, (int)nan, o) != 0;
+    }
+    if (k == 0 && t < T_) mxs[t] = nan ? __int_as_float(0x7FC00000) : mx;
+  }
+  __syncthreads();
+  // e = exp_taylor(x - max), in place: 16 threads per token, no index division
+  {
+    const int t = tid >> 4, k = tid & 15;
+    if (t < T_) {
+      float* r = rows + t * pitch;
+      const float mx = mxs[t];
+#pragma unroll 4
+      for (int f = k; f < F; f += 16) r[f] = exp_taylor(__fsub_rn(r[f], mx));
+    }
+  }
+  __syncthreads();
+  // the reference's ascending sum: one serial chain per token
+  if (tid < T_) {
+    const float* r = rows + tid * pitch;
     float tot = 0.0f;
-    for (int f = 0; f < F; ++f) {
-      const float e = exp_taylor(__fsub_rn(r[f], mx));
-      r[f] = e;
-      tot = __fadd_rn(tot, e);
+    int f = 0;
+    for (; f + 8 <= F; f += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = r[f + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tot = __fadd_rn(tot, v[u]);
     }
+    for (; f < F; ++f) tot = __fadd_rn(tot, r[f]);
     const float rc = __fdiv_rn(1.0f, tot);
-    rcp[threadIdx.x] = rc;
-    const int64_t tok = (int64_t)nb * bn + n0 + threadIdx.x;
-    const int tg = targets[tok];
-    if (loss) loss[tok] = -logf(__fmul_rn(r[tg], rc));
+    rcp[tid] = rc;
+    const int64_t tok = (int64_t)nb * bn + n0 + tid;
+    if (loss) loss[tok] = -logf(__fmul_rn(r[targets[tok]], rc));
   }
   __syncthreads();
-  for (int mb = 0; mb < m_b; ++mb) {
-    uint16_t* dst = dlog + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
-    for (int e = threadIdx.x; e < T_ * bm; e += blockDim.x) {
-      const int t = e / bm, m = e - t * bm;
-      const int f = mb * bm + m;
-      const float pr = __fmul_rn(rows[t * pitch + f], rcp[t]);
+  // dlogits: 16 threads per token, 4 consecutive features each (8-byte stores)
+  if (bm % 64 == 0) {
+    const int t = tid >> 4, k = tid & 15;
+    if (t < T_) {
+      const float rc = rcp[t];
       const int tg = targets[(int64_t)nb * bn + n0 + t];
-      const float g = __fmul_rn(__fsub_rn(pr, f == tg ? 1.0f : 0.0f), scale);
-      dst[e] = f32_to_bf16(g);
+      const float* r = rows + t * pitch;
+      for (int mb = 0; mb < m_b; ++mb) {
+        uint16_t* dst = dlog + ((((int64_t)nb * m_b + mb) * bn + n0 + t) * bm);
+        for (int m = 4 * k; m < bm; m += 64) {
+          const int f = mb * bm + m;
+          float g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            g[u] = __fmul_rn(__fsub_rn(__fmul_rn(r[f + u], rc), f + u == tg ? 1.0f : 0.0f), scale);
+          *reinterpret_cast<uint2*>(dst + m) = make_uint2(pack2_bf16_ref(g[0], g[1]), pack2_bf16_ref(g[2], g[3]));
+        }
+      }
+    }
+  } else {
+    for (int mb = 0; mb < m_b; ++mb) {
+      uint16_t* dst = dlog + (((int64_t)nb * m_b + mb) * bn + n0) * bm;
+      for (int e = tid; e < T_ * bm; e += blockDim.x) {
+        const int t = e / bm, m = e - t * bm;
+        const int f = mb * bm + m;
+        const float pr = __fmul_rn(rows[t * pitch + f], rcp[t]);
+        const int tg = targets[(int64_t)nb * bn + n0 + t];
+        const float g = __fmul_rn(__fsub_rn(pr, f == tg ? 1.0f : 0.0f), scale);
+        dst[e] = f32_to_bf16(g);
+      }
     }
   }
 }
@@ -686,9 +770,9 @@ int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* l
                                 const int32_t* targets, float scale, void* dlogits, float* loss,
                                 cudaStream_t s) {
   const int F = m_b * bm;
-  const size_t smem = (size_t)32 * (F + 1) * sizeof(float) + 32 * sizeof(float);
+  const size_t smem = (size_t)kXentTok * (F + 1) * sizeof(float) + 2 * kXentTok * sizeof(float);
   TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "softmax_xent: class dimension too long for smem");
-  const int blocks = n_b * ((bn + 31) / 32);
+  const int blocks = n_b * ((bn + kXentTok - 1) / kXentTok);
   if (blocks == 0) return TPP_OK;
   cudaError_t e = cudaFuncSetAttribute(softmax_xent_blocked_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
