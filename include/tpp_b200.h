@@ -238,6 +238,12 @@ int tpp_layernorm(const tpp_tensor_desc* x_d, const void* x,
 int tpp_layernorm_blocked(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, int32_t dtype,
                           const void* x, const float* gamma, const float* beta, double eps,
                           void* out, float* mean_out, float* var_out, void* stream);
+/* exact = 1: as tpp_layernorm_blocked (the reference order, bitwise);
+ * exact = 0: tolerance mode for BF16 (tree-ordered sums, FMA-contracted
+ * scaling; within 1e-5 relative of the exact statistics) */
+int tpp_layernorm_blocked_ex(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, int32_t dtype,
+                             const void* x, const float* gamma, const float* beta, double eps,
+                             void* out, float* mean_out, float* var_out, int32_t exact, void* stream);
 /* kernels.py:84-99 softmax(SoftmaxSpec(s1, s2, s3)) on a FP32 s1 x (s2*s3) view */
 int tpp_softmax(int32_t s1, int32_t s2, int32_t s3, const tpp_tensor_desc* x_d,
                 const void* x, const tpp_tensor_desc* y_d, void* y, void* stream);

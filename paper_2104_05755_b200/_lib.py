@@ -94,6 +94,8 @@ _SIGS = {
                                 _P, _P, _P, _P]),
     "tpp_layernorm_blocked": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, C.c_double, _P,
                                         _P, _P, _P]),
+    "tpp_layernorm_blocked_ex": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _P, _P, _P, C.c_double, _P,
+                                        _P, _P, _I32, _P]),
     "tpp_softmax": (C.c_int, [_I32, _I32, _I32, C.POINTER(TensorDescC), _P,
                               C.POINTER(TensorDescC), _P, _P]),
     "tpp_split_sgd": (C.c_int, [_I64, _P, _P, _P, _I32, C.c_float, _P]),

@@ -559,6 +559,18 @@ int tpp_layernorm_blocked(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, int3
                                   var_out, as_stream(stream));
 }
 
+int tpp_layernorm_blocked_ex(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, int32_t dtype,
+                             const void* x, const float* gamma, const float* beta, double eps,
+                             void* out, float* mean_out, float* var_out, int32_t exact, void* stream) {
+  TPP_REQUIRE(n_b >= 1 && m_b >= 1 && bn >= 1 && bm >= 1, TPP_E_TENSOR, "bad blocking");
+  TPP_REQUIRE(m_b * bm >= 2, TPP_E_TENSOR, "layernorm needs a feature dimension of at least 2");
+  TPP_REQUIRE(eps > 0, TPP_E_TENSOR, "eps must be positive");
+  TPP_REQUIRE(dtype == TPP_FP32 || dtype == TPP_BF16, TPP_E_SPEC_DTYPE, "dtype must be FP32 or BF16");
+  TPP_REQUIRE(x && out, TPP_E_TENSOR, "null operand");
+  return launch_layernorm_blocked(n_b, m_b, bn, bm, dtype, x, gamma, beta, eps, out, mean_out,
+                                  var_out, as_stream(stream), exact ? 1 : 0);
+}
+
 int tpp_softmax(int32_t s1, int32_t s2, int32_t s3, const tpp_tensor_desc* x_d, const void* x,
                 const tpp_tensor_desc* y_d, void* y, void* stream) {
   TPP_REQUIRE(valid_view(x_d) && valid_view(y_d), TPP_E_TENSOR, "bad descriptor");

@@ -82,7 +82,7 @@ int launch_layernorm_view(const DView& x, const DView& g, const DView& b, double
                           cudaStream_t s);
 int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
                              const float* gamma, const float* beta, double eps, void* out,
-                             float* mean_out, float* var_out, cudaStream_t s);
+                             float* mean_out, float* var_out, cudaStream_t s, int exact = 1);
 int launch_softmax(int s1, int s2, int s3, const DView& x, float* y, int y_ld, cudaStream_t s);
 int launch_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad, int grad_dtype,
                      float lr, cudaStream_t s);

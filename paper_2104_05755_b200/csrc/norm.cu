@@ -279,6 +279,11 @@ __device__ __forceinline__ void sts128(uint32_t a, const uint4& v) {
                : "memory");
 }
 
+// FAST = 1: the tolerance mode (tree order allowed within
+// 1e-5): per token 8 interleaved partial sums (chain 8x shorter) with fused
+// x*x, and the scaling equation as two FMAs on element pairs.  FAST = 0 is
+// the bitwise reference order.
+template <int FAST>
 __global__ void __launch_bounds__(lnt::kThreads, 1)
 layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_o,
                       int n_groups, int bn, int m_b, int stages, const float* __restrict__ gamma,
@@ -359,6 +364,9 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
       const uint32_t row = sbase + s * gbytes + t * 128;
       const int sw = t & 7;
       float a = 0.0f, b = 0.0f;
+      float pa[8], pb[8];  // FAST: one partial pair per chunk slot
+#pragma unroll
+      for (int c = 0; c < 8; ++c) { pa[c] = 0.0f; pb[c] = 0.0f; }
       // software pipeline: the next slab's 8 chunks are in flight while this
       // slab is folded (the fold itself is a 2 x F-long FADD chain per token)
       uint4 cur[8], nxt[8];
@@ -368,10 +376,27 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
         const uint32_t nrow = row + (cb + 1 < m_b ? cb + 1 : cb) * (kTok * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) nxt[c] = lds128(nrow + ((c ^ sw) << 4));
+        if (FAST) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) fold8(cur[c], a, b);
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t w[4] = {cur[c].x, cur[c].y, cur[c].z, cur[c].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
+              pa[c] += x0 + x1;
+              pb[c] = fmaf(x0, x0, fmaf(x1, x1, pb[c]));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) fold8(cur[c], a, b);
+        }
 #pragma unroll
         for (int c = 0; c < 8; ++c) cur[c] = nxt[c];
+      }
+      if (FAST) {
+        a = ((pa[0] + pa[1]) + (pa[2] + pa[3])) + ((pa[4] + pa[5]) + (pa[6] + pa[7]));
+        b = ((pb[0] + pb[1]) + (pb[2] + pb[3])) + ((pb[4] + pb[5]) + (pb[6] + pb[7]));
       }
       if (live) {
         float scale, shift;
@@ -433,8 +458,15 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
           const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
           const float g0 = (q & 1) ? g4[q >> 1].z : g4[q >> 1].x, g1 = (q & 1) ? g4[q >> 1].w : g4[q >> 1].y;
           const float b0 = (q & 1) ? b4[q >> 1].z : b4[q >> 1].x, b1 = (q & 1) ? b4[q >> 1].w : b4[q >> 1].y;
-          r[8 * u + 2 * q] = __fadd_rn(b0, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x0, sc.x)), g0));
-          r[8 * u + 2 * q + 1] = __fadd_rn(b1, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x1, sc.x)), g1));
+          if (FAST) {
+            const float2 t = __ffma2_rn(make_float2(x0, x1), make_float2(sc.x, sc.x), make_float2(sc.y, sc.y));
+            const float2 y = __ffma2_rn(t, make_float2(g0, g1), make_float2(b0, b1));
+            r[8 * u + 2 * q] = y.x;
+            r[8 * u + 2 * q + 1] = y.y;
+          } else {
+            r[8 * u + 2 * q] = __fadd_rn(b0, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x0, sc.x)), g0));
+            r[8 * u + 2 * q + 1] = __fadd_rn(b1, __fmul_rn(__fadd_rn(sc.y, __fmul_rn(x1, sc.x)), g1));
+          }
         }
        }
        // one NaN check for the 32 results, then the 4 stores
@@ -455,7 +487,7 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
 
 int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
                              const float* gamma, const float* beta, double eps, void* out,
-                             float* mean_out, float* var_out, cudaStream_t s) {
+                             float* mean_out, float* var_out, cudaStream_t s, int exact) {
   const bool al16 = reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
                     reinterpret_cast<uintptr_t>(gamma) % 16 == 0 && reinterpret_cast<uintptr_t>(beta) % 16 == 0;
   const int gbytes = lnt::kTok * m_b * 128;
@@ -477,7 +509,10 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
                         lnt::kMaxStages * 4 + 1024;
     static bool attr = false;
     if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(lnt::kRingBytes + 3 * 1024));
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(layernorm_blocked_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(lnt::kRingBytes + 3 * 1024));
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_tma)");
       attr = true;
@@ -492,7 +527,7 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, layernorm_blocked_tma, mx, mo, n_groups, bn, m_b, stages, gamma, beta,
+    cudaError_t e = cudaLaunchKernelEx(&cfg, exact ? layernorm_blocked_tma<0> : layernorm_blocked_tma<1>, mx, mo, n_groups, bn, m_b, stages, gamma, beta,
                                        eps, mean_out, var_out, getenv("TPP_LN_SPIN") ? atoi(getenv("TPP_LN_SPIN")) : 0,
                                        debug_timestamps());
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(layernorm_blocked_tma)");

@@ -264,10 +264,13 @@ def layernorm(x: TensorView, g: TensorView, b: TensorView, eps: float, out: Tens
 def layernorm_blocked(x: torch.Tensor, n_b: int, m_b: int, bn: int, bm: int, eps: float = 1e-5,
                       gamma: Optional[torch.Tensor] = None, beta: Optional[torch.Tensor] = None,
                       out: Optional[torch.Tensor] = None, mean_out: Optional[torch.Tensor] = None,
-                      var_out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                      var_out: Optional[torch.Tensor] = None, stream=None, exact: bool = True) -> torch.Tensor:
     """LayerNorm of every token of a blocked [n_b][m_b][bn][bm] activation
     over its m_b*bm features (ascending feature order), gamma/beta FP32
-    [m_b*bm] (default 1 / 0, still applied as MULADD so signed zeros match)."""
+    [m_b*bm] (default 1 / 0, still applied as MULADD so signed zeros match).
+    ``exact=False`` selects the tolerance mode (BF16 blocked layout): tree-
+    ordered statistics and FMA-contracted scaling, within 1e-5 relative of the
+    exact statistics; everything else is the reference order."""
     if x.dtype not in (torch.bfloat16, torch.float32) or not x.is_cuda:
         raise TensorError("x must be a CUDA bf16/fp32 buffer")
     n = n_b * m_b * bn * bm
@@ -281,9 +284,9 @@ def layernorm_blocked(x: torch.Tensor, n_b: int, m_b: int, bn: int, bm: int, eps
     lib = _lib.load()
     dt = _lib.BF16 if x.dtype == torch.bfloat16 else _lib.FP32
     p = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    _lib.check(lib.tpp_layernorm_blocked(n_b, m_b, bn, bm, dt, x.data_ptr(), p(gamma), p(beta),
-                                         float(eps), out.data_ptr(), p(mean_out), p(var_out),
-                                         _lib.stream_ptr(stream)), "layernorm_blocked")
+    _lib.check(lib.tpp_layernorm_blocked_ex(n_b, m_b, bn, bm, dt, x.data_ptr(), p(gamma), p(beta),
+                                            float(eps), out.data_ptr(), p(mean_out), p(var_out),
+                                            1 if exact else 0, _lib.stream_ptr(stream)), "layernorm_blocked")
     return out
 
 

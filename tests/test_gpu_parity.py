@@ -560,3 +560,24 @@ def test_conv_backward_weights():
     assert _conv_dw_case(rng, 2, 1, 1, 9, 12) <= 1e-5
     assert _conv_dw_case(rng, 3, 2, 2, 7, 20) <= 1e-5
     assert _conv_dw_case(rng, 4, 1, 1, 56, 56) <= 1e-5
+
+
+def test_layernorm_blocked_tolerance_mode():
+    """exact=False (tree-ordered sums, FMA scaling): statistics within 1e-5
+    relative, outputs within the BF16 tolerance and nearly all bit-identical."""
+    rng = np.random.default_rng(23)
+    n_b, m_b, bn, bm = 40, 16, 32, 64
+    x = O.fp32_to_bf16_rne(rng.normal(0, 1, (n_b, m_b, bn, bm)).astype(np.float32) + 0.3)
+    gam = (1 + 0.1 * rng.standard_normal(m_b * bm)).astype(np.float32)
+    bet = (0.1 * rng.standard_normal(m_b * bm)).astype(np.float32)
+    res = {}
+    for exact in (True, False):
+        mean = torch.empty(n_b * bn, dtype=torch.float32, device="cuda")
+        var = torch.empty_like(mean)
+        out = tpp.layernorm_blocked(to_dev(x), n_b, m_b, bn, bm, 1e-5, to_dev(gam), to_dev(bet),
+                                    mean_out=mean, var_out=var, exact=exact)
+        res[exact] = (to_host(out), to_host(mean), to_host(var))
+    (oe, me, ve), (of, mf, vf) = res[True], res[False]
+    assert normwise(mf, me) <= 1e-5 and normwise(vf, ve) <= 1e-5
+    assert normwise(bf16_bits_to_f32(of), bf16_bits_to_f32(oe)) <= BF16_TOL
+    assert np.mean(of == oe) > 0.95
