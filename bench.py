@@ -297,8 +297,9 @@ def run_ours(args, rank, world, dist):
     e2e_ms_step = statistics.median(e2e_times) / K
     e2e_value = FLOPS_CFG2 * world / (e2e_ms_step * 1e-3) / 1e12
 
+    # the other configs and the CPU baseline are single-GPU reports (N = 1 runs)
     extra = {}
-    if rank == 0 and not args.no_extra:
+    if rank == 0 and world == 1 and not args.no_extra:
         extra = run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm)
 
     traffic = None
@@ -310,7 +311,7 @@ def run_ours(args, rank, world, dist):
             traffic = None
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample()
 
     if rank == 0:
