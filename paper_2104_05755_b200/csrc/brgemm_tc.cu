@@ -1032,7 +1032,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     if (rc) return rc;
   }
   // output [N][K_b][H][W][64] through TMA stores: box 32 channels x 32 pixels
-  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0 && !getenv("TPP_NO_TMA_STORE");
   mc = ma;
   if (p.tma_store) {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Kb, (uint64_t)N};

@@ -419,6 +419,83 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
     const int aw = warp - 1 - kFoldWarps;
     const int team = aw / kTeamWarps;
     const int tid = (aw % kTeamWarps) * 32 + lane;
+    if (m_b * 8 <= kTeamWarps * 32) {
+      // feature-stationary mapping (F <= 1024): a thread owns one 8-feature
+      // chunk (slab cb, chunk c) for the whole kernel, so its gamma / beta are
+      // loaded once into registers, and walks the group's 16 tokens; a warp's
+      // 16-byte reads cover 4 full 128-byte rows (conflict-free)
+      const int c = tid & 7, cb = tid >> 3;
+      const bool own = cb < m_b;
+      float g[8], bb[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { g[e] = 1.0f; bb[e] = 0.0f; }
+      if (own) {
+        const int f0 = cb * 64 + c * 8;
+        if (gamma) {
+          const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + f0));
+          const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + f0 + 4));
+          g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w; g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+        }
+        if (beta) {
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + f0));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + f0 + 4));
+          bb[0] = b0.x; bb[1] = b0.y; bb[2] = b0.z; bb[3] = b0.w; bb[4] = b1.x; bb[5] = b1.y; bb[6] = b1.z; bb[7] = b1.w;
+        }
+      }
+      for (int i = team; i < my; i += kApplyTeams) {
+        const int s = i % stages;
+        LN_WAIT(&full[s], (i / stages) & 1);  // (already complete: the fold waited on it)
+        LN_WAIT(&stat[s], (i / stages) & 1);
+        if (own) {
+          const uint32_t slab = sbase + s * gbytes + cb * (kTok * 128);
+#pragma unroll 1
+          for (int t0 = 0; t0 < kTok; t0 += 4) {
+            uint4 vv[4];
+            float2 sc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int t = t0 + u;
+              vv[u] = lds128(slab + t * 128 + ((c ^ (t & 7)) << 4));
+              sc[u] = st[s * kTok + t];
+            }
+            float r[32];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t w[4] = {vv[u].x, vv[u].y, vv[u].z, vv[u].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const float x0 = __uint_as_float(w[q] << 16), x1 = __uint_as_float(w[q] & 0xFFFF0000u);
+                if (FAST) {
+                  const float2 tt = __ffma2_rn(make_float2(x0, x1), make_float2(sc[u].x, sc[u].x),
+                                               make_float2(sc[u].y, sc[u].y));
+                  const float2 y = __ffma2_rn(tt, make_float2(g[2 * q], g[2 * q + 1]),
+                                              make_float2(bb[2 * q], bb[2 * q + 1]));
+                  r[8 * u + 2 * q] = y.x;
+                  r[8 * u + 2 * q + 1] = y.y;
+                } else {
+                  // B + (shift + x*scale)*G, every product and sum rounded separately
+                  r[8 * u + 2 * q] = __fadd_rn(bb[2 * q], __fmul_rn(__fadd_rn(sc[u].y, __fmul_rn(x0, sc[u].x)), g[2 * q]));
+                  r[8 * u + 2 * q + 1] =
+                      __fadd_rn(bb[2 * q + 1], __fmul_rn(__fadd_rn(sc[u].y, __fmul_rn(x1, sc[u].x)), g[2 * q + 1]));
+                }
+              }
+            }
+            uint32_t o[16];
+            pack_bf16_ref_n<16>(r, o);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int t = t0 + u;
+              sts128(slab + t * 128 + ((c ^ (t & 7)) << 4), make_uint4(o[4 * u], o[4 * u + 1], o[4 * u + 2], o[4 * u + 3]));
+            }
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);
+        if (lane == 0 && aw % kTeamWarps == 0) { if (dbg && blockIdx.x == 0 && (i) < 16) dbg[8 + 5 * (i) + 3] = globaltimer_ns(); }
+      }
+      return;
+    }
     const int t = (tid >> 3) & (kTok - 1), c = (tid & 7) ^ (t & 7);
     for (int i = team; i < my; i += kApplyTeams) {
       const int s = i % stages;

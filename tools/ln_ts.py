@@ -10,7 +10,10 @@ lib = _lib.load()
 buf = torch.zeros(600, dtype=torch.int64, device=dev)
 x = torch.randn(16384 * 1024, device=dev).to(torch.bfloat16)
 o = torch.empty_like(x)
-fn = lambda: tpp.layernorm_blocked(x, 512, 16, 32, 64, 1e-5, out=o, exact=os.environ.get("LN_EXACT", "1") == "1")
+gam = torch.ones(1024, device=dev) if os.environ.get("LN_AFFINE") else None
+bet = torch.zeros(1024, device=dev) if os.environ.get("LN_AFFINE") else None
+fn = lambda: tpp.layernorm_blocked(x, 512, 16, 32, 64, 1e-5, gam, bet, out=o,
+                                   exact=os.environ.get("LN_EXACT", "1") == "1")
 NL = int(os.environ.get("NL", "3"))
 for it in range(2):
     buf.zero_()
