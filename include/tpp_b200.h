@@ -193,6 +193,25 @@ enum tpp_unary {
 int tpp_unary(int32_t kind, const tpp_tensor_desc* in_d, const void* inp, const void* aux,
               const tpp_tensor_desc* out_d, void* out, void* mask_out, void* stream);
 
+/* ---- PRNG / dropout (ops.py:195-236 PrngState, 326-328 PRNG, 378-382
+ * DROPOUT_INV, 430-444 DROPOUT).  A stream state is device memory holding
+ * uint32 [4][ncols] (the x, y, z, w words of every column's xorshift128
+ * stream).  Calls that advance a stream read state_in and write the advanced
+ * stream to state_out; the two buffers must not overlap. */
+/* PrngState(seed, ncols): splitmix64(seed ^ col) seeding, never all-zero */
+int tpp_prng_seed(uint64_t seed, int32_t ncols, uint32_t* state, void* stream);
+/* UnaryKind.PRNG: out (FP32, rows x cols) = uniform_block(rows) */
+int tpp_prng_fill(const uint32_t* state_in, uint32_t* state_out, const tpp_tensor_desc* out_d,
+                  float* out, void* stream);
+/* UnaryKind.DROPOUT: keep = u >= float32(p); mask_out = keep bitmask
+ * (tensor.py:246-254 layout); out = keep ? x * (1 / (1 - p)) : 0.  0 <= p < 1. */
+int tpp_dropout(const tpp_tensor_desc* in_d, const void* inp, const uint32_t* state_in,
+                uint32_t* state_out, double p, const tpp_tensor_desc* out_d, void* out,
+                uint8_t* mask_out, void* stream);
+/* UnaryKind.DROPOUT_INV: out = mask ? x * (1 / (1 - p)) : 0 (scale 0 if p >= 1) */
+int tpp_dropout_inv(const tpp_tensor_desc* in_d, const void* inp, const uint8_t* mask, double p,
+                    const tpp_tensor_desc* out_d, void* out, void* stream);
+
 /* ops.py:66-75 BinaryKind elementwise subset */
 enum tpp_binary { TPP_BIN_ADD = 0, TPP_BIN_SUB = 1, TPP_BIN_MUL = 2, TPP_BIN_DIV = 3,
                   TPP_BIN_MAX = 4, TPP_BIN_MIN = 5 };

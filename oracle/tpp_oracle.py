@@ -224,6 +224,72 @@ def mask_to_bool(mask: np.ndarray, rows: int, cols: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# PRNG / dropout — ops.py:195-236 (PrngState), 416-444 (_prng_fill, _dropout),
+# 378-382 (DROPOUT_INV)
+# ---------------------------------------------------------------------------
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """ops.py:195-199 (wrapping uint64 arithmetic)."""
+    with np.errstate(over="ignore"):
+        z = np.asarray(x, dtype=np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def prng_seed(seed: int, ncols: int) -> np.ndarray:
+    """ops.py:210-221 — returns uint32 [4, ncols] = (x, y, z, w)."""
+    base = np.arange(ncols, dtype=np.uint64) ^ np.uint64(int(seed) & 0xFFFFFFFFFFFFFFFF)
+    a = splitmix64(base)
+    b = splitmix64(a)
+    st = np.stack([a & np.uint64(0xFFFFFFFF), a >> np.uint64(32),
+                   b & np.uint64(0xFFFFFFFF), b >> np.uint64(32)]).astype(np.uint32)
+    dead = (st[0] | st[1] | st[2] | st[3]) == 0
+    st[3] = np.where(dead, np.uint32(1), st[3])
+    return st
+
+
+def prng_step(st: np.ndarray) -> np.ndarray:
+    """ops.py:223-228 — advances st in place, returns the new w words."""
+    x = st[0]
+    t = x ^ (x << np.uint32(11))
+    w = st[3]
+    nw = (w ^ (w >> np.uint32(19))) ^ (t ^ (t >> np.uint32(8)))
+    st[0], st[1], st[2] = st[1].copy(), st[2].copy(), w.copy()
+    st[3] = nw
+    return nw
+
+
+def prng_uniform_block(st: np.ndarray, rows: int) -> np.ndarray:
+    """ops.py:230-236 — rows x ncols FP32 in [0, 1); row i from step i+1."""
+    out = np.empty((rows, st.shape[1]), dtype=np.float32)
+    for i in range(rows):
+        w = prng_step(st)
+        out[i] = (w >> np.uint32(8)).astype(np.float32) * np.float32(2.0 ** -24)
+    return out
+
+
+def dropout(x: np.ndarray, st: np.ndarray, p: float):
+    """ops.py:430-444 — x already widened to its compute dtype; returns
+    (values in the compute dtype, keep bool[rows, cols])."""
+    u = prng_uniform_block(st, x.shape[0])
+    keep = u >= np.float32(p)
+    scale = x.dtype.type(1.0 / (1.0 - p))
+    with np.errstate(all="ignore"):
+        return np.where(keep, x * scale, x.dtype.type(0)), keep
+
+
+def dropout_inv(x: np.ndarray, keep: np.ndarray, p: float) -> np.ndarray:
+    """ops.py:378-382."""
+    scale = x.dtype.type(1.0 / (1.0 - p)) if p < 1.0 else x.dtype.type(0)
+    with np.errstate(all="ignore"):
+        return np.where(keep, x * scale, x.dtype.type(0))
+
+
+# ---------------------------------------------------------------------------
 # elementwise TPPs — ops.py:284-386, 747-816
 # ---------------------------------------------------------------------------
 

@@ -36,6 +36,7 @@ from .ops import (
     InvalidSpecError,
     Kernel,
     KernelSpec,
+    PrngState,
     ReduceAxis,
     ReduceOp,
     ReduceSpec,

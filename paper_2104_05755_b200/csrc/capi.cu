@@ -371,6 +371,59 @@ int tpp_unary(int32_t kind, const tpp_tensor_desc* in_d, const void* inp, const 
                       as_stream(stream));
 }
 
+// ---- PRNG / dropout (ops.py:195-236, 326-328, 378-382, 430-444) --------------
+int tpp_prng_seed(uint64_t seed, int32_t ncols, uint32_t* state, void* stream) {
+  TPP_REQUIRE(ncols >= 1 && state, TPP_E_TENSOR, "PrngState needs ncols >= 1 and a state buffer");
+  return launch_prng_seed(seed, ncols, state, as_stream(stream));
+}
+
+static bool states_disjoint(const uint32_t* a, const uint32_t* b, int cols) {
+  const uintptr_t n = (uintptr_t)4 * cols * sizeof(uint32_t);
+  const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+  return x + n <= y || y + n <= x;
+}
+
+int tpp_prng_fill(const uint32_t* state_in, uint32_t* state_out, const tpp_tensor_desc* out_d,
+                  float* out, void* stream) {
+  TPP_REQUIRE(valid_view(out_d) && out_d->bcast == TPP_BCAST_NONE, TPP_E_TENSOR, "bad PRNG output");
+  TPP_REQUIRE(out_d->dtype == TPP_FP32, TPP_E_SPEC_DTYPE, "PRNG output must be FP32");
+  TPP_REQUIRE(state_in && state_out && states_disjoint(state_in, state_out, out_d->cols), TPP_E_SPEC_FLAG,
+              "PRNG needs disjoint state_in / state_out buffers");
+  DView o = dview(out_d, out);
+  return launch_prng_tile(0, o, state_in, state_out, 0.0, out, TPP_FP32, out_d->ld, nullptr, out_d->rows,
+                          out_d->cols, false, as_stream(stream));
+}
+
+int tpp_dropout(const tpp_tensor_desc* in_d, const void* inp, const uint32_t* state_in, uint32_t* state_out,
+                double p, const tpp_tensor_desc* out_d, void* out, uint8_t* mask_out, void* stream) {
+  TPP_REQUIRE(valid_view(in_d) && valid_view(out_d), TPP_E_TENSOR, "bad dropout descriptor");
+  TPP_REQUIRE(in_d->rows == out_d->rows && in_d->cols == out_d->cols, TPP_E_TENSOR,
+              "DROPOUT output shape mismatch");
+  TPP_REQUIRE(out_d->bcast == TPP_BCAST_NONE, TPP_E_TENSOR, "output must not be a broadcast view");
+  TPP_REQUIRE(is_float(in_d->dtype) && is_float(out_d->dtype), TPP_E_UNSUPPORTED,
+              "GPU dropout covers FP32/BF16/FP64");
+  TPP_REQUIRE(p >= 0.0 && p < 1.0, TPP_E_SPEC_FLAG, "dropout p must be in [0, 1)");
+  TPP_REQUIRE(state_in && state_out && states_disjoint(state_in, state_out, in_d->cols), TPP_E_SPEC_FLAG,
+              "DROPOUT needs disjoint state_in / state_out buffers");
+  TPP_REQUIRE(mask_out, TPP_E_TENSOR, "DROPOUT needs a mask buffer");
+  const bool f64 = in_d->dtype == TPP_FP64;
+  return launch_prng_tile(1, dview(in_d, inp), state_in, state_out, p, out, out_d->dtype, out_d->ld, mask_out,
+                          in_d->rows, in_d->cols, f64, as_stream(stream));
+}
+
+int tpp_dropout_inv(const tpp_tensor_desc* in_d, const void* inp, const uint8_t* mask, double p,
+                    const tpp_tensor_desc* out_d, void* out, void* stream) {
+  TPP_REQUIRE(valid_view(in_d) && valid_view(out_d), TPP_E_TENSOR, "bad dropout descriptor");
+  TPP_REQUIRE(in_d->rows == out_d->rows && in_d->cols == out_d->cols, TPP_E_TENSOR,
+              "DROPOUT_INV output shape mismatch");
+  TPP_REQUIRE(out_d->bcast == TPP_BCAST_NONE, TPP_E_TENSOR, "output must not be a broadcast view");
+  TPP_REQUIRE(is_float(in_d->dtype) && is_float(out_d->dtype), TPP_E_UNSUPPORTED,
+              "GPU dropout covers FP32/BF16/FP64");
+  TPP_REQUIRE(mask, TPP_E_TENSOR, "DROPOUT_INV requires a recorded bitmask in secondary");
+  return launch_dropout_inv(dview(in_d, inp), mask, p, out, out_d->dtype, out_d->ld, in_d->dtype == TPP_FP64,
+                            as_stream(stream));
+}
+
 static int join_check(const tpp_tensor_desc* const* ds, int n, int* rows, int* cols) {
   int r = 0, c = 0;
   for (int i = 0; i < n; ++i) {

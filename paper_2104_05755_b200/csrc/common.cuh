@@ -201,4 +201,33 @@ __device__ __forceinline__ float exp_taylor(float x) {
   return out;
 }
 
+// Logical element (i, j) of a column-major view with ROW/COL/SCALAR broadcast
+// (tensor.py:207-217), widened exactly; stores narrow once (RNE for BF16).
+template <typename T>
+__device__ __forceinline__ T load_elem(const DView& v, int i, int j) {
+  const int pi = (v.bcast == TPP_BCAST_ROW || v.bcast == TPP_BCAST_SCALAR) ? 0 : i;
+  const int pj = (v.bcast == TPP_BCAST_COL || v.bcast == TPP_BCAST_SCALAR) ? 0 : j;
+  const int64_t idx = pi + (int64_t)pj * v.ld;
+  switch (v.dtype) {
+    case TPP_FP32: return (T) reinterpret_cast<const float*>(v.p)[idx];
+    case TPP_BF16: return (T)bf16_to_f32(reinterpret_cast<const uint16_t*>(v.p)[idx]);
+    case TPP_FP64: return (T) reinterpret_cast<const double*>(v.p)[idx];
+    case TPP_INT32: return (T) reinterpret_cast<const int32_t*>(v.p)[idx];
+    default: return T(0);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_elem(void* p, int dtype, int64_t idx, T v) {
+  switch (dtype) {
+    case TPP_FP32: reinterpret_cast<float*>(p)[idx] = (float)v; break;
+    case TPP_BF16: reinterpret_cast<uint16_t*>(p)[idx] = f32_to_bf16((float)v); break;
+    case TPP_FP64: reinterpret_cast<double*>(p)[idx] = (double)v; break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+
 }  // namespace tpp

@@ -266,6 +266,21 @@ vnni2_kernel(const uint16_t* __restrict__ in, int64_t in_ld, uint16_t* __restric
   }
 }
 
+// DROPOUT_INV (ops.py:378-382) on dense views: group g = mask byte g
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256)
+dropout_inv_vec_kernel(const void* __restrict__ in, const uint8_t* __restrict__ mask, float scale,
+                       void* __restrict__ out, int64_t groups) {
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups; g += (int64_t)gridDim.x * blockDim.x) {
+    float x[8];
+    Vec8<TI>::load(in, g, x);
+    const uint32_t b = __ldg(mask + g);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = ((b >> u) & 1u) ? __fmul_rn(x[u], scale) : 0.0f;
+    Vec8<TO>::store(out, g, x);
+  }
+}
+
 }  // namespace fast
 
 // 0 = handled, 1 = not applicable (fall back to the generic kernel)
@@ -367,6 +382,26 @@ int fast_transform(int kind, int esize, const void* in, int in_ld, void* out, in
     return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   return 1;
+}
+
+int fast_dropout_inv(const DView& in, const uint8_t* mask, float scale, void* out, int out_dtype, int out_ld,
+                     cudaStream_t s) {
+  using namespace fast;
+  const int rows = in.rows;
+  if (rows % 8 || out_ld != rows || !dense(in, rows) || reinterpret_cast<uintptr_t>(out) % 16) return 1;
+  if ((in.dtype != TPP_BF16 && in.dtype != TPP_FP32) || (out_dtype != TPP_BF16 && out_dtype != TPP_FP32)) return 1;
+  const int64_t groups = (int64_t)rows / 8 * in.cols;
+  if (groups == 0) return 0;
+  const unsigned grid = grid_for(groups);
+  if (in.dtype == TPP_BF16 && out_dtype == TPP_BF16)
+    dropout_inv_vec_kernel<uint16_t, uint16_t><<<grid, 256, 0, s>>>(in.p, mask, scale, out, groups);
+  else if (in.dtype == TPP_BF16)
+    dropout_inv_vec_kernel<uint16_t, float><<<grid, 256, 0, s>>>(in.p, mask, scale, out, groups);
+  else if (out_dtype == TPP_BF16)
+    dropout_inv_vec_kernel<float, uint16_t><<<grid, 256, 0, s>>>(in.p, mask, scale, out, groups);
+  else
+    dropout_inv_vec_kernel<float, float><<<grid, 256, 0, s>>>(in.p, mask, scale, out, groups);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
 
 }  // namespace tpp

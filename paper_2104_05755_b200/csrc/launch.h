@@ -64,12 +64,21 @@ struct DView {
   int rows, cols, ld, dtype, bcast;
 };
 // dense fast paths (eltwise_fast.cu): 0 handled, 1 not applicable, 2 launch error
+int fast_dropout_inv(const DView& in, const uint8_t* mask, float scale, void* out, int out_dtype, int out_ld,
+                     cudaStream_t s);
 int fast_unary(int kind, const DView& in, const DView& aux, void* out, int out_dtype, int out_ld, uint8_t* mask_out,
                cudaStream_t s);
 int fast_nary(int arity, int kind, const DView& a, const DView& b, const DView& c, void* out, int rows, int cols,
               int out_dtype, int out_ld, cudaStream_t s);
 int fast_transform(int kind, int esize, const void* in, int in_ld, void* out, int out_rows, int out_cols,
                    int out_ld, int alpha, int alpha_out, int lrows, int lcols, cudaStream_t s);
+// prng.cu (K8): xorshift128 streams, state SoA [4][cols]
+int launch_prng_seed(uint64_t seed, int cols, uint32_t* state, cudaStream_t s);
+int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t* st_out, double p,
+                     void* out, int out_dtype, int out_ld, uint8_t* mask_out, int rows, int cols, bool f64,
+                     cudaStream_t s);
+int launch_dropout_inv(const DView& in, const uint8_t* mask, double p, void* out, int out_dtype, int out_ld,
+                       bool f64, cudaStream_t s);
 int launch_unary(int kind, const DView& in, const DView& aux, void* out, int out_dtype, int out_ld,
                  uint8_t* mask_out, bool f64, cudaStream_t s);
 int launch_nary(int arity, int kind, const DView& a, const DView& b, const DView& c, void* out,

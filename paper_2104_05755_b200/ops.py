@@ -5,8 +5,10 @@ the GPU — a drop-in for ops.py of the reference
 Same operator enums, argument order, output-shape inference and exceptions.
 The kinds on the BRGEMM hot path
 run as sm_100a kernels, bitwise identical to the reference; kinds outside
-that scope (PRNG/dropout, quantize, gather/scatter, tanh/sigmoid, shuffle
-transpose) raise NotImplementedError instead of silently running elsewhere.
+that scope (quantize, gather/scatter, tanh/sigmoid, shuffle transpose) raise
+NotImplementedError instead of silently running elsewhere.  PRNG / DROPOUT /
+DROPOUT_INV run on the GPU with the reference's per-column
+xorshift128 streams, bitwise.
 """
 
 from __future__ import annotations
@@ -181,6 +183,124 @@ def _cuda(*views):
 
 
 # ---------------------------------------------------------------------------
+# PRNG state (ops.py:195-236)
+# ---------------------------------------------------------------------------
+
+class PrngState:
+    """Per-column Marsaglia xorshift128 streams (ops.py:202-236), resident on
+    the GPU as uint32 [4][ncols] (x, y, z, w rows).
+
+    Seeding is the reference's: splitmix64(seed ^ col), never all-zero.  A
+    call that draws advances the streams in place (the kernel writes the
+    advanced words to a second buffer and the two are swapped), so successive
+    DROPOUT calls see successive uniforms exactly as the reference's do.
+    """
+
+    def __init__(self, seed: int, ncols: int = 1, device=None):
+        if ncols < 1:
+            raise TensorError("PrngState needs ncols >= 1")
+        self.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        self.ncols = int(ncols)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self._bufs = [torch.empty((4, self.ncols), dtype=torch.int32, device=dev) for _ in range(2)]
+        self._cur = 0
+        lib = _lib.load()
+        _lib.check(lib.tpp_prng_seed(C.c_uint64(self.seed), self.ncols, self._bufs[0].data_ptr(),
+                                     _lib.stream_ptr(None)), "PrngState")
+
+    @property
+    def device(self) -> torch.device:
+        return self._bufs[0].device
+
+    def _io(self):
+        return self._bufs[self._cur], self._bufs[1 - self._cur]
+
+    def _advance(self) -> None:
+        self._cur = 1 - self._cur
+
+    def words(self) -> torch.Tensor:
+        """Current stream words as a uint32-valued int64 tensor [4, ncols]."""
+        return self._bufs[self._cur].to(torch.int64) & 0xFFFFFFFF
+
+    def _word(self, r: int):
+        return (self.words()[r].cpu().numpy()).astype("uint32")
+
+    x = property(lambda self: self._word(0))
+    y = property(lambda self: self._word(1))
+    z = property(lambda self: self._word(2))
+    w = property(lambda self: self._word(3))
+
+    def uniform_block(self, rows: int) -> torch.Tensor:
+        """rows x ncols FP32 uniforms in [0, 1) (ops.py:230-236), on the GPU."""
+        from .tensor import alloc
+        out = alloc(TensorDesc(rows, self.ncols, rows, DType.FP32), device=self.device)
+        _prng_fill_state(self, out, None)
+        return out.primary.view(self.ncols, rows).t()
+
+    def step(self):
+        """Advance every stream once; returns one 32-bit word per stream."""
+        self.uniform_block(1)
+        return self.w
+
+
+def _prng_fill_state(state: PrngState, out: TensorView, stream) -> None:
+    lib = _cuda(out)
+    src, dst = state._io()
+    _lib.check(lib.tpp_prng_fill(src.data_ptr(), dst.data_ptr(), out.desc.c(), out.ptr,
+                                 _lib.stream_ptr(stream)), "PRNG")
+    state._advance()
+
+
+def _prng_state_for(view: Optional[TensorView], cols: int, what: str) -> PrngState:
+    state = (view.tertiary or {}).get("prng") if view is not None else None
+    if state is None:
+        raise InvalidSpecError("flag", f"{what} needs a PrngState in tertiary")
+    if state.ncols != cols:  # ops.py:425-426 / 438-439: a fresh stream set, not persisted
+        state = PrngState(state.seed, cols, device=state.device)
+    return state
+
+
+def _prng_fill(inp: Optional[TensorView], out: TensorView, stream=None) -> None:
+    """ops.py:416-427."""
+    if out.desc.dtype is not DType.FP32:
+        raise InvalidSpecError("dtype", "PRNG output must be FP32")
+    state = _prng_state_for(inp, out.desc.cols, "PRNG")
+    _prng_fill_state(state, out, stream)
+
+
+def _dropout(inp: TensorView, out: TensorView, p: Optional[float], stream=None) -> None:
+    """ops.py:430-444: keep = u >= float32(p); out = keep ? x / (1 - p) : 0."""
+    _require_logical_shape(out, inp.desc.rows, inp.desc.cols, f"{UnaryKind.DROPOUT} output")
+    if p is None:
+        raise InvalidSpecError("flag", "DROPOUT needs the drop probability p")
+    if not 0.0 <= p < 1.0:
+        raise InvalidSpecError("flag", f"dropout p must be in [0, 1), got {p}")
+    state = _prng_state_for(inp, inp.desc.cols, "DROPOUT")
+    lib = _cuda(inp, out)
+    # every mask byte (padding bits included) is written by the kernel
+    mask = torch.empty(bitmask_bytes(inp.desc.rows, inp.desc.cols), dtype=torch.uint8,
+                       device=out.primary.device)
+    src, dst = state._io()
+    _lib.check(lib.tpp_dropout(inp.desc.c(), inp.ptr, src.data_ptr(), dst.data_ptr(), float(p),
+                               out.desc.c(), out.ptr, mask.data_ptr(), _lib.stream_ptr(stream)),
+               "DROPOUT")
+    state._advance()
+    out.secondary = mask
+
+
+def _dropout_inv(inp: TensorView, out: TensorView, p: Optional[float], stream=None) -> None:
+    """ops.py:378-382."""
+    _require_logical_shape(out, inp.desc.rows, inp.desc.cols, f"{UnaryKind.DROPOUT_INV} output")
+    if p is None:
+        raise InvalidSpecError("flag", "DROPOUT_INV needs the keep probability")
+    if inp.secondary is None:
+        raise TensorError("DROPOUT_INV requires a recorded bitmask in secondary")
+    lib = _cuda(inp, out)
+    _lib.check(lib.tpp_dropout_inv(inp.desc.c(), inp.ptr, inp.secondary.data_ptr(), float(p),
+                                   out.desc.c(), out.ptr, _lib.stream_ptr(stream)), "DROPOUT_INV")
+
+
+# ---------------------------------------------------------------------------
 # unary (ops.py:284-386)
 # ---------------------------------------------------------------------------
 
@@ -209,8 +329,17 @@ def apply_unary(kind: UnaryKind, inp: Optional[TensorView], out: TensorView,
             raise InvalidSpecError("flag", "TRANSFORM needs a TransformSpec")
         transform(inp, transform_spec, out, stream=stream)
         return
+    if kind is UnaryKind.PRNG:
+        _prng_fill(inp, out, stream)
+        return
     if kind in (UnaryKind.STRIDED_LOAD, UnaryKind.STRIDED_STORE):
         raise InvalidSpecError("flag", "use strided_load/strided_store helpers")
+    if kind is UnaryKind.DROPOUT:
+        _dropout(inp, out, dropout_p, stream)
+        return
+    if kind is UnaryKind.DROPOUT_INV:
+        _dropout_inv(inp, out, dropout_p, stream)
+        return
     if kind not in _UNARY_CODE:
         raise NotImplementedError(f"{kind}: {_OUT_OF_SCOPE}")
     sel = approx_flag or DEFAULT_APPROX.get(kind)

@@ -375,6 +375,67 @@ def gen_dilated():
     save("dilated.npz", **out)
 
 
+def gen_prng():
+    """PrngState seeding, PRNG fills and DROPOUT / DROPOUT_INV through the
+    reference's apply_unary (ops.py:195-236, 326-328, 378-382, 430-444)."""
+    P = tp.ops.PrngState
+    seeds = np.array([0, 1, 123, 2024, (1 << 64) - 1], dtype=np.uint64)
+    seed_words = np.stack([np.stack([P(int(s), 8).x, P(int(s), 8).y, P(int(s), 8).z, P(int(s), 8).w])
+                           for s in seeds])
+    # two successive PRNG fills from one state (the second continues the streams)
+    src = tp.alloc(tp.TensorDesc(1, 1, 1, tp.DType.FP32))
+    st = P(123, 6)
+    src.tertiary = {"prng": st}
+    f1 = tp.alloc(tp.TensorDesc(64, 6, 64, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.PRNG, src, f1)
+    f2 = tp.alloc(tp.TensorDesc(37, 6, 40, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.PRNG, src, f2)
+    state_after = np.stack([st.x, st.y, st.z, st.w])
+    # a long fill: jump-ahead across many 64-row segments; keep sampled rows
+    lst = P(99, 3)
+    lsrc = tp.alloc(tp.TensorDesc(1, 1, 1, tp.DType.FP32))
+    lsrc.tertiary = {"prng": lst}
+    long_rows = 70_001
+    lf = tp.alloc(tp.TensorDesc(long_rows, 3, long_rows, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.PRNG, lsrc, lf)
+    long_idx = np.concatenate([np.arange(0, long_rows, 997), np.arange(long_rows - 70, long_rows)])
+    long_sample = tp.to_array(lf)[long_idx]
+    long_state = np.stack([lst.x, lst.y, lst.z, lst.w])
+    # dropout fp32, twice from one state, then the backward of the first
+    rng = np.random.default_rng(16)
+    m, n = 37, 29
+    x = rng.standard_normal((m, n)).astype(np.float32)
+    x[0, :4] = [np.nan, np.inf, -0.0, 0.0]
+    xv = tp.from_array(x)
+    dst = P(7, n)
+    xv.tertiary = {"prng": dst}
+    d1 = tp.alloc(tp.TensorDesc(m, n, m, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.DROPOUT, xv, d1, dropout_p=0.3)
+    d2 = tp.alloc(tp.TensorDesc(m, n, m, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.DROPOUT, xv, d2, dropout_p=0.3)
+    dy = rng.standard_normal((m, n)).astype(np.float32)
+    dyv = tp.from_array(dy)
+    dyv.secondary = d1.secondary
+    di = tp.alloc(tp.TensorDesc(m, n, m, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.DROPOUT_INV, dyv, di, dropout_p=0.3)
+    di1 = tp.alloc(tp.TensorDesc(m, n, m, tp.DType.FP32))
+    tp.apply_unary(tp.UnaryKind.DROPOUT_INV, dyv, di1, dropout_p=1.0)
+    # bf16 in / out, p = 0.1; state built for the wrong width (fresh streams)
+    xb = tp.from_array(x, tp.DType.BF16)
+    wrong = P(5, 4)
+    xb.tertiary = {"prng": wrong}
+    db = tp.alloc(tp.TensorDesc(m, n, m, tp.DType.BF16))
+    tp.apply_unary(tp.UnaryKind.DROPOUT, xb, db, dropout_p=0.1)
+    wrong_after = np.stack([wrong.x, wrong.y, wrong.z, wrong.w])
+    save("prng.npz", seeds=seeds, seed_words=seed_words, fill1=np.array(f1.primary),
+         fill2=np.array(f2.primary), state_after=state_after, long_rows=np.int64(long_rows),
+         long_idx=long_idx, long_sample=long_sample, long_state=long_state, x=x, dy=dy,
+         d1=np.array(d1.primary), m1=np.array(d1.secondary), d2=np.array(d2.primary),
+         m2=np.array(d2.secondary), dinv=np.array(di.primary), dinv_p1=np.array(di1.primary),
+         xb=np.array(xb.primary), db=np.array(db.primary), mb=np.array(db.secondary),
+         wrong_after=wrong_after)
+
+
 if __name__ == "__main__":
     gen_dtypes()
     gen_cfg1()
@@ -386,3 +447,4 @@ if __name__ == "__main__":
     gen_fc()
     gen_conv()
     gen_dilated()
+    gen_prng()

@@ -581,3 +581,130 @@ def test_layernorm_blocked_tolerance_mode():
     assert normwise(mf, me) <= 1e-5 and normwise(vf, ve) <= 1e-5
     assert normwise(bf16_bits_to_f32(of), bf16_bits_to_f32(oe)) <= BF16_TOL
     assert np.mean(of == oe) > 0.95
+
+
+# ---------------------------------------------------------------------------
+# PRNG / DROPOUT / DROPOUT_INV (ops.py:195-236, 378-382, 430-444): bitwise
+# ---------------------------------------------------------------------------
+
+def _words(st):
+    return st.words().cpu().numpy().astype(np.uint32)
+
+
+def test_prng_seed_and_fill_bitwise(golden):
+    g = golden("prng.npz")
+    for s, want in zip(g["seeds"], g["seed_words"]):
+        assert np.array_equal(_words(tpp.PrngState(int(s), 8)), want)
+    src = tpp.alloc(tpp.TensorDesc(1, 1, 1, tpp.DType.FP32))
+    st = tpp.PrngState(123, 6)
+    src.tertiary = {"prng": st}
+    f1 = tpp.alloc(tpp.TensorDesc(64, 6, 64, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.PRNG, src, f1)
+    assert bits(to_host(f1.primary)) == bits(g["fill1"])
+    f2 = tpp.alloc(tpp.TensorDesc(37, 6, 40, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.PRNG, src, f2)
+    got = O.strided2d(to_host(f2.primary), 0, 37, 6, 40)
+    assert bits(got) == bits(O.strided2d(g["fill2"], 0, 37, 6, 40))
+    assert np.array_equal(_words(st), g["state_after"])
+    # 70001 rows: 1094 row segments reached through the GF(2) jump tables
+    lst = tpp.PrngState(99, 3)
+    lsrc = tpp.alloc(tpp.TensorDesc(1, 1, 1, tpp.DType.FP32))
+    lsrc.tertiary = {"prng": lst}
+    n = int(g["long_rows"])
+    lf = tpp.alloc(tpp.TensorDesc(n, 3, n, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.PRNG, lsrc, lf)
+    assert bits(tpp.to_array(lf)[g["long_idx"]]) == bits(g["long_sample"])
+    assert np.array_equal(_words(lst), g["long_state"])
+
+
+def test_dropout_bitwise(golden):
+    g = golden("prng.npz")
+    x = g["x"]
+    m, n = x.shape
+    xv = tpp.from_array(x)
+    xv.tertiary = {"prng": tpp.PrngState(7, n)}
+    d1 = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT, xv, d1, dropout_p=0.3)
+    d2 = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT, xv, d2, dropout_p=0.3)
+    assert bits(to_host(d1.primary)) == bits(g["d1"]) and bits(to_host(d2.primary)) == bits(g["d2"])
+    assert np.array_equal(to_host(d1.secondary), g["m1"])
+    assert np.array_equal(to_host(d2.secondary), g["m2"])
+    dyv = tpp.from_array(g["dy"])
+    dyv.secondary = d1.secondary
+    di = tpp.alloc(d1.desc)
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT_INV, dyv, di, dropout_p=0.3)
+    assert bits(to_host(di.primary)) == bits(g["dinv"])
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT_INV, dyv, di, dropout_p=1.0)
+    assert bits(to_host(di.primary)) == bits(g["dinv_p1"])
+    xb = tpp.from_array(x, tpp.DType.BF16)
+    wrong = tpp.PrngState(5, 4)
+    xb.tertiary = {"prng": wrong}
+    db = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.BF16))
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT, xb, db, dropout_p=0.1)
+    assert bf16_equal(to_host(db.primary), g["db"])
+    assert np.array_equal(to_host(db.secondary), g["mb"])
+    assert np.array_equal(_words(wrong), g["wrong_after"])
+
+
+@pytest.mark.parametrize("rows,cols,ld,p,dt", [
+    (4096, 1024, 4096, 0.1, "fp32"),    # full-size activation block
+    (1000, 77, 1003, 0.5, "fp32"),      # ragged tile edges, padded ld
+    (513, 33, 513, 0.9, "bf16"),
+    (130, 5, 130, 0.25, "fp64"),
+    (64, 3, 64, 0.99999999, "fp32"),    # float32(p) == 1.0: nothing kept
+    (4100, 40, 4100, 0.0, "bf16"),      # p = 0: everything kept, scale 1
+])
+def test_dropout_matches_oracle(rows, cols, ld, p, dt):
+    rng = np.random.default_rng(rows + cols)
+    x = rng.standard_normal((rows, cols))
+    if dt == "fp32":
+        x = x.astype(np.float32)
+    dtype = {"fp32": tpp.DType.FP32, "bf16": tpp.DType.BF16, "fp64": tpp.DType.FP64}[dt]
+    buf = np.zeros(ld * (cols - 1) + rows, dtype=np.float64 if dt == "fp64" else np.float32)
+    for j in range(cols):
+        buf[j * ld: j * ld + rows] = x[:, j]
+    desc = tpp.TensorDesc(rows, cols, ld, dtype)
+    if dt == "bf16":
+        xv = tpp.from_array(x.astype(np.float32), dtype)
+        xw = O.bf16_to_fp32(tpp.bits_of(xv))
+    else:
+        xv = tpp.TensorView(desc, to_dev(buf))
+        xw = x
+    xv.tertiary = {"prng": tpp.PrngState(2024, cols)}
+    out = tpp.alloc(tpp.TensorDesc(rows, cols, rows, dtype))
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT, xv, out, dropout_p=p)
+    want, keep = O.dropout(xw, O.prng_seed(2024, cols), p)
+    assert np.array_equal(to_host(out.secondary), O.bool_to_mask(keep))
+    if dt == "bf16":
+        assert np.array_equal(tpp.bits_of(out), O.fp32_to_bf16_rne(want))
+    else:
+        assert bits(tpp.to_array(out)) == bits(want)
+
+
+def test_dropout_statistics_and_errors():
+    """verify.check_dropout: keep rate within 3 sigma of 1-p over 10^6 draws,
+    kept values exactly 1/(1-p); InvalidSpecError without a state or p out of
+    range (test_ops.py:526-556)."""
+    m = n = 1000
+    ones = np.ones((m, n), dtype=np.float32)
+    for p in (0.1, 0.5, 0.9):
+        v = tpp.from_array(ones)
+        v.tertiary = {"prng": tpp.PrngState(2024, n)}
+        out = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+        tpp.apply_unary(tpp.UnaryKind.DROPOUT, v, out, dropout_p=p)
+        keep = tpp.mask_to_bool(out.secondary, m, n)
+        vals = tpp.to_array(out)
+        sigma = (p * (1 - p) / (m * n)) ** 0.5
+        assert abs(keep.mean() - (1 - p)) <= 3 * sigma
+        assert np.all(vals[~keep] == 0)
+        assert np.all(vals[keep] == np.float32(1 / (1 - p)))
+    x = tpp.from_array(np.ones((2, 2), dtype=np.float32))
+    out = tpp.alloc(tpp.TensorDesc(2, 2, 2, tpp.DType.FP32))
+    with pytest.raises(tpp.InvalidSpecError):
+        tpp.apply_unary(tpp.UnaryKind.DROPOUT, x, out, dropout_p=0.5)
+    x.tertiary = {"prng": tpp.PrngState(0, 2)}
+    with pytest.raises(tpp.InvalidSpecError):
+        tpp.apply_unary(tpp.UnaryKind.DROPOUT, x, out, dropout_p=1.5)
+    tpp.apply_unary(tpp.UnaryKind.DROPOUT, x, out, dropout_p=0.0)
+    assert np.all(tpp.to_array(out) == 1.0)

@@ -159,3 +159,34 @@ def test_dilated_conv1d(golden):
         c, k, s, d, w, q = (int(v) for v in g[f"{name}_shape"])
         out = O.dilated_conv1d(g[f"{name}_x"], g[f"{name}_w"], c, k, s, d, q)
         assert bits(out) == bits(g[f"{name}_out"]), name
+
+
+def test_prng_and_dropout(golden):
+    """PrngState seeding, uniform fills (incl. a 70001-row stream) and
+    DROPOUT / DROPOUT_INV, bitwise (ops.py:195-236, 378-382, 430-444)."""
+    g = golden("prng.npz")
+    for s, want in zip(g["seeds"], g["seed_words"]):
+        assert np.array_equal(O.prng_seed(int(s), 8), want)
+    st = O.prng_seed(123, 6)
+    assert bits(O.prng_uniform_block(st, 64).T.reshape(-1)) == bits(g["fill1"])
+    f2 = O.prng_uniform_block(st, 37)
+    assert bits(f2) == bits(O.strided2d(g["fill2"], 0, 37, 6, 40))
+    assert np.array_equal(st, g["state_after"])
+    lst = O.prng_seed(99, 3)
+    lf = O.prng_uniform_block(lst, int(g["long_rows"]))
+    assert bits(lf[g["long_idx"]]) == bits(g["long_sample"])
+    assert np.array_equal(lst, g["long_state"])
+    x = g["x"]
+    m, n = x.shape
+    dst = O.prng_seed(7, n)
+    r1, k1 = O.dropout(x, dst, 0.3)
+    r2, k2 = O.dropout(x, dst, 0.3)
+    assert bits(r1.T.reshape(-1)) == bits(g["d1"]) and bits(r2.T.reshape(-1)) == bits(g["d2"])
+    assert np.array_equal(O.bool_to_mask(k1), g["m1"]) and np.array_equal(O.bool_to_mask(k2), g["m2"])
+    assert bits(O.dropout_inv(g["dy"], k1, 0.3).T.reshape(-1)) == bits(g["dinv"])
+    assert bits(O.dropout_inv(g["dy"], k1, 1.0).T.reshape(-1)) == bits(g["dinv_p1"])
+    xb = O.bf16_to_fp32(g["xb"]).reshape(n, m).T
+    rb, kb = O.dropout(xb, O.prng_seed(5, n), 0.1)
+    assert np.array_equal(O.fp32_to_bf16_rne(rb.T.reshape(-1)), g["db"])
+    assert np.array_equal(O.bool_to_mask(kb), g["mb"])
+    assert np.array_equal(O.prng_seed(5, 4), g["wrong_after"])  # wrong-width state untouched
