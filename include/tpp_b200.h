@@ -212,6 +212,19 @@ int tpp_dropout(const tpp_tensor_desc* in_d, const void* inp, const uint32_t* st
 int tpp_dropout_inv(const tpp_tensor_desc* in_d, const void* inp, const uint8_t* mask, double p,
                     const tpp_tensor_desc* out_d, void* out, void* stream);
 
+/* ---- QUANTIZE / DEQUANTIZE (ops.py:447-469), symmetric per-tensor INT8 ----
+ * tpp_quantize: FP32 view -> INT8 (same logical shape).  has_scale = 0:
+ * scale = max|x| / 127 (1.0 if that max is not > 0); else the given scale.
+ * q = clip(rint(x / scale), -127, 127) in double, NaN -> 0.  workspace: 4
+ * bytes of device memory; scale_out: device double receiving the scale used
+ * (the reference's out.tertiary["scale"]). */
+int tpp_quantize(const tpp_tensor_desc* in_d, const float* inp, int32_t has_scale, double scale,
+                 const tpp_tensor_desc* out_d, int8_t* out, void* workspace, double* scale_out,
+                 void* stream);
+/* tpp_dequantize: INT8 view -> FP32, float32(q) * float32(scale) */
+int tpp_dequantize(const tpp_tensor_desc* in_d, const int8_t* inp, double scale,
+                   const tpp_tensor_desc* out_d, float* out, void* stream);
+
 /* ops.py:66-75 BinaryKind elementwise subset */
 enum tpp_binary { TPP_BIN_ADD = 0, TPP_BIN_SUB = 1, TPP_BIN_MUL = 2, TPP_BIN_DIV = 3,
                   TPP_BIN_MAX = 4, TPP_BIN_MIN = 5 };

@@ -290,6 +290,28 @@ def dropout_inv(x: np.ndarray, keep: np.ndarray, p: float) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# QUANTIZE / DEQUANTIZE — ops.py:447-469
+# ---------------------------------------------------------------------------
+
+
+def quantize(x: np.ndarray, scale=None):
+    """ops.py:447-460 — returns (int8 array, scale used)."""
+    xd = np.asarray(x, dtype=np.float32).astype(np.float64)
+    if scale is None:
+        amax = float(np.max(np.abs(xd))) if xd.size else 0.0
+        scale = amax / 127.0 if amax > 0 else 1.0
+    with np.errstate(all="ignore"):
+        q = np.clip(np.rint(xd / scale), -127, 127)
+    q = np.where(np.isnan(q), 0.0, q).astype(np.int8)  # float64 NaN -> int8 is 0 on x86
+    return q, float(scale)
+
+
+def dequantize(q: np.ndarray, scale: float) -> np.ndarray:
+    """ops.py:463-469."""
+    return np.asarray(q).astype(np.float32) * np.float32(scale)
+
+
+# ---------------------------------------------------------------------------
 # elementwise TPPs — ops.py:284-386, 747-816
 # ---------------------------------------------------------------------------
 

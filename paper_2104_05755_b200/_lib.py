@@ -100,6 +100,10 @@ _SIGS = {
                               C.POINTER(TensorDescC), _P, _P]),
     "tpp_split_sgd": (C.c_int, [_I64, _P, _P, _P, _I32, C.c_float, _P]),
     "tpp_debug_phase_timestamps": (C.c_int, [_P]),
+    "tpp_quantize": (C.c_int, [C.POINTER(TensorDescC), _P, _I32, C.c_double,
+                               C.POINTER(TensorDescC), _P, _P, _P, _P]),
+    "tpp_dequantize": (C.c_int, [C.POINTER(TensorDescC), _P, C.c_double,
+                                 C.POINTER(TensorDescC), _P, _P]),
     "tpp_prng_seed": (C.c_int, [C.c_uint64, _I32, _P, _P]),
     "tpp_prng_fill": (C.c_int, [_P, _P, C.POINTER(TensorDescC), _P, _P]),
     "tpp_dropout": (C.c_int, [C.POINTER(TensorDescC), _P, _P, _P, C.c_double,

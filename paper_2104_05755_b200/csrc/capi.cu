@@ -424,6 +424,29 @@ int tpp_dropout_inv(const tpp_tensor_desc* in_d, const void* inp, const uint8_t*
                             as_stream(stream));
 }
 
+// ---- QUANTIZE / DEQUANTIZE (ops.py:447-469) -----------------------------------
+int tpp_quantize(const tpp_tensor_desc* in_d, const float* inp, int32_t has_scale, double scale,
+                 const tpp_tensor_desc* out_d, int8_t* out, void* workspace, double* scale_out, void* stream) {
+  TPP_REQUIRE(valid_view(in_d) && valid_view(out_d), TPP_E_TENSOR, "bad quantize descriptor");
+  TPP_REQUIRE(in_d->dtype == TPP_FP32 && out_d->dtype == TPP_INT8, TPP_E_SPEC_DTYPE, "QUANTIZE is FP32 -> INT8");
+  TPP_REQUIRE(in_d->rows == out_d->rows && in_d->cols == out_d->cols, TPP_E_TENSOR,
+              "QUANTIZE output shape mismatch");
+  TPP_REQUIRE(out_d->bcast == TPP_BCAST_NONE, TPP_E_TENSOR, "output must not be a broadcast view");
+  TPP_REQUIRE(has_scale || workspace, TPP_E_TENSOR, "QUANTIZE without a scale needs a 4-byte workspace");
+  return launch_quantize(dview(in_d, inp), has_scale, scale, out, out_d->ld,
+                         reinterpret_cast<uint32_t*>(workspace), scale_out, as_stream(stream));
+}
+
+int tpp_dequantize(const tpp_tensor_desc* in_d, const int8_t* inp, double scale, const tpp_tensor_desc* out_d,
+                   float* out, void* stream) {
+  TPP_REQUIRE(valid_view(in_d) && valid_view(out_d), TPP_E_TENSOR, "bad dequantize descriptor");
+  TPP_REQUIRE(in_d->dtype == TPP_INT8 && out_d->dtype == TPP_FP32, TPP_E_SPEC_DTYPE, "DEQUANTIZE is INT8 -> FP32");
+  TPP_REQUIRE(in_d->rows == out_d->rows && in_d->cols == out_d->cols, TPP_E_TENSOR,
+              "DEQUANTIZE output shape mismatch");
+  TPP_REQUIRE(out_d->bcast == TPP_BCAST_NONE, TPP_E_TENSOR, "output must not be a broadcast view");
+  return launch_dequantize(dview(in_d, inp), scale, out, out_d->ld, as_stream(stream));
+}
+
 static int join_check(const tpp_tensor_desc* const* ds, int n, int* rows, int* cols) {
   int r = 0, c = 0;
   for (int i = 0; i < n; ++i) {

@@ -213,6 +213,7 @@ __device__ __forceinline__ T load_elem(const DView& v, int i, int j) {
     case TPP_BF16: return (T)bf16_to_f32(reinterpret_cast<const uint16_t*>(v.p)[idx]);
     case TPP_FP64: return (T) reinterpret_cast<const double*>(v.p)[idx];
     case TPP_INT32: return (T) reinterpret_cast<const int32_t*>(v.p)[idx];
+    case TPP_INT8: return (T) reinterpret_cast<const int8_t*>(v.p)[idx];
     default: return T(0);
   }
 }

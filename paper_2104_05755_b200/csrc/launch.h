@@ -79,6 +79,10 @@ int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t*
                      cudaStream_t s);
 int launch_dropout_inv(const DView& in, const uint8_t* mask, double p, void* out, int out_dtype, int out_ld,
                        bool f64, cudaStream_t s);
+// quant.cu (K9)
+int launch_quantize(const DView& in, int has_scale, double scale, int8_t* out, int out_ld, uint32_t* amax_ws,
+                    double* scale_out, cudaStream_t s);
+int launch_dequantize(const DView& in, double scale, float* out, int out_ld, cudaStream_t s);
 int launch_unary(int kind, const DView& in, const DView& aux, void* out, int out_dtype, int out_ld,
                  uint8_t* mask_out, bool f64, cudaStream_t s);
 int launch_nary(int arity, int kind, const DView& a, const DView& b, const DView& c, void* out,

@@ -5,10 +5,11 @@ the GPU — a drop-in for ops.py of the reference
 Same operator enums, argument order, output-shape inference and exceptions.
 The kinds on the BRGEMM hot path
 run as sm_100a kernels, bitwise identical to the reference; kinds outside
-that scope (quantize, gather/scatter, tanh/sigmoid, shuffle transpose) raise
+that scope (gather/scatter, tanh/sigmoid, shuffle transpose) raise
 NotImplementedError instead of silently running elsewhere.  PRNG / DROPOUT /
 DROPOUT_INV run on the GPU with the reference's per-column
-xorshift128 streams, bitwise.
+xorshift128 streams, bitwise; QUANTIZE / DEQUANTIZE (the INT8 BRGEMM's
+neighbours) likewise.
 """
 
 from __future__ import annotations
@@ -300,6 +301,37 @@ def _dropout_inv(inp: TensorView, out: TensorView, p: Optional[float], stream=No
                                    out.desc.c(), out.ptr, _lib.stream_ptr(stream)), "DROPOUT_INV")
 
 
+def _quantize(inp: TensorView, out: TensorView, stream=None) -> None:
+    """ops.py:447-460: symmetric per-tensor INT8; the scale lands in
+    out.tertiary['scale'] (read back to the host, as the reference's is a
+    Python float)."""
+    if inp.desc.dtype is not DType.FP32 or out.desc.dtype is not DType.INT8:
+        raise InvalidSpecError("dtype", "QUANTIZE is FP32 -> INT8")
+    _require_logical_shape(out, inp.desc.rows, inp.desc.cols, "QUANTIZE output")
+    lib = _cuda(inp, out)
+    scale = (inp.tertiary or {}).get("scale")
+    dev = out.primary.device
+    ws = torch.empty(2, dtype=torch.float64, device=dev)  # [0]: amax word, [1]: scale used
+    _lib.check(lib.tpp_quantize(inp.desc.c(), inp.ptr, 0 if scale is None else 1,
+                                0.0 if scale is None else float(scale), out.desc.c(), out.ptr,
+                                ws.data_ptr(), ws.data_ptr() + 8, _lib.stream_ptr(stream)), "QUANTIZE")
+    out.tertiary = dict(out.tertiary or {})
+    out.tertiary["scale"] = float(ws[1].item())
+
+
+def _dequantize(inp: TensorView, out: TensorView, stream=None) -> None:
+    """ops.py:463-469."""
+    if inp.desc.dtype is not DType.INT8 or out.desc.dtype is not DType.FP32:
+        raise InvalidSpecError("dtype", "DEQUANTIZE is INT8 -> FP32")
+    scale = (inp.tertiary or {}).get("scale")
+    if scale is None:
+        raise InvalidSpecError("flag", "DEQUANTIZE needs tertiary['scale']")
+    _require_logical_shape(out, inp.desc.rows, inp.desc.cols, "DEQUANTIZE output")
+    lib = _cuda(inp, out)
+    _lib.check(lib.tpp_dequantize(inp.desc.c(), inp.ptr, float(scale), out.desc.c(), out.ptr,
+                                  _lib.stream_ptr(stream)), "DEQUANTIZE")
+
+
 # ---------------------------------------------------------------------------
 # unary (ops.py:284-386)
 # ---------------------------------------------------------------------------
@@ -331,6 +363,12 @@ def apply_unary(kind: UnaryKind, inp: Optional[TensorView], out: TensorView,
         return
     if kind is UnaryKind.PRNG:
         _prng_fill(inp, out, stream)
+        return
+    if kind is UnaryKind.QUANTIZE:
+        _quantize(inp, out, stream)
+        return
+    if kind is UnaryKind.DEQUANTIZE:
+        _dequantize(inp, out, stream)
         return
     if kind in (UnaryKind.STRIDED_LOAD, UnaryKind.STRIDED_STORE):
         raise InvalidSpecError("flag", "use strided_load/strided_store helpers")

@@ -436,6 +436,41 @@ def gen_prng():
          wrong_after=wrong_after)
 
 
+def gen_quant():
+    """QUANTIZE / DEQUANTIZE through the reference's apply_unary (ops.py:447-469)."""
+    rng = np.random.default_rng(17)
+    cases = {
+        "uniform": rng.uniform(-2, 2, (8, 8)).astype(np.float32),
+        "normal": (rng.standard_normal((37, 29)) * 3).astype(np.float32),
+        "nan": rng.standard_normal((9, 5)).astype(np.float32),
+        "zeros": np.zeros((4, 3), dtype=np.float32),
+    }
+    cases["nan"][2, 3] = np.nan
+    # exact ties: amax 127 -> scale 1.0, so k + 0.5 must round to even
+    ties = np.arange(-16, 16, dtype=np.float32).reshape(8, 4) + np.float32(0.5)
+    ties[0, 0] = 127.0
+    cases["ties"] = ties
+    out = {}
+    for name, x in cases.items():
+        xv = tp.from_array(x)
+        q = tp.alloc(tp.TensorDesc(x.shape[0], x.shape[1], x.shape[0], tp.DType.INT8))
+        tp.apply_unary(tp.UnaryKind.QUANTIZE, xv, q)
+        d = tp.alloc(tp.TensorDesc(x.shape[0], x.shape[1], x.shape[0], tp.DType.FP32))
+        tp.apply_unary(tp.UnaryKind.DEQUANTIZE, q, d)
+        out[name + "_x"] = x
+        out[name + "_q"] = np.array(q.primary)
+        out[name + "_scale"] = np.float64(q.tertiary["scale"])
+        out[name + "_d"] = np.array(d.primary)
+    # caller-provided scale (saturates at +-127)
+    x = cases["normal"]
+    xv = tp.from_array(x)
+    xv.tertiary = {"scale": 0.01}
+    q = tp.alloc(tp.TensorDesc(37, 29, 37, tp.DType.INT8))
+    tp.apply_unary(tp.UnaryKind.QUANTIZE, xv, q)
+    out["given_q"] = np.array(q.primary)
+    save("quant.npz", **out)
+
+
 if __name__ == "__main__":
     gen_dtypes()
     gen_cfg1()
@@ -448,3 +483,4 @@ if __name__ == "__main__":
     gen_conv()
     gen_dilated()
     gen_prng()
+    gen_quant()

@@ -708,3 +708,39 @@ def test_dropout_statistics_and_errors():
         tpp.apply_unary(tpp.UnaryKind.DROPOUT, x, out, dropout_p=1.5)
     tpp.apply_unary(tpp.UnaryKind.DROPOUT, x, out, dropout_p=0.0)
     assert np.all(tpp.to_array(out) == 1.0)
+
+
+# ---------------------------------------------------------------------------
+# QUANTIZE / DEQUANTIZE (ops.py:447-469): bitwise
+# ---------------------------------------------------------------------------
+
+def test_quantize_dequantize_bitwise(golden):
+    g = golden("quant.npz")
+    for name in ("uniform", "normal", "nan", "zeros", "ties"):
+        x = g[name + "_x"]
+        m, n = x.shape
+        q = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.INT8))
+        tpp.apply_unary(tpp.UnaryKind.QUANTIZE, tpp.from_array(x), q)
+        assert q.tertiary["scale"] == float(g[name + "_scale"]), name
+        assert np.array_equal(to_host(q.primary), g[name + "_q"]), name
+        d = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+        tpp.apply_unary(tpp.UnaryKind.DEQUANTIZE, q, d)
+        assert bits(to_host(d.primary)) == bits(g[name + "_d"]), name
+    xv = tpp.from_array(g["normal_x"])
+    xv.tertiary = {"scale": 0.01}
+    q = tpp.alloc(tpp.TensorDesc(37, 29, 37, tpp.DType.INT8))
+    tpp.apply_unary(tpp.UnaryKind.QUANTIZE, xv, q)
+    assert np.array_equal(to_host(q.primary), g["given_q"])
+
+
+def test_quantize_full_size_matches_oracle():
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((2048, 1536)) * 4).astype(np.float32)
+    q = tpp.alloc(tpp.TensorDesc(2048, 1536, 2048, tpp.DType.INT8))
+    tpp.apply_unary(tpp.UnaryKind.QUANTIZE, tpp.from_array(x), q)
+    want, scale = O.quantize(x)
+    assert q.tertiary["scale"] == scale
+    assert np.array_equal(tpp.to_array(q), want)
+    with pytest.raises(tpp.InvalidSpecError):
+        tpp.apply_unary(tpp.UnaryKind.DEQUANTIZE, tpp.from_array(np.zeros((2, 2), np.int8)),
+                        tpp.alloc(tpp.TensorDesc(2, 2, 2, tpp.DType.FP32)))

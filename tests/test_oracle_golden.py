@@ -190,3 +190,17 @@ def test_prng_and_dropout(golden):
     assert np.array_equal(O.fp32_to_bf16_rne(rb.T.reshape(-1)), g["db"])
     assert np.array_equal(O.bool_to_mask(kb), g["mb"])
     assert np.array_equal(O.prng_seed(5, 4), g["wrong_after"])  # wrong-width state untouched
+
+
+def test_quantize_dequantize(golden):
+    """ops.py:447-469 incl. ties-to-even, a NaN (scale 1, NaN -> 0), all-zero
+    input and a caller scale that saturates."""
+    g = golden("quant.npz")
+    for name in ("uniform", "normal", "nan", "zeros", "ties"):
+        x = g[name + "_x"]
+        q, scale = O.quantize(x)
+        assert scale == float(g[name + "_scale"]), name
+        assert np.array_equal(q.T.reshape(-1), g[name + "_q"]), name
+        assert bits(O.dequantize(q, scale).T.reshape(-1)) == bits(g[name + "_d"]), name
+    q, _ = O.quantize(g["normal_x"], 0.01)
+    assert np.array_equal(q.T.reshape(-1), g["given_q"])
