@@ -64,9 +64,11 @@ typedef struct {
 
 /* ---- BRGEMM TPP: contraction.py:154-195 (GemmSpec) --------------------- */
 enum tpp_engine {
-  TPP_ENGINE_AUTO = 0,     /* BF16 -> tensor cores when the shape allows, else ordered */
+  TPP_ENGINE_AUTO = 0,     /* INT8 STRIDE -> tcgen05 kind::i8 (exact); else ordered;
+                              BF16 layer drivers -> tensor cores                     */
   TPP_ENGINE_ORDERED = 1,  /* SIMT, the reference's per-element order: bitwise parity  */
-  TPP_ENGINE_TENSOR = 2    /* tcgen05.mma, TMEM accumulation (BF16 only)              */
+  TPP_ENGINE_TENSOR = 2    /* tcgen05.mma, TMEM accumulation (layer drivers; INT8
+                              STRIDE BRGEMMs with plain A)                           */
 };
 
 typedef struct {

@@ -38,9 +38,11 @@ class ComputePath(enum.Enum):
 
 class Engine(enum.Enum):
     """Which sm_100a engine runs a BRGEMM (not in the reference)."""
-    AUTO = "auto"          # ordered SIMT for single BRGEMMs; tensor cores in the layer drivers
+    AUTO = "auto"          # ordered SIMT for float BRGEMMs, tcgen05 kind::i8 for INT8 STRIDE
+                           # batches (integer sums: any order is the reference's bits);
+                           # tensor cores in the layer drivers
     ORDERED = "ordered"    # reference per-element order, bitwise parity
-    TENSOR = "tensor"      # tcgen05 (layer drivers only)
+    TENSOR = "tensor"      # tcgen05 (layer drivers; INT8 STRIDE BRGEMMs)
 
 
 @dataclass(frozen=True)

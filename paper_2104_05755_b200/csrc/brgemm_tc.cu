@@ -632,7 +632,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // 5-D bf16 map, dims innermost first, strides in bytes for dims 1..4
 static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
                        const uint64_t strides[4], const uint32_t box[5],
-                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+                       CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
+                       CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
   auto enc = get_encode();
   if (!enc) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail(TPP_E_TENSOR, "TMA base not 16B aligned");
@@ -648,7 +649,7 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
     if (strides[i] % 16) return fail(TPP_E_TENSOR, "TMA stride not a multiple of 16 bytes");
     gs[i] = strides[i];
   }
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gd, gs, bd,
+  CUresult r = enc(m, dt, 5, const_cast<void*>(base), gd, gs, bd,
                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -764,6 +765,11 @@ int make_tma_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5], co
                                  : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                                        : CU_TENSOR_MAP_SWIZZLE_NONE;
   return tc::make_map_5d(m, base, dims, strides, box, swz);
+}
+
+int make_tma_map_5d_u8(CUtensorMap* m, const void* base, const uint64_t dims[5], const uint64_t strides[4],
+                       const uint32_t box[5]) {
+  return tc::make_map_5d(m, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_UINT8);
 }
 
 // ---------------------------------------------------------------------------

@@ -47,8 +47,8 @@ static int check_gemm(const tpp_gemm_desc* d) {
               "EMULATED_SPLIT applies to BF16 inputs");
   TPP_REQUIRE(!d->a_vnni || d->in_dtype == TPP_BF16 || d->in_dtype == TPP_INT8, TPP_E_TENSOR,
               "VNNI A layout needs a 16- or 8-bit input dtype");
-  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED,
-              "single-BRGEMM tensor-core engine: use the FC / conv layer entry points");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR || d->in_dtype == TPP_INT8, TPP_E_UNSUPPORTED,
+              "single-BRGEMM tensor-core engine is INT8-only: use the FC / conv layer entry points");
   return TPP_OK;
 }
 
@@ -93,6 +93,20 @@ int tpp_brgemm_stride(const tpp_gemm_desc* d, const void* a, const void* b, int6
   int rc = check_gemm(d);
   if (rc) return rc;
   TPP_REQUIRE(count >= 0, TPP_E_TENSOR, "negative batch count");
+  // INT8: integer sums are order-independent, so the tcgen05 kind::i8 engine
+  // is bitwise the reference (plain A, 16-byte aligned strides)
+  if (d->in_dtype == TPP_INT8 && d->engine != TPP_ENGINE_ORDERED) {
+    if (count == 0) {
+      TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "INT8 tensor engine needs a non-empty batch");
+    } else if (!d->a_vnni) {
+      const int r = brgemm_i8_stride_tc(d->m, d->n, d->k, reinterpret_cast<const int8_t*>(a), d->lda,
+                                        reinterpret_cast<const int8_t*>(b), d->ldb, stride_a, stride_b, count,
+                                        reinterpret_cast<int32_t*>(c), d->ldc, d->beta, as_stream(stream));
+      if (r != 1) return r;
+    }
+    TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED,
+                "INT8 tensor engine: plain A and 16-byte aligned pointers / lda / ldb / strides");
+  }
   OrderedParams p = base_params(d, c);
   p.mode = 0;
   p.count = count;
@@ -110,6 +124,7 @@ int tpp_brgemm_offset(const tpp_gemm_desc* d, const void* a, const void* b,
   if (rc) return rc;
   TPP_REQUIRE(count >= 0, TPP_E_TENSOR, "negative batch count");
   TPP_REQUIRE(count == 0 || (a_offsets && b_offsets), TPP_E_TENSOR, "null offset arrays");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "INT8 tensor engine serves STRIDE batches");
   OrderedParams p = base_params(d, c);
   p.mode = 1;
   p.count = count;
@@ -126,6 +141,7 @@ int tpp_brgemm_address(const tpp_gemm_desc* d, const void* const* a_ptrs,
   if (rc) return rc;
   TPP_REQUIRE(count >= 0, TPP_E_TENSOR, "negative batch count");
   TPP_REQUIRE(count == 0 || (a_ptrs && b_ptrs), TPP_E_TENSOR, "null pointer arrays");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "INT8 tensor engine serves STRIDE batches");
   OrderedParams p = base_params(d, c);
   p.mode = 2;
   p.count = count;

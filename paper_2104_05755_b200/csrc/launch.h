@@ -34,6 +34,13 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
                void* mask_out, const void* mask_in, cudaStream_t stream);
 void set_debug_timestamps(unsigned long long* p);
 unsigned long long* debug_timestamps();
+// brgemm_i8.cu (K10): INT8 STRIDE BRGEMM on tcgen05 kind::i8; 1 = not applicable
+int brgemm_i8_stride_tc(int m, int n, int k, const int8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
+                        int64_t stride_a, int64_t stride_b, int64_t count, int32_t* c, int64_t ldc, double beta,
+                        cudaStream_t s);
+// 1-byte elements, 128-byte swizzle (INT8 BRGEMM operands)
+int make_tma_map_5d_u8(CUtensorMap* m, const void* base, const uint64_t dims[5], const uint64_t strides[4],
+                       const uint32_t box[5]);
 // bf16 5-D TMA map (dims innermost first, byte strides of dims 1..4)
 int make_tma_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5], const uint64_t strides[4],
                     const uint32_t box[5], int swizzle_bytes);

@@ -744,3 +744,86 @@ def test_quantize_full_size_matches_oracle():
     with pytest.raises(tpp.InvalidSpecError):
         tpp.apply_unary(tpp.UnaryKind.DEQUANTIZE, tpp.from_array(np.zeros((2, 2), np.int8)),
                         tpp.alloc(tpp.TensorDesc(2, 2, 2, tpp.DType.FP32)))
+
+
+# ---------------------------------------------------------------------------
+# INT8 BRGEMM on tcgen05 kind::i8 (contraction.py:75-85, 184-189): integer
+# sums are order-independent, so the tensor engine must equal the reference
+# bit for bit (including int32 wrap-around)
+# ---------------------------------------------------------------------------
+
+def _int8_ref(a_list, b_list, c0, beta):
+    """Modular int32 reference: int64 sums wrapped to int32 == numpy's
+    wrapping int32 accumulation in any order."""
+    acc = np.zeros(c0.shape, dtype=np.int64)
+    for a, b in zip(a_list, b_list):  # |partial| < 2^53: float64 BLAS is exact here
+        acc += (a.astype(np.float64) @ b.astype(np.float64)).astype(np.int64)
+    if beta == 0.0:
+        base = np.zeros(c0.shape, np.int64)
+    else:
+        base = c0.astype(np.int64) * (1 if beta == 1.0 else int(np.int32(beta)))
+    return ((base + acc) & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+
+
+@pytest.mark.parametrize("m,n,k,count,beta,engine", [
+    (64, 64, 64, 16, 1.0, "tensor"),       # cfg 1 shape: sliced reduction + red.add
+    (300, 200, 520, 3, 0.0, "tensor"),     # ragged M/N/K tiles (TMA zero fill)
+    (1024, 1024, 1024, 4, 1.0, "auto"),    # full tiles, BN 256
+    (128, 96, 4096, 1, 0.5, "tensor"),     # beta 0.5 -> int32(0) (truncation)
+    (256, 48, 384, 5, -2.7, "tensor"),     # beta -2.7 -> -2, BN 64
+])
+def test_int8_tensor_engine_exact(m, n, k, count, beta, engine):
+    rng = np.random.default_rng(m + n + k)
+    lda = -(-m // 16) * 16
+    ldb = -(-k // 16) * 16
+    a_l = [rng.integers(-128, 128, (m, k), dtype=np.int8) for _ in range(count)]
+    b_l = [rng.integers(-128, 128, (k, n), dtype=np.int8) for _ in range(count)]
+    abuf = np.zeros((count, k, lda), np.int8)
+    bbuf = np.zeros((count, n, ldb), np.int8)
+    for i in range(count):
+        abuf[i, :, :m] = a_l[i].T
+        bbuf[i, :, :k] = b_l[i].T
+    c0 = rng.integers(-1000, 1000, (m, n), dtype=np.int32)
+    c = tpp.from_array(c0)
+    eng = tpp.Engine.TENSOR if engine == "tensor" else tpp.Engine.AUTO
+    spec = tpp.GemmSpec(m, n, k, lda, ldb, m, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32,
+                        beta=beta, engine=eng)
+    tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(abuf.reshape(-1)), to_dev(bbuf.reshape(-1)),
+                                            k * lda, n * ldb, count), c)
+    want = _int8_ref(a_l, b_l, c0, beta)
+    assert np.array_equal(tpp.to_array(c), want)
+    if m * n * k * count <= 64 * 64 * 64 * 16:  # the reference's own ordered loop, small case
+        c2 = tpp.from_array(c0)
+        spec2 = tpp.GemmSpec(m, n, k, lda, ldb, m, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32,
+                             beta=beta, engine=tpp.Engine.ORDERED)
+        tpp.brgemm(spec2, tpp.BrgemmBatch.stride(to_dev(abuf.reshape(-1)), to_dev(bbuf.reshape(-1)),
+                                                 k * lda, n * ldb, count), c2)
+        assert np.array_equal(tpp.to_array(c2), want)
+
+
+def test_int8_tensor_engine_wraps_and_saturation_free():
+    """127*127*K beyond 2^31 wraps exactly like numpy int32 (no saturation);
+    and the reference's 127^2 * 300 known answer (test_gemm.py:245-250)."""
+    m, n, k = 16, 16, 140_000
+    a = np.full((k, m), 127, np.int8)  # stored [k][lda=m]: A(m, k) = 127
+    b = np.full((n, k), 127, np.int8)  # stored [n][ldb=k]
+    c = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.INT32))
+    spec = tpp.GemmSpec(m, n, k, m, k, m, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32,
+                        engine=tpp.Engine.TENSOR)
+    tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(a.reshape(-1)), to_dev(b.reshape(-1)), 0, 0, 1), c)
+    want = np.int64(127 * 127 * k)
+    want32 = np.array([want & 0xFFFFFFFF], np.uint32).view(np.int32)[0]
+    assert np.all(tpp.to_array(c) == want32) and want > 2**31
+    k = 300
+    a = np.full((k, 16), 127, np.int8)
+    b = np.full((16, 304), 127, np.int8)
+    c = tpp.alloc(tpp.TensorDesc(16, 16, 16, tpp.DType.INT32))
+    spec = tpp.GemmSpec(16, 16, k, 16, 304, 16, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32,
+                        engine=tpp.Engine.TENSOR)
+    tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(a.reshape(-1)), to_dev(b.reshape(-1)), 0, 0, 1), c)
+    assert np.all(tpp.to_array(c) == 127 * 127 * 300)
+    with pytest.raises(Exception):  # unaligned lda: the tensor engine refuses, AUTO would fall back
+        spec = tpp.GemmSpec(15, 16, k, 15, 304, 15, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32,
+                            engine=tpp.Engine.TENSOR)
+        tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(a.reshape(-1)), to_dev(b.reshape(-1)), 0, 0, 1),
+                   tpp.alloc(tpp.TensorDesc(15, 16, 15, tpp.DType.INT32)))
