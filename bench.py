@@ -478,7 +478,15 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
             "vnni_to_vnnit": (lambda k: transform(vns[k], TransformSpec(TransformKind.VNNI_TO_VNNIT, alpha=2,
                                                                         alpha_out=2, rows=R, cols=Cc),
                                                   sets_[k][2]), 2 * nb),
+            # per-column xorshift128 draws + mask + scaled copy (bitwise the reference)
+            "dropout": (lambda k: tpp.apply_unary(tpp.UnaryKind.DROPOUT, sets_[k][0], sets_[k][1],
+                                                  dropout_p=0.1), 2 * nb + R * Cc // 8),
+            "dropout_inv": (lambda k: tpp.apply_unary(tpp.UnaryKind.DROPOUT_INV, sets_[k][0], sets_[k][2],
+                                                      dropout_p=0.1), 2 * nb + R * Cc // 8),
         }
+        for k in range(3):
+            sets_[k][0].tertiary = {"prng": tpp.PrngState(k, Cc)}
+            sets_[k][0].secondary = torch.zeros(R * Cc // 8, dtype=torch.uint8, device=dev)
         res = {}
         for name, (fn, byts) in cases.items():
             g = graph_of(torch, [(lambda k=k: fn(k)) for k in range(3)] * 2)
@@ -490,6 +498,24 @@ def run_extra(args, torch, tpp, dev, gen, peak_bf16, peak_hbm):
         del sets_, trs, vns
     except Exception as e:
         out["memory_bound_tpps"] = {"error": str(e)[:200]}
+    # ---- INT8 BRGEMM on tcgen05 kind::i8 (exact: integer sums) -------------------
+    try:
+        m = n = 4096
+        k, cnt = 1024, 8
+        a = torch.randint(-128, 128, (cnt * k * m,), generator=gen, device=dev, dtype=torch.int8)
+        b = torch.randint(-128, 128, (cnt * n * k,), generator=gen, device=dev, dtype=torch.int8)
+        cs = [tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.INT32), device=dev) for _ in range(2)]
+        spec8 = tpp.GemmSpec(m, n, k, m, k, m, in_dtype=tpp.DType.INT8, out_dtype=tpp.DType.INT32)
+        batch8 = tpp.BrgemmBatch.stride(a, b, k * m, n * k, cnt)
+        g = graph_of(torch, [lambda: tpp.brgemm(spec8, batch8, cs[0]), lambda: tpp.brgemm(spec8, batch8, cs[1])] * 2)
+        ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.3)) / 4
+        tops = 2.0 * m * n * k * cnt / ms / 1e9
+        out["int8_brgemm_tc"] = {"shape": "M=N=4096, K=1024, STRIDE batch of 8", "ms": round(ms, 4),
+                                 "TOPS": round(tops, 1), "frac_nominal_int8_dense": round(tops / 4500.0, 4),
+                                 "parity": "bitwise (integer sums) vs the reference in tests/test_gpu_parity.py"}
+        del a, b, cs
+    except Exception as e:
+        out["int8_brgemm_tc"] = {"error": str(e)[:200]}
     # ---- cfg 1: FP32 BRGEMM 16 x 64^3, beta = 1, reference order (bitwise) ------
     try:
         m = n = k = 64
