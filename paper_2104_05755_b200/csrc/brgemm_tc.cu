@@ -249,6 +249,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
+    if (p.tma_store) prefetch_tmap(&map_c);  // the epilogue's first store must not fetch it
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -456,12 +457,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
       mbar_wait(&tfull[as], aph);
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[4] = gtimer();
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[189] = clock64();
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[18 + 4 * tcount] = gtimer();
       tc_fence_after();
       // first chunk's TMEM load goes out before any index arithmetic
       const int nch = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
       uint32_t v[32];
       if (nch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + grp * 32, v);
+      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[188] = clock64();
       // token coordinates only for the paths that address rows themselves
       const bool need_rows = !p.tma_store || (p.flags & (TPP_FC_RELU_INV | TPP_FC_RESIDUAL | TPP_FC_OUT_FP32)) ||
                              (p.act == TPP_ACT_RELU && (p.flags & TPP_FC_RELU_MASK));
@@ -504,7 +507,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         tmem_ld_wait();
         if (ch == nch - 1) release();
         if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0) p.dbg[7] = gtimer();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 0] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 0] = clock64();
         const int f0 = tn * BN + col;
         if (p.dbg_mode & 1) continue;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
@@ -540,7 +543,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], smem_u32(gelu_tab));
         }
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 1] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 1] = clock64();
         if ((p.flags & TPP_FC_RESIDUAL) && t >= 0) {
           const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
 #pragma unroll
@@ -562,7 +565,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         } else if (p.tma_store) {
           uint32_t w[16];
           pack_bf16_ref_n<16>(x, w);
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 2] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 2] = clock64();
           uint4 val[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) val[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
@@ -584,7 +587,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             // per-buffer wait_group counts stay aligned with nstore
             if (warp_rows) tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
             bulk_commit();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == 4 && ch < 8) p.dbg[150 + 4 * ch + 3] = gtimer();
+        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 3] = clock64();
           }
         } else {
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
@@ -598,7 +601,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[5] = gtimer();
       if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[19 + 4 * tcount] = gtimer();
     }
-    if (lane == 0 && p.tma_store) bulk_wait_all();
+    // smem must outlive the bulk stores' reads; their global writes complete
+    // with the grid (what the next kernel's griddepcontrol.wait observes)
+    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[190] = clock64();
+    if (lane == 0 && p.tma_store) bulk_wait_read<0>();
+    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[191] = clock64();
   }
 
   tc_fence_before();
@@ -610,6 +617,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     else tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
   if (p.dbg && blockIdx.x == 0 && threadIdx.x == 64) p.dbg[6] = gtimer();
+  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[192] = clock64();
 }
 
 // ---------------------------------------------------------------------------

@@ -346,7 +346,7 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
         if (dbg && blockIdx.x == 0 && (ns) < 16) dbg[8 + 5 * (ns) + 4] = globaltimer_ns();
         ++ns;
       }
-      bulk_wait_all();
+      bulk_wait_read<0>();  // smem outlives the stores' reads; the writes complete with the grid
       if (dbg) dbg[201 + 2 * blockIdx.x] = globaltimer_ns();
     }
   } else if (warp <= kFoldWarps) {
