@@ -105,9 +105,10 @@ struct Smem {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int RES_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = RES_OFF + (RES ? kResMaxBytes : 0);
-  // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base + gelu table (float4 x 16)
+  // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base +
+  // gelu table (float4 x 512: one entry per 9-bit |x| exponent prefix)
   static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
-  static constexpr int BIAS_OFF = TAB_OFF + 16 * 16;                      // float [2][256]
+  static constexpr int BIAS_OFF = TAB_OFF + 512 * 16;                     // float [2][256]
   // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
   // when the smem budget allows (a chunk's store need not have left the
   // buffer before the next chunk is staged)
@@ -201,14 +202,16 @@ __device__ __forceinline__ float4 lds_f4(uint32_t saddr) {
 // GELU with the table as one float4 {c0,c1,c2,c3} per interval: one
 // ld.shared.v4 at tab_s (shared address) + 16 * clamp(exp-code - 244, 0, 15);
 // ~18 instructions per element (the epilogue's issue budget).
+// The table is indexed by the 9-bit prefix (|x| bits >> 22) directly, the
+// reference's clip(prefix - 244, 0, 15) baked into its 512 entries; prefixes
+// >= 260 (|x| >= 8, inf, NaN) hold (1, 0, 0, 0) and |x| is clamped to 8 there,
+// so the Horner chain yields exactly the reference's saturated h = 1 (and a
+// NaN x still gives NaN through 0.5*x).
 __device__ __forceinline__ float gelu4(float x, uint32_t tab_s) {
   const uint32_t xb = __float_as_uint(x);
-  const uint32_t ab = xb & 0x7FFFFFFFu;
-  const float ax = __uint_as_float(ab);
-  const uint32_t e = min(max(ab >> 22, (uint32_t)kGeluBase), (uint32_t)kGeluBase + 15u);
-  const float4 c = lds_f4(tab_s + ((e - kGeluBase) << 4));
+  const float ax = fminf(fabsf(x), kGeluRangeMax);
+  const float4 c = lds_f4(tab_s + ((xb & 0x7FC00000u) >> 18));
   float h = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c.w, ax), c.z), ax), c.y), ax), c.x);
-  h = ax >= kGeluRangeMax ? 1.0f : h;
   h = __uint_as_float((__float_as_uint(h) & 0x7FFFFFFFu) | (xb & 0x80000000u));  // copysign(h, x)
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
 }
@@ -265,9 +268,15 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (PAIR) tmem_alloc_pair(tmem_slot, S::TMEM_COLS);
     else tmem_alloc(tmem_slot, S::TMEM_COLS);
   }
-  if (warp == 3 && lane < 16)
-    gelu_tab[lane] = make_float4(__uint_as_float(c_gelu_bits[lane]), __uint_as_float(c_gelu_bits[16 + lane]),
-                                 __uint_as_float(c_gelu_bits[32 + lane]), __uint_as_float(c_gelu_bits[48 + lane]));
+  if (warp == 3 && p.act == TPP_ACT_GELU) {
+    for (int e = lane; e < 512; e += 32) {
+      const int j = min(max(e - kGeluBase, 0), 15);
+      gelu_tab[e] = e >= kGeluBase + 16
+                        ? make_float4(1.0f, 0.0f, 0.0f, 0.0f)
+                        : make_float4(__uint_as_float(c_gelu_bits[j]), __uint_as_float(c_gelu_bits[16 + j]),
+                                      __uint_as_float(c_gelu_bits[32 + j]), __uint_as_float(c_gelu_bits[48 + j]));
+    }
+  }
   tc_fence_before();
   if (PAIR) cluster_sync();  // the peer signals the leader's barriers
   else __syncthreads();

@@ -827,3 +827,29 @@ def test_int8_tensor_engine_wraps_and_saturation_free():
                             engine=tpp.Engine.TENSOR)
         tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(a.reshape(-1)), to_dev(b.reshape(-1)), 0, 0, 1),
                    tpp.alloc(tpp.TensorDesc(15, 16, 15, tpp.DType.INT32)))
+
+
+def test_fc_gelu_epilogue_special_values():
+    """The fused GELU epilogue on exact accumulators (identity weights: one
+    non-zero product per output, so the tensor-core sum is exact) is bitwise
+    the reference's GELU: range edges around |x| = 8, tiny, signed zero, large,
+    +-inf and NaN (approx.py:267-276)."""
+    rng = np.random.default_rng(33)
+    Nb, bn, bc = 2, 64, 64
+    specials = np.array([0.0, -0.0, 7.9921875, -7.9921875, 8.0, -8.0, 8.0625, -8.0625, 100.0, -100.0,
+                         1e-30, -1e-30, 0.5, -0.5, 2.9, -2.9, 3.0e38, -3.0e38, np.inf, -np.inf, np.nan,
+                         0.03125, -0.03125, 6.0, -6.0, 5.99, 1.0, -1.0], dtype=np.float32)
+    x = rng.normal(0, 3, (Nb, 1, bn, bc)).astype(np.float32)
+    flat = x.reshape(-1)
+    flat[: specials.size] = specials
+    xb = O.fp32_to_bf16_rne(x)
+    eye = np.eye(64, dtype=np.float32)  # W[k, c]
+    wv = np.zeros((1, 1, 32, 64, 2), dtype=np.uint16)
+    wbits = O.fp32_to_bf16_rne(eye)
+    for c in range(64):
+        wv[0, 0, c // 2, :, c % 2] = wbits[:, c]
+    layer = tpp.FcLayer(1, 1, 64, 64, to_dev(wv), activation=tpp.UnaryKind.GELU)
+    out = layer.forward(to_dev(xb), Nb, bn)
+    got = to_host(out).reshape(Nb, 1, bn, 64)
+    want, _, _ = O.fc_forward_bf16(xb, wv, None, activation="gelu")
+    assert bf16_equal(got.reshape(-1), np.asarray(want).reshape(-1))
