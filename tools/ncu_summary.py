@@ -15,15 +15,15 @@ KEYS = [
 ]
 
 
-def raw(rep):
+def raw(rep, idx=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + idx]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
 
-def summarize(rep, title):
-    d = raw(rep)
+def summarize(rep, title, idx=0):
+    d = raw(rep, idx)
     lines = [f"# {title}", f"report: {rep}", f"kernel: {d.get('Kernel Name', ('?',))[0]}"]
     for k in KEYS:
         for name, (v, u) in d.items():
@@ -56,6 +56,6 @@ def launches(csv_path, out):
 if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "rep":
-        print(summarize(sys.argv[2], sys.argv[3]))
+        print(summarize(sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 0))
     else:
         launches(sys.argv[2], sys.argv[3])
