@@ -42,10 +42,10 @@ constexpr int BM = 128;       // output rows per tile (UMMA M, TMEM lanes)
 constexpr int BKB = 128;      // K bytes per stage (one 128-byte swizzle row)
 constexpr int kThreads = 192;
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG = 1>
 struct Smem {
-  static constexpr int A_BYTES = BM * BKB;  // 16 KB: 128 K-rows x 128 M bytes
-  static constexpr int B_BYTES = BN * BKB;  // BN N-rows x 128 K bytes
+  static constexpr int A_BYTES = BM * BKB;         // 16 KB: 128 K-rows x 128 M bytes
+  static constexpr int B_BYTES = (BN / CG) * BKB;  // this CTA's BN/CG N-rows x 128 K bytes
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int BAR_OFF = STAGES * STAGE;
@@ -55,7 +55,7 @@ struct Smem {
 struct Params {
   int m, n, kblocks;
   int64_t iters;        // count * kblocks
-  int tiles_m, tiles_n, slices;
+  int tiles_m, tiles_n, slices;   // tiles_m: row tiles (pairs of 128-row tiles for CTA pairs)
   int64_t units;
   int32_t* c;
   int64_t ldc;
@@ -71,6 +71,17 @@ __device__ __forceinline__ void umma_i8_warp(uint32_t tmem_d, uint64_t adesc, ui
       "setp.ne.b32 p, %4, 0;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_i8_pair_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -95,11 +106,16 @@ __device__ __forceinline__ void unit_coords(const Params& p, int64_t u, int& tm,
   it1 = it0 + per < p.iters ? it0 + per : p.iters;
 }
 
-template <int BN, int STAGES>
+// CG = 2: CTA pairs (cluster of 2, cta_group::2): a 256 x BN tile per pair;
+// each CTA stages its own 128 A rows and half of B, the leader issues M=256
+// MMAs and commits to both CTAs -- per-CTA shared-memory traffic per MAC
+// drops by a third, which is what the BN=256 1-CTA form is bound by.
+template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                  const Params p) {
-  using S = Smem<BN, STAGES>;
+  using S = Smem<BN, STAGES, CG>;
+  constexpr bool PAIR = CG == 2;
   extern __shared__ uint8_t raw_smem[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw_smem) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + S::BAR_OFF);
@@ -108,6 +124,10 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int64_t cl0 = PAIR ? blockIdx.x >> 1 : blockIdx.x;
+  const int64_t ncl = PAIR ? gridDim.x >> 1 : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -116,15 +136,19 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one elected arrive per epilogue warp
+      mbar_init(&tempty[b], 4 * CG);  // one elected arrive per epilogue warp (of both CTAs)
     }
     fence_mbar_init();
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_b);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(tmem_slot, S::TMEM_COLS);
+    else tmem_alloc(tmem_slot, S::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's TMA and arrivals target the leader's barriers
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -133,29 +157,37 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
+      for (int64_t u = cl0; u < p.units; u += ncl) {
         int tm, tn;
         int64_t it0, it1;
         unit_coords(p, u, tm, tn, it0, it1);
+        const int row0 = (tm * CG + (int)rank) * BM, col0 = tn * BN + (int)rank * (BN / CG);
         for (int64_t it = it0; it < it1; ++it) {
           const int i = (int)(it / p.kblocks), kb = (int)(it - (int64_t)i * p.kblocks);
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = sm + stage * S::STAGE;
-          mbar_arrive_expect_tx(&full[stage], S::STAGE);
-          tma_load_5d(sa, &map_a, &full[stage], tm * BM, kb * BKB, i, 0, 0);
-          tma_load_5d(sa + S::A_BYTES, &map_b, &full[stage], kb * BKB, tn * BN, i, 0, 0);
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE);
+            tma_load_5d_pair(sa, &map_a, full_cl + 8 * stage, row0, kb * BKB, i, 0, 0);
+            tma_load_5d_pair(sa + S::A_BYTES, &map_b, full_cl + 8 * stage, kb * BKB, col0, i, 0, 0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], S::STAGE);
+            tma_load_5d(sa, &map_a, &full[stage], row0, kb * BKB, i, 0, 0);
+            tma_load_5d(sa + S::A_BYTES, &map_b, &full[stage], kb * BKB, col0, i, 0, 0);
+          }
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (whole warp, elected lane issues) ----
-    constexpr uint32_t idesc = idesc_s8_s32(BM, BN);
+    // ---- MMA issuer (whole warp, elected lane issues; pairs: the leader) ----
+    constexpr uint32_t idesc = idesc_s8_s32(BM * CG, BN);
     int stage = 0;
     uint32_t phase = 0;
     int buf = 0;
     uint32_t tphase = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (int64_t u = cl0; u < p.units && leader; u += ncl) {
       int tm, tn;
       int64_t it0, it1;
       unit_coords(p, u, tm, tn, it0, it1);
@@ -173,12 +205,15 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           const uint64_t ad = sw128_mnmajor_desc(sa + kk * 32 * 128, 16384);
           // B: K-major, 32 bytes of K per MMA inside the 128-byte row
           const uint64_t bd = sw128_kmajor_desc(sb + kk * 32);
-          umma_i8_warp(acc, ad, bd, idesc, (it > it0 || kk > 0) ? 1u : 0u);
+          if (PAIR) umma_i8_pair_warp(acc, ad, bd, idesc, (it > it0 || kk > 0) ? 1u : 0u);
+          else umma_i8_warp(acc, ad, bd, idesc, (it > it0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit_warp(&empty[stage]);
+        if (PAIR) umma_commit_pair_warp(&empty[stage], 3);
+        else umma_commit_warp(&empty[stage]);
         if (++stage == STAGES) stage = 0, phase ^= 1;
       }
-      umma_commit_warp(&tfull[buf]);
+      if (PAIR) umma_commit_pair_warp(&tfull[buf], 3);
+      else umma_commit_warp(&tfull[buf]);
       if (++buf == 2) buf = 0, tphase ^= 1;
     }
   } else {
@@ -186,13 +221,14 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const int quarter = warp & 3;
     int buf = 0;
     uint32_t tphase = 0;
-    for (int64_t u = blockIdx.x; u < p.units; u += gridDim.x) {
+    const uint32_t tempty_leader = PAIR ? mapa_shared(smem_u32(tempty), 0) : 0;
+    for (int64_t u = cl0; u < p.units; u += ncl) {
       int tm, tn;
       int64_t it0, it1;
       unit_coords(p, u, tm, tn, it0, it1);
       mbar_wait(&tfull[buf], tphase);
       tc_fence_after();
-      const int row = tm * BM + quarter * 32 + lane;
+      const int row = (tm * CG + (int)rank) * BM + quarter * 32 + lane;
       const bool has = it1 > it0;  // an empty slice contributes nothing (accumulator untouched)
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -218,15 +254,20 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (lane == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(tempty_leader + 8 * buf);
+        else mbar_arrive(&tempty[buf]);
+      }
       if (++buf == 2) buf = 0, tphase ^= 1;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // neither CTA leaves while the pair still uses its smem / TMEM
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::TMEM_COLS);
+    if (PAIR) tmem_dealloc_pair(tmem_base, S::TMEM_COLS);
+    else tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
 }
 
@@ -251,18 +292,46 @@ static int sm_count() {
   return n;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, cudaStream_t s) {
-  using S = Smem<BN, STAGES>;
+  using S = Smem<BN, STAGES, CG>;
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
+  auto kern = brgemm_i8_kernel<BN, STAGES, CG>;
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(brgemm_i8_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+  static int max_clusters = 0;
+  std::call_once(once, [&] {
+    attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+    max_clusters = sm_count() / CG;
+    if (CG > 1 && attr == cudaSuccess) {
+      cudaLaunchConfig_t q{};
+      q.gridDim = dim3(sm_count());
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = S::BYTES;
+      cudaLaunchAttribute ca[1];
+      ca[0].id = cudaLaunchAttributeClusterDimension;
+      ca[0].val.clusterDim.x = CG; ca[0].val.clusterDim.y = 1; ca[0].val.clusterDim.z = 1;
+      q.attrs = ca;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0 && n < max_clusters) max_clusters = n;
+      cudaGetLastError();
+    }
   });
   if (attr != cudaSuccess) return cuda_status(attr, "cudaFuncSetAttribute(brgemm_i8_kernel)");
-  const int64_t grid = p.units < sm_count() ? p.units : sm_count();
-  brgemm_i8_kernel<BN, STAGES><<<(unsigned)grid, kThreads, S::BYTES, s>>>(ma, mb, p);
+  const int64_t clusters = p.units < max_clusters ? p.units : max_clusters;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CG > 1 ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
+  if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_i8_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_i8_kernel");
   return TPP_OK;
 }
@@ -283,9 +352,14 @@ int brgemm_i8_stride_tc(int m, int n, int k, const int8_t* a, int64_t lda, const
   p.n = n;
   p.kblocks = (k + BKB - 1) / BKB;
   p.iters = count * p.kblocks;
-  p.tiles_m = (m + BM - 1) / BM;
+  const int tiles_m1 = (m + BM - 1) / BM;
   const int BN = n > 128 ? 256 : (n > 64 ? 128 : 64);
   p.tiles_n = (n + BN - 1) / BN;
+  // CTA pairs for the wide tiles when there are row tiles to pair up
+  static const int forced_cg = getenv("TPP_I8_CG") ? atoi(getenv("TPP_I8_CG")) : 0;
+  const bool pair_wave = BN == 256 && (int64_t)(tiles_m1 / 2) * p.tiles_n >= sm_count() / 2;
+  const int CG = tiles_m1 < 2 || forced_cg == 1 ? 1 : (pair_wave || forced_cg == 2 ? 2 : 1);
+  p.tiles_m = (tiles_m1 + CG - 1) / CG;
   const int64_t tiles = (int64_t)p.tiles_m * p.tiles_n;
   // slice the reduction when the tiles alone leave SMs idle (>= 4 stages per slice)
   int64_t slices = 1;
@@ -319,16 +393,23 @@ int brgemm_i8_stride_tc(int m, int n, int k, const int8_t* a, int64_t lda, const
   const uint32_t ba[5] = {BM, BKB, 1, 1, 1};
   const uint64_t db[5] = {(uint64_t)k, (uint64_t)n, (uint64_t)count, 1, 1};
   const uint64_t sb[4] = {(uint64_t)ldb, (uint64_t)(count > 1 ? stride_b : (int64_t)ldb * n), 16, 16};
-  const uint32_t bb[5] = {BKB, (uint32_t)BN, 1, 1, 1};
+  const uint32_t bb[5] = {BKB, (uint32_t)(BN / CG), 1, 1, 1};
   if ((sa[1] % 16) || (sb[1] % 16)) return 1;
   int rc = make_tma_map_5d_u8(&ma, a, da, sa, ba);
   if (rc) return rc;
   rc = make_tma_map_5d_u8(&mb, b, db, sb, bb);
   if (rc) return rc;
+  if (CG == 2) {
+    switch (BN) {
+      case 256: return launch_cfg<256, 6, 2>(ma, mb, p, s);
+      case 128: return launch_cfg<128, 8, 2>(ma, mb, p, s);
+      default: return launch_cfg<64, 8, 2>(ma, mb, p, s);
+    }
+  }
   switch (BN) {
-    case 256: return launch_cfg<256, 4>(ma, mb, p, s);
-    case 128: return launch_cfg<128, 6>(ma, mb, p, s);
-    default: return launch_cfg<64, 8>(ma, mb, p, s);
+    case 256: return launch_cfg<256, 4, 1>(ma, mb, p, s);
+    case 128: return launch_cfg<128, 6, 1>(ma, mb, p, s);
+    default: return launch_cfg<64, 8, 1>(ma, mb, p, s);
   }
 }
 

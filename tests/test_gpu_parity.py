@@ -771,6 +771,8 @@ def _int8_ref(a_list, b_list, c0, beta):
     (1024, 1024, 1024, 4, 1.0, "auto"),    # full tiles, BN 256
     (128, 96, 4096, 1, 0.5, "tensor"),     # beta 0.5 -> int32(0) (truncation)
     (256, 48, 384, 5, -2.7, "tensor"),     # beta -2.7 -> -2, BN 64
+    (4096, 2048, 256, 2, 1.0, "auto"),     # a full wave of CTA pairs (cta_group::2)
+    (4000, 2000, 200, 1, 0.0, "tensor"),   # pairs with ragged M / N / K edges
 ])
 def test_int8_tensor_engine_exact(m, n, k, count, beta, engine):
     rng = np.random.default_rng(m + n + k)
