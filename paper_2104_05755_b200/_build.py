@@ -26,6 +26,9 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr",
 ]
+# diagnostic build: per-phase timestamps in the tensor-core kernels (tools/*_ts.py)
+if os.environ.get("TPP_PHASE_STAMPS"):
+    FLAGS.append("-DTPP_PHASE_STAMPS")
 
 
 def _stale() -> bool:

@@ -32,6 +32,22 @@
 #include "common.cuh"
 #include "sm100.cuh"
 
+// Phase stamps and the TPP_DBG_MODE experiments are compiled in only for
+// diagnostic builds (TPP_PHASE_STAMPS=1 at build time): in the product build
+// they cost parameter loads and branches on the epilogue's critical path.
+#ifdef TPP_PHASE_STAMPS
+#define TPP_STAMP(cond, idx, val) \
+  do {                            \
+    if (p.dbg && (cond)) p.dbg[idx] = (val); \
+  } while (0)
+#define TPP_DBG_MODE (p.dbg_mode)
+#else
+#define TPP_STAMP(cond, idx, val) \
+  do {                            \
+  } while (0)
+#define TPP_DBG_MODE 0
+#endif
+
 namespace tpp {
 
 using namespace sm100;
@@ -236,7 +252,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
-  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[0] = gtimer();
+  TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 0, 0, gtimer());
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // pair mode: work items are 256-row pair tiles, one per cluster; this CTA
@@ -282,7 +298,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 0) p.dbg[1] = gtimer();
+  TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 0, 1, gtimer());
   // Programmatic dependent launch: let the next kernel in the stream be
   // scheduled now (its prologue overlaps our tail).  Each role that touches
   // global memory waits for the previous kernel (griddepcontrol.wait) only
@@ -306,7 +322,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
       pdl_wait_after(f.ai.c[0] + f.ai.c[1] + f.ai.c[2] + f.ai.c[3] + f.ai.c[4] + f.bi.c[0] + f.bi.c[1] + f.bi.c[2] +
                      f.bi.c[3] + f.bi.c[4] + nstages);
-      if (p.dbg && blockIdx.x == 0 && pid == 0) p.dbg[10] = gtimer();
+      TPP_STAMP(blockIdx.x == 0 && pid == 0, 10, gtimer());
       if (RES && pid == 0) {
         // resident weights: every tap block once, on the bres barrier
         const int J = p.kblocks;
@@ -342,7 +358,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
               tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
-              if (p.dbg && blockIdx.x == 0 && it == 0) p.dbg[11] = gtimer();
+              TPP_STAMP(blockIdx.x == 0 && it == 0, 11, gtimer());
               if (!RES)
                 tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
             }
@@ -375,8 +391,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint32_t tmem_d = tmem_base + as * BN;
         for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
-          if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0) p.dbg[2] = gtimer();
-          if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount < 32 && j == 0) p.dbg[16 + 4 * tcount] = gtimer();
+          TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0, 2, gtimer());
+          TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32 && j == 0, 16 + 4 * tcount, gtimer());
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
@@ -396,7 +412,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint64_t bd = b0 + btap * tap;
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
-                  if (!(p.dbg_mode & 2))
+                  if (!(TPP_DBG_MODE & 2))
                     umma_f16_warp(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (j > 0 || tap > 0 || kk > 0) ? 1u : 0u);
               }
             } else {
@@ -416,7 +432,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               const uint64_t bd = RES ? bres0 + (uint64_t)((j * BN * BK * 2) >> 4) : bdesc0 + soff + bsub * kb;
 #pragma unroll
               for (int kk = 0; kk < BK / 16; ++kk) {
-                if (p.dbg_mode & 2) continue;
+                if (TPP_DBG_MODE & 2) continue;
                 if (PAIR)
                   umma_f16_pair_warp(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk, idesc,
                                 (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
@@ -432,8 +448,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         if (PAIR) umma_commit_pair_warp(&tfull[as], 3);
         else umma_commit_warp(&tfull[as]);
-        if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile) p.dbg[3] = gtimer();
-        if (p.dbg && blockIdx.x == 0 && lane == 0 && tcount < 32) p.dbg[17 + 4 * tcount] = gtimer();
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile, 3, gtimer());
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32, 17 + 4 * tcount, gtimer());
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -464,16 +480,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         named_bar_sync(1, kEpiWarps * 32);
       }
-      mbar_wait(&tfull[as], aph);
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[4] = gtimer();
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[189] = clock64();
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[18 + 4 * tcount] = gtimer();
-      tc_fence_after();
-      // first chunk's TMEM load goes out before any index arithmetic
-      const int nch = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
-      uint32_t v[32];
-      if (nch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + grp * 32, v);
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[188] = clock64();
+      // Index arithmetic (integer divisions) is done while the accumulator is
+      // still being computed; the empty asm pins it before the wait.
       // token coordinates only for the paths that address rows themselves
       const bool need_rows = !p.tma_store || (p.flags & (TPP_FC_RELU_INV | TPP_FC_RESIDUAL | TPP_FC_OUT_FP32)) ||
                              (p.act == TPP_ACT_RELU && (p.flags & TPP_FC_RELU_MASK));
@@ -497,6 +505,16 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         sc1 = (q & 1) * 32; sc4 = img;
         warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
       }
+      asm volatile("" ::"r"(t), "r"(nb), "r"(n_in), "r"(sc1), "r"(sc2), "r"(sc4), "r"((int)warp_rows));
+      mbar_wait(&tfull[as], aph);
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 4, gtimer());
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 189, clock64());
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 18 + 4 * tcount, gtimer());
+      tc_fence_after();
+      const int nch = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
+      uint32_t v[32];
+      if (nch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + grp * 32, v);
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 188, clock64());
       // release this warp's share of the accumulator as soon as its last
       // chunk is in registers, so the next tile's MMAs can start while the
       // math and stores of this one proceed
@@ -515,10 +533,10 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         if (ch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
         if (ch == nch - 1) release();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0) p.dbg[7] = gtimer();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 0] = clock64();
+        TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0, 7, gtimer());
+        TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 0, clock64());
         const int f0 = tn * BN + col;
-        if (p.dbg_mode & 1) continue;
+        if (TPP_DBG_MODE & 1) continue;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
         const int mb = p.o_bm == 64 ? f0 >> 6 : f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
@@ -552,7 +570,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
           for (int i = 0; i < 32; ++i) x[i] = gelu4(x[i], smem_u32(gelu_tab));
         }
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 1] = clock64();
+        TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 1, clock64());
         if ((p.flags & TPP_FC_RESIDUAL) && t >= 0) {
           const uint4* rp = reinterpret_cast<const uint4*>(p.residual + row_off * p.o_bm + m_in);
 #pragma unroll
@@ -574,7 +592,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         } else if (p.tma_store) {
           uint32_t w[16];
           pack_bf16_ref_n<16>(x, w);
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 2] = clock64();
+        TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 2, clock64());
           uint4 val[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) val[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
@@ -596,7 +614,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             // per-buffer wait_group counts stay aligned with nstore
             if (warp_rows) tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
             bulk_commit();
-        if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8) p.dbg[150 + 4 * ch + 3] = clock64();
+        TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 3, clock64());
           }
         } else {
           uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
@@ -606,15 +624,15 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[8] = gtimer();
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile) p.dbg[5] = gtimer();
-      if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32) p.dbg[19 + 4 * tcount] = gtimer();
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 8, gtimer());
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 5, gtimer());
+      TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 19 + 4 * tcount, gtimer());
     }
     // smem must outlive the bulk stores' reads; their global writes complete
     // with the grid (what the next kernel's griddepcontrol.wait observes)
-    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[190] = clock64();
+    TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128, 190, clock64());
     if (lane == 0 && p.tma_store) bulk_wait_read<0>();
-    if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[191] = clock64();
+    TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128, 191, clock64());
   }
 
   tc_fence_before();
@@ -625,8 +643,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (PAIR) tmem_dealloc_pair(tmem_base, S::TMEM_COLS);
     else tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
-  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 64) p.dbg[6] = gtimer();
-  if (p.dbg && blockIdx.x == 0 && threadIdx.x == 128) p.dbg[192] = clock64();
+  TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 64, 6, gtimer());
+  TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128, 192, clock64());
 }
 
 // ---------------------------------------------------------------------------
