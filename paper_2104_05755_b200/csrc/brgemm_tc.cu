@@ -530,9 +530,13 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll 1
       for (int ch = 0; ch < nch; ++ch) {
         const int col = (grp + ch * kEpiGroups) * 32;
-        if (ch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col, v);
         tmem_ld_wait();
-        if (ch == nch - 1) release();
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
+        // the next chunk's TMEM load overlaps this chunk's math and stores
+        if (ch + 1 < nch) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col + kEpiGroups * 32, v);
+        else release();
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0, 7, gtimer());
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 0, clock64());
         const int f0 = tn * BN + col;
@@ -540,9 +544,6 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
         const int mb = p.o_bm == 64 ? f0 >> 6 : f0 / p.o_bm, m_in = f0 - mb * p.o_bm;
         const int64_t row_off = ((int64_t)(nb * p.o_mb + mb) * p.o_bn + n_in);
-        float x[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
         if (p.flags & TPP_FC_BIAS) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
