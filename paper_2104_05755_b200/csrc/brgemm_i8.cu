@@ -123,7 +123,7 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp-uniform (uniform-datapath MMA issue)
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
   const int64_t cl0 = PAIR ? blockIdx.x >> 1 : blockIdx.x;
@@ -150,7 +150,7 @@ brgemm_i8_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   if (PAIR) cluster_sync();  // the peer's TMA and arrivals target the leader's barriers
   else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // uniform (MMA operand)
 
   if (warp == 0) {
     // ---- TMA producer ----

@@ -124,11 +124,12 @@ struct Smem {
   // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base +
   // gelu table (float4 x 512: one entry per 9-bit |x| exponent prefix)
   static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
-  static constexpr int BIAS_OFF = TAB_OFF + 512 * 16;                     // float [2][256]
+  // the conv (RES = 2) epilogue has no bias / GELU: no table, no bias staging
+  static constexpr int BIAS_OFF = TAB_OFF + (RES == 2 ? 0 : 512 * 16);    // float [2][256]
   // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
   // when the smem budget allows (a chunk's store need not have left the
   // buffer before the next chunk is staged)
-  static constexpr int STG_OFF = (BIAS_OFF + 2 * 256 * 4 + 1023) & ~1023;
+  static constexpr int STG_OFF = (BIAS_OFF + (RES == 2 ? 0 : 2 * 256 * 4) + 1023) & ~1023;
   static constexpr int STG_BUFS = STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1;
   static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 * STG_BUFS + 1024;
 };
@@ -253,7 +254,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
   TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 0, 0, gtimer());
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // provably warp-uniform: keeps the MMA issuer's descriptor math on the uniform datapath
   const int lane = threadIdx.x & 31;
   // pair mode: work items are 256-row pair tiles, one per cluster; this CTA
   // owns row tile 2*tm + rank and B rows [rank*BN/2, (rank+1)*BN/2) of the tile
@@ -284,7 +285,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (PAIR) tmem_alloc_pair(tmem_slot, S::TMEM_COLS);
     else tmem_alloc(tmem_slot, S::TMEM_COLS);
   }
-  if (warp == 3 && p.act == TPP_ACT_GELU) {
+  if (RES != 2 && warp == 3 && p.act == TPP_ACT_GELU) {
     for (int e = lane; e < 512; e += 32) {
       const int j = min(max(e - kGeluBase, 0), 15);
       gelu_tab[e] = e >= kGeluBase + 16
@@ -297,7 +298,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   if (PAIR) cluster_sync();  // the peer signals the leader's barriers
   else __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // uniform (MMA operand)
   TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 0, 1, gtimer());
   // Programmatic dependent launch: let the next kernel in the stream be
   // scheduled now (its prologue overlaps our tail).  Each role that touches
@@ -354,11 +355,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               tma_load_5d_pair(sa, &map_a, full_cl + 8 * s, f.ai.c[0], f.ai.c[1], f.ai.c[2], f.ai.c[3], f.ai.c[4]);
               tma_load_5d_pair(sa + S::A_BYTES, &map_b, full_cl + 8 * s, f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3],
                                f.bi.c[4]);
+            } else if ((TPP_DBG_MODE & 4) && it >= STAGES) {
+              mbar_arrive(&full[s]);  // diagnostics: reuse the resident stage, no TMA traffic
             } else {
               mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
               tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
               TPP_STAMP(blockIdx.x == 0 && it == 0, 11, gtimer());
+              TPP_STAMP(blockIdx.x == 0 && j == 0 && it / nstages < 32, 200 + it / nstages, gtimer());
               if (!RES)
                 tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
             }
@@ -387,6 +391,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
         const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32, 240 + tcount, gtimer());
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 320 + (tcount == 30) * 2, clock64());
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 321 + (tcount == 30) * 2, gtimer());
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * BN;
         for (int j = 0; j < nstages; ++j) {
@@ -518,7 +525,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       // release this warp's share of the accumulator as soon as its last
       // chunk is in registers, so the next tile's MMAs can start while the
       // math and stores of this one proceed
+      TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == 20, 300 + ew, gtimer());
       auto release = [&] {
+        TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == 20, 280 + ew, gtimer());
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -628,6 +637,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 8, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 5, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 19 + 4 * tcount, gtimer());
+      TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == 20, 290 + ew, gtimer());
     }
     // smem must outlive the bulk stores' reads; their global writes complete
     // with the grid (what the next kernel's griddepcontrol.wait observes)

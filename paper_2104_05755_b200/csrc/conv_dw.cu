@@ -58,7 +58,7 @@ conv_dw_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   uint64_t* empty = full + kStages;
   uint64_t* done = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp-uniform (uniform-datapath MMA issue)
 
   const int item = blockIdx.x;
   const int kbcb = item / p.Z, z = item % p.Z;
@@ -80,7 +80,7 @@ conv_dw_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // uniform (MMA operand)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 

@@ -150,7 +150,8 @@ int main() {
          b1, b0, p1);
   printf("grid threads smem  pdl : us per launch\n");
   const int cfgs[][4] = {{128, 384, 200 * 1024, 1}, {128, 384, 200 * 1024, 0}, {128, 384, 0, 1},
-                         {128, 128, 0, 1},          {148, 384, 200 * 1024, 1}, {1, 32, 0, 1}};
+                         {128, 128, 0, 1},          {148, 384, 200 * 1024, 1}, {1, 32, 0, 1},
+                         {128, 256, 100 * 1024, 1}, {128, 256, 100 * 1024, 0}, {256, 256, 100 * 1024, 1}};
   for (auto& c : cfgs)
     printf("%4d %6d %6d %3d : %.2f  (%s)\n", c[0], c[1], c[2], c[3], run(c[0], c[1], c[2], c[3]),
            cudaGetErrorString(cudaGetLastError()));

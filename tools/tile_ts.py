@@ -11,7 +11,7 @@ from paper_2104_05755_b200 import _lib
 dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev); gen.manual_seed(0)
 lib = _lib.load()
-buf = torch.zeros(200, dtype=torch.int64, device=dev)
+buf = torch.zeros(400, dtype=torch.int64, device=dev)
 which = sys.argv[1] if len(sys.argv) > 1 else "conv"
 if which == "conv":
     spec = tpp.ConvSpec(256, 1, 1, 56, 56)
@@ -39,7 +39,8 @@ for it in range(2):
         if f == 0:
             break
         z = lambda v: (v - t[0]) / 1e3 if v else float("nan")
-        print(f"  tile {k:2d}: full {z(f):7.2f}  mma_done {z(m):7.2f}  acc_ready {z(a):7.2f}  released {z(r):7.2f}"
+        print(f"  tile {k:2d}: load_issued {z(t[200 + k]):7.2f}  tempty_ok {z(t[240 + k]):7.2f}"
+              f"  full {z(f):7.2f}  mma_done {z(m):7.2f}  acc_ready {z(a):7.2f}  released {z(r):7.2f}"
               f"  epi {(r - a) / 1e3 if a and r else float('nan'):5.2f}  mma {(m - f) / 1e3:5.2f}")
     # epilogue chunk stamps of tile 4 (warp 4): after tcgen05.ld, after activation, after pack, after store issue
     base = t[16 + 4 * 4 + 2]
@@ -49,3 +50,9 @@ for it in range(2):
             if not v[0]:
                 break
             print(f"    chunk {ch}: " + " ".join(f"{(x - base) / 1e3:6.2f}" if x else "   nan" for x in v))
+
+    z = lambda v: (v - t[0]) / 1e3 if v else float("nan")
+    for w in range(8):
+        print(f"  tile 20 epilogue warp {w}: acc_ready {z(t[300 + w]):7.2f}  tmem_released {z(t[280 + w]):7.2f}  done {z(t[290 + w]):7.2f}")
+    if t[320] and t[322]:
+        print(f"  SM clock over tiles 4..30 (CTA 0): {(t[322] - t[320]) / (t[323] - t[321]) * 1e3:.0f} MHz")
