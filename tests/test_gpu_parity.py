@@ -418,6 +418,19 @@ def test_conv_golden(golden):
     assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
 
 
+def test_conv_multi_wave_shapes():
+    """More than one wave of 2-row tiles (persistent CTAs walk several tiles and
+    reuse their accumulator / halo rings), odd and even tile counts per image,
+    ragged widths."""
+    rng = np.random.default_rng(42)
+    err_f, err_b = _conv_case(rng, 6, 1, 1, 56, 56, n_sel=[0, 3, 5])   # 168 tiles, 28 per image: pairs
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+    err_f, err_b = _conv_case(rng, 12, 1, 1, 26, 40, n_sel=[0, 11])   # 13 tiles per image: single CTAs
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+    err_f, err_b = _conv_case(rng, 12, 1, 1, 28, 20, n_sel=[4, 7])    # 14 per image, ragged width: pairs
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+
+
 # ---------------------------------------------------------------------------
 # 1-D dilated conv (kernels.py:336-378): stride BRGEMM over taps, bitwise
 # ---------------------------------------------------------------------------

@@ -30,19 +30,20 @@ __global__ void __launch_bounds__(128, 1) halo_kernel(const __grid_constant__ CU
   __syncthreads();
   if (threadIdx.x != 0) return;
   prefetch_tmap(&m);
-  const int bytes = variant == 0 ? 32768 : variant == 3 ? 16384 : 4 * 56 * 128;
+  const int bytes = variant == 0 ? 32768 : variant == 3 ? 16384 : 4 * 56 * 128;  // 4: as 2
   int issued = 0;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++issued) {
     const int s = issued % STAGES;
     if (issued >= STAGES) mbar_wait(&full[s], ((issued / STAGES) - 1) & 1);  // the stage's previous load landed
-    const int n = tile / 28, pr = tile % 28;
+    const int n = variant == 4 ? (tile / 28) % 4 : tile / 28, pr = tile % 28;  // 4: an L2-resident 3.2 MB window
     uint8_t* dst = sm + s * STAGE;
     mbar_arrive_expect_tx(&full[s], bytes);
     if (variant == 0) tma_load_5d(dst, &m, &full[s], 0, -1, 2 * pr - 1, 0, n);
     else if (variant == 1)
       for (int r = 0; r < 4; ++r) tma_load_5d(dst + r * 8192 + 128, &m, &full[s], 0, 0, 2 * pr - 1 + r, 0, n);
     else if (variant == 2) tma_load_5d(dst, &m, &full[s], 0, 0, 2 * pr - 1, 0, n);
-    else tma_load_5d(dst, &m, &full[s], 0, -1, 2 * pr, 0, n);
+    else if (variant == 3) tma_load_5d(dst, &m, &full[s], 0, -1, 2 * pr, 0, n);
+    else tma_load_5d(dst, &m, &full[s], 0, 0, 2 * pr - 1, 0, n);
   }
   // drain the last STAGES loads
   for (int k = issued - STAGES; k < issued; ++k)
@@ -67,12 +68,12 @@ int main() {
   const int tiles = N * 28;
   cudaFuncSetAttribute(halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, STAGES * STAGE + 2048);
   const char* names[] = {"box 64px x 4 rows at w=-1 (product)", "4 boxes 56px x 1 row", "box 56px x 4 rows (dense)",
-                         "box 64px x 2 rows at w=-1"};
-  for (int v = 0; v < 4; ++v) {
+                         "box 64px x 2 rows at w=-1", "box 56px x 4 rows, L2-resident window"};
+  for (int v = 0; v < 5; ++v) {
     CUtensorMap m;
     cuuint64_t gd[5] = {64, (cuuint64_t)W, (cuuint64_t)H, 1, (cuuint64_t)N};
     cuuint64_t gs[4] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128, (cuuint64_t)H * W * 128};
-    cuuint32_t bd[5] = {64, v == 1 || v == 2 ? 56u : 64u, v == 1 ? 1u : (v == 3 ? 2u : 4u), 1, 1};
+    cuuint32_t bd[5] = {64, v == 1 || v == 2 || v == 4 ? 56u : 64u, v == 1 ? 1u : (v == 3 ? 2u : 4u), 1, 1};
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = enc()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, x, gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -91,7 +92,7 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       if (ms < best) best = ms;
     }
-    const double moved = v == 0 || v == 1 || v == 2 ? (double)tiles * 4 * 56 * 128 : (double)tiles * 2 * 56 * 128;
+    const double moved = v != 3 ? (double)tiles * 4 * 56 * 128 : (double)tiles * 2 * 56 * 128;
     printf("%-40s %7.2f us  %7.1f GB/s (L2->SM, valid bytes)  %s\n", names[v], best * 1e3, moved / (best * 1e-3) / 1e9,
            cudaGetErrorString(cudaGetLastError()));
   }
