@@ -233,7 +233,14 @@ __device__ __forceinline__ float gelu4(float x, uint32_t tab_s) {
   return __fmul_rn(__fmul_rn(0.5f, x), __fadd_rn(1.0f, h));
 }
 
-template <int BN, int STAGES, int KPS, int RES, int CG>
+// MC > 1: a cluster of MC CTAs along N shares each A (activation) tile: the
+// CTAs own consecutive column tiles of one row tile, every reduce block's A box
+// is loaded once by CTA (block % MC) and TMA-multicast into all MC CTAs, and a
+// stage is free only when every CTA of the cluster has consumed it (each MMA
+// commit arrives on the stage's empty barrier in all MC CTAs).  Per-SM L2->SM
+// bytes of A drop by MC: the single-wave small layers (cfg 2) are bound by
+// the per-SM operand feed, not by the tensor pipe.
+template <int BN, int STAGES, int KPS, int RES, int CG, int MC>
 __global__ void __launch_bounds__(kThreads, 1)
 brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                  const __grid_constant__ CUtensorMap map_b,
@@ -241,6 +248,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   using S = Smem<BN, STAGES, KPS, RES, CG>;
   constexpr bool PAIR = CG == 2;
   static_assert(!PAIR || RES == 0, "CTA pairs stream both operands");
+  static_assert(MC == 1 || (CG == 1 && RES == 0), "A multicast: single-CTA MMAs, streamed operands");
+  constexpr bool MCAST = MC > 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B-swizzled tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -260,9 +269,16 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   // owns row tile 2*tm + rank and B rows [rank*BN/2, (rank+1)*BN/2) of the tile
   const uint32_t rank = PAIR ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
-  const int cl_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int n_cl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int num_tiles = (PAIR ? (p.tiles_m + 1) >> 1 : p.tiles_m) * p.tiles_n;
+  const uint32_t mrank = MCAST ? cluster_ctarank() : 0;
+  const int cl_id = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / MC;
+  const int n_cl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x / MC;
+  // work items: pair tiles, multicast groups (MC column tiles of one row tile) or tiles
+  const int tiles_ng = p.tiles_n / MC;
+  const int num_tiles = (PAIR ? (p.tiles_m + 1) >> 1 : p.tiles_m) * tiles_ng;
+  auto tile_mn = [&](int tile, int& tm, int& tn) {
+    tm = tile / tiles_ng;
+    tn = (tile - tm * tiles_ng) * MC + (int)mrank;
+  };
   // stages per tile; halo conv: one per channel block
   const int nstages = RES == 2 ? p.cv_Cb : p.kblocks / KPS;
 
@@ -272,7 +288,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (p.tma_store) prefetch_tmap(&map_c);  // the epilogue's first store must not fetch it
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -295,7 +311,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     }
   }
   tc_fence_before();
-  if (PAIR) cluster_sync();  // the peer signals the leader's barriers
+  if (PAIR || MCAST) cluster_sync();  // the peer signals the leader's barriers / multicast targets ready
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // uniform (MMA operand)
@@ -317,7 +333,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (lane == 0) {
       FeedIter f;
       if (cl_id < num_tiles) {
-        const int tm = cl_id / p.tiles_n, tn = cl_id % p.tiles_n;
+        int tm, tn;
+        tile_mn(cl_id, tm, tn);
         if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
         else f.start(p, tm, tn);
       }
@@ -342,7 +359,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
       for (int tile = cl_id; tile < num_tiles; tile += n_cl) {
         if (tile != cl_id) {  // the first tile's feed was set up before the wait
-          const int tm = tile / p.tiles_n, tn = tile % p.tiles_n;
+          int tm, tn;
+          tile_mn(tile, tm, tn);
           if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
           else f.start(p, tm, tn);
         }
@@ -360,7 +378,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             } else {
               mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
-              tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
+              if (!MCAST)
+                tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
+              else if (j % MC == (int)mrank)  // this CTA's share of the cluster's A boxes
+                tma_load_5d_mc(sa, &map_a, &full[s], (uint16_t)((1u << MC) - 1), f.ai.c[0], f.ai.c[1], f.ai.c[2],
+                               f.ai.c[3], f.ai.c[4]);
               TPP_STAMP(blockIdx.x == 0 && it == 0, 11, gtimer());
               TPP_STAMP(blockIdx.x == 0 && j == 0 && it / nstages < 32, 200 + it / nstages, gtimer());
               if (!RES)
@@ -450,6 +472,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             }
           }
           if (PAIR) umma_commit_pair_warp(&empty[s], 3);
+          else if (MCAST) umma_commit_mc_warp(&empty[s], (uint16_t)((1u << MC) - 1));
           else umma_commit_warp(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -471,8 +494,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     uint32_t nstore = 0;
     uint32_t tcount = 0;
     for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
-      const int tn = tile % p.tiles_n;
-      const int tm = PAIR ? 2 * (tile / p.tiles_n) + (int)rank : tile / p.tiles_n;
+      int tm, tn;
+      tile_mn(tile, tm, tn);
+      if (PAIR) tm = 2 * tm + (int)rank;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       float* bs = bias_s + as * 256;
       if (p.flags & TPP_FC_BIAS) {
@@ -647,7 +671,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   }
 
   tc_fence_before();
-  if (PAIR) cluster_sync();  // neither CTA leaves while the pair still uses its smem / TMEM
+  if (PAIR || MCAST) cluster_sync();  // no CTA leaves while the cluster still uses its smem / TMEM / barriers
   else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
@@ -702,18 +726,19 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
   return TPP_OK;
 }
 
-template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1>
+template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1, int MC = 1>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       const Params& p, cudaStream_t stream) {
   using S = Smem<BN, STAGES, KPS, RES, CG>;
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
-  auto kern = brgemm_tc_kernel<BN, STAGES, KPS, RES, CG>;
+  auto kern = brgemm_tc_kernel<BN, STAGES, KPS, RES, CG, MC>;
+  constexpr int CL = CG * MC;  // cluster size (one of CG, MC is 1)
   static int max_clusters = -1;
   if (max_clusters < 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
-    max_clusters = num_sms() / CG;
-    if (CG > 1) {
+    max_clusters = num_sms() / CL;
+    if (CL > 1) {
       // co-resident pairs (SM pairs of one TPC) — a persistent grid must not exceed it
       cudaLaunchConfig_t q{};
       q.gridDim = dim3(num_sms());
@@ -721,7 +746,7 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
       q.dynamicSmemBytes = S::BYTES;
       cudaLaunchAttribute ca[1];
       ca[0].id = cudaLaunchAttributeClusterDimension;
-      ca[0].val.clusterDim.x = CG; ca[0].val.clusterDim.y = 1; ca[0].val.clusterDim.z = 1;
+      ca[0].val.clusterDim.x = CL; ca[0].val.clusterDim.y = 1; ca[0].val.clusterDim.z = 1;
       q.attrs = ca;
       q.numAttrs = 1;
       int n = 0;
@@ -729,8 +754,8 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
       cudaGetLastError();
     }
   }
-  const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * p.tiles_n;
-  const int grid = CG * (units < max_clusters ? units : max_clusters);
+  const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * (p.tiles_n / MC);
+  const int grid = CL * (units < max_clusters ? units : max_clusters);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -740,9 +765,9 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CG; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
+  attr[1].val.clusterDim.x = CL; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = CG > 1 ? 2 : 1;
+  cfg.numAttrs = CL > 1 ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
@@ -751,7 +776,14 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
 
 // (tile width, reduce blocks per stage, CTAs per MMA) -> instantiation; stages fill ~192 KB
 static int launch(int bn_tile, int kps, int cg, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                  const Params& p, cudaStream_t s) {
+                  const Params& p, cudaStream_t s, int mcast = 1) {
+  if (mcast > 1) {  // A-multicast clusters (1-CTA MMAs, one reduce block per stage)
+    if (cg == 1 && kps == 2 && bn_tile == 64) {
+      if (mcast == 2) return launch_cfg<64, 4, 2, 0, 1, 2>(ma, mb, mc, p, s);
+      if (mcast == 4) return launch_cfg<64, 4, 2, 0, 1, 4>(ma, mb, mc, p, s);
+    }
+    return fail(TPP_E_UNSUPPORTED, "no A-multicast kernel instantiation for this tile shape");
+  }
   if (cg == 2) {
     if (kps == 1) {
       switch (bn_tile) {
@@ -906,7 +938,7 @@ int pick_kps(int BN, int kblocks, bool kmajor_ok, int cg) {
   // 1-CTA wide tiles: keep the deeper pipeline (48 KB per block already);
   // pairs: 32 KB per block, two per TMA box halve the producer's issue count
   if (BN == 256) return (cg == 2 && kblocks % 2 == 0) ? 2 : 1;
-  if (BN == 64 && kblocks % 4 == 0) return 4;
+  // BN = 64: two blocks per box (cfg 2: 6.25 us vs 6.7 us with four, 8.2 with one)
   if (kblocks % 2 == 0) return 2;
   return 1;
 }
@@ -925,8 +957,22 @@ int pick_cg(int BN, int tiles_m, int tiles_n, bool b_mn) {
   return (BN == 256 && (int64_t)((tiles_m + 1) / 2) * tiles_n >= num_sms() / 2) ? 2 : 1;
 }
 
+// A-multicast cluster size for forward FC (experiments: TPP_MC=2|4).  Off by
+// default: on cfg 2 (one 128x64 tile per CTA) clusters of 2 / 4 sharing the
+// activation boxes measured 6.96 / 7.12 us against 6.25 us without -- halving
+// the per-SM A bytes does not pay for coupling every stage to the slowest CTA.
+int pick_mc(int BN, int cg, int kps, int tiles_m, int tiles_n) {
+  static const int forced = [] {
+    const char* e = getenv("TPP_MC");
+    return e ? atoi(e) : 0;
+  }();
+  if (BN != 64 || cg != 1 || kps != 2 || (forced != 2 && forced != 4)) return 1;
+  (void)tiles_m;
+  return tiles_n % forced == 0 ? forced : 1;
+}
+
 int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* b_ptr, tc::Params p,
-             int BN, int kps, int cg, cudaStream_t stream) {
+             int BN, int kps, int cg, cudaStream_t stream, int mcast = 1) {
   CUtensorMap ma, mb, mc;
   int rc = tc::make_map_5d(&ma, a_ptr, A.dims, A.strides, A.box);
   if (rc) return rc;
@@ -949,7 +995,7 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   }
   p.fa = A.feed;
   p.fb = B.feed;
-  return tc::launch(BN, kps, cg, ma, mb, mc, p, stream);
+  return tc::launch(BN, kps, cg, ma, mb, mc, p, stream, mcast);
 }
 
 }  // namespace
@@ -988,11 +1034,12 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     const int kblocks = k_b * (bk / 64);
     const int cg = pick_cg(BN, tiles_m, feats / BN, false);
     const int kps = pick_kps(BN, kblocks, bk == 64, cg);
+    const int mc = pick_mc(BN, cg, kps, tiles_m, feats / BN);
     p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
     p.o_bn = bn; p.o_bm = bm; p.o_mb = m_b;
     return run_gemm(kmajor_operand(n_b, k_b, bn, bk, BM, kps), kmajor_operand(m_b, k_b, bm, bk, BN / cg, kps),
-                    x_or_dy, w_packed, p, BN, kps, cg, stream);
+                    x_or_dy, w_packed, p, BN, kps, cg, stream, mc);
   }
   if (flavor == 1) {
     // dx[n_b][k_b][bn][bk] = dy[n_b][m_b][bn][bm] . W ; B = W as MN-major over its bk

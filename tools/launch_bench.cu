@@ -52,7 +52,7 @@ __global__ void empty_kernel(int* flag, int pdl, int touch) {
   if (threadIdx.x == 0 && blockIdx.x == 0 && flag) atomicAdd(flag, touch ? smem[0] + 1 : 1);
 }
 
-static float run(int grid, int threads, int smem, int pdl, int n = 200) {
+static float run(int grid, int threads, int smem, int pdl, int n = 200, int cluster = 1) {
   int* flag;
   CK(cudaMalloc(&flag, 4));
   CK(cudaFuncSetAttribute(empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -67,11 +67,18 @@ static float run(int grid, int threads, int smem, int pdl, int n = 200) {
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+      at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (cluster > 1) {
+      at[na].id = cudaLaunchAttributeClusterDimension;
+      at[na].val.clusterDim.x = cluster; at[na].val.clusterDim.y = 1; at[na++].val.clusterDim.z = 1;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     CK(cudaLaunchKernelEx(&cfg, empty_kernel, flag, pdl, smem > 0 ? 1 : 0));
   }
   CK(cudaStreamEndCapture(s, &g));
@@ -155,5 +162,8 @@ int main() {
   for (auto& c : cfgs)
     printf("%4d %6d %6d %3d : %.2f  (%s)\n", c[0], c[1], c[2], c[3], run(c[0], c[1], c[2], c[3]),
            cudaGetErrorString(cudaGetLastError()));
+  for (int cl = 1; cl <= 4; cl *= 2)
+    printf("cluster %d: 128 CTAs x 384 thr, 200 KB smem, pdl: %.2f us per launch (%s)\n", cl,
+           run(128, 384, 200 * 1024, 1, 200, cl), cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
