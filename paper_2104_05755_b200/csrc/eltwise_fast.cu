@@ -240,6 +240,46 @@ transpose16_kernel(const uint32_t* __restrict__ in, int64_t in_ld2, uint32_t* __
   }
 }
 
+// A/B switch for the 32-bit-access transpose below (experiments)
+static bool use_word_transpose() {
+  static const bool v = getenv("TPP_TRANSPOSE32") != nullptr;
+  return v;
+}
+
+// 16-bit transpose with 16-byte global accesses, full 64x64 tiles (R, C
+// multiples of 64, 16-byte aligned columns).  Each thread loads 8 rows of a
+// column pair (two 16-byte loads), pairs them into 8 output words (row r+k,
+// columns j, j+1) in registers, stages the words in a [64][33] shared tile
+// (2-way bank conflicts on the writes, none on the reads) and stores 16-byte
+// chunks of output rows.
+__global__ void __launch_bounds__(256)
+transpose16_v16_kernel(const uint16_t* __restrict__ in, int64_t in_ld, uint16_t* __restrict__ out, int64_t out_ld,
+                       int R) {
+  __shared__ uint32_t tile[64][33];  // [i][j/2]
+  const int tiles_i = R / 64;
+  const int i0 = (blockIdx.x % tiles_i) * 64, j0 = (blockIdx.x / tiles_i) * 64;
+  const int t = threadIdx.x;
+  {
+    const int jp = t >> 3, c = t & 7;  // column pair (32), 8-row chunk (8)
+    const uint16_t* src = in + i0 + 8 * c + (int64_t)(j0 + 2 * jp) * in_ld;
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(src));
+    const uint4 b = __ldg(reinterpret_cast<const uint4*>(src + in_ld));
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      tile[8 * c + 2 * q][jp] = __byte_perm(aw[q], bw[q], 0x5410);      // row 2q: (a lo, b lo)
+      tile[8 * c + 2 * q + 1][jp] = __byte_perm(aw[q], bw[q], 0x7632);  // row 2q+1: (a hi, b hi)
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int i = (t >> 3) + 32 * pass, q = t & 7;  // output row, 16-byte chunk
+    const uint4 v = make_uint4(tile[i][4 * q], tile[i][4 * q + 1], tile[i][4 * q + 2], tile[i][4 * q + 3]);
+    *reinterpret_cast<uint4*>(out + j0 + 8 * q + (int64_t)(i0 + i) * out_ld) = v;
+  }
+}
+
 // VNNI alpha 2, 16-bit: out column g = interleave(in columns 2g, 2g+1), with a
 // zero column past lcols; 8 rows of one column pair per thread-step
 __global__ void __launch_bounds__(256)
@@ -340,7 +380,11 @@ int fast_transform(int kind, int esize, const void* in, int in_ld, void* out, in
     if (grid == 0) return 0;
     switch (esize) {
       case 2:
-        if (R % 2 == 0 && C % 2 == 0 && in_ld % 2 == 0 && out_ld % 2 == 0 && reinterpret_cast<uintptr_t>(in) % 4 == 0 &&
+        if (R % 64 == 0 && C % 64 == 0 && in_ld % 8 == 0 && out_ld % 8 == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0 &&
+            reinterpret_cast<uintptr_t>(out) % 16 == 0 && !use_word_transpose()) {
+          const unsigned g64 = (unsigned)((R / 64) * (C / 64));
+          fast::transpose16_v16_kernel<<<g64, 256, 0, s>>>((const uint16_t*)in, in_ld, (uint16_t*)out, out_ld, R);
+        } else if (R % 2 == 0 && C % 2 == 0 && in_ld % 2 == 0 && out_ld % 2 == 0 && reinterpret_cast<uintptr_t>(in) % 4 == 0 &&
             reinterpret_cast<uintptr_t>(out) % 4 == 0) {
           const unsigned g64 = (unsigned)(((R + 63) / 64) * ((C + 63) / 64));
           fast::transpose16_kernel<<<g64, 256, 0, s>>>((const uint32_t*)in, in_ld / 2, (uint32_t*)out, out_ld / 2, R, C);

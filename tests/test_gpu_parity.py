@@ -538,6 +538,15 @@ def test_dense_fast_paths_match_generic():
     t = tpp.alloc(tpp.TensorDesc(48, 64, 48, tpp.DType.BF16))
     tpp.transform(av, tpp.TransformSpec(tpp.TransformKind.TRANSPOSE), t)
     assert np.array_equal(tpp.bits_of(t), a.T)
+    # full 64x64 tiles: the 16-byte-access transpose (incl. a padded output ld)
+    for (rr, cc, old) in ((128, 192, 192), (192, 64, 72)):
+        b = rng.integers(0, 1 << 16, size=(rr, cc), dtype=np.uint16)
+        bv = tpp.TensorView(tpp.TensorDesc(rr, cc, rr, tpp.DType.BF16),
+                            torch.from_numpy(b.reshape(-1, order="F").view(np.int16).copy()).cuda().view(torch.bfloat16))
+        tb = tpp.TensorView(tpp.TensorDesc(cc, rr, old, tpp.DType.BF16),
+                            torch.zeros(old * rr, dtype=torch.bfloat16, device="cuda"))
+        tpp.transform(bv, tpp.TransformSpec(tpp.TransformKind.TRANSPOSE), tb)
+        assert np.array_equal(tpp.bits_of(tb), b.T), (rr, cc, old)
     vn = tpp.alloc(tpp.TensorDesc(128, 24, 128, tpp.DType.BF16))
     tpp.transform(av, tpp.TransformSpec(tpp.TransformKind.VNNI, alpha=2), vn)
     got = tpp.bits_of(vn)
