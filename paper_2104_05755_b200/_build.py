@@ -29,6 +29,8 @@ FLAGS = [
 # diagnostic build: per-phase timestamps in the tensor-core kernels (tools/*_ts.py)
 if os.environ.get("TPP_PHASE_STAMPS"):
     FLAGS.append("-DTPP_PHASE_STAMPS")
+# experiment builds: extra nvcc flags (e.g. -DTPP_GELU_FMA)
+FLAGS += os.environ.get("TPP_NVCC_EXTRA", "").split()
 
 
 def _stale() -> bool:
