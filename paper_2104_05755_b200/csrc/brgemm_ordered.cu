@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "sm100.cuh"
 
 namespace tpp {
 
@@ -129,7 +130,11 @@ brgemm_ordered_kernel(OrderedParams p) {
 // entries in shared memory, so the serial per-element chain reads operands
 // at shared-memory latency instead of waiting on L2 every step.  Same order,
 // same bits as brgemm_ordered_kernel.
-constexpr int kOTM = 16, kOTN = 8;  // 128 threads
+constexpr int kOTM = 16, kOTN = 8;  // 128 C elements per CTA
+// entry slots: kES threads per C element, each running the partial-sum chains
+// of every kES-th batch entry (independent chains); slot 0 then adds the
+// parts to the accumulator in entry order
+constexpr int kES = 4;
 
 template <typename TIn>
 __device__ __forceinline__ const TIn* batch_a(const OrderedParams& p, int64_t inst, int64_t i) {
@@ -164,22 +169,38 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // fast: FP32, plain layouts, 16-byte aligned rows/columns, full tile ->
 // 16-byte cp.async staging.
 template <typename TIn, typename TAcc, int KC>
-__global__ void __launch_bounds__(kOTM * kOTN)
-brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long* dbg) {
+__global__ void __launch_bounds__(kOTM * kOTN * kES)
+brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long* dbg,
+                           const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                           int use_tma) {
   using A = Arith<TAcc>;
   using W = Widen<TIn, TAcc>;
   const int K = KC ? KC : p.k;
-  extern __shared__ __align__(16) unsigned char osm[];
+  extern __shared__ __align__(128) unsigned char osm[];
+  __shared__ uint64_t tma_bar;  // TMA staging: one box of A rows + one of B columns per chunk
+  uint32_t tma_ph = 0;
   TIn* As = reinterpret_cast<TIn*>(osm);            // [nb][K][kOTM]  (rows contiguous)
   TIn* Bs = As + (size_t)nb * K * kOTM;             // [nb][kOTN][K]  (columns contiguous)
+  // [nb][kOTM * kOTN] partial sums, 16-byte aligned after the B columns
+  TAcc* Ps = reinterpret_cast<TAcc*>((reinterpret_cast<uintptr_t>(Bs + (size_t)nb * K * kOTN) + 15) & ~uintptr_t(15));
   const int tiles_m = (p.m + kOTM - 1) / kOTM;
   const int m0 = (blockIdx.x % tiles_m) * kOTM, n0 = (blockIdx.x / tiles_m) * kOTN;
-  const int tid = threadIdx.x, r = tid % kOTM, cidx = tid / kOTM;
+  const int tid = threadIdx.x, es = tid / (kOTM * kOTN), etid = tid % (kOTM * kOTN);
+  const int r = etid % kOTM, cidx = etid / kOTM;
   const int mi = m0 + r, ni = n0 + cidx;
   const bool live = mi < p.m && ni < p.n;
-  constexpr int nthr = kOTM * kOTN;
+  constexpr int nthr = kOTM * kOTN * kES;
   auto gt = [] { unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; };
   if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[0] = gt();
+  if (use_tma) {
+    if (tid == 0) {
+      sm100::mbar_init(&tma_bar, 1);
+      sm100::fence_mbar_init();
+      sm100::prefetch_tmap(&tma_a);
+      sm100::prefetch_tmap(&tma_b);
+    }
+    __syncthreads();
+  }
   for (int64_t inst = blockIdx.y; inst < p.instances; inst += gridDim.y) {
     TAcc* c = reinterpret_cast<TAcc*>(p.c) + inst * p.inst_c;
     TAcc acc = TAcc(0);
@@ -192,7 +213,18 @@ brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long
       const int cnt = (int)min((int64_t)nb, p.count - i0);
       __syncthreads();  // previous chunk fully consumed
       // stage the chunk's A rows [m0, m0+kOTM) and B columns [n0, n0+kOTN)
-      for (int bi = 0; bi < cnt; ++bi) {
+      if (use_tma) {
+        // [nb][K][kOTM] A rows and [nb][kOTN][K] B columns, entries past
+        // `count` zero-filled (never read)
+        if (tid == 0) {
+          sm100::mbar_arrive_expect_tx(&tma_bar, (uint32_t)(nb * K * (kOTM + kOTN) * (int)sizeof(TIn)));
+          sm100::tma_load_5d(As, &tma_a, &tma_bar, 2 * m0, 0, (int)i0, (int)inst, 0);
+          sm100::tma_load_5d(Bs, &tma_b, &tma_bar, 0, n0, (int)i0, (int)inst, 0);
+        }
+        sm100::mbar_wait(&tma_bar, tma_ph);
+        tma_ph ^= 1u;
+      }
+      for (int bi = 0; bi < (use_tma ? 0 : cnt); ++bi) {
         const TIn* ab = batch_a<TIn>(p, inst, i0 + bi);
         const TIn* bb = batch_b<TIn>(p, inst, i0 + bi);
         TIn* as = As + (size_t)bi * K * kOTM;
@@ -232,7 +264,11 @@ brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
       if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[1] = gt();
-      for (int bi = 0; bi < cnt; ++bi) {
+      // The per-entry partial sums are independent chains (part_i depends
+      // only on entry i); only acc = acc + part_i is ordered across entries
+      // (contraction.py:417-424).  Slot es runs entries es, es + kES, ...
+      int bi = es;
+      for (; bi < cnt; bi += kES) {
         const TIn* a = As + (size_t)bi * K * kOTM + r;
         const TIn* b = Bs + (size_t)bi * K * kOTN + cidx * K;
         TAcc part = TAcc(0);
@@ -248,16 +284,37 @@ brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long
 #pragma unroll 8
           for (int kk = 0; kk < K; ++kk) part = A::add(part, A::mul(W::w(a[kk * kOTM]), W::w(b[kk])));
         }
-        acc = A::add(acc, part);
+        Ps[(size_t)bi * (kOTM * kOTN) + etid] = part;
       }
+      __syncthreads();
+      if (es == 0)
+        for (int e = 0; e < cnt; ++e) acc = A::add(acc, Ps[(size_t)e * (kOTM * kOTN) + etid]);
     }
-    if (live) c[mi + (int64_t)ni * p.ldc] = acc;
+    if (live && es == 0) c[mi + (int64_t)ni * p.ldc] = acc;
     if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[2] = gt();
   }
 }
 
 template <typename TIn, typename TAcc, int KC>
 static int launch_smem_kc(const OrderedParams& p, cudaStream_t s, int nb, int fast, size_t smem) {
+  // FP32 stride batches with box-sized extents: stage each chunk with two TMA
+  // boxes (A rows: FP32 seen as BF16 pairs {2m, k, entry, instance}; B
+  // columns {2k, n, entry, instance}) instead of 16-byte cp.async
+  CUtensorMap ma{}, mb{};
+  int use_tma = 0;
+  if (fast && sizeof(TIn) == 4 && p.k <= 128 && nb <= 256 && p.stride_a > 0 && p.stride_b > 0 && p.instances <= 0x7fffffff && p.count <= 0x7fffffff &&
+      !getenv("TPP_ORDERED_CPASYNC")) {
+    const uint64_t da[5] = {2 * (uint64_t)p.m, (uint64_t)p.k, (uint64_t)p.count, (uint64_t)p.instances, 1};
+    const uint64_t sa[4] = {(uint64_t)p.lda * 4, (uint64_t)p.stride_a * 4, (uint64_t)(p.inst_a ? p.inst_a * 4 : 16),
+                            16};
+    const uint32_t ba[5] = {2 * kOTM, (uint32_t)p.k, (uint32_t)nb, 1, 1};
+    const uint64_t db[5] = {2 * (uint64_t)p.k, (uint64_t)p.n, (uint64_t)p.count, (uint64_t)p.instances, 1};
+    const uint64_t sb[4] = {(uint64_t)p.ldb * 4, (uint64_t)p.stride_b * 4, (uint64_t)(p.inst_b ? p.inst_b * 4 : 16),
+                            16};
+    const uint32_t bb[5] = {2 * (uint32_t)p.k, kOTN, (uint32_t)nb, 1, 1};
+    if (make_tma_map_5d(&ma, p.a, da, sa, ba, 0) == TPP_OK && make_tma_map_5d(&mb, p.b, db, sb, bb, 0) == TPP_OK)
+      use_tma = 1;
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(brgemm_ordered_smem_kernel<TIn, TAcc, KC>,
@@ -267,7 +324,9 @@ static int launch_smem_kc(const OrderedParams& p, cudaStream_t s, int nb, int fa
   }
   const int tiles = ((p.m + kOTM - 1) / kOTM) * ((p.n + kOTN - 1) / kOTN);
   dim3 grid((unsigned)tiles, (unsigned)(p.instances < 65535 ? p.instances : 65535));
-  brgemm_ordered_smem_kernel<TIn, TAcc, KC><<<grid, kOTM * kOTN, smem, s>>>(p, nb, fast, debug_timestamps());
+  smem += (size_t)nb * kOTM * kOTN * sizeof(TAcc) + 16;  // partial sums
+  brgemm_ordered_smem_kernel<TIn, TAcc, KC><<<grid, kOTM * kOTN * kES, smem, s>>>(p, nb, fast, debug_timestamps(), ma, mb,
+                                                                            use_tma);
   TPP_CUDA_LAUNCH_CHECK("brgemm_ordered_smem_kernel");
   return TPP_OK;
 }
