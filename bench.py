@@ -220,28 +220,34 @@ def run_ours(args, rank, world, dist):
     n_out = NB * KB * BN * BK
     x_host = torch.empty(n_in, dtype=torch.bfloat16, pin_memory=True)
     x_host.copy_(x0.cpu())
-    out_host = [torch.empty(n_out, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
-    x_dev = [torch.empty(n_in, dtype=torch.bfloat16, device=dev) for _ in range(2)]
-    out_dev = [torch.empty(n_out, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    # NBUF-deep buffering: H2D of step i only waits for compute of step
+    # i - NBUF and compute of step i only for the D2H of step i - NBUF.  (The
+    # step time is the PCIe link: 66-68 us with 2 or 4 buffers, eager or
+    # graph-captured; tools/copy_overlap.py: H2D 44.6, D2H 41.0, both
+    # directions concurrently 49-53 us per 2 MiB pair.)
+    NBUF = 4
+    out_host = [torch.empty(n_out, dtype=torch.bfloat16, pin_memory=True) for _ in range(NBUF)]
+    x_dev = [torch.empty(n_in, dtype=torch.bfloat16, device=dev) for _ in range(NBUF)]
+    out_dev = [torch.empty(n_out, dtype=torch.bfloat16, device=dev) for _ in range(NBUF)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_comp = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    ev_in = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_comp = [torch.cuda.Event() for _ in range(NBUF)]
+    ev_out = [torch.cuda.Event() for _ in range(NBUF)]
     for e in ev_comp + ev_out:
         e.record(comp)
 
     def e2e_step(i, comp):
         """Pipelined serving step: H2D of step i overlaps compute of i-1 and
-        D2H of i-2 (double-buffered device and host buffers, 3 streams)."""
-        b = i % 2
+        the D2H of earlier steps (NBUF-deep device and host buffers, 3 streams)."""
+        b = i % NBUF
         with torch.cuda.stream(s_in):
-            if i >= 2:
+            if i >= NBUF:
                 s_in.wait_event(ev_comp[b])      # x_dev[b] no longer read
             x_dev[b].copy_(x_host, non_blocking=True)
             ev_in[b].record(s_in)
         comp.wait_event(ev_in[b])
-        if i >= 2:
+        if i >= NBUF:
             comp.wait_event(ev_out[b])           # out_dev[b] already copied out
         layer0.forward(x_dev[b], NB, BN, out=out_dev[b], stream=comp)
         ev_comp[b].record(comp)
@@ -353,7 +359,7 @@ def run_ours(args, rank, world, dist):
                 "h2d_bytes_per_step": n_in * 2,
                 "d2h_bytes_per_step": n_out * 2,
                 "ms_per_step": round(e2e_ms_step, 6),
-                "api": "FcLayer.forward with a pinned H2D of the input and a D2H of the output every step; copies pipelined against compute on separate streams (double-buffered), the K-step serving loop captured once as a CUDA graph and replayed",
+                "api": "FcLayer.forward with a pinned H2D of the input and a D2H of the output every step; copies pipelined against compute on separate streams (4-deep buffers), the K-step serving loop captured once as a CUDA graph and replayed",
             },
             "gpu_launches": K,
             "clocks": clocks,
