@@ -182,20 +182,50 @@ conv_dw_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant_
   }
 }
 
-// dW[kbcb][tap][c][k] = sum over the Z partials of that block pair, ascending z
-__global__ void conv_dw_reduce(const float4* __restrict__ partial, float4* __restrict__ dw, int Z, int64_t per4,
-                               int64_t blocks) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per4 * blocks;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = e / per4, o = e % per4;
-    const float4* src = partial + (b * Z) * per4 + o;
-    float4 acc = src[0];
-    for (int zz = 1; zz < Z; ++zz) {
-      const float4 v = src[(int64_t)zz * per4];
-      acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
-      acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+// dW[kbcb][tap][c][k] = sum over the Z partials of that block pair in a
+// fixed order: kZS slices of consecutive partials (ascending z inside a
+// slice, loads issued 8 at a time), then the slice sums in slice order.  A CTA
+// owns 64 float4 outputs x kZS slices, so the ~22 MB of partials stream with
+// every SM loading (one thread per output over all Z left 36 CTAs with a
+// 148-long load-latency chain each: 25 us).
+constexpr int kZS = 4;
+__device__ __forceinline__ void add4(float4& a, const float4& v) {
+  a.x = __fadd_rn(a.x, v.x); a.y = __fadd_rn(a.y, v.y);
+  a.z = __fadd_rn(a.z, v.z); a.w = __fadd_rn(a.w, v.w);
+}
+__global__ void __launch_bounds__(64 * kZS) conv_dw_reduce(const float4* __restrict__ partial,
+                                                           float4* __restrict__ dw, int Z, int64_t per4,
+                                                           int64_t blocks) {
+  __shared__ float4 slice_sum[kZS][64];
+  const int lo = threadIdx.x & 63, sl = threadIdx.x >> 6;
+  const int zs = (Z + kZS - 1) / kZS, z0 = sl * zs, z1 = min(Z, z0 + zs);
+  for (int64_t e0 = (int64_t)blockIdx.x * 64; e0 < per4 * blocks; e0 += (int64_t)gridDim.x * 64) {
+    const int64_t e = e0 + lo;
+    const bool on = e < per4 * blocks;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (on && z0 < z1) {
+      const int64_t b = e / per4, o = e % per4;
+      const float4* src = partial + (b * Z) * per4 + o;
+      acc = src[(int64_t)z0 * per4];
+      int zz = z0 + 1;
+      for (; zz + 8 <= z1; zz += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (int64_t)(zz + u) * per4);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) add4(acc, v[u]);
+      }
+      for (; zz < z1; ++zz) add4(acc, __ldg(src + (int64_t)zz * per4));
     }
-    dw[e] = acc;
+    slice_sum[sl][lo] = acc;
+    __syncthreads();
+    if (sl == 0 && on) {
+      float4 r = slice_sum[0][lo];
+      for (int q = 1; q < kZS; ++q)
+        if (q * zs < Z) add4(r, slice_sum[q][lo]);
+      dw[e] = r;
+    }
+    __syncthreads();
   }
 }
 
@@ -263,9 +293,9 @@ int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, 
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(conv_dw_kernel)");
   TPP_CUDA_LAUNCH_CHECK("conv_dw_kernel");
   const int64_t per4 = (int64_t)p.taps * 64 * 64 / 4, blocks = (int64_t)Kb * Cb;
-  int64_t grid = (per4 * blocks + 255) / 256;
+  int64_t grid = (per4 * blocks + 63) / 64;
   if (grid > 4096) grid = 4096;
-  conv_dw_reduce<<<(unsigned)grid, 256, 0, stream>>>(reinterpret_cast<const float4*>(workspace),
+  conv_dw_reduce<<<(unsigned)grid, 64 * cdw::kZS, 0, stream>>>(reinterpret_cast<const float4*>(workspace),
                                                        reinterpret_cast<float4*>(dw), p.Z, per4, blocks);
   TPP_CUDA_LAUNCH_CHECK("conv_dw_reduce");
   return TPP_OK;

@@ -42,6 +42,13 @@ def main():
         conv = tpp.Conv2d(spec, w)
         y = torch.empty_like(x)
         fn = (lambda: conv.forward(x, out=y)) if a.op == "conv" else (lambda: conv.backward_data(x, din=y))
+    elif a.op == "convdw":
+        spec = tpp.ConvSpec(256, 1, 1, 56, 56)
+        x = torch.rand(256 * 56 * 56 * 64, generator=gen, device=dev).to(torch.bfloat16)
+        dy = torch.randn(256 * 56 * 56 * 64, generator=gen, device=dev).to(torch.bfloat16)
+        wv = (torch.randn(9 * 64 * 64, generator=gen, device=dev) * 0.1).to(torch.bfloat16)
+        conv = tpp.Conv2d(spec, wv)
+        fn = lambda: conv.backward_weights(x, dy)  # noqa: E731
     elif a.op == "ln":
         x = torch.randn(16384 * 1024, generator=gen, device=dev).to(torch.bfloat16)
         o = torch.empty_like(x)
