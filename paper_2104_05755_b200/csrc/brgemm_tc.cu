@@ -98,6 +98,7 @@ struct Params {
   int dbg_tile;
   int dbg_mode;  // experiments: bit0 skip epilogue math, bit1 skip MMAs
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
+  int cv_rows;              // conv: output rows per tile (2, or 4 for RES = 3)
 };
 
 // RES = 1: the B operand (conv weights, J = R*S*C_b tap blocks of BN x 64)
@@ -107,6 +108,16 @@ struct Params {
 // it through row-shifted descriptors), instead of one A box per tap.
 constexpr int kResMaxBytes = 72 * 1024;
 constexpr int kHaloRows = 4;   // 2 output rows + R - 1 (R <= 3)
+// RES = 3: halo tiles of 4 output rows (two M = 128 accumulators sharing each
+// weight tap, 6 halo rows per stage): per output row 1.5 halo rows cross L2->smem
+// instead of 2, and the per-tile handoff (commit, accumulator wait, stage wait)
+// is paid once per 4 rows
+template <int RES> struct ConvTile {
+  static constexpr bool HALO = RES >= 2;
+  static constexpr int ROWS = RES == 3 ? 4 : 2;  // output rows per tile
+  static constexpr int NACC = ROWS / 2;           // M = 128 accumulators per tile
+  static constexpr int HROWS = ROWS + 2;          // input rows per halo (R <= 3)
+};
 
 // CG = 2: CTA pair (cluster of 2, tcgen05 cta_group::2).  The pair computes a
 // 256 x BN tile: each CTA stages its own 128 rows of A and HALF of the B rows
@@ -115,21 +126,21 @@ constexpr int kHaloRows = 4;   // 2 output rows + R - 1 (R <= 3)
 // smem reads) drops by a quarter (BN=256: 48 KB -> 32 KB per 64-deep block).
 template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1>
 struct Smem {
-  static constexpr int A_BYTES = RES == 2 ? kHaloRows * 64 * BK * 2 : KPS * BM * BK * 2;
+  static constexpr int A_BYTES = ConvTile<RES>::HALO ? ConvTile<RES>::HROWS * 64 * BK * 2 : KPS * BM * BK * 2;
   static constexpr int B_BYTES = RES ? 0 : KPS * (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = 2 * BN * ConvTile<RES>::NACC;
   static constexpr int RES_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = RES_OFF + (RES ? kResMaxBytes : 0);
   // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base +
   // gelu table (float4 x 512: one entry per 9-bit |x| exponent prefix)
   static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
   // the conv (RES = 2) epilogue has no bias / GELU: no table, no bias staging
-  static constexpr int BIAS_OFF = TAB_OFF + (RES == 2 ? 0 : 512 * 16);    // float [2][256]
+  static constexpr int BIAS_OFF = TAB_OFF + (RES >= 2 ? 0 : 512 * 16);    // float [2][256]
   // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
   // when the smem budget allows (a chunk's store need not have left the
   // buffer before the next chunk is staged)
-  static constexpr int STG_OFF = (BIAS_OFF + (RES == 2 ? 0 : 2 * 256 * 4) + 1023) & ~1023;
+  static constexpr int STG_OFF = (BIAS_OFF + (RES >= 2 ? 0 : 2 * 256 * 4) + 1023) & ~1023;
   static constexpr int STG_BUFS = STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1;
   static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 * STG_BUFS + 1024;
 };
@@ -174,7 +185,7 @@ struct FeedIter {
       cb_n = p.cv_Cb; s_n = p.cv_S; pad = p.cv_pad;
       const int n = tm / p.cv_tiles_per_img, pr = tm % p.cv_tiles_per_img;
       s = 0;
-      ai.c[0] = 0; ai.c[1] = -pad; ai.c[2] = 2 * pr - pad; ai.c[3] = 0; ai.c[4] = n;
+      ai.c[0] = 0; ai.c[1] = -pad; ai.c[2] = p.cv_rows * pr - pad; ai.c[3] = 0; ai.c[4] = n;
     }
   }
   __device__ __forceinline__ void next() {
@@ -199,7 +210,7 @@ __device__ __forceinline__ int row_token(const Params& p, int tm, int r) {
   }
   const int n = tm / p.cv_tiles_per_img;
   const int pr = tm % p.cv_tiles_per_img;
-  const int oh = 2 * pr + (r >> 6), ow = r & 63;
+  const int oh = p.cv_rows * pr + (r >> 6), ow = r & 63;  // accumulator 0 (RES 3 stores through TMA only)
   if (oh >= p.cv_P || ow >= p.cv_Q) return -1;
   return (n * p.cv_P + oh) * p.cv_Q + ow;
 }
@@ -280,7 +291,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     tn = (tile - tm * tiles_ng) * MC + (int)mrank;
   };
   // stages per tile; halo conv: one per channel block
-  const int nstages = RES == 2 ? p.cv_Cb : p.kblocks / KPS;
+  using CT = ConvTile<RES>;
+  const int nstages = CT::HALO ? p.cv_Cb : p.kblocks / KPS;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&map_a);
@@ -301,7 +313,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     if (PAIR) tmem_alloc_pair(tmem_slot, S::TMEM_COLS);
     else tmem_alloc(tmem_slot, S::TMEM_COLS);
   }
-  if (RES != 2 && warp == 3 && p.act == TPP_ACT_GELU) {
+  if (!CT::HALO && warp == 3 && p.act == TPP_ACT_GELU) {
     for (int e = lane; e < 512; e += 32) {
       const int j = min(max(e - kGeluBase, 0), 15);
       gelu_tab[e] = e >= kGeluBase + 16
@@ -379,7 +391,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
               if (!MCAST)
-                tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], RES == 2 ? j : f.ai.c[3], f.ai.c[4]);
+                tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], CT::HALO ? j : f.ai.c[3], f.ai.c[4]);
               else if (j % MC == (int)mrank)  // this CTA's share of the cluster's A boxes
                 tma_load_5d_mc(sa, &map_a, &full[s], (uint16_t)((1u << MC) - 1), f.ai.c[0], f.ai.c[1], f.ai.c[2],
                                f.ai.c[3], f.ai.c[4]);
@@ -389,7 +401,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                 tma_load_5d(sa + S::A_BYTES, &map_b, &full[s], f.bi.c[0], f.bi.c[1], f.bi.c[2], f.bi.c[3], f.bi.c[4]);
             }
           }
-          if (RES != 2) f.next();
+          if (!CT::HALO) f.next();
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -417,7 +429,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 320 + (tcount == 30) * 2, clock64());
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 321 + (tcount == 30) * 2, gtimer());
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + as * BN;
+        const uint32_t tmem_d = tmem_base + as * (BN * CT::NACC);
         for (int j = 0; j < nstages; ++j) {
           mbar_wait(&full[s], ph);
           TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0, 2, gtimer());
@@ -425,7 +437,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           tc_fence_after();
           // descriptor start-address field is in 16-byte units
           const uint64_t soff = (uint64_t)((s * S::STAGE_BYTES) >> 4);
-          if (RES == 2) {
+          if (CT::HALO) {
             // tap (r, s) of channel block j: A rows start at halo row r*64 + s
             // (the 128B swizzle is address-based, so a row-shifted start is a
             // valid K-major view); weights block (r*S + s)*C_b + j is resident
@@ -437,21 +449,29 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
               // issuing thread must keep pace with 48-cycle N=64 MMAs)
 #pragma unroll
               for (int tap = 0; tap < 9; ++tap) {
-                const uint64_t ad = a0 + (uint64_t)((((tap / 3) * 64 + tap % 3) * 128) >> 4);
                 const uint64_t bd = b0 + btap * tap;
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk)
-                  if (!(TPP_DBG_MODE & 2))
-                    umma_f16_warp(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (j > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+                for (int h = 0; h < CT::NACC; ++h) {  // accumulator h: output rows 2h, 2h + 1 of the tile
+                  const uint64_t ad = a0 + (uint64_t)(((((tap / 3) + 2 * h) * 64 + tap % 3) * 128) >> 4);
+#pragma unroll
+                  for (int kk = 0; kk < BK / 16; ++kk)
+                    if (!(TPP_DBG_MODE & 2))
+                      umma_f16_warp(tmem_d + h * BN, ad + 2 * kk, bd + 2 * kk, idesc,
+                                    (j > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+                }
               }
             } else {
               for (int rr = 0; rr < p.cv_R; ++rr) {
                 for (int ss = 0; ss < p.cv_S; ++ss) {
-                  const uint64_t ad = a0 + (uint64_t)(((rr * 64 + ss) * 128) >> 4);
                   const uint64_t bd = b0 + btap * (rr * p.cv_S + ss);
 #pragma unroll
-                  for (int kk = 0; kk < BK / 16; ++kk)
-                    umma_f16_warp(tmem_d, ad + 2 * kk, bd + 2 * kk, idesc, (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+                  for (int h = 0; h < CT::NACC; ++h) {
+                    const uint64_t ad = a0 + (uint64_t)((((rr + 2 * h) * 64 + ss) * 128) >> 4);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                      umma_f16_warp(tmem_d + h * BN, ad + 2 * kk, bd + 2 * kk, idesc,
+                                    (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+                  }
                 }
               }
             }
@@ -532,7 +552,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         warp_rows = p.tma_store && t0 < p.tokens;
       } else {
         const int img = tm / p.cv_tiles_per_img;
-        sc2 = 2 * (tm - img * p.cv_tiles_per_img) + (q >> 1);
+        sc2 = CT::ROWS * (tm - img * p.cv_tiles_per_img) + (q >> 1);
         sc1 = (q & 1) * 32; sc4 = img;
         warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
       }
@@ -542,9 +562,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 189, clock64());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 18 + 4 * tcount, gtimer());
       tc_fence_after();
-      const int nch = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
+      // chunk c: accumulator c / nch1, 32 columns (grp + (c % nch1) * kEpiGroups) * 32
+      const int nch1 = (BN / 32 - grp + kEpiGroups - 1) / kEpiGroups;
+      const int nch = nch1 * CT::NACC;
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + as * (BN * CT::NACC);
+      auto chunk_col = [&](int c) { return (grp + (CT::NACC > 1 ? c % nch1 : c) * kEpiGroups) * 32; };
+      auto chunk_acc = [&](int c) { return CT::NACC > 1 ? c / nch1 : 0; };
       uint32_t v[32];
-      if (nch > 0) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + grp * 32, v);
+      if (nch > 0) tmem_ld32(tacc + grp * 32, v);
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 188, clock64());
       // release this warp's share of the accumulator as soon as its last
       // chunk is in registers, so the next tile's MMAs can start while the
@@ -562,13 +587,14 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (nch <= 0) release();
 #pragma unroll 1
       for (int ch = 0; ch < nch; ++ch) {
-        const int col = (grp + ch * kEpiGroups) * 32;
+        const int col = chunk_col(ch);
+        const int hacc = chunk_acc(ch);
         tmem_ld_wait();
         float x[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
         // the next chunk's TMEM load overlaps this chunk's math and stores
-        if (ch + 1 < nch) tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + col + kEpiGroups * 32, v);
+        if (ch + 1 < nch) tmem_ld32(tacc + chunk_acc(ch + 1) * BN + chunk_col(ch + 1), v);
         else release();
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0, 7, gtimer());
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 0, clock64());
@@ -646,7 +672,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           if (lane == 0) {
             // every chunk commits a bulk group (possibly empty) so that the
             // per-buffer wait_group counts stay aligned with nstore
-            if (warp_rows) tma_store_5d(&map_c, stg, m_in, sc1, sc2, mb, sc4);
+            // RES 3: accumulator h holds output rows 2h, 2h + 1 of the tile
+            if (CT::NACC == 1 ? warp_rows : (p.tma_store && sc2 + 2 * hacc < p.cv_P && sc1 < p.cv_Q))
+              tma_store_5d(&map_c, stg, m_in, sc1, sc2 + 2 * hacc, mb, sc4);
             bulk_commit();
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 3, clock64());
           }
@@ -829,6 +857,11 @@ static int launch(int bn_tile, int kps, int cg, const CUtensorMap& ma, const CUt
     // B resident + one input halo per channel block (conv)
     switch (bn_tile) {
       case 64: return launch_cfg<64, 3, 1, 2>(ma, mb, mc, p, s);
+    }
+  } else if (kps == -3) {
+    // as -2 with 4-row tiles (two accumulators per tile, 6-row halos)
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 2, 1, 3>(ma, mb, mc, p, s);
     }
   }
   return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
@@ -1107,7 +1140,13 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   p.cv_S = S;
   p.cv_pad = pad;
   p.cv_Cb = Cb;
-  p.cv_tiles_per_img = (P + 1) / 2;
+  // output rows per tile: 4 (RES 3) when the halo path and TMA stores apply
+  static const bool two_row = getenv("TPP_CONV_2ROW") != nullptr;  // experiments
+  const bool res_ok = BN == 64 && feats / BN == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
+  const bool halo_ok = res_ok && 2 + R - 1 <= tc::kHaloRows && W + S - 1 <= 64;
+  const bool rows4 = halo_ok && !two_row && reinterpret_cast<uintptr_t>(out) % 16 == 0 && !getenv("TPP_NO_TMA_STORE");
+  p.cv_rows = rows4 ? 4 : 2;
+  p.cv_tiles_per_img = (P + p.cv_rows - 1) / p.cv_rows;
   p.tiles_m = N * p.cv_tiles_per_img;
   p.tiles_n = feats / BN;
   p.feats = feats;
@@ -1126,7 +1165,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Cb, (uint64_t)N};
     const uint64_t str[4] = {128, (uint64_t)W * 128, (uint64_t)H * W * 128, (uint64_t)Cb * H * W * 128};
-    const uint32_t box[5] = {64, 64, halo ? (uint32_t)tc::kHaloRows : 2u, 1, 1};
+    const uint32_t box[5] = {64, 64, halo ? (uint32_t)(p.cv_rows + 2) : 2u, 1, 1};
     int rc = make_map_5d(&ma, x, dims, str, box);
     if (rc) return rc;
   }
@@ -1147,7 +1186,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
-  return launch(BN, halo ? -2 : (res ? -1 : 1), 1, ma, mb, mc, p, stream);
+  return launch(BN, halo ? (rows4 ? -3 : -2) : (res ? -1 : 1), 1, ma, mb, mc, p, stream);
 }
 
 }  // namespace tpp
