@@ -953,6 +953,8 @@ Operand mnmajor_operand(int red_blk, int mn_blk, int red_in, int tile_mn, int kp
 
 int pick_bn(int feats, int tiles_m, int pref) {
   if (pref) return pref;
+  static const int forced = getenv("TPP_BN") ? atoi(getenv("TPP_BN")) : 0;  // experiments
+  if (forced && feats % forced == 0) return forced;
   int BN = 256;
   while (BN > 64 && (feats % BN != 0 || (int64_t)tiles_m * (feats / BN) < num_sms())) BN /= 2;
   return BN;
