@@ -87,6 +87,29 @@ def test_brgemm_cases_bitwise(golden, variant):
         assert bits(to_host(c.primary)) == bits(g[key + "_c"]), f"case {i} ({dt}, {variant})"
 
 
+@pytest.mark.parametrize("m,n,k,count,beta", [(32, 16, 128, 37, 0.5), (32, 16, 132, 9, 1.0), (48, 24, 64, 16, 0.0)])
+def test_brgemm_fp32_stride_staging_paths(m, n, k, count, beta):
+    """FP32 STRIDE batches through the staged ordered engine: TMA-box staging
+    (k <= 128, chunks of entries with a ragged last chunk zero-filled past
+    `count`, padded lda / ldb / ldc, entry strides beyond the block) and the
+    cp.async fallback (k > 128); bitwise vs the reference order."""
+    rng = np.random.default_rng(100 + k + count)
+    lda, ldb, ldc = m + 8, k + 4, m + 4
+    sa, sb = lda * k + 8, ldb * n + 4
+    af = rng.standard_normal(sa * count).astype(np.float32)
+    bf = rng.standard_normal(sb * count).astype(np.float32)
+    c0 = rng.standard_normal((ldc, n)).astype(np.float32)
+    a_blocks = [af[i * sa: i * sa + lda * k].reshape(k, lda).T[:m, :] for i in range(count)]
+    b_blocks = [bf[i * sb: i * sb + ldb * n].reshape(n, ldb).T[:k, :] for i in range(count)]
+    want = O.brgemm(a_blocks, b_blocks, c0[:m, :], beta)
+    c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32),
+                       torch.from_numpy(c0.T.reshape(-1).copy()).cuda())
+    sp = tpp.GemmSpec(m, n, k, lda, ldb, ldc, beta=beta)
+    tpp.brgemm(sp, tpp.BrgemmBatch.stride(torch.from_numpy(af).cuda(), torch.from_numpy(bf).cuda(), sa, sb, count), c)
+    got = tpp.to_array(c)
+    assert bits(got) == bits(np.asarray(want, dtype=np.float32)), (m, n, k, count)
+
+
 def test_brgemm_cancellation_and_doubling():
     """test_gemm.py:117-137 properties on the GPU (FP64, exact)."""
     rng = np.random.default_rng(3)
