@@ -51,6 +51,11 @@ enum tpp_bcast { TPP_BCAST_NONE = 0, TPP_BCAST_ROW = 1, TPP_BCAST_COL = 2,
                  TPP_BCAST_SCALAR = 3 };
 
 const char* tpp_last_error(void);
+/* Thread-local description of the last tensor-core kernel this thread
+ * launched: its template instantiation <BN,STAGES,KPS,RES,CG,MC>, grid and
+ * tile counts (e.g. "brgemm_tc_kernel<256,3,2,0,2,1> grid=148 tiles=64x16").
+ * Lets tests assert which kernel a dispatch really ran. */
+const char* tpp_last_config(void);
 int tpp_version(void);
 /* number of SMs of the current device (0 if no device) */
 int tpp_device_sm_count(void);
@@ -62,7 +67,7 @@ typedef struct {
   int32_t bcast;   /* tpp_bcast */
 } tpp_tensor_desc;
 
-/* ---- BRGEMM TPP: contraction.py:154-195 (GemmSpec) --------------------- */
+/* ---- BRGEMM TPP: contraction.py:44-85 (GemmSpec) --------------------- */
 enum tpp_engine {
   TPP_ENGINE_AUTO = 0,     /* INT8 STRIDE -> tcgen05 kind::i8 (exact); else ordered;
                               BF16 layer drivers -> tensor cores                     */
@@ -81,20 +86,20 @@ typedef struct {
   double beta;                  /* C = beta*C + sum_i A_i B_i                        */
 } tpp_gemm_desc;
 
-/* contraction.py:371-432 brgemm() with BrgemmBatch.stride (contraction.py:272-278).
+/* contraction.py:261-322 brgemm() with BrgemmBatch.stride (contraction.py:162-168).
  * a, b: base pointers; strides and offsets are in ELEMENTS of in_dtype. */
 int tpp_brgemm_stride(const tpp_gemm_desc* d, const void* a, const void* b,
                       int64_t stride_a, int64_t stride_b, int64_t count,
                       void* c, void* stream);
-/* ... with BrgemmBatch.offset (contraction.py:262-270): device int64 offset arrays */
+/* ... with BrgemmBatch.offset (contraction.py:152-160): device int64 offset arrays */
 int tpp_brgemm_offset(const tpp_gemm_desc* d, const void* a, const void* b,
                       const int64_t* a_offsets, const int64_t* b_offsets, int64_t count,
                       void* c, void* stream);
-/* ... with BrgemmBatch.address (contraction.py:254-260): device arrays of block pointers */
+/* ... with BrgemmBatch.address (contraction.py:144-150): device arrays of block pointers */
 int tpp_brgemm_address(const tpp_gemm_desc* d, const void* const* a_ptrs,
                        const void* const* b_ptrs, int64_t count, void* c, void* stream);
 /* Many independent stride-BRGEMMs in one launch (the GPU form of the
- * reference's `threads=` job loop over disjoint C tiles, contraction.py:427-432
+ * reference's `threads=` job loop over disjoint C tiles, contraction.py:317-322
  * and kernels.py:323-329): instance j uses a + j*inst_a, b + j*inst_b,
  * c + j*inst_c (elements). */
 int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void* b,

@@ -16,7 +16,7 @@ Arithmetic rules (the reference's, restated):
   * numpy float32/float64 ``+``/``*`` are separately rounded IEEE ops (no FMA
     contraction), so evaluating the same expression in the same order gives
     the same bits;
-  * BRGEMM order (contraction.py:405-425): acc = beta-rule(C); for every batch
+  * BRGEMM order (contraction.py:295-315): acc = beta-rule(C); for every batch
     entry i: part = +0, then part += a[m,k]*b[k,n] for k ascending; acc += part.
 """
 
@@ -55,12 +55,12 @@ def round_bf16(values: np.ndarray) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
-# VNNI layouts — contraction.py:348-364, ops.py:573-588
+# VNNI layouts — contraction.py:238-254, ops.py:573-588
 # ---------------------------------------------------------------------------
 
 
 def vnni_pack_a(a: np.ndarray, alpha: int) -> np.ndarray:
-    """contraction.py:348-357 — (M,K) -> flat [ceil(K/alpha)][M][alpha]."""
+    """contraction.py:238-247 — (M,K) -> flat [ceil(K/alpha)][M][alpha]."""
     m, k = a.shape
     groups = -(-k // alpha)
     out = np.zeros((groups, m, alpha), dtype=a.dtype)
@@ -73,7 +73,7 @@ def vnni_pack_a(a: np.ndarray, alpha: int) -> np.ndarray:
 
 
 def vnni_unpack_a(flat: np.ndarray, alpha: int, m: int, k: int) -> np.ndarray:
-    """contraction.py:360-364."""
+    """contraction.py:250-254."""
     groups = -(-k // alpha)
     grid = np.asarray(flat)[: groups * m * alpha].reshape(groups, m, alpha)
     return grid.transpose(1, 0, 2).reshape(m, groups * alpha)[:, :k]
@@ -100,12 +100,12 @@ def vnni_to_vnnit(packed: np.ndarray, alpha: int, alpha_out: int, rows: int, col
 
 
 # ---------------------------------------------------------------------------
-# BRGEMM — contraction.py:285-432
+# BRGEMM — contraction.py:175-322
 # ---------------------------------------------------------------------------
 
 
 def strided2d(buf: np.ndarray, off: int, rows: int, cols: int, ld: int) -> np.ndarray:
-    """contraction.py:285-291 — column-major (rows x cols) window."""
+    """contraction.py:175-181 — column-major (rows x cols) window."""
     need = off + ld * (cols - 1) + rows
     if off < 0 or need > buf.size:
         raise ValueError(f"block exceeds buffer: need {need}, have {buf.size}")
@@ -114,7 +114,7 @@ def strided2d(buf: np.ndarray, off: int, rows: int, cols: int, ld: int) -> np.nd
 
 
 def widen(a: np.ndarray, in_dtype: str) -> np.ndarray:
-    """contraction.py:294-299."""
+    """contraction.py:184-189."""
     if in_dtype == "bf16":
         return bf16_to_fp32(a)
     if in_dtype == "int8":
@@ -123,8 +123,8 @@ def widen(a: np.ndarray, in_dtype: str) -> np.ndarray:
 
 
 def load_a(buf, off, m, k, lda, in_dtype, vnni=False):
-    """contraction.py:302-319 (NATIVE path; EMULATED_SPLIT is bit-identical,
-    contraction.py:333-345)."""
+    """contraction.py:192-209 (NATIVE path; EMULATED_SPLIT is bit-identical,
+    contraction.py:223-235)."""
     if not vnni:
         return widen(strided2d(buf, off, m, k, lda), in_dtype)
     alpha = 4 if in_dtype == "int8" else 2
@@ -137,7 +137,7 @@ def load_a(buf, off, m, k, lda, in_dtype, vnni=False):
 
 
 def load_b(buf, off, k, n, ldb, in_dtype):
-    """contraction.py:398-399."""
+    """contraction.py:288-289."""
     return widen(strided2d(buf, off, k, n, ldb), in_dtype)
 
 
@@ -145,7 +145,7 @@ _ACC = {"fp64": np.float64, "fp32": np.float32, "bf16": np.float32, "int8": np.i
 
 
 def brgemm(a_blocks, b_blocks, c0, beta: float, in_dtype: str = "fp32") -> np.ndarray:
-    """contraction.py:371-432 — returns the new C (m x n, accumulator dtype).
+    """contraction.py:261-322 — returns the new C (m x n, accumulator dtype).
 
     ``a_blocks`` are logical (M,K) widened arrays, ``b_blocks`` (K,N); the
     order is the reference's: beta rule (410-415), then per entry a partial
@@ -558,7 +558,7 @@ def fc_forward_fp32(a4: np.ndarray, b4: np.ndarray, activation=None) -> np.ndarr
 def fc_forward_bf16(x_bits, w_vnni_bits, bias_bits=None, activation=None,
                     residual_bits=None, nb_sel=None):
     """BF16 blocked FC as the reference composition:
-    per output block brgemm(BF16, VNNI A, FP32 acc, beta=0) (contraction.py:371),
+    per output block brgemm(BF16, VNNI A, FP32 acc, beta=0) (contraction.py:261),
     + bias (apply_binary ADD, COL broadcast, ops.py:747-782), activation
     (ops.py:361-366), + residual (apply_binary ADD), then convert to BF16 RNE
     (tensor.py:328-355).
@@ -599,7 +599,7 @@ def fc_forward_bf16(x_bits, w_vnni_bits, bias_bits=None, activation=None,
 
 def conv2d_fwd_bf16(x_bits, w_vnni_bits, pad: int = 1, n_sel=None):
     """Direct 2-D convolution as an OFFSET-addressed BRGEMM over the R*S taps
-    (contraction.py:262-270), on an explicitly zero-padded
+    (contraction.py:152-160), on an explicitly zero-padded
     input; FP32 accumulation then BF16 RNE.  Per output row the batch entries
     are the taps in (r, s) order with the Cb input-channel blocks inner.
 
@@ -651,7 +651,7 @@ def conv_weights_bwd_data(w_vnni_bits):
 
 # ---------------------------------------------------------------------------
 # blocked MLP training step (BASELINE cfg 5) as a composition of the
-# reference TPPs: brgemm over 64-wide reduce blocks (contraction.py:371),
+# reference TPPs: brgemm over 64-wide reduce blocks (contraction.py:261),
 # RELU + bitmask / RELU_INV (ops.py:363-369), softmax (kernels.py:84-99),
 # split-SGD (kernels.py:235-251).  Logical row-major matrices; BF16 values
 # are carried as exactly-representable FP32.
@@ -661,7 +661,7 @@ def conv_weights_bwd_data(w_vnni_bits):
 def blocked_matmul(x: np.ndarray, w: np.ndarray, blk: int = 64) -> np.ndarray:
     """out[t, o] = sum_c x[t, c] * w[o, c] with the BRGEMM order: batch entries
     are the 64-wide blocks of c (ascending), each a partial from +0 along
-    ascending c (contraction.py:405-425).  x [T, C], w [O, C] -> [T, O] FP32."""
+    ascending c (contraction.py:295-315).  x [T, C], w [O, C] -> [T, O] FP32."""
     x = np.asarray(x, np.float32)
     w = np.asarray(w, np.float32)
     t, c = x.shape

@@ -59,6 +59,7 @@ _I32 = C.c_int32
 _I64 = C.c_int64
 _SIGS = {
     "tpp_last_error": (C.c_char_p, []),
+    "tpp_last_config": (C.c_char_p, []),
     "tpp_version": (C.c_int, []),
     "tpp_device_sm_count": (C.c_int, []),
     "tpp_brgemm_stride": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _I64, _I64, _I64, _P, _P]),
@@ -165,6 +166,12 @@ def check(status: int, what: str = "") -> None:
     if status == E_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(f"CUDA error in TPP library: {msg}")
+
+
+def last_config() -> str:
+    """Instantiation / grid of the last tensor-core kernel launched by this
+    thread (tpp_last_config), e.g. 'brgemm_tc_kernel<256,3,2,0,2,1> grid=148 ...'."""
+    return load(require_gpu=False).tpp_last_config().decode()
 
 
 def stream_ptr(stream=None) -> int:

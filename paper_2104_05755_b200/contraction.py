@@ -1,5 +1,5 @@
 """The BRGEMM TPP on the GPU — a drop-in for contraction.py of the reference
-(/root/reference/pkg/src/tensorprim/contraction.py:1-457).
+(/root/reference/pkg/src/tensorprim/contraction.py:1-347).
 
 ``brgemm(spec, batch, c)`` computes C = beta*C + sum_i A_i x B_i over the
 three addressing variants of ``BrgemmBatch`` with the reference's argument
@@ -47,7 +47,7 @@ class Engine(enum.Enum):
 
 @dataclass(frozen=True)
 class GemmSpec:
-    """contraction.py:154-195."""
+    """contraction.py:44-85."""
     m: int
     n: int
     k: int
@@ -101,7 +101,7 @@ class GemmSpec:
 
 @dataclass(frozen=True)
 class BlockingParams:
-    """contraction.py:198-206.  Results never depend on blocking; the GPU
+    """contraction.py:88-96.  Results never depend on blocking; the GPU
     kernels choose their own tiles."""
     m_b: int
     n_b: int
@@ -130,7 +130,7 @@ Ref = tuple  # (flat device buffer, element offset)
 
 
 def _as_ref(x) -> Ref:
-    """contraction.py:227-235."""
+    """contraction.py:117-125."""
     if isinstance(x, TensorView):
         return (x.primary, 0)
     if isinstance(x, torch.Tensor):
@@ -142,7 +142,7 @@ def _as_ref(x) -> Ref:
 
 
 class BrgemmBatch:
-    """The (A_i, B_i) block sequence (contraction.py:238-278).  Device-side
+    """The (A_i, B_i) block sequence (contraction.py:128-168).  Device-side
     offset / pointer arrays are built once per batch and cached."""
 
     __slots__ = ("kind", "a_refs", "b_refs", "stride_a", "stride_b", "_dev")
@@ -185,24 +185,37 @@ class BrgemmBatch:
                            tuple((bb, bo + i * int(stride_b)) for i in range(count)),
                            int(stride_a), int(stride_b))
 
-    def device_arrays(self, device):
+    def device_arrays(self, device, stream=None):
         """int64 arrays on the device: element offsets (OFFSET) or absolute
-        addresses (ADDRESS)."""
+        addresses (ADDRESS).  Built once per batch: a pinned host staging
+        buffer and an asynchronous copy on the issuing stream (no host
+        synchronisation); later uses on other streams wait for that copy."""
         if self._dev is None:
             if self.kind is BatchKind.OFFSET:
-                a = torch.tensor([o for _, o in self.a_refs], dtype=torch.int64)
-                b = torch.tensor([o for _, o in self.b_refs], dtype=torch.int64)
+                a = [o for _, o in self.a_refs]
+                b = [o for _, o in self.b_refs]
             else:
-                a = torch.tensor([buf.data_ptr() + o * buf.element_size() for buf, o in self.a_refs],
-                                 dtype=torch.int64)
-                b = torch.tensor([buf.data_ptr() + o * buf.element_size() for buf, o in self.b_refs],
-                                 dtype=torch.int64)
-            self._dev = (a.to(device, non_blocking=False), b.to(device, non_blocking=False))
-        return self._dev
+                a = [buf.data_ptr() + o * buf.element_size() for buf, o in self.a_refs]
+                b = [buf.data_ptr() + o * buf.element_size() for buf, o in self.b_refs]
+            host = torch.tensor([a, b], dtype=torch.int64).pin_memory()
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+            with torch.cuda.stream(s):
+                dev = torch.empty((2, len(a)), dtype=torch.int64, device=device)
+                dev.copy_(host, non_blocking=True)
+            ev = None
+            if not torch.cuda.is_current_stream_capturing():
+                ev = torch.cuda.Event()
+                ev.record(s)
+            self._dev = (dev[0], dev[1], host, ev)
+        a, b, _, ev = self._dev
+        if ev is not None and not torch.cuda.is_current_stream_capturing():
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+            s.wait_event(ev)
+        return a, b
 
 
 def _check_block(buf: torch.Tensor, off: int, rows: int, cols: int, ld: int, dtype: DType):
-    """contraction.py:285-291 bounds rule."""
+    """contraction.py:175-181 bounds rule."""
     if buf.dtype != dtype.storage:
         raise TensorError(f"block buffer dtype {buf.dtype} does not match {dtype}")
     need = off + ld * (cols - 1) + rows
@@ -211,7 +224,7 @@ def _check_block(buf: torch.Tensor, off: int, rows: int, cols: int, ld: int, dty
 
 
 def _check_vnni_block(buf: torch.Tensor, off: int, m: int, k: int, alpha: int, dtype: DType):
-    """contraction.py:310-314."""
+    """contraction.py:200-204."""
     if buf.dtype != dtype.storage:
         raise TensorError(f"block buffer dtype {buf.dtype} does not match {dtype}")
     groups = -(-k // alpha)
@@ -221,7 +234,7 @@ def _check_vnni_block(buf: torch.Tensor, off: int, m: int, k: int, alpha: int, d
 
 def brgemm(spec: GemmSpec, batch: BrgemmBatch, c: TensorView,
            blocking: BlockingParams | None = None, threads: int = 1, stream=None) -> None:
-    """C = beta*C + sum_i A_i x B_i (contraction.py:371-432), on the GPU.
+    """C = beta*C + sum_i A_i x B_i (contraction.py:261-322), on the GPU.
 
     Validation (shape, dtype, ld, aliasing, block bounds) happens before any
     launch and raises the reference's TensorError.  ``blocking``/``threads``
@@ -264,40 +277,40 @@ def brgemm(spec: GemmSpec, batch: BrgemmBatch, c: TensorView,
             sa, sb = batch.stride_a, batch.stride_b
         rc = lib.tpp_brgemm_stride(C.byref(d), a_ptr, b_ptr, sa, sb, n, c.ptr, s)
     elif batch.kind is BatchKind.OFFSET:
-        ao, bo = batch.device_arrays(c.primary.device)
+        ao, bo = batch.device_arrays(c.primary.device, stream)
         rc = lib.tpp_brgemm_offset(C.byref(d), batch.a_refs[0][0].data_ptr(),
                                    batch.b_refs[0][0].data_ptr(), ao.data_ptr(), bo.data_ptr(),
                                    n, c.ptr, s)
     else:
-        ap, bp = batch.device_arrays(c.primary.device)
+        ap, bp = batch.device_arrays(c.primary.device, stream)
         rc = lib.tpp_brgemm_address(C.byref(d), ap.data_ptr(), bp.data_ptr(), n, c.ptr, s)
     _lib.check(rc, "brgemm")
 
 
 def gemm(spec: GemmSpec, a, b, c: TensorView, blocking: BlockingParams | None = None,
          threads: int = 1, stream=None) -> None:
-    """contraction.py:435-439 — a one-entry batch."""
+    """contraction.py:325-329 — a one-entry batch."""
     brgemm(spec, BrgemmBatch.address([_as_ref(a)], [_as_ref(b)]), c, blocking, threads, stream)
 
 
 def spec_for_views(a: TensorView, b: TensorView, c: TensorView, beta: float = 0.0,
                    a_layout: ALayout = ALayout.PLAIN,
                    compute_path: ComputePath = ComputePath.NATIVE) -> GemmSpec:
-    """contraction.py:442-449."""
+    """contraction.py:332-339."""
     return GemmSpec(m=a.desc.rows, n=b.desc.cols, k=a.desc.cols, lda=a.desc.ld, ldb=b.desc.ld,
                     ldc=c.desc.ld, in_dtype=a.desc.dtype, out_dtype=c.desc.dtype, beta=beta,
                     a_layout=a_layout, compute_path=compute_path)
 
 
 def matmul(a: TensorView, b: TensorView, out: TensorView) -> None:
-    """contraction.py:452-457 — GEMM with beta = 0."""
+    """contraction.py:342-347 — GEMM with beta = 0."""
     if a.desc.cols != b.desc.rows:
         raise TensorError(f"matmul inner dims {a.desc.cols} != {b.desc.rows}")
     gemm(spec_for_views(a, b, out, beta=0.0), a, b, out)
 
 
 def vnni_pack_a(a: TensorView, alpha: int) -> torch.Tensor:
-    """contraction.py:348-357 on the GPU: a logical (M, K) view -> flat
+    """contraction.py:238-247 on the GPU: a logical (M, K) view -> flat
     [ceil(K/alpha)][M][alpha] buffer (tail zero-padded), via the VNNI
     transform kernel."""
     from .ops import TransformKind, TransformSpec, transform
@@ -312,7 +325,7 @@ def vnni_pack_a(a: TensorView, alpha: int) -> torch.Tensor:
 
 
 def vnni_unpack_a(flat: torch.Tensor, alpha: int, m: int, k: int) -> torch.Tensor:
-    """contraction.py:360-364 — returns the logical (M, K) as a torch view."""
+    """contraction.py:250-254 — returns the logical (M, K) as a torch view."""
     groups = -(-k // alpha)
     grid = flat[:groups * m * alpha].reshape(groups, m, alpha)
     return grid.permute(1, 0, 2).reshape(m, groups * alpha)[:, :k]

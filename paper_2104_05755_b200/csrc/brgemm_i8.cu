@@ -298,12 +298,11 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const Params
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   auto kern = brgemm_i8_kernel<BN, STAGES, CG>;
   static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
+  cudaError_t attr = cudaSuccess;
   static int max_clusters = 0;
   std::call_once(once, [&] {
-    attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
     max_clusters = sm_count() / CG;
-    if (CG > 1 && attr == cudaSuccess) {
+    if (CG > 1 && ensure_smem_attr((const void*)kern, S::BYTES) == cudaSuccess) {
       cudaLaunchConfig_t q{};
       q.gridDim = dim3(sm_count());
       q.blockDim = dim3(kThreads);
@@ -318,6 +317,7 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const Params
       cudaGetLastError();
     }
   });
+  attr = ensure_smem_attr((const void*)kern, S::BYTES);
   if (attr != cudaSuccess) return cuda_status(attr, "cudaFuncSetAttribute(brgemm_i8_kernel)");
   const int64_t clusters = p.units < max_clusters ? p.units : max_clusters;
   cudaLaunchConfig_t cfg{};

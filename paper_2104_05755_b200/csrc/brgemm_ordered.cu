@@ -1,6 +1,6 @@
 // K1: BRGEMM in the reference's exact per-element order (SIMT).
 //
-// contraction.py:371-432: for every C element
+// contraction.py:261-322: for every C element
 //     acc  = beta==0 ? 0 : beta==1 ? C : C*beta          (410-415)
 //     for i in batch:  part = +0;  for k ascending: part = part + a*b   (417-423)
 //                      acc  = acc + part                  (424)
@@ -266,7 +266,7 @@ brgemm_ordered_smem_kernel(OrderedParams p, int nb, int fast, unsigned long long
       if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) dbg[1] = gt();
       // The per-entry partial sums are independent chains (part_i depends
       // only on entry i); only acc = acc + part_i is ordered across entries
-      // (contraction.py:417-424).  Slot es runs entries es, es + kES, ...
+      // (contraction.py:307-314).  Slot es runs entries es, es + kES, ...
       int bi = es;
       for (; bi < cnt; bi += kES) {
         const TIn* a = As + (size_t)bi * K * kOTM + r;
@@ -302,8 +302,13 @@ static int launch_smem_kc(const OrderedParams& p, cudaStream_t s, int nb, int fa
   // columns {2k, n, entry, instance}) instead of 16-byte cp.async
   CUtensorMap ma{}, mb{};
   int use_tma = 0;
-  if (fast && sizeof(TIn) == 4 && p.k <= 128 && nb <= 256 && p.stride_a > 0 && p.stride_b > 0 && p.instances <= 0x7fffffff && p.count <= 0x7fffffff &&
-      !getenv("TPP_ORDERED_CPASYNC")) {
+  // (a zero instance stride -- every instance shares that operand, as the FP32
+  // fc_forward's inst_b = 0 -- has no TMA encoding: the cp.async path then
+  // indexes inst * p.inst_x itself)
+  static const bool no_tma = getenv("TPP_ORDERED_CPASYNC") != nullptr;  // experiments
+  const bool inst_ok = p.instances == 1 || (p.inst_a > 0 && p.inst_b > 0);
+  if (fast && sizeof(TIn) == 4 && p.k <= 128 && nb <= 256 && p.stride_a > 0 && p.stride_b > 0 && inst_ok &&
+      p.instances <= 0x7fffffff && p.count <= 0x7fffffff && !no_tma) {
     const uint64_t da[5] = {2 * (uint64_t)p.m, (uint64_t)p.k, (uint64_t)p.count, (uint64_t)p.instances, 1};
     const uint64_t sa[4] = {(uint64_t)p.lda * 4, (uint64_t)p.stride_a * 4, (uint64_t)(p.inst_a ? p.inst_a * 4 : 16),
                             16};
@@ -315,12 +320,9 @@ static int launch_smem_kc(const OrderedParams& p, cudaStream_t s, int nb, int fa
     if (make_tma_map_5d(&ma, p.a, da, sa, ba, 0) == TPP_OK && make_tma_map_5d(&mb, p.b, db, sb, bb, 0) == TPP_OK)
       use_tma = 1;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(brgemm_ordered_smem_kernel<TIn, TAcc, KC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  {
+    cudaError_t e = ensure_smem_attr((const void*)brgemm_ordered_smem_kernel<TIn, TAcc, KC>, 200 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_ordered_smem)");
-    attr = true;
   }
   const int tiles = ((p.m + kOTM - 1) / kOTM) * ((p.n + kOTN - 1) / kOTN);
   dim3 grid((unsigned)tiles, (unsigned)(p.instances < 65535 ? p.instances : 65535));
@@ -346,7 +348,8 @@ static int launch_smem_t(const OrderedParams& p, cudaStream_t s, int nb, size_t 
 template <typename TIn, typename TAcc>
 static int launch_t(const OrderedParams& p, cudaStream_t s) {
   // staged variant: chunks of up to nb batch entries (<= 96 KB of operands)
-  if (p.k > 0 && p.count > 0 && !getenv("TPP_ORDERED_GLOBAL")) {
+  static const bool global_only = getenv("TPP_ORDERED_GLOBAL") != nullptr;  // experiments
+  if (p.k > 0 && p.count > 0 && !global_only) {
     const size_t per = (size_t)p.k * (kOTM + kOTN) * sizeof(TIn);
     int64_t nb = (int64_t)(96 * 1024) / (int64_t)per;
     if (nb > p.count) nb = p.count;
@@ -363,7 +366,7 @@ static int launch_t(const OrderedParams& p, cudaStream_t s) {
   return TPP_OK;
 }
 
-// zero-count batches only apply the beta rule (contraction.py:410-425)
+// zero-count batches only apply the beta rule (contraction.py:300-315)
 int launch_brgemm_ordered(const OrderedParams& p, int in_dtype, cudaStream_t s) {
   if (p.m == 0 || p.n == 0 || p.instances == 0) return TPP_OK;
   switch (in_dtype) {

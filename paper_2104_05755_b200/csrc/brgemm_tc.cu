@@ -761,10 +761,13 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   auto kern = brgemm_tc_kernel<BN, STAGES, KPS, RES, CG, MC>;
   constexpr int CL = CG * MC;  // cluster size (one of CG, MC is 1)
-  static int max_clusters = -1;
-  if (max_clusters < 0) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::BYTES);
+  {
+    cudaError_t e = ensure_smem_attr((const void*)kern, S::BYTES);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_tc_kernel)");
+  }
+  static int max_clusters = 0;
+  static std::once_flag once;
+  std::call_once(once, [&] {
     max_clusters = num_sms() / CL;
     if (CL > 1) {
       // co-resident pairs (SM pairs of one TPC) — a persistent grid must not exceed it
@@ -781,7 +784,7 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
       if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0 && n < max_clusters) max_clusters = n;
       cudaGetLastError();
     }
-  }
+  });
   const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * (p.tiles_n / MC);
   const int grid = CL * (units < max_clusters ? units : max_clusters);
   cudaLaunchConfig_t cfg{};
@@ -799,6 +802,10 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
+  set_last_config("brgemm_tc_kernel<" + std::to_string(BN) + "," + std::to_string(STAGES) + "," +
+                  std::to_string(KPS) + "," + std::to_string(RES) + "," + std::to_string(CG) + "," +
+                  std::to_string(MC) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(p.tiles_m) +
+                  "x" + std::to_string(p.tiles_n));
   return TPP_OK;
 }
 
@@ -951,9 +958,26 @@ Operand mnmajor_operand(int red_blk, int mn_blk, int red_in, int tile_mn, int kp
   return o;
 }
 
+// experiment / diagnostic switches, read once per process
+int env_dbg_mode() {
+  static const int v = getenv("TPP_DBG_MODE") ? atoi(getenv("TPP_DBG_MODE")) : 0;
+  return v;
+}
+int env_dbg_tile() {
+  static const int v = getenv("TPP_DBG_TILE") ? atoi(getenv("TPP_DBG_TILE")) : 0;
+  return v;
+}
+bool env_no_tma_store() {
+  static const bool v = getenv("TPP_NO_TMA_STORE") != nullptr;
+  return v;
+}
+
 int pick_bn(int feats, int tiles_m, int pref) {
   if (pref) return pref;
-  static const int forced = getenv("TPP_BN") ? atoi(getenv("TPP_BN")) : 0;  // experiments
+  static const int forced = [] {  // experiments: 64 / 128 / 256 only
+    const int v = getenv("TPP_BN") ? atoi(getenv("TPP_BN")) : 0;
+    return (v == 64 || v == 128 || v == 256) ? v : 0;
+  }();
   if (forced && feats % forced == 0) return forced;
   int BN = 256;
   while (BN > 64 && (feats % BN != 0 || (int64_t)tiles_m * (feats / BN) < num_sms())) BN /= 2;
@@ -1015,8 +1039,7 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   if (rc) return rc;
   // BF16 outputs leave through smem staging + TMA stores: output tensor
   // [ntb][o_mb][o_bn][o_bm], box = 32 tokens x 32 features, 64B swizzle
-  static const bool no_tma_store = getenv("TPP_NO_TMA_STORE") != nullptr;  // experiments
-  p.tma_store = !no_tma_store && !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
+  p.tma_store = !env_no_tma_store() && !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
                 reinterpret_cast<uintptr_t>(p.out) % 16 == 0;
   mc = ma;
   if (p.tma_store) {
@@ -1055,8 +1078,8 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
   p.mask = reinterpret_cast<uint8_t*>(mask_out);
   p.mask_in = reinterpret_cast<const uint8_t*>(mask_in);
   p.dbg = g_dbg_ts;
-  p.dbg_tile = (g_dbg_ts && getenv("TPP_DBG_TILE")) ? atoi(getenv("TPP_DBG_TILE")) : 0;
-  p.dbg_mode = getenv("TPP_DBG_MODE") ? atoi(getenv("TPP_DBG_MODE")) : 0;
+  p.dbg_tile = g_dbg_ts ? env_dbg_tile() : 0;
+  p.dbg_mode = env_dbg_mode();
   TPP_REQUIRE((bn < BM && BM % bn == 0) || (bn >= BM && bn % BM == 0), TPP_E_UNSUPPORTED,
               "tensor-core FC needs bn | 128 or 128 | bn");
   if (flavor == 0) {
@@ -1134,7 +1157,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   Params p{};
   p.mode = FEED_CONV;
   p.dbg = g_dbg_ts;
-  p.dbg_mode = getenv("TPP_DBG_MODE") ? atoi(getenv("TPP_DBG_MODE")) : 0;
+  p.dbg_mode = env_dbg_mode();
   p.kblocks = R * S * Cb;
   p.cv_P = P;
   p.cv_Q = Q;
@@ -1146,7 +1169,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   static const bool two_row = getenv("TPP_CONV_2ROW") != nullptr;  // experiments
   const bool res_ok = BN == 64 && feats / BN == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
   const bool halo_ok = res_ok && 2 + R - 1 <= tc::kHaloRows && W + S - 1 <= 64;
-  const bool rows4 = halo_ok && !two_row && reinterpret_cast<uintptr_t>(out) % 16 == 0 && !getenv("TPP_NO_TMA_STORE");
+  const bool rows4 = halo_ok && !two_row && reinterpret_cast<uintptr_t>(out) % 16 == 0 && !env_no_tma_store();
   p.cv_rows = rows4 ? 4 : 2;
   p.cv_tiles_per_img = (P + p.cv_rows - 1) / p.cv_rows;
   p.tiles_m = N * p.cv_tiles_per_img;
@@ -1172,7 +1195,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     if (rc) return rc;
   }
   // output [N][K_b][H][W][64] through TMA stores: box 32 channels x 32 pixels
-  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0 && !getenv("TPP_NO_TMA_STORE");
+  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0 && !env_no_tma_store();
   mc = ma;
   if (p.tma_store) {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Kb, (uint64_t)N};

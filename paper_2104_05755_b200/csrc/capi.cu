@@ -12,6 +12,9 @@
 namespace tpp {
 
 static thread_local std::string g_last_error;
+static thread_local std::string g_last_config;
+
+void set_last_config(const std::string& cfg) { g_last_config = cfg; }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int status, const std::string& msg) {
@@ -31,7 +34,7 @@ static int acc_dtype_of(int in) {
   return TPP_FP32;
 }
 
-// contraction.py:168-183 (GemmSpec.__post_init__)
+// contraction.py:58-73 (GemmSpec.__post_init__)
 static int check_gemm(const tpp_gemm_desc* d) {
   TPP_REQUIRE(d != nullptr, TPP_E_TENSOR, "null GEMM descriptor");
   TPP_REQUIRE(d->m >= 1 && d->n >= 1 && d->k >= 1, TPP_E_TENSOR, "GEMM extents must be positive");
@@ -75,6 +78,7 @@ using namespace tpp;
 extern "C" {
 
 const char* tpp_last_error(void) { return g_last_error.c_str(); }
+const char* tpp_last_config(void) { return g_last_config.c_str(); }
 
 int tpp_debug_phase_timestamps(uint64_t* dev_buf) {
   set_debug_timestamps(reinterpret_cast<unsigned long long*>(dev_buf));
@@ -530,21 +534,6 @@ int tpp_ternary(int32_t kind, const tpp_tensor_desc* a_d, const void* a,
                      as_stream(stream));
 }
 
-static void* reduce_scratch(size_t bytes) {
-  static std::mutex mu;
-  static void* buf = nullptr;
-  static size_t cap = 0;
-  std::lock_guard<std::mutex> lock(mu);
-  if (bytes > cap) {
-    if (buf) cudaFree(buf);
-    buf = nullptr;
-    cap = 0;
-    if (cudaMalloc(&buf, bytes) != cudaSuccess) return nullptr;
-    cap = bytes;
-  }
-  return buf;
-}
-
 int tpp_reduce(const tpp_tensor_desc* in_d, const void* inp, int32_t axis, int32_t op,
                int32_t squared, const tpp_tensor_desc* out_d, void* out, void* stream) {
   TPP_REQUIRE(valid_view(in_d) && valid_view(out_d), TPP_E_TENSOR, "bad descriptor");
@@ -554,13 +543,21 @@ int tpp_reduce(const tpp_tensor_desc* in_d, const void* inp, int32_t axis, int32
   const int ec = axis == 1 ? in_d->cols : 1;
   TPP_REQUIRE(out_d->rows == er && out_d->cols == ec, TPP_E_TENSOR, "reduce output: wrong shape");
   const bool f64 = in_d->dtype == TPP_FP64;
+  if (axis != 2)
+    return launch_reduce(dview(in_d, inp), axis, op, squared, out, out_d->dtype, out_d->ld, nullptr, f64,
+                         as_stream(stream));
+  // ALL: per-column partials in a stream-ordered scratch vector (the pool
+  // allocator: no device synchronisation, private to this call's stream
+  // order, capturable in CUDA graphs)
+  const cudaStream_t st = as_stream(stream);
   void* scratch = nullptr;
-  if (axis == 2) {
-    scratch = reduce_scratch((size_t)in_d->cols * (f64 ? 8 : 4));
-    TPP_REQUIRE(scratch, TPP_E_CUDA, "reduce scratch allocation failed");
-  }
-  return launch_reduce(dview(in_d, inp), axis, op, squared, out, out_d->dtype, out_d->ld, scratch,
-                       f64, as_stream(stream));
+  cudaError_t e = cudaMallocAsync(&scratch, (size_t)in_d->cols * (f64 ? 8 : 4), st);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(reduce scratch)");
+  const int rc = launch_reduce(dview(in_d, inp), axis, op, squared, out, out_d->dtype, out_d->ld, scratch, f64, st);
+  e = cudaFreeAsync(scratch, st);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_status(e, "cudaFreeAsync(reduce scratch)");
+  return TPP_OK;
 }
 
 int tpp_transform(int32_t kind, const tpp_tensor_desc* in_d, const void* inp, int32_t alpha,

@@ -16,6 +16,9 @@ namespace tpp {
 void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);
+// the instantiation / grid of the last tensor-core launch of this thread
+// (tpp_last_config(): tests assert which kernel a dispatch really runs)
+void set_last_config(const std::string& cfg);
 
 #define TPP_REQUIRE(cond, status, msg) \
   do {                                 \

@@ -271,13 +271,10 @@ int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, 
   const int smem = kStages * kStageBytes + (2 * kStages + 1) * 8 + 16 + 1024;
   const bool rs3 = R == 3 && S == 3;
   auto kern = rs3 ? conv_dw_kernel<1> : conv_dw_kernel<0>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv_dw_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(conv_dw_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  {
+    cudaError_t e = ensure_smem_attr((const void*)conv_dw_kernel<1>, smem);
+    if (e == cudaSuccess) e = ensure_smem_attr((const void*)conv_dw_kernel<0>, smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(conv_dw_kernel)");
-    attr = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(Kb * Cb * p.Z);

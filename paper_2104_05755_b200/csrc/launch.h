@@ -4,10 +4,31 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/tpp_b200.h"
 
 namespace tpp {
+
+// cudaFuncSetAttribute(max dynamic shared memory) once per (kernel, device):
+// thread-safe, and a second device used by the same process gets its own
+// opt-in (the attribute is per device)
+inline cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
+}
 
 struct OrderedParams {
   int m, n, k, lda, ldb, ldc, vnni, alpha;

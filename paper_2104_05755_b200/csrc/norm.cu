@@ -562,6 +562,11 @@ layernorm_blocked_tma(const __grid_constant__ CUtensorMap map_x, const __grid_co
   }
 }
 
+static bool ln_simple() {  // experiments: skip the TMA-ring kernel
+  static const bool v = getenv("TPP_LN_SIMPLE") != nullptr;
+  return v;
+}
+
 int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const void* x,
                              const float* gamma, const float* beta, double eps, void* out,
                              float* mean_out, float* var_out, cudaStream_t s, int exact) {
@@ -569,7 +574,7 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
                     reinterpret_cast<uintptr_t>(gamma) % 16 == 0 && reinterpret_cast<uintptr_t>(beta) % 16 == 0;
   const int gbytes = lnt::kTok * m_b * 128;
   if (dtype == TPP_BF16 && bm == 64 && bn % lnt::kTok == 0 && al16 && m_b <= 256 &&
-      2 * gbytes <= lnt::kRingBytes && !getenv("TPP_LN_SIMPLE")) {
+      2 * gbytes <= lnt::kRingBytes && !ln_simple()) {
     const int n_groups = n_b * bn / lnt::kTok;
     if (n_groups == 0) return TPP_OK;
     int stages = lnt::kRingBytes / gbytes;
@@ -584,15 +589,10 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     if (rc) return rc;
     const size_t smem = (size_t)stages * gbytes + 3 * lnt::kMaxStages * 8 + lnt::kMaxStages * lnt::kTok * 8 +
                         lnt::kMaxStages * 4 + 1024;
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(lnt::kRingBytes + 3 * 1024));
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(layernorm_blocked_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(lnt::kRingBytes + 3 * 1024));
+    {
+      cudaError_t e = ensure_smem_attr((const void*)layernorm_blocked_tma<0>, (int)(lnt::kRingBytes + 3 * 1024));
+      if (e == cudaSuccess) e = ensure_smem_attr((const void*)layernorm_blocked_tma<1>, (int)(lnt::kRingBytes + 3 * 1024));
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_tma)");
-      attr = true;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_groups < num_sms() ? n_groups : num_sms());
@@ -604,8 +604,9 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    static const int ln_spin = getenv("TPP_LN_SPIN") ? atoi(getenv("TPP_LN_SPIN")) : 0;  // diagnostics
     cudaError_t e = cudaLaunchKernelEx(&cfg, exact ? layernorm_blocked_tma<0> : layernorm_blocked_tma<1>, mx, mo, n_groups, bn, m_b, stages, gamma, beta,
-                                       eps, mean_out, var_out, getenv("TPP_LN_SPIN") ? atoi(getenv("TPP_LN_SPIN")) : 0,
+                                       eps, mean_out, var_out, ln_spin,
                                        debug_timestamps());
     if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(layernorm_blocked_tma)");
     TPP_CUDA_LAUNCH_CHECK("layernorm_blocked_tma");
@@ -618,8 +619,7 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     if (smem <= 227 * 1024) {
       const int blocks = n_b * (bn / 32);
       if (blocks == 0) return TPP_OK;
-      cudaError_t e = cudaFuncSetAttribute(layernorm_blocked_bf16_v,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = ensure_smem_attr((const void*)layernorm_blocked_bf16_v, 227 * 1024);
       if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked_bf16_v)");
       layernorm_blocked_bf16_v<<<blocks, 256, smem, s>>>(n_b, m_b, bn, (const uint4*)x, (const float4*)gamma,
                                                          (const float4*)beta, eps,
@@ -637,14 +637,12 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
   if (blocks == 0) return TPP_OK;
   cudaError_t e;
   if (es == 2) {
-    e = cudaFuncSetAttribute(layernorm_blocked_kernel<uint16_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_smem_attr((const void*)layernorm_blocked_kernel<uint16_t>, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked)");
     layernorm_blocked_kernel<uint16_t><<<blocks, 256, smem, s>>>(
         n_b, m_b, bn, bm, (const uint16_t*)x, gamma, beta, eps, (uint16_t*)out, mean_out, var_out);
   } else {
-    e = cudaFuncSetAttribute(layernorm_blocked_kernel<float>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_smem_attr((const void*)layernorm_blocked_kernel<float>, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(layernorm_blocked)");
     layernorm_blocked_kernel<float><<<blocks, 256, smem, s>>>(
         n_b, m_b, bn, bm, (const float*)x, gamma, beta, eps, (float*)out, mean_out, var_out);
@@ -920,8 +918,7 @@ int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* l
   TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "softmax_xent: class dimension too long for smem");
   const int blocks = n_b * ((bn + kXentTok - 1) / kXentTok);
   if (blocks == 0) return TPP_OK;
-  cudaError_t e = cudaFuncSetAttribute(softmax_xent_blocked_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem_attr((const void*)softmax_xent_blocked_kernel, 227 * 1024);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(softmax_xent)");
   softmax_xent_blocked_kernel<<<blocks, 256, smem, s>>>(n_b, m_b, bn, bm, logits, targets, scale,
                                                          reinterpret_cast<uint16_t*>(dlogits), loss);

@@ -448,10 +448,10 @@ int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t*
     parts = ((int64_t)rows + (int64_t)run * kWarps - 1) / ((int64_t)run * kWarps);
     if (cgroups * parts > 0x7fffffff) return TPP_E_UNSUPPORTED;
     const int smem = kTileCols * kFillStride * (int)sizeof(float);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-      cudaFuncSetAttribute(prng_fill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
+    {
+      cudaError_t e = ensure_smem_attr((const void*)prng_fill_kernel, smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(prng_fill_kernel)");
+    }
     const int vec = (out_ld & 7) == 0 && ((uintptr_t)out & 15) == 0;
     prng_fill_kernel<<<(unsigned)(cgroups * parts), kWarps * 32, smem, s>>>(
         st_in, st_out, reinterpret_cast<float*>(out), out_ld, rows, cols, run, (int)parts, vec, tab);

@@ -1,7 +1,7 @@
 // K6: layout transforms (bit-exact, HBM-bound).
 //
 //  * weight packing VNNI -> UMMA-canonical K-major blocks.  A VNNI-2 block
-//    [K/2][M][2] (contraction.py:348-357) viewed as 32-bit words is a
+//    [K/2][M][2] (contraction.py:238-247) viewed as 32-bit words is a
 //    (K/2) x M word matrix; its word transpose is [M][K] K-major, the layout
 //    the tcgen05 B operand (and TMA 128B swizzle) wants.  Done once per
 //    weight tensor (inference) or once per step (training).

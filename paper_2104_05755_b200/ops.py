@@ -195,6 +195,11 @@ class PrngState:
     call that draws advances the streams in place (the kernel writes the
     advanced words to a second buffer and the two are swapped), so successive
     DROPOUT calls see successive uniforms exactly as the reference's do.
+
+    Stream safety: every launch that writes the state (seeding, each draw)
+    records an event on its stream, and the next draw -- on whatever stream
+    it is issued -- waits for that event first, so the ping-pong buffers
+    are never read before the previous writer finished.
     """
 
     def __init__(self, seed: int, ncols: int = 1, device=None):
@@ -205,9 +210,30 @@ class PrngState:
         dev = torch.device(device) if device is not None else torch.device("cuda")
         self._bufs = [torch.empty((4, self.ncols), dtype=torch.int32, device=dev) for _ in range(2)]
         self._cur = 0
+        self._ready = None
         lib = _lib.load()
-        _lib.check(lib.tpp_prng_seed(C.c_uint64(self.seed), self.ncols, self._bufs[0].data_ptr(),
-                                     _lib.stream_ptr(None)), "PrngState")
+        with torch.cuda.device(dev):
+            _lib.check(lib.tpp_prng_seed(C.c_uint64(self.seed), self.ncols, self._bufs[0].data_ptr(),
+                                         _lib.stream_ptr(None)), "PrngState")
+            self._mark(None)
+
+    def _mark(self, stream) -> None:
+        """Record that the state was last written on ``stream``.  Inside a
+        CUDA-graph capture the graph's own stream order applies (an event
+        recorded in a capture cannot be waited on outside it)."""
+        if torch.cuda.is_current_stream_capturing():
+            self._ready = None
+            return
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        self._ready = ev
+
+    def _acquire(self, stream) -> None:
+        """Order ``stream`` after the last write of the state."""
+        if self._ready is not None and not torch.cuda.is_current_stream_capturing():
+            s = stream if stream is not None else torch.cuda.current_stream(self.device)
+            s.wait_event(self._ready)
 
     @property
     def device(self) -> torch.device:
@@ -221,6 +247,7 @@ class PrngState:
 
     def words(self) -> torch.Tensor:
         """Current stream words as a uint32-valued int64 tensor [4, ncols]."""
+        self._acquire(None)
         return self._bufs[self._cur].to(torch.int64) & 0xFFFFFFFF
 
     def _word(self, r: int):
@@ -247,9 +274,11 @@ class PrngState:
 def _prng_fill_state(state: PrngState, out: TensorView, stream) -> None:
     lib = _cuda(out)
     src, dst = state._io()
+    state._acquire(stream)
     _lib.check(lib.tpp_prng_fill(src.data_ptr(), dst.data_ptr(), out.desc.c(), out.ptr,
                                  _lib.stream_ptr(stream)), "PRNG")
     state._advance()
+    state._mark(stream)
 
 
 def _prng_state_for(view: Optional[TensorView], cols: int, what: str) -> PrngState:
@@ -282,10 +311,12 @@ def _dropout(inp: TensorView, out: TensorView, p: Optional[float], stream=None) 
     mask = torch.empty(bitmask_bytes(inp.desc.rows, inp.desc.cols), dtype=torch.uint8,
                        device=out.primary.device)
     src, dst = state._io()
+    state._acquire(stream)
     _lib.check(lib.tpp_dropout(inp.desc.c(), inp.ptr, src.data_ptr(), dst.data_ptr(), float(p),
                                out.desc.c(), out.ptr, mask.data_ptr(), _lib.stream_ptr(stream)),
                "DROPOUT")
     state._advance()
+    state._mark(stream)
     out.secondary = mask
 
 

@@ -5,7 +5,7 @@ parallel over the minibatch with one dW allreduce per layer.
 Composition of the reference TPPs (SURVEY §0.2 row "MLP training"):
   forward    fc_forward + RELU with bitmask        (kernels.py:300-329, ops.py:363-366)
   loss       softmax per token                     (kernels.py:84-99) -> (p - onehot)/B
-  backward   brgemm for dX and dW, RELU_INV        (contraction.py:371, ops.py:367-369)
+  backward   brgemm for dX and dW, RELU_INV        (contraction.py:261, ops.py:367-369)
   update     split_sgd_step on hi/lo FP32 masters  (kernels.py:235-251)
 Weights live in the UMMA-canonical packed layout [out/64][in/64][64][64]; the
 hi halves of the split FP32 master ARE the BF16 weights the GEMMs read, so no

@@ -322,7 +322,7 @@ def gen_fc():
 
 def gen_conv():
     """3x3 'same' conv as OFFSET BRGEMM over (r, s, cb) taps on a padded input
-    (contraction.py:262-270) — tiny shape; BF16 in, FP32 acc, BF16 out."""
+    (contraction.py:152-160) — tiny shape; BF16 in, FP32 acc, BF16 out."""
     rng = np.random.default_rng(16)
     N, Cb, H, W, bc, Kb, bk, R, S = 2, 2, 5, 6, 8, 2, 8, 3, 3
     x = fp32_to_bf16_rne(rng.random((N, Cb, H, W, bc)).astype(np.float32))

@@ -38,7 +38,7 @@ def normwise(got, ref) -> float:
 
 def vnni_weights(rng, Kb, Cb, bk, bc, std):
     """Random BF16 weights, logical blocks (bk x bc) packed to VNNI-2
-    [Kb][Cb][bc/2][bk][2] — the reference layout (contraction.py:348-357)."""
+    [Kb][Cb][bc/2][bk][2] — the reference layout (contraction.py:238-247)."""
     from oracle import tpp_oracle as O
     wl = O.fp32_to_bf16_rne(rng.normal(0, std, (Kb, Cb, bk, bc)).astype(np.float32))
     # vnni of each (bk x bc) block: [bc/2][bk][2], element (m, k) at (k//2, m, k%2)

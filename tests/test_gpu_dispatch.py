@@ -1,0 +1,306 @@
+"""Parity AT THE DISPATCH THE BENCHMARK TIMES.
+
+The cfg 3 FFN and the cfg 5 training step run the CTA-pair tcgen05 kernel
+(`brgemm_tc_kernel<256,3,2,0,2,1>`: 256-wide tiles, 2 reduce blocks per TMA
+box, `cta_group::2`), chosen by pick_bn / pick_cg only at full-size shapes.
+These tests run those shapes, assert through `tpp_last_config()` that the pair
+instantiation really ran, and check the results against the CPU oracle
+(oracle/tpp_oracle.py, pinned to the reference):
+
+* every BF16 output on sampled token blocks against the oracle composition
+  of the reference TPPs fed with the GPU's own inputs to that kernel
+  (blocks are independent, so a sampled block is an exact oracle), normwise
+  <= 2e-2 (north_star BF16 tolerance);
+* FP32 logits normwise <= 1e-5 (only the summation order differs);
+* FP32 dW (BF16 inputs, 8192-token reductions) against the reference-order
+  oracle <= 2e-2 and against an FP64 restatement <= 1e-3, with both
+  distances printed beside the reference order's own FP64 distance;
+* the softmax-CE gradient and the split-SGD update bitwise (same order).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tpp_oracle as O
+
+from gpu_util import bf16_bits_to_f32, normwise, to_dev, to_host, vnni_weights
+
+pytestmark = pytest.mark.gpu
+tpp = pytest.importorskip("paper_2104_05755_b200")
+from paper_2104_05755_b200 import _lib  # noqa: E402
+from paper_2104_05755_b200 import kernels as K  # noqa: E402
+from paper_2104_05755_b200 import training as T  # noqa: E402
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-5
+PAIR256 = "brgemm_tc_kernel<256,3,2,0,2,1>"
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.synchronize()
+
+
+class _Recorder:
+    """Wraps the FcLayer entry points to log the tensor-core instantiation each
+    call dispatched (tpp_last_config right after the launch)."""
+
+    def __init__(self, monkeypatch):
+        self.log = []
+        for name in ("forward", "backward_data", "backward_weights"):
+            orig = getattr(K.FcLayer, name)
+
+            def wrapped(layer, *a, _orig=orig, _name=name, **kw):
+                r = _orig(layer, *a, **kw)
+                self.log.append((_name, _lib.last_config()))
+                return r
+
+            monkeypatch.setattr(K.FcLayer, name, wrapped)
+
+
+def _blk_tokens(buf: torch.Tensor, n_b: int, d: int, bn: int, sel) -> np.ndarray:
+    """Token blocks `sel` of a blocked [n_b][d/64][bn][64] buffer -> logical
+    [len(sel)*bn, d] host array (FP32 values; BF16 widened exactly)."""
+    v = buf.reshape(n_b, d // 64, bn, 64)[list(sel)]
+    v = v.permute(0, 2, 1, 3).reshape(len(sel) * bn, d)
+    h = to_host(v.contiguous())
+    return bf16_bits_to_f32(h) if h.dtype == np.uint16 else h
+
+
+def _blk_feature_cols(buf: torch.Tensor, n_b: int, d: int, bn: int, fblk: int) -> np.ndarray:
+    """All tokens of feature block `fblk` -> [n_b*bn, 64] FP64."""
+    v = buf.reshape(n_b, d // 64, bn, 64)[:, fblk].reshape(n_b * bn, 64)
+    return bf16_bits_to_f32(to_host(v.contiguous())).astype(np.float64)
+
+
+def _logical_all(buf: torch.Tensor, n_b: int, d: int, bn: int) -> np.ndarray:
+    v = buf.reshape(n_b, d // 64, bn, 64).permute(0, 2, 1, 3).reshape(n_b * bn, d)
+    return bf16_bits_to_f32(to_host(v.contiguous()))
+
+
+def _mask_tokens(mask: torch.Tensor, n_b: int, d: int, bn: int, sel) -> np.ndarray:
+    m = to_host(mask.reshape(n_b, d // 64, bn, 8)[list(sel)].contiguous())
+    bits = np.unpackbits(m, axis=-1, bitorder="little").astype(bool)     # [s, d/64, bn, 64]
+    return bits.transpose(0, 2, 1, 3).reshape(len(sel) * bn, d)
+
+
+# ---------------------------------------------------------------------------
+# FC forward at >= 2048 tokens x 4096 features: bias + GELU + residual, pairs
+# ---------------------------------------------------------------------------
+
+def test_fc_pair_bias_gelu_residual(monkeypatch):
+    rec = _Recorder(monkeypatch)
+    rng = np.random.default_rng(70)
+    Nb, Cb, bn, Kb = 32, 16, 64, 64        # 2048 tokens, 1024 -> 4096 features
+    x = O.fp32_to_bf16_rne(rng.standard_normal((Nb, Cb, bn, 64), dtype=np.float32))
+    wv = vnni_weights(rng, Kb, Cb, 64, 64, 0.02)
+    b = O.fp32_to_bf16_rne(rng.normal(0, 0.5, Kb * 64).astype(np.float32))
+    res = O.fp32_to_bf16_rne(rng.standard_normal((Nb, Kb, bn, 64), dtype=np.float32))
+    layer = tpp.FcLayer(Kb, Cb, 64, 64, to_dev(wv), bias=to_dev(b), activation=tpp.UnaryKind.GELU)
+    out = layer.forward(to_dev(x), Nb, bn, residual=to_dev(res))
+    assert rec.log[-1][1].startswith(PAIR256), rec.log
+    sel = [0, 13, 31]
+    got = to_host(out).reshape(Nb, Kb, bn, 64)[sel]
+    want, _, _ = O.fc_forward_bf16(x, wv, b, activation="gelu", residual_bits=res, nb_sel=sel)
+    err = normwise(bf16_bits_to_f32(got), O.bf16_to_fp32(want))
+    assert err <= BF16_TOL, err
+    assert float(np.mean(got == want)) > 0.9
+
+
+def test_fc_pair_relu_mask(monkeypatch):
+    """ReLU + bitmask epilogue on the pair kernel (the cfg 5 hidden layers)."""
+    rec = _Recorder(monkeypatch)
+    rng = np.random.default_rng(71)
+    Nb, Cb, bn, Kb = 40, 16, 64, 64        # 2560 tokens: a ragged last pair tile row
+    x = O.fp32_to_bf16_rne(rng.standard_normal((Nb, Cb, bn, 64), dtype=np.float32))
+    wv = vnni_weights(rng, Kb, Cb, 64, 64, 0.02)
+    layer = tpp.FcLayer(Kb, Cb, 64, 64, to_dev(wv), activation=tpp.UnaryKind.RELU)
+    mbuf = torch.zeros(Nb * Kb * bn * 8, dtype=torch.uint8, device="cuda")
+    out = layer.forward(to_dev(x), Nb, bn, relu_mask=mbuf)
+    assert rec.log[-1][1].startswith(PAIR256), rec.log
+    sel = [1, 20, 39]
+    got = to_host(out).reshape(Nb, Kb, bn, 64)[sel]
+    want, want_mask, _ = O.fc_forward_bf16(x, wv, None, activation="relu", nb_sel=sel)
+    assert normwise(bf16_bits_to_f32(got), O.bf16_to_fp32(want)) <= BF16_TOL
+    gm = np.unpackbits(to_host(mbuf).reshape(Nb, Kb, bn, 8)[sel], axis=-1, bitorder="little").astype(bool)
+    assert float(np.mean(gm == want_mask)) > 0.999
+    # the mask is exactly "output > 0" of this kernel's own results
+    assert np.array_equal(gm, bf16_bits_to_f32(got) > 0)
+
+
+# ---------------------------------------------------------------------------
+# cfg 3 at full size: FC1 (GELU) -> FC2 (+ residual) -> LayerNorm, 16384 tokens
+# ---------------------------------------------------------------------------
+
+def test_cfg3_chain_full_size(monkeypatch):
+    rec = _Recorder(monkeypatch)
+    rng = np.random.default_rng(72)
+    nb, bn, h, f = 512, 32, 16, 64          # 16384 tokens (bn = 32), 1024 / 4096 features
+    x = O.fp32_to_bf16_rne(rng.standard_normal((nb, h, bn, 64), dtype=np.float32))
+    w1 = vnni_weights(rng, f, h, 64, 64, 0.02)
+    w2 = vnni_weights(rng, h, f, 64, 64, 0.02)
+    fc1 = tpp.FcLayer(f, h, 64, 64, to_dev(w1), activation=tpp.UnaryKind.GELU)
+    fc2 = tpp.FcLayer(h, f, 64, 64, to_dev(w2))
+    xd = to_dev(x)
+    mid = fc1.forward(xd, nb, bn)
+    cfg1 = rec.log[-1][1]
+    o2 = fc2.forward(mid, nb, bn, residual=xd)
+    cfg2 = rec.log[-1][1]
+    ln = tpp.layernorm_blocked(o2, nb, h, bn, 64, 1e-5,
+                               torch.ones(1024, device="cuda"), torch.zeros(1024, device="cuda"))
+    torch.cuda.synchronize()
+    assert cfg1.startswith(PAIR256), cfg1
+    assert cfg2.startswith(PAIR256), cfg2
+    sel = [0, 211, 511]
+    mid_h = to_host(mid).reshape(nb, f, bn, 64)
+    o2_h = to_host(o2).reshape(nb, h, bn, 64)
+    ln_h = to_host(ln).reshape(nb, h, bn, 64)
+    # FC1 + GELU from the input
+    want1, _, _ = O.fc_forward_bf16(x, w1, None, activation="gelu", nb_sel=sel)
+    assert normwise(bf16_bits_to_f32(mid_h[sel]), O.bf16_to_fp32(want1)) <= BF16_TOL
+    # FC2 + residual from the GPU's FC1 output
+    want2, _, _ = O.fc_forward_bf16(mid_h, w2, None, residual_bits=x, nb_sel=sel)
+    assert normwise(bf16_bits_to_f32(o2_h[sel]), O.bf16_to_fp32(want2)) <= BF16_TOL
+    # LayerNorm from the GPU's FC2 output: bitwise (reference order)
+    xs = O.bf16_to_fp32(o2_h[sel]).transpose(0, 2, 1, 3).reshape(len(sel) * bn, 1024)
+    ref, _, _ = O.layernorm(xs, np.ones((1, 1024), np.float32), np.zeros((1, 1024), np.float32), 1e-5)
+    ref = O.fp32_to_bf16_rne(ref.reshape(len(sel), bn, h, 64).transpose(0, 2, 1, 3))
+    assert np.array_equal(ln_h[sel], ref)
+    # the whole chain, errors compounded, from the input alone
+    c2, _, _ = O.fc_forward_bf16(want1, w2, None, residual_bits=x[sel])
+    cs = O.bf16_to_fp32(c2).transpose(0, 2, 1, 3).reshape(len(sel) * bn, 1024)
+    cref, _, _ = O.layernorm(cs, np.ones((1, 1024), np.float32), np.zeros((1, 1024), np.float32), 1e-5)
+    cref = cref.reshape(len(sel), bn, h, 64).transpose(0, 2, 1, 3)
+    assert normwise(bf16_bits_to_f32(ln_h[sel]), cref) <= BF16_TOL
+
+
+# ---------------------------------------------------------------------------
+# cfg 5 at full size: one training step of the 1024-4096-4096-4096-1024 MLP
+# on 8192 tokens, every kernel checked on the GPU's own inputs to it
+# ---------------------------------------------------------------------------
+
+def test_cfg5_full_train_step(monkeypatch):
+    rec = _Recorder(monkeypatch)
+    rng = np.random.default_rng(73)
+    dims = [1024, 4096, 4096, 4096, 1024]
+    Tk, bn, lr = 8192, 64, 0.01
+    n_b = Tk // bn
+    nl = len(dims) - 1
+    ws = [rng.standard_normal((dims[l + 1], dims[l]), dtype=np.float32) * np.float32(0.02) for l in range(nl)]
+    x = O.fp32_to_bf16_rne(rng.standard_normal((Tk, dims[0]), dtype=np.float32))
+    tg = rng.integers(0, dims[-1], Tk).astype(np.int32)
+    mlp = tpp.BlockedMLP(dims, Tk, bn=bn, lr=lr, global_batch=Tk, weights=[torch.from_numpy(w) for w in ws])
+    xb = x.reshape(n_b, bn, dims[0] // 64, 64).transpose(0, 2, 1, 3).copy()
+    loss = mlp.train_step(to_dev(xb), to_dev(tg))
+    torch.cuda.synchronize()
+
+    # ---- dispatch: every 4096-wide GEMM of the step ran the pair kernel ----
+    kinds = [k for k, _ in rec.log]
+    assert kinds == ["forward"] * 4 + ["backward_weights", "backward_data"] * 3 + ["backward_weights"], kinds
+    fwd = [c for k, c in rec.log if k == "forward"]
+    bwd_d = [c for k, c in rec.log if k == "backward_data"]
+    bwd_w = [c for k, c in rec.log if k == "backward_weights"]
+    assert all(c.startswith(PAIR256) for c in fwd), fwd
+    assert all(c.startswith(PAIR256) for c in bwd_d), bwd_d
+    assert bwd_w[1].startswith(PAIR256) and bwd_w[2].startswith(PAIR256), bwd_w  # layers 3 and 2 (4096 x 4096)
+
+    wb = [O.bf16_to_fp32((w.view(np.uint32) >> 16).astype(np.uint16)) for w in ws]  # the hi halves the GEMMs read
+    sel = [0, 97]
+    # ---- forward, layer by layer from the GPU's own layer inputs ----
+    h_in = O.bf16_to_fp32(x).reshape(Tk, dims[0])
+    for l in range(nl):
+        hs = (h_in[np.concatenate([np.arange(s * bn, (s + 1) * bn) for s in sel])] if l == 0
+              else _blk_tokens(mlp.h[l], n_b, dims[l], bn, sel))
+        z = O.blocked_matmul(hs, wb[l])
+        if l < nl - 1:
+            got = _blk_tokens(mlp.h[l + 1], n_b, dims[l + 1], bn, sel)
+            assert normwise(got, O.round_bf16(O.relu(z))) <= BF16_TOL, l
+            gm = _mask_tokens(mlp.mask[l + 1], n_b, dims[l + 1], bn, sel)
+            assert np.array_equal(gm, got > 0), l                      # mask = this kernel's own sign
+            assert float(np.mean(gm == (z > 0))) > 0.999, l
+        else:
+            got = to_host(mlp.logits).reshape(n_b, dims[-1] // 64, bn, 64)[sel]
+            got = got.transpose(0, 2, 1, 3).reshape(len(sel) * bn, dims[-1])
+            assert normwise(got, z) <= FP32_TOL
+    # ---- softmax-CE gradient: bitwise from the GPU logits ----
+    lg = to_host(mlp.logits).reshape(n_b, dims[-1] // 64, bn, 64)[sel].transpose(0, 2, 1, 3).reshape(-1, dims[-1])
+    p = np.stack([O.softmax_slice(lg[i:i + 1])[0] for i in range(lg.shape[0])])
+    ts = np.concatenate([tg[s * bn:(s + 1) * bn] for s in sel])
+    onehot = np.zeros_like(p)
+    onehot[np.arange(len(ts)), ts] = 1
+    g_ref = O.fp32_to_bf16_rne((p - onehot) * np.float32(1.0 / Tk))
+    g_got = to_host(mlp.g[nl - 1].reshape(n_b, dims[-1] // 64, bn, 64)[sel].contiguous())
+    assert np.array_equal(g_got.transpose(0, 2, 1, 3).reshape(-1, dims[-1]), g_ref)
+    lsel = to_host(loss)[np.concatenate([np.arange(s * bn, (s + 1) * bn) for s in sel])]
+    assert np.allclose(lsel, -np.log(p[np.arange(len(ts)), ts]), rtol=1e-5, atol=1e-6)
+    # ---- backward-data with the fused RELU_INV, from the GPU's gradients ----
+    for l in range(nl - 1, 0, -1):
+        gs = _blk_tokens(mlp.g[l], n_b, dims[l + 1], bn, sel)
+        ref = O.round_bf16(O.relu_inv(O.blocked_matmul(gs, wb[l].T.copy()),
+                                      _mask_tokens(mlp.mask[l], n_b, dims[l], bn, sel)))
+        got = _blk_tokens(mlp.g[l - 1], n_b, dims[l], bn, sel)
+        assert normwise(got, ref) <= BF16_TOL, l
+    # ---- backward-weights (FP32 out, BF16 in): sampled output-feature blocks
+    # against the reference-order oracle (north_star BF16 tolerance) and
+    # against FP64.  The 8192-token reductions of the CE gradient cancel
+    # heavily (p/B over all tokens against -1/B at the ~8 target tokens), so
+    # the FP64 distance is reported next to the reference order's own.
+    dws = []
+    for l in range(nl):
+        h32 = h_in if l == 0 else _logical_all(mlp.h[l], n_b, dims[l], bn)
+        h_all = h32.astype(np.float64)
+        dw_gpu = T.unpack_weight(mlp.dw[l].cpu(), dims[l + 1], dims[l]).numpy()
+        dws.append(dw_gpu)
+        for fb in (0, dims[l + 1] // 64 - 1):
+            gcol = _blk_feature_cols(mlp.g[l], n_b, dims[l + 1], bn, fb)       # [T, 64]
+            ref64 = gcol.T @ h_all                                            # [64, in]
+            ref32 = O.blocked_matmul(gcol.T.astype(np.float32).copy(), h32.T.copy())
+            got = dw_gpu[fb * 64:(fb + 1) * 64]
+            e_gpu, e_ref = normwise(got, ref64), normwise(ref32, ref64)
+            print(f"dW layer {l} block {fb}: GPU vs FP64 {e_gpu:.2e}, reference order vs FP64 {e_ref:.2e}, "
+                  f"GPU vs reference {normwise(got, ref32):.2e}")
+            assert normwise(got, ref32) <= BF16_TOL, (l, fb)
+            assert e_gpu <= 1e-3, (l, fb, e_gpu, e_ref)
+        del h_all, h32
+    # ---- split-SGD on the FP32 masters: bitwise from the GPU's dW ----
+    for l in range(nl):
+        want = O.split_sgd_step(ws[l], dws[l], lr)
+        got = mlp.master_weight(l).cpu().numpy()
+        assert got.tobytes() == np.asarray(want, np.float32).tobytes(), l
+
+
+def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):
+    """Standalone backward-data / backward-weights at the 4096 x 4096 x 8192
+    dispatch with random gradients (independent of the training chain)."""
+    rec = _Recorder(monkeypatch)
+    rng = np.random.default_rng(74)
+    Tk, bn, D = 8192, 64, 4096
+    n_b = Tk // bn
+    w = O.fp32_to_bf16_rne(rng.standard_normal((D, D), dtype=np.float32) * np.float32(0.02))
+    dy = O.fp32_to_bf16_rne(rng.standard_normal((Tk, D), dtype=np.float32))
+    xh = O.fp32_to_bf16_rne(rng.standard_normal((Tk, D), dtype=np.float32))
+    blk = lambda a: a.reshape(n_b, bn, D // 64, 64).transpose(0, 2, 1, 3).copy()  # noqa: E731
+    wp = T.pack_logical_weight(torch.from_numpy(w.view(np.int16)).view(torch.bfloat16)).view(torch.int16).numpy()
+    layer = tpp.FcLayer(D // 64, D // 64, 64, 64, None, w_packed=to_dev(wp.view(np.uint16)))
+    dyd, xd = to_dev(blk(dy)), to_dev(blk(xh))
+    dx = layer.backward_data(dyd, n_b, bn)
+    assert rec.log[-1][1].startswith(PAIR256), rec.log[-1]
+    dw = layer.backward_weights(dyd, xd, n_b, bn)
+    assert rec.log[-1][1].startswith(PAIR256), rec.log[-1]
+    torch.cuda.synchronize()
+    wf = O.bf16_to_fp32(w).astype(np.float64)
+    dyf = O.bf16_to_fp32(dy).astype(np.float64)
+    xf = O.bf16_to_fp32(xh).astype(np.float64)
+    rows = np.r_[0:64, 4032:4096]
+    got_dx = bf16_bits_to_f32(to_host(dx).reshape(n_b, D // 64, bn, 64)[[0, 127]].transpose(0, 2, 1, 3).reshape(-1, D))
+    ref_dx = dyf[rows] @ wf
+    assert normwise(got_dx, ref_dx) <= BF16_TOL
+    got_dw = T.unpack_weight(dw.cpu(), D, D).numpy()
+    for fb in (0, 31, 63):
+        ref = dyf[:, fb * 64:(fb + 1) * 64].T @ xf
+        assert normwise(got_dw[fb * 64:(fb + 1) * 64], ref) <= FP32_TOL, fb

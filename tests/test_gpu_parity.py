@@ -286,6 +286,49 @@ def test_fc_fp32_bitwise(golden):
         assert bits(to_host(c.primary)) == bits(g[f"fp32_{i}_c"]), i
 
 
+@pytest.mark.parametrize("mb,nb,kb,act", [(3, 2, 4, None), (2, 3, 2, "relu")])
+def test_fc_fp32_multi_block_staged(mb, nb, kb, act):
+    """FP32 fc_forward with m_b >= 2 and 64 x 64 x 64 blocks: the staged
+    ordered engine with instances = m_b sharing one B per token block
+    (instance stride 0 on B), bitwise vs the reference order."""
+    rng = np.random.default_rng(200 + mb * 10 + nb)
+    bm = bn = bk = 64
+    a4 = rng.standard_normal((mb, kb, bk, bm)).astype(np.float32)
+    b4 = rng.standard_normal((nb, kb, bn, bk)).astype(np.float32)
+    spec = tpp.FcSpec(mb, nb, kb, bm, bn, bk, activation=tpp.UnaryKind.RELU if act else None)
+    c = tpp.alloc(tpp.TensorDesc(bm, nb * mb * bn, bm, tpp.DType.FP32))
+    tpp.fc_forward(spec, to_dev(a4), to_dev(b4), c)
+    want = O.fc_forward_fp32(a4, b4, activation=act)
+    assert bits(to_host(c.primary)) == bits(np.ascontiguousarray(want).reshape(-1))
+
+
+def test_brgemm_stride_batched_shared_operand():
+    """tpp_brgemm_stride_batched with inst_b = 0 (every instance reads the same
+    B batch) and with both instance strides set: bitwise vs the oracle."""
+    import ctypes as C
+    from paper_2104_05755_b200 import _lib
+    rng = np.random.default_rng(210)
+    m = n = k = 64
+    count, inst = 4, 3
+    a = rng.standard_normal(inst * count * m * k).astype(np.float32)
+    b = rng.standard_normal(inst * count * k * n).astype(np.float32)
+    lib = _lib.load()
+    d = tpp.GemmSpec(m, n, k, m, k, m, beta=0.0).c()
+    ad, bd = to_dev(a), to_dev(b)
+    for inst_b in (0, count * k * n):
+        c = torch.zeros(inst * m * n, dtype=torch.float32, device="cuda")
+        rc = lib.tpp_brgemm_stride_batched(C.byref(d), ad.data_ptr(), bd.data_ptr(), m * k, k * n, count,
+                                           c.data_ptr(), inst, count * m * k, inst_b, m * n,
+                                           _lib.stream_ptr(None))
+        _lib.check(rc, "stride_batched")
+        got = to_host(c).reshape(inst, n, m)
+        for j in range(inst):
+            ab = [O.load_a(a, j * count * m * k + i * m * k, m, k, m, "fp32") for i in range(count)]
+            bb = [O.load_b(b, j * inst_b + i * k * n, k, n, k, "fp32") for i in range(count)]
+            want = O.brgemm(ab, bb, np.zeros((m, n), np.float32), beta=0.0)
+            assert bits(got[j].T.copy()) == bits(want), (inst_b, j)
+
+
 def test_layernorm_blocked_bitwise():
     rng = np.random.default_rng(21)
     # (4,16,32,64) and (700,1,32,64) take the TMA pipeline (the latter wraps
