@@ -21,7 +21,7 @@ import torch
 
 from . import kernels as K
 from .ops import UnaryKind
-from .parallel import GradAllreduce, world
+from .parallel import GradSync, world
 
 BLK = 64
 
@@ -56,7 +56,15 @@ class BlockedMLP:
 
     def __init__(self, dims: Sequence[int], tokens: int, bn: int = 64, lr: float = 0.01,
                  global_batch: Optional[int] = None, init_std: float = 0.02, seed: int = 0,
-                 device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None):
+                 device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None,
+                 grad_dtype: str = "fp32", reduce_fn=None):
+        """``grad_dtype``: "fp32" (dW written and applied in FP32) or "bf16"
+        (dW written as BF16 by the backward-weights epilogue, exchanged as
+        BF16 — half the allreduce bytes — and applied by split-SGD, which
+        accepts BF16 gradients like the reference's, kernels.py:235-251).
+        ``reduce_fn`` replaces the dW collective (rank emulation in tests)."""
+        if grad_dtype not in ("fp32", "bf16"):
+            raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         if any(d % BLK for d in dims) or tokens % bn or bn % BLK:
             raise ValueError("dims must be multiples of 64 and tokens a multiple of bn (itself a multiple of 64)")
         self.dims = list(dims)
@@ -88,9 +96,14 @@ class BlockedMLP:
                               for l in range(1, self.nl)]
         self.logits = torch.empty(tokens * dims[-1], dtype=torch.float32, device=dev)
         self.g = [torch.empty(tokens * dims[l], dtype=torch.bfloat16, device=dev) for l in range(1, self.nl + 1)]
-        self.dw = [torch.empty(dims[l + 1] * dims[l], dtype=torch.float32, device=dev) for l in range(self.nl)]
+        self.grad_dtype = grad_dtype
+        dwt = torch.float32 if grad_dtype == "fp32" else torch.bfloat16
+        self.dw = [torch.empty(dims[l + 1] * dims[l], dtype=dwt, device=dev) for l in range(self.nl)]
         self.loss = torch.empty(tokens, dtype=torch.float32, device=dev)
-        self.comm = GradAllreduce(group)
+        self.sync = GradSync(group, reduce_fn=reduce_fn, device=dev)
+        # optional per-launch hook (label) called right after each main-stream
+        # launch -- bench.py records CUDA events there for the step breakdown
+        self.trace = None
 
     # ------------------------------------------------------------------
     def forward(self, x: torch.Tensor) -> torch.Tensor:
@@ -101,27 +114,46 @@ class BlockedMLP:
                 layer.forward(self.h[l], self.n_b, self.bn, out=self.h[l + 1], relu_mask=self.mask[l + 1])
             else:
                 layer.forward(self.h[l], self.n_b, self.bn, out=self.logits, out_fp32=True)
+            if self.trace:
+                self.trace(f"fwd{l}")
         return self.logits
 
     def backward(self, targets: torch.Tensor) -> None:
-        """Softmax-CE gradient, then per layer dW (allreduce launched at once,
-        overlapping the next dX) and dX with the ReLU mask fused."""
+        """Softmax-CE gradient, then per layer (last first) dW and dX with
+        the ReLU mask fused.  Each layer's dW bucket is handed to the
+        gradient exchange as soon as it is written (it overlaps the remaining
+        backward GEMMs) and its split-SGD update as soon as the layer's
+        backward-data GEMM — the last reader of its weights — is issued."""
         nl = self.nl
+        tr = self.trace
         K.softmax_xent_blocked(self.logits, targets, self.n_b, self.dims[-1] // BLK, self.bn, BLK,
                                1.0 / self.global_batch, dlogits=self.g[nl - 1], loss=self.loss)
+        if tr:
+            tr("xent")
         for l in range(nl - 1, -1, -1):
             layer = self.layers[l]
             layer.backward_weights(self.g[l], self.h[l], self.n_b, self.bn, out=self.dw[l])
-            self.comm.push(self.dw[l])
+            if tr:
+                tr(f"dw{l}")
+            self.sync.grad_ready(self.dw[l])
             if l > 0:
                 layer.backward_data(self.g[l], self.n_b, self.bn, relu_mask_in=self.mask[l],
                                     out=self.g[l - 1])
+                if tr:
+                    tr(f"dx{l}")
+            self.sync.update_ready(lambda l=l: self._update(l))
+
+    def _update(self, l: int) -> None:
+        K.split_sgd_flat(self.hi[l], self.lo[l], self.dw[l], self.lr)
+        if self.trace and not self.sync.active:
+            self.trace(f"sgd{l}")
 
     def step(self) -> None:
-        """Wait for the dW allreduce, then split-SGD on every layer."""
-        self.comm.wait()
-        for l in range(self.nl):
-            K.split_sgd_flat(self.hi[l], self.lo[l], self.dw[l], self.lr)
+        """Complete the step: every layer's exchange and split-SGD update is
+        ordered before whatever the caller issues next."""
+        self.sync.finish()
+        if self.trace:
+            self.trace("step")
 
     def train_step(self, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         self.forward(x)
@@ -133,6 +165,13 @@ class BlockedMLP:
     def master_weight(self, l: int) -> torch.Tensor:
         """FP32 master weight of layer l as a logical [out, in] matrix."""
         return unpack_weight(pack_master(self.hi[l], self.lo[l]), self.dims[l + 1], self.dims[l])
+
+    def gemm_flops(self, label: str) -> int:
+        """Algorithmic flops of the GEMM behind a trace label (fwd{l}, dw{l}, dx{l})."""
+        if not (label.startswith("fwd") or label[:2] in ("dw", "dx")):
+            return 0
+        l = int(label[-1])
+        return 2 * self.tokens * self.dims[l] * self.dims[l + 1]
 
     @property
     def flops_per_step(self) -> int:

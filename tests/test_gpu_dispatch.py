@@ -13,7 +13,7 @@ instantiation really ran, and check the results against the CPU oracle
   <= 2e-2 (north_star BF16 tolerance);
 * FP32 logits normwise <= 1e-5 (only the summation order differs);
 * FP32 dW (BF16 inputs, 8192-token reductions) against the reference-order
-  oracle <= 2e-2 and against an FP64 restatement <= 1e-3, with both
+  oracle <= 2e-2 and against an FP64 restatement <= 1e-4, with both
   distances printed beside the reference order's own FP64 distance;
 * the softmax-CE gradient and the split-SGD update bitwise (same order).
 """
@@ -265,7 +265,7 @@ def test_cfg5_full_train_step(monkeypatch):
             print(f"dW layer {l} block {fb}: GPU vs FP64 {e_gpu:.2e}, reference order vs FP64 {e_ref:.2e}, "
                   f"GPU vs reference {normwise(got, ref32):.2e}")
             assert normwise(got, ref32) <= BF16_TOL, (l, fb)
-            assert e_gpu <= 1e-3, (l, fb, e_gpu, e_ref)
+            assert e_gpu <= 1e-4, (l, fb, e_gpu, e_ref)
         del h_all, h32
     # ---- split-SGD on the FP32 masters: bitwise from the GPU's dW ----
     for l in range(nl):
@@ -296,7 +296,7 @@ def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):
     wf = O.bf16_to_fp32(w).astype(np.float64)
     dyf = O.bf16_to_fp32(dy).astype(np.float64)
     xf = O.bf16_to_fp32(xh).astype(np.float64)
-    rows = np.r_[0:64, 4032:4096]
+    rows = np.r_[0:64, 8128:8192]
     got_dx = bf16_bits_to_f32(to_host(dx).reshape(n_b, D // 64, bn, 64)[[0, 127]].transpose(0, 2, 1, 3).reshape(-1, D))
     ref_dx = dyf[rows] @ wf
     assert normwise(got_dx, ref_dx) <= BF16_TOL

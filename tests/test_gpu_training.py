@@ -108,3 +108,111 @@ def test_mlp_train_step_vs_oracle():
         assert normwise(dw, dws_ref[l]) <= TOL, l
         got_w = mlp.master_weight(l).cpu().numpy()
         assert normwise(got_w - ws[l], new_ref[l] - ws[l]) <= TOL, l
+
+
+# ---------------------------------------------------------------------------
+# data parallelism: a sharded step equals the global-batch step
+# ---------------------------------------------------------------------------
+
+def _mlp_case(seed=60):
+    rng = np.random.default_rng(seed)
+    dims = [128, 256, 256, 128]
+    T_ = 512
+    ws = [(rng.standard_normal((dims[l + 1], dims[l])) * 0.05).astype(np.float32) for l in range(3)]
+    x = _bf16(rng, (T_, dims[0]), 1.0)
+    tg = rng.integers(0, dims[-1], T_).astype(np.int32)
+    return dims, T_, ws, x, tg
+
+
+@pytest.mark.parametrize("grad_dtype", ["fp32", "bf16"])
+def test_sharded_step_equals_global_step_emulated(grad_dtype):
+    """Two emulated ranks (half the tokens each, loss scaled by the global
+    batch) whose dW buckets are summed before split-SGD reproduce the
+    single-rank global-batch step."""
+    dims, T_, ws, x, tg = _mlp_case()
+    lr = 0.5
+    wt = [torch.from_numpy(w) for w in ws]
+    full = tpp.BlockedMLP(dims, T_, bn=64, lr=lr, global_batch=T_, weights=wt)
+    full.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
+    half = T_ // 2
+    shards = [tpp.BlockedMLP(dims, half, bn=64, lr=lr, global_batch=T_, weights=wt, grad_dtype=grad_dtype)
+              for _ in range(2)]
+    for r, m in enumerate(shards):
+        m.forward(to_dev(_blocked(x[r * half:(r + 1) * half], 64)))
+        m.backward(to_dev(tg[r * half:(r + 1) * half]))
+    for l in range(3):                                    # the allreduce(sum)
+        s = shards[0].dw[l] + shards[1].dw[l]
+        for m in shards:
+            m.dw[l].copy_(s)
+    for m in shards:
+        m.step()
+    torch.cuda.synchronize()
+    # forward activations are row-independent: bitwise equal to the global run
+    for r, m in enumerate(shards):
+        for l in range(1, 3):
+            a = full.h[l].reshape(T_ // 64, -1)[r * (half // 64):(r + 1) * (half // 64)].reshape(-1)
+            assert torch.equal(a.view(torch.int16), m.h[l].view(torch.int16)), (r, l)
+    tol_dw = 1e-5 if grad_dtype == "fp32" else TOL
+    for l in range(3):
+        got = shards[0].dw[l].float().cpu().numpy()
+        assert normwise(got, full.dw[l].cpu().numpy()) <= tol_dw, l
+        w0 = ws[l]
+        d_full = full.master_weight(l).cpu().numpy() - w0
+        for m in shards:
+            assert normwise(m.master_weight(l).cpu().numpy() - w0, d_full) <= tol_dw, l
+        assert torch.equal(shards[0].hi[l].view(torch.int16), shards[1].hi[l].view(torch.int16))
+
+
+def _dp_worker(rank, ws_, port, grad_dtype, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws_))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=ws_)
+    try:
+        import paper_2104_05755_b200 as tp
+        dims, T_, ws, x, tg = _mlp_case()
+        half = T_ // ws_
+        m = tp.BlockedMLP(dims, half, bn=64, lr=0.5, global_batch=T_, weights=[torch.from_numpy(w) for w in ws],
+                          grad_dtype=grad_dtype)
+        assert m.sync.active and m.sync.stream is not None
+        m.train_step(to_dev(_blocked(x[rank * half:(rank + 1) * half], 64)), to_dev(tg[rank * half:(rank + 1) * half]))
+        torch.cuda.synchronize()
+        q.put((rank, [m.master_weight(l).cpu().numpy() for l in range(3)], m.sync.issued))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grad_dtype", ["fp32", "bf16"])
+def test_sharded_step_two_processes_gloo(grad_dtype):
+    """The real exchange path: 2 processes (both on cuda:0, gloo — collectives
+    wait on the host, no kernel waits on another), GradSync's side stream
+    all-reducing each dW bucket and running that layer's split-SGD after it.
+    Both ranks end with the same weights as the global-batch step."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dp_worker, args=(r, 2, port, grad_dtype, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=300) for _ in range(2)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dims, T_, ws, x, tg = _mlp_case()
+    full = tpp.BlockedMLP(dims, T_, bn=64, lr=0.5, global_batch=T_, weights=[torch.from_numpy(w) for w in ws])
+    full.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
+    torch.cuda.synchronize()
+    tol = 1e-5 if grad_dtype == "fp32" else TOL
+    for rank, wts, issued in res:
+        assert issued == 3
+        for l in range(3):
+            d_full = full.master_weight(l).cpu().numpy() - ws[l]
+            assert normwise(wts[l] - ws[l], d_full) <= tol, (rank, l)
+    for l in range(3):
+        assert np.array_equal(res[0][1][l], res[1][1][l])

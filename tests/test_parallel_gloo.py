@@ -67,3 +67,58 @@ def test_grad_allreduce_world2_gloo():
     assert all(ok for _, ok, *_ in res)
     assert [(r, w) for _, _, r, w, _, _ in res] == [(0, 2), (1, 2)]
     assert [(s, c) for *_, s, c in res] == [(0, 64), (64, 64)]
+
+
+def _sync_worker(rank, ws, port, q):
+    """GradSync on host tensors (gloo): every bucket is summed over the ranks
+    before its update callback runs, callbacks run in bucket order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        sync = parallel.GradSync()
+        seen = []
+        grads = [torch.full((n,), float(rank + 1) * (l + 1)) for l, n in enumerate((7, 300, 64))]
+        for l in range(len(grads) - 1, -1, -1):      # backward order: last layer first
+            sync.grad_ready(grads[l])
+            sync.update_ready(lambda l=l: seen.append((l, float(grads[l][0]))))
+        sync.finish()
+        total = float(sum(range(1, ws + 1)))
+        ok = seen == [(l, total * (l + 1)) for l in range(len(grads) - 1, -1, -1)]
+        q.put((rank, ok, sync.issued, sync.active))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grad_sync_world2_gloo():
+    ws = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sync_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(ws))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, True, 3, True), (1, True, 3, True)]
+
+
+def test_grad_sync_single_rank_defers_updates_in_order():
+    sync = parallel.GradSync()
+    assert not sync.active
+    seen = []
+    t = torch.ones(3)
+    for l in (2, 1, 0):
+        sync.grad_ready(t)
+        sync.update_ready(lambda l=l: seen.append(l))
+    assert seen == []            # nothing to exchange: updates wait for finish()
+    sync.finish()
+    assert seen == [2, 1, 0]
+    # a reduce_fn stands in for the collective (rank emulation)
+    red = []
+    sync = parallel.GradSync(reduce_fn=lambda x: red.append(x.clone()))
+    sync.grad_ready(torch.arange(3.0))
+    sync.update_ready(lambda: red.append("upd"))
+    sync.finish()
+    assert torch.equal(red[0], torch.arange(3.0)) and red[1] == "upd"
