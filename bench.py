@@ -308,10 +308,11 @@ def run_e2e(torch, tpp, mlp, dist, K, W, graph: bool):
     for e in ev_done:
         e.record(comp0)
 
-    def step(i, comp):
+    def step(i, comp, capturing=False):
         b = i % NBUF
         with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_done[b])            # buffers b no longer read
+            if not (capturing and i < NBUF):       # (a capture may not wait on pre-capture work)
+                s_in.wait_event(ev_done[b])        # buffers b no longer read
             x_dev[b].copy_(x_host, non_blocking=True)
             t_dev[b].copy_(t_host, non_blocking=True)
             ev_in[b].record(s_in)
@@ -329,7 +330,7 @@ def run_e2e(torch, tpp, mlp, dist, K, W, graph: bool):
             cap = torch.cuda.current_stream()
             s_in.wait_stream(cap)
             for i in range(K):
-                step(i, cap)
+                step(i, cap, capturing=True)
             cap.wait_stream(s_in)
         torch.cuda.synchronize()
         for _ in range(3):

@@ -69,11 +69,14 @@ typedef struct {
 
 /* ---- BRGEMM TPP: contraction.py:44-85 (GemmSpec) --------------------- */
 enum tpp_engine {
-  TPP_ENGINE_AUTO = 0,     /* INT8 STRIDE -> tcgen05 kind::i8 (exact); else ordered;
-                              BF16 layer drivers -> tensor cores                     */
+  TPP_ENGINE_AUTO = 0,     /* BF16 (STRIDE / OFFSET / ADDRESS, count >= 1) -> tcgen05
+                              kind::f16 (normwise <= 2e-2); INT8 STRIDE -> tcgen05
+                              kind::i8 (exact); everything else -> ordered         */
   TPP_ENGINE_ORDERED = 1,  /* SIMT, the reference's per-element order: bitwise parity  */
-  TPP_ENGINE_TENSOR = 2    /* tcgen05.mma, TMEM accumulation (layer drivers; INT8
-                              STRIDE BRGEMMs with plain A)                           */
+  TPP_ENGINE_TENSOR = 2    /* tcgen05.mma, TMEM accumulation: BF16 (all three batch
+                              kinds; 16-byte aligned blocks with m, k, ldb, lda
+                              multiples of 8 are staged with 16-byte copies, any
+                              other block element-wise) and INT8 STRIDE, plain A  */
 };
 
 typedef struct {
@@ -98,6 +101,23 @@ int tpp_brgemm_offset(const tpp_gemm_desc* d, const void* a, const void* b,
 /* ... with BrgemmBatch.address (contraction.py:144-150): device arrays of block pointers */
 int tpp_brgemm_address(const tpp_gemm_desc* d, const void* const* a_ptrs,
                        const void* const* b_ptrs, int64_t count, void* c, void* stream);
+/* Many independent BF16 BRGEMMs of one GemmSpec in ONE tcgen05 launch (the
+ * GPU form of the reference's per-block job loops, kernels.py:312-329, and of
+ * composing a layer from brgemm calls, contraction.py:261-322): group g
+ * computes C_g = beta*C_g + sum_{i<count} A_{g,i} B_{g,i} with
+ *   C_g = c + c_offsets[g] (elements; c_offsets may be NULL when groups == 1)
+ *   kind 0 STRIDE:  A_{g,i} = a + (a_index ? a_index[g] : 0) + i*stride_a (b alike)
+ *   kind 1 OFFSET:  A_{g,i} = a + a_index[g*count + i]              (b alike)
+ *   kind 2 ADDRESS: A_{g,i} = ((const void* const*)a_index)[g*count + i]
+ * All index arrays are device memory; engine AUTO or TENSOR, BF16 only, any
+ * shape / alignment (16-byte aligned blocks with m, k, ldb, lda multiples of
+ * 8 take the 16-byte staging path, others element-wise staging).
+ * FP32 C, accumulated in TMEM over the whole batch (sum order differs from
+ * the reference: <= 2e-2 normwise, north_star's BF16 tolerance). */
+int tpp_brgemm_grouped(const tpp_gemm_desc* d, int32_t kind, const void* a, const void* b,
+                       int64_t stride_a, int64_t stride_b, const int64_t* a_index,
+                       const int64_t* b_index, int64_t count, void* c, const int64_t* c_offsets,
+                       int64_t groups, void* stream);
 /* Many independent stride-BRGEMMs in one launch (the GPU form of the
  * reference's `threads=` job loop over disjoint C tiles, contraction.py:317-322
  * and kernels.py:323-329): instance j uses a + j*inst_a, b + j*inst_b,

@@ -60,7 +60,9 @@ from .contraction import (
     DEFAULT_BLOCKING,
     Engine,
     GemmSpec,
+    GroupedBatch,
     brgemm,
+    brgemm_grouped,
     gemm,
     matmul,
     spec_for_views,

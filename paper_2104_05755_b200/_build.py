@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtpp_b200.so")
-SOURCES = ["capi.cu", "brgemm_ordered.cu", "brgemm_tc.cu", "transform.cu", "eltwise.cu", "eltwise_fast.cu", "norm.cu", "conv_dw.cu", "prng.cu", "quant.cu", "brgemm_i8.cu"]
+SOURCES = ["capi.cu", "brgemm_ordered.cu", "brgemm_tc.cu", "transform.cu", "eltwise.cu", "eltwise_fast.cu", "norm.cu", "conv_dw.cu", "prng.cu", "quant.cu", "brgemm_i8.cu", "brgemm_grouped.cu"]
 HEADERS = ["common.cuh", "sm100.cuh", "launch.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -65,6 +65,8 @@ _SIGS = {
     "tpp_brgemm_stride": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _I64, _I64, _I64, _P, _P]),
     "tpp_brgemm_offset": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _P, _P, _I64, _P, _P]),
     "tpp_brgemm_address": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _I64, _P, _P]),
+    "tpp_brgemm_grouped": (C.c_int, [C.POINTER(GemmDescC), _I32, _P, _P, _I64, _I64, _P, _P, _I64, _P, _P,
+                                     _I64, _P]),
     "tpp_brgemm_stride_batched": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _I64, _I64, _I64, _P,
                                             _I64, _I64, _I64, _I64, _P]),
     "tpp_fc_packed_weight_bytes": (C.c_int64, [C.POINTER(FcDescC)]),

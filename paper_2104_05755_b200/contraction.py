@@ -3,12 +3,20 @@
 
 ``brgemm(spec, batch, c)`` computes C = beta*C + sum_i A_i x B_i over the
 three addressing variants of ``BrgemmBatch`` with the reference's argument
-validation and exceptions.  The single-BRGEMM entry points run the ordered
-SIMT kernel (K1), which reproduces the reference's per-element order and is
-therefore bitwise identical for every dtype; blocking and thread count do
-not change results, and they are accepted and ignored here as
-the GPU owns the tiling.  Layer-level drivers (kernels.FcLayer, conv) run the
-tcgen05 tensor-core BRGEMM.
+validation and exceptions.  Engines (``GemmSpec.engine``):
+
+* AUTO (default): BF16 batches run the tcgen05 BRGEMM (K11,
+  brgemm_grouped.cu) for all three addressing variants — FP32 accumulation in TMEM over the whole batch,
+  normwise <= 2e-2 of the reference (north_star's BF16 tolerance); INT8
+  STRIDE batches run tcgen05 kind::i8 (exact); everything else runs the
+  ordered SIMT engine (K1).
+* ORDERED: K1 for every dtype — the reference's per-element order, bitwise.
+* TENSOR: tensor cores or NotImplementedError.
+
+Blocking and thread count never change results; they are
+accepted and ignored, the GPU owns the tiling.  ``brgemm_grouped`` runs many
+C blocks of one GemmSpec in one tcgen05 launch (the GPU form of composing a
+layer from brgemm calls, kernels.py:312-329).
 """
 
 from __future__ import annotations
@@ -38,11 +46,10 @@ class ComputePath(enum.Enum):
 
 class Engine(enum.Enum):
     """Which sm_100a engine runs a BRGEMM (not in the reference)."""
-    AUTO = "auto"          # ordered SIMT for float BRGEMMs, tcgen05 kind::i8 for INT8 STRIDE
-                           # batches (integer sums: any order is the reference's bits);
-                           # tensor cores in the layer drivers
+    AUTO = "auto"          # tcgen05 for aligned BF16 batches (all variants) and INT8 STRIDE
+                           # batches; the ordered SIMT engine otherwise
     ORDERED = "ordered"    # reference per-element order, bitwise parity
-    TENSOR = "tensor"      # tcgen05 (layer drivers; INT8 STRIDE BRGEMMs)
+    TENSOR = "tensor"      # tcgen05 (BF16 any variant, INT8 STRIDE) or NotImplementedError
 
 
 @dataclass(frozen=True)
@@ -285,6 +292,214 @@ def brgemm(spec: GemmSpec, batch: BrgemmBatch, c: TensorView,
         ap, bp = batch.device_arrays(c.primary.device, stream)
         rc = lib.tpp_brgemm_address(C.byref(d), ap.data_ptr(), bp.data_ptr(), n, c.ptr, s)
     _lib.check(rc, "brgemm")
+
+
+def _tensor_eligible(spec: GemmSpec, a_refs, b_refs) -> bool:
+    """The tcgen05 BRGEMM (K11) takes any non-empty BF16 batch: 16-byte
+    aligned blocks with m, k, ldb (lda) multiples of 8 are staged with
+    16-byte copies, any other block element-wise."""
+    return spec.in_dtype is DType.BF16 and len(a_refs) > 0
+
+
+class GroupedBatch:
+    """Many independent BRGEMM batches of one GemmSpec, each feeding its own C
+    block (group), for ``brgemm_grouped``.  Device index arrays are built once
+    (pinned staging, asynchronous copy) and reused by every call.
+
+    * ``stride(a, b, stride_a, stride_b, count, a_group_offsets, b_group_offsets)``:
+      group g, entry i reads A at a + a_group_offsets[g] + i*stride_a (B alike);
+    * ``offset(a, b, a_offsets, b_offsets)``: [groups][count] element offsets;
+    * ``address(a_refs, b_refs)``: [groups][count] (buffer, offset) refs;
+    * ``from_batches(batches)``: the narrowest of the three that describes a
+      list of BrgemmBatch objects of equal length.
+    """
+
+    def __init__(self, kind: BatchKind, a_refs, b_refs, count: int, stride_a=0, stride_b=0,
+                 a_goff=None, b_goff=None):
+        self.kind = kind
+        self.a_refs, self.b_refs = a_refs, b_refs      # [groups][count] (buffer, offset)
+        self.count = count
+        self.groups = len(a_refs)
+        self.stride_a, self.stride_b = stride_a, stride_b
+        self.a_goff, self.b_goff = a_goff, b_goff
+        self._dev = None
+        self._checked = set()   # (spec, C buffer, C offsets) combinations already validated
+
+    @staticmethod
+    def stride(a_base, b_base, stride_a: int, stride_b: int, count: int,
+               a_group_offsets: Sequence[int], b_group_offsets: Sequence[int]) -> "GroupedBatch":
+        if len(a_group_offsets) != len(b_group_offsets):
+            raise TensorError("group count mismatch")
+        ab, ao = _as_ref(a_base)
+        bb, bo = _as_ref(b_base)
+        a_refs = [tuple((ab, ao + int(ga) + i * int(stride_a)) for i in range(count)) for ga in a_group_offsets]
+        b_refs = [tuple((bb, bo + int(gb) + i * int(stride_b)) for i in range(count)) for gb in b_group_offsets]
+        return GroupedBatch(BatchKind.STRIDE, a_refs, b_refs, count, int(stride_a), int(stride_b),
+                            [ao + int(x) for x in a_group_offsets], [bo + int(x) for x in b_group_offsets])
+
+    @staticmethod
+    def offset(a_base, b_base, a_offsets, b_offsets) -> "GroupedBatch":
+        ab, ao = _as_ref(a_base)
+        bb, bo = _as_ref(b_base)
+        if len(a_offsets) != len(b_offsets) or any(len(x) != len(y) for x, y in zip(a_offsets, b_offsets)):
+            raise TensorError("offset batch length mismatch")
+        count = len(a_offsets[0]) if len(a_offsets) else 0
+        if any(len(x) != count for x in a_offsets):
+            raise TensorError("every group needs the same batch length")
+        a_refs = [tuple((ab, ao + int(o)) for o in row) for row in a_offsets]
+        b_refs = [tuple((bb, bo + int(o)) for o in row) for row in b_offsets]
+        return GroupedBatch(BatchKind.OFFSET, a_refs, b_refs, count)
+
+    @staticmethod
+    def address(a_refs, b_refs) -> "GroupedBatch":
+        a = [tuple(_as_ref(r) for r in row) for row in a_refs]
+        b = [tuple(_as_ref(r) for r in row) for row in b_refs]
+        if len(a) != len(b) or any(len(x) != len(y) for x, y in zip(a, b)):
+            raise TensorError("batch length mismatch")
+        count = len(a[0]) if a else 0
+        if any(len(x) != count for x in a):
+            raise TensorError("every group needs the same batch length")
+        return GroupedBatch(BatchKind.ADDRESS, a, b, count)
+
+    @staticmethod
+    def from_batches(batches: Sequence[BrgemmBatch]) -> "GroupedBatch":
+        if not batches:
+            raise TensorError("no batches")
+        n = batches[0].n
+        if any(bt.n != n for bt in batches):
+            raise TensorError("every group needs the same batch length")
+        kinds = {bt.kind for bt in batches}
+        a0, b0 = batches[0].a_refs[0][0] if n else None, batches[0].b_refs[0][0] if n else None
+        same_bufs = n > 0 and all(r[0] is a0 for bt in batches for r in bt.a_refs) and \
+            all(r[0] is b0 for bt in batches for r in bt.b_refs)
+        if kinds == {BatchKind.STRIDE} and same_bufs and len({(bt.stride_a, bt.stride_b) for bt in batches}) == 1:
+            return GroupedBatch(BatchKind.STRIDE, [bt.a_refs for bt in batches], [bt.b_refs for bt in batches], n,
+                                batches[0].stride_a, batches[0].stride_b,
+                                [bt.a_refs[0][1] for bt in batches], [bt.b_refs[0][1] for bt in batches])
+        if same_bufs:
+            return GroupedBatch(BatchKind.OFFSET, [bt.a_refs for bt in batches], [bt.b_refs for bt in batches], n)
+        return GroupedBatch(BatchKind.ADDRESS, [bt.a_refs for bt in batches], [bt.b_refs for bt in batches], n)
+
+    def device_arrays(self, device, stream=None):
+        """(a_index, b_index) device int64 arrays for the C ABI (see
+        tpp_brgemm_grouped), built once on the issuing stream."""
+        if self._dev is None:
+            if self.kind is BatchKind.STRIDE:
+                rows = [list(self.a_goff), list(self.b_goff)]
+            elif self.kind is BatchKind.OFFSET:
+                rows = [[o for grp in self.a_refs for _, o in grp], [o for grp in self.b_refs for _, o in grp]]
+            else:
+                rows = [[buf.data_ptr() + o * buf.element_size() for grp in self.a_refs for buf, o in grp],
+                        [buf.data_ptr() + o * buf.element_size() for grp in self.b_refs for buf, o in grp]]
+            host = torch.tensor(rows, dtype=torch.int64).pin_memory()
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+            with torch.cuda.stream(s):
+                dev = torch.empty(host.shape, dtype=torch.int64, device=device)
+                dev.copy_(host, non_blocking=True)
+            ev = None
+            if not torch.cuda.is_current_stream_capturing():
+                ev = torch.cuda.Event()
+                ev.record(s)
+            self._dev = (dev[0], dev[1], host, ev)
+        a, b, _, ev = self._dev
+        if ev is not None and not torch.cuda.is_current_stream_capturing():
+            (stream if stream is not None else torch.cuda.current_stream(device)).wait_event(ev)
+        return a, b
+
+
+class _COffsets:
+    """Per-group C offsets on the device, cached per (tensor, offsets)."""
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, offs: tuple, device, stream):
+        key = (offs, str(device))
+        hit = cls._cache.get(key)
+        if hit is None:
+            host = torch.tensor(offs, dtype=torch.int64).pin_memory()
+            s = stream if stream is not None else torch.cuda.current_stream(device)
+            with torch.cuda.stream(s):
+                dev = torch.empty(len(offs), dtype=torch.int64, device=device)
+                dev.copy_(host, non_blocking=True)
+            hit = (dev, host)
+            if len(cls._cache) > 64:
+                cls._cache.clear()
+            cls._cache[key] = hit
+        return hit[0]
+
+
+def _check_grouped(spec: GemmSpec, gbatch: GroupedBatch, cbuf: torch.Tensor, c_offsets) -> None:
+    """brgemm()'s validation (contraction.py:271-290) for every group, before any launch."""
+    if len(c_offsets) != gbatch.groups:
+        raise TensorError(f"{gbatch.groups} groups but {len(c_offsets)} C offsets")
+    if len(set(int(o) for o in c_offsets)) != len(c_offsets):
+        raise TensorError("C blocks of a grouped BRGEMM must be distinct")
+    if cbuf.dtype != spec.out_dtype.storage:
+        raise TensorError(f"C dtype {cbuf.dtype} != {spec.out_dtype}")
+    for off in c_offsets:
+        _check_block(cbuf, int(off), spec.m, spec.n, spec.ldc, spec.out_dtype)
+    bufs = {id(buf): buf for grp in (*gbatch.a_refs, *gbatch.b_refs) for buf, _ in grp}
+    for buf in bufs.values():
+        if may_share_memory(cbuf, buf):
+            raise TensorError("C must not alias any batch input")
+    for grp in gbatch.a_refs:
+        for buf, off in grp:
+            if spec.a_layout is ALayout.VNNI:
+                _check_vnni_block(buf, off, spec.m, spec.k, spec.alpha, spec.in_dtype)
+            else:
+                _check_block(buf, off, spec.m, spec.k, spec.lda, spec.in_dtype)
+    for grp in gbatch.b_refs:
+        for buf, off in grp:
+            _check_block(buf, off, spec.k, spec.n, spec.ldb, spec.in_dtype)
+
+
+def brgemm_grouped(spec: GemmSpec, gbatch: GroupedBatch, c, c_offsets: Sequence[int], stream=None) -> None:
+    """For every group g: C_g = beta*C_g + sum_i A_{g,i} B_{g,i}, where C_g is
+    the m x n (ldc) FP32 block at element offset c_offsets[g] of ``c`` —
+    exactly ``brgemm(spec, batch_g, C_g)`` for each g (contraction.py:261-322),
+    in ONE tcgen05 launch for aligned BF16 batches.  Other dtypes / layouts
+    (and Engine.ORDERED) run one ordered brgemm call per group.  C blocks
+    must be disjoint and must not alias any input block."""
+    cbuf = c.primary if isinstance(c, TensorView) else c
+    key = (spec, cbuf.data_ptr(), cbuf.numel(), cbuf.dtype, tuple(int(o) for o in c_offsets))
+    if key not in gbatch._checked:
+        _check_grouped(spec, gbatch, cbuf, c_offsets)
+        gbatch._checked.add(key)
+    if not cbuf.is_cuda:
+        raise _lib.TppUnavailableError("brgemm_grouped: C must live in CUDA memory")
+    if gbatch.groups == 0:
+        return
+    ekey = ("tc", spec)
+    if ekey not in gbatch._checked and ("no-tc", spec) not in gbatch._checked:
+        flat_a = [r for grp in gbatch.a_refs for r in grp]
+        flat_b = [r for grp in gbatch.b_refs for r in grp]
+        gbatch._checked.add(ekey if _tensor_eligible(spec, flat_a, flat_b) else ("no-tc", spec))
+    use_tc = spec.engine is not Engine.ORDERED and ekey in gbatch._checked
+    if not use_tc:
+        if spec.engine is Engine.TENSOR:
+            raise NotImplementedError("grouped tensor-core BRGEMM: BF16, count >= 1, m, k, ldb (lda) multiples "
+                                      "of 8, 16-byte aligned blocks")
+        for g in range(gbatch.groups):
+            cv = TensorView(TensorDesc(spec.m, spec.n, spec.ldc, spec.out_dtype), cbuf[int(c_offsets[g]):])
+            bt = BrgemmBatch(gbatch.kind, gbatch.a_refs[g], gbatch.b_refs[g], gbatch.stride_a, gbatch.stride_b)
+            brgemm(spec, bt, cv, stream=stream)
+        return
+    lib = _lib.load()
+    d = spec.c()
+    d.engine = _lib.ENGINE_TENSOR
+    dev = cbuf.device
+    ai, bi = gbatch.device_arrays(dev, stream)
+    coff = _COffsets.get(tuple(int(o) for o in c_offsets), dev, stream)
+    kind = {BatchKind.STRIDE: 0, BatchKind.OFFSET: 1, BatchKind.ADDRESS: 2}[gbatch.kind]
+    if kind == 2:
+        a_ptr = b_ptr = 0
+    else:
+        (abuf, _), (bbuf, _) = gbatch.a_refs[0][0], gbatch.b_refs[0][0]
+        a_ptr, b_ptr = abuf.data_ptr(), bbuf.data_ptr()
+    rc = lib.tpp_brgemm_grouped(C.byref(d), kind, a_ptr, b_ptr, gbatch.stride_a, gbatch.stride_b,
+                                ai.data_ptr(), bi.data_ptr(), gbatch.count, cbuf.data_ptr(), coff.data_ptr(),
+                                gbatch.groups, _lib.stream_ptr(stream))
+    _lib.check(rc, "brgemm_grouped")
 
 
 def gemm(spec: GemmSpec, a, b, c: TensorView, blocking: BlockingParams | None = None,

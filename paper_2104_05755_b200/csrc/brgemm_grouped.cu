@@ -1,0 +1,474 @@
+// K11: the BRGEMM TPP itself on tcgen05 — brgemm() over STRIDE / OFFSET /
+// ADDRESS batches of arbitrary (aligned) BF16 blocks, many C blocks per launch.
+//
+// Reference semantics (contraction.py:261-322): for every group g (one C
+// block; a single brgemm() call is one group)
+//     C_g = beta * C_g + sum_i A_{g,i} x B_{g,i}
+// with A_{g,i} an m x k block (PLAIN column-major with lda, or VNNI-2
+// [ceil(k/2)][m][2], contraction.py:238-247), B_{g,i} a k x n column-major
+// block (ldb), C an m x n FP32 column-major block (ldc).  The blocks live at
+// arbitrary (16-byte aligned) addresses — the batch is an address / offset /
+// stride list, not a tensor — so operands cannot come through a TMA tensor
+// map.  Instead 4 producer warps move each (entry i, 64-deep k chunk) stage
+// from global memory straight into the UMMA-canonical 128B-swizzled smem
+// layouts:
+//   B        K-major (k contiguous per column): 16-byte cp.async per chunk
+//   A PLAIN  MN-major (m contiguous per k):     16-byte cp.async per chunk
+//   A VNNI   K-major: a 32-bit word transpose in registers — 4 x 16-byte
+//            loads of (4 k-pairs x 4 rows) become 4 x 16-byte row chunks
+// (zero fill past m, n, k), several stages in flight (cp.async groups + a
+// one-stage register lookahead for VNNI), then fence.proxy.async and an
+// mbarrier arrive hand the stage to the MMA warp.  The MMA warp issues
+// tcgen05.mma kind::f16 (M = 64 when the C block has <= 64 rows, else 128;
+// N = 64/128/256) into a double-buffered TMEM accumulator — the whole batch
+// of a tile accumulates on chip — and 4 epilogue warps apply beta and store
+// FP32 C (coalesced: a warp writes 32 consecutive rows of a column).
+//
+// Persistent CTAs walk work items (group, row tile, column tile).
+
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace tpp {
+using namespace sm100;
+namespace grp {
+
+constexpr int kEpiWarps = 4;    // warps 0-3: epilogue (TMEM lane quarter = warp)
+constexpr int kProdWarp0 = 4;   // warps 4-7: producers
+constexpr int kProd = 128;
+constexpr int kMmaWarp = 8;     // MMA issue + TMEM allocation
+constexpr int kThreads = 32 * 9;
+constexpr int kLag = 2;         // cp.async groups in flight per producer thread
+
+struct GParams {
+  int m, n, k, lda, ldb, ldc;
+  int vnni;         // A layout: 0 PLAIN, 1 VNNI-2
+  int kind;         // 0 STRIDE, 1 OFFSET, 2 ADDRESS
+  const uint16_t* a;
+  const uint16_t* b;
+  long long stride_a, stride_b;
+  const long long* a_idx;  // STRIDE: per-group offsets [groups] (or null); OFFSET: [groups*count]; ADDRESS: pointers
+  const long long* b_idx;
+  long long count;
+  float* c;
+  const long long* c_off;  // per-group C offsets (elements) or null (one group)
+  long long groups;
+  int tiles_m, tiles_n, kchunks;
+  int dims_ok;      // m, k, ldb (lda for PLAIN A) multiples of 8: 16-byte chunks never straddle an edge
+  float beta;
+  int beta_mode;    // 0: beta == 0, 1: beta == 1, 2: general
+};
+
+template <int BM, int BN, int STAGES>
+struct GSmem {
+  static constexpr int A_BYTES = BM * 128;  // BM rows x 64 k (bf16)
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ uint4 ldg_nc16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ const uint16_t* op_ptr(int kind, const uint16_t* base, const long long* idx,
+                                                  long long stride, long long count, long long g, long long i) {
+  if (kind == 0) return base + (idx ? idx[g] : 0) + i * stride;
+  if (kind == 1) return base + idx[g * count + i];
+  return reinterpret_cast<const uint16_t*>(idx[g * count + i]);
+}
+
+// the producer's walk over (work item, batch entry, k chunk)
+struct StageIt {
+  long long tile, i;
+  int kc;
+};
+
+template <int BM, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GParams p) {
+  using S = GSmem<BM, BN, STAGES>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const long long ntiles = p.groups * p.tiles_m * p.tiles_n;
+  const long long per_tile = p.count * p.kchunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kProd);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  if (warp >= kProdWarp0 && warp < kProdWarp0 + 4) {
+    // ============================ producers ============================
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int t = threadIdx.x - kProdWarp0 * 32;
+    constexpr int AU = BM * 2 / kProd;  // VNNI units (4 k-pairs x 4 rows) per thread: 8 * BM/4 / 128
+    auto tile_coords = [&](long long tile, long long& g, int& tm, int& tn) {
+      const long long per_g = (long long)p.tiles_m * p.tiles_n;
+      g = tile / per_g;
+      const int rem = (int)(tile - g * per_g);
+      tm = rem / p.tiles_n;
+      tn = rem - tm * p.tiles_n;
+    };
+    auto advance = [&](StageIt& s) {
+      if (++s.kc == p.kchunks) {
+        s.kc = 0;
+        if (++s.i == p.count) {
+          s.i = 0;
+          s.tile += gridDim.x;
+        }
+      }
+    };
+    // A stage takes the fast path (16-byte cp.async / vector loads) when the
+    // problem's extents and strides are multiples of 8 elements and both
+    // block addresses are 16-byte aligned; otherwise every 16-byte smem chunk
+    // is assembled from 2-byte loads (any shape, any alignment).
+    auto stage_ptrs = [&](const StageIt& st, long long& g, int& tm, int& tn, const uint16_t*& ap,
+                          const uint16_t*& bp) -> bool {
+      tile_coords(st.tile, g, tm, tn);
+      ap = op_ptr(p.kind, p.a, p.a_idx, p.stride_a, p.count, g, st.i);
+      bp = op_ptr(p.kind, p.b, p.b_idx, p.stride_b, p.count, g, st.i);
+      return p.dims_ok && ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(bp)) & 15) == 0;
+    };
+    // VNNI A: (k-pair quad pq, row quad mq) units; 4 x 16 B loads = words (p, m..m+3) for 4 k-pairs
+    auto load_vnni = [&](const StageIt& st, uint4 (&r)[AU][4]) {
+      long long g;
+      int tm, tn;
+      const uint16_t *ap, *bp;
+      if (!stage_ptrs(st, g, tm, tn, ap, bp)) return;  // generic stage: assembled at store time
+#pragma unroll
+      for (int u = 0; u < AU; ++u) {
+        const int unit = t + u * kProd;
+        const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+        const int mrow = tm * BM + mq * 4;
+        const int k0 = st.kc * 64 + pq * 8;
+        const bool ok = mrow < p.m && k0 < p.k;
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+          const long long pr = (long long)(k0 >> 1) + pp;
+          r[u][pp] = ok ? ldg_nc16(ap + pr * 2 * p.m + 2 * mrow) : make_uint4(0, 0, 0, 0);
+        }
+      }
+    };
+    auto store_vnni = [&](uint32_t sA, const uint4 (&r)[AU][4]) {
+#pragma unroll
+      for (int u = 0; u < AU; ++u) {
+        const int unit = t + u * kProd;
+        const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+          const int row = mq * 4 + mm;
+          const uint32_t w0 = mm == 0 ? r[u][0].x : mm == 1 ? r[u][0].y : mm == 2 ? r[u][0].z : r[u][0].w;
+          const uint32_t w1 = mm == 0 ? r[u][1].x : mm == 1 ? r[u][1].y : mm == 2 ? r[u][1].z : r[u][1].w;
+          const uint32_t w2 = mm == 0 ? r[u][2].x : mm == 1 ? r[u][2].y : mm == 2 ? r[u][2].z : r[u][2].w;
+          const uint32_t w3 = mm == 0 ? r[u][3].x : mm == 1 ? r[u][3].y : mm == 2 ? r[u][3].z : r[u][3].w;
+          sts16(sA + (row >> 3) * 1024 + (row & 7) * 128 + ((pq ^ (row & 7)) << 4), make_uint4(w0, w1, w2, w3));
+        }
+      }
+    };
+    auto ld16 = [](const uint16_t* q) -> uint32_t {
+      unsigned short v;
+      asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(q));
+      return v;
+    };
+    // fast path: cp.async for B (K-major) and PLAIN A (MN-major)
+    auto issue_fast = [&](int tm, int tn, int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA,
+                          uint32_t sB) {
+      const int kb = kc * 64;
+      for (int c = t; c < BN * 8; c += kProd) {
+        const int r = c >> 3, q = c & 7;
+        const int nn = tn * BN + r, kk = kb + q * 8;
+        const bool ok = nn < p.n && kk < p.k;
+        cp_async16(sB + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4),
+                   ok ? (const void*)(bp + (long long)nn * p.ldb + kk) : (const void*)bp, ok ? 16 : 0);
+      }
+      if (!p.vnni) {
+        constexpr int CPR = BM / 8;  // 16-byte chunks per k row
+        for (int c = t; c < 64 * CPR; c += kProd) {
+          const int kk = c / CPR, ch = c % CPR;
+          const int j = ch >> 3, cc = ch & 7;
+          const int mrow = tm * BM + ch * 8, kg = kb + kk;
+          const bool ok = mrow < p.m && kg < p.k;
+          cp_async16(sA + j * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((cc ^ (kk & 7)) << 4),
+                     ok ? (const void*)(ap + mrow + (long long)kg * p.lda) : (const void*)ap, ok ? 16 : 0);
+        }
+      }
+    };
+    // generic path: every chunk from 2-byte loads, bounds per element
+    auto issue_generic = [&](int tm, int tn, int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA,
+                             uint32_t sB) {
+      const int kb = kc * 64;
+      for (int c = t; c < BN * 8; c += kProd) {  // B: column nn, k = kk .. kk+7
+        const int r = c >> 3, q = c & 7;
+        const int nn = tn * BN + r, kk = kb + q * 8;
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (nn < p.n) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (kk + e < p.k) w[e >> 1] |= ld16(bp + (long long)nn * p.ldb + kk + e) << (16 * (e & 1));
+        }
+        sts16(sB + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+      }
+      if (!p.vnni) {  // A PLAIN, MN-major chunks: 8 rows at one k
+        constexpr int CPR = BM / 8;
+        for (int c = t; c < 64 * CPR; c += kProd) {
+          const int kk = c / CPR, ch = c % CPR;
+          const int j = ch >> 3, cc = ch & 7;
+          const int mrow = tm * BM + ch * 8, kg = kb + kk;
+          uint32_t w[4] = {0, 0, 0, 0};
+          if (kg < p.k) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (mrow + e < p.m) w[e >> 1] |= ld16(ap + mrow + e + (long long)kg * p.lda) << (16 * (e & 1));
+          }
+          sts16(sA + j * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((cc ^ (kk & 7)) << 4),
+                make_uint4(w[0], w[1], w[2], w[3]));
+        }
+      } else {  // A VNNI, K-major chunks: one row at 8 k
+        for (int c = t; c < BM * 8; c += kProd) {
+          const int r = c >> 3, q = c & 7;
+          const int mrow = tm * BM + r, kk = kb + q * 8;
+          uint32_t w[4] = {0, 0, 0, 0};
+          if (mrow < p.m) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int ke = kk + e;
+              if (ke < p.k) w[e >> 1] |= ld16(ap + (long long)(ke >> 1) * 2 * p.m + 2 * mrow + (ke & 1)) << (16 * (e & 1));
+            }
+          }
+          sts16(sA + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
+        }
+      }
+    };
+    StageIt cur{blockIdx.x, 0, 0};
+    StageIt pre = cur;
+    uint4 ra[AU][4], rb[AU][4];
+    if (p.vnni && pre.tile < ntiles) {
+      load_vnni(pre, ra);
+      advance(pre);
+    }
+    uint32_t it = 0;
+    auto one = [&](uint4 (&mine)[AU][4], uint4 (&next)[AU][4]) -> bool {
+      if (cur.tile >= ntiles) return false;
+      const int s = it % STAGES;
+      const uint32_t ph = (it / STAGES) & 1;
+      if (p.vnni && pre.tile < ntiles) {  // one stage of register lookahead
+        load_vnni(pre, next);
+        advance(pre);
+      }
+      long long g;
+      int tm, tn;
+      const uint16_t *ap, *bp;
+      const bool fast = stage_ptrs(cur, g, tm, tn, ap, bp);
+      mbar_wait(&empty[s], ph ^ 1);
+      const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
+      if (fast) {
+        issue_fast(tm, tn, cur.kc, ap, bp, sA, sB);
+        if (p.vnni) store_vnni(sA, mine);
+      } else {
+        issue_generic(tm, tn, cur.kc, ap, bp, sA, sB);
+      }
+      cp_async_commit();
+      if (it >= (uint32_t)kLag) {
+        cp_async_wait<kLag>();
+        fence_async_smem();
+        mbar_arrive(&full[(it - kLag) % STAGES]);
+      }
+      advance(cur);
+      ++it;
+      return true;
+    };
+    while (one(ra, rb) && one(rb, ra)) {
+    }
+    cp_async_wait<0>();
+    fence_async_smem();
+    for (uint32_t j = it > (uint32_t)kLag ? it - kLag : 0; j < it; ++j) mbar_arrive(&full[j % STAGES]);
+  } else if (warp == kMmaWarp) {
+    // ============================ MMA issue ============================
+    const uint32_t idesc = idesc_bf16_f32(BM, BN, p.vnni ? 0 : 1, 0);
+    const uint64_t a0 = p.vnni ? sw128_kmajor_desc(smem_u32(smem)) : sw128_mnmajor_desc(smem_u32(smem), 8192);
+    const uint64_t b0 = sw128_kmajor_desc(smem_u32(smem + S::A_BYTES));
+    const uint32_t astep = p.vnni ? (32 >> 4) : (2048 >> 4);
+    uint32_t it = 0, tcount = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+      mbar_wait(&tempty[as], aph ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + as * BN;
+      for (long long j = 0; j < per_tile; ++j, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint64_t soff = (uint64_t)((s * S::STAGE) >> 4);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16_warp(tmem_d, a0 + soff + astep * kk, b0 + soff + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit_warp(&empty[s]);
+      }
+      umma_commit_warp(&tfull[as]);
+    }
+  } else if (warp < kEpiWarps) {
+    // ============================ epilogue ============================
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int q = warp;
+    // accumulator row of this lane: M = 128 -> lane q*32 + l; M = 64 -> the
+    // 64 rows sit in lanes 0-15 of each 32-lane quarter
+    const int lrow = BM == 128 ? q * 32 + lane : q * 16 + lane;
+    const bool lane_ok = BM == 128 || lane < 16;
+    uint32_t tcount = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const long long per_g = (long long)p.tiles_m * p.tiles_n;
+      const long long g = tile / per_g;
+      const int rem = (int)(tile - g * per_g);
+      const int tm = rem / p.tiles_n, tn = rem - tm * p.tiles_n;
+      float* cg = p.c + (p.c_off ? p.c_off[g] : 0);
+      const int row = tm * BM + lrow;
+      const bool row_ok = lane_ok && row < p.m;
+      const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
+      uint32_t v[32];
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        tmem_ld32(tacc + ch * 32, v);
+        tmem_ld_wait();
+        if (ch == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[as]);
+        }
+        const int col0 = tn * BN + ch * 32;
+        if (row_ok) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = col0 + i;
+            if (col < p.n) {
+              float* dst = cg + row + (long long)col * p.ldc;
+              const float acc = __uint_as_float(v[i]);
+              *dst = p.beta_mode == 0 ? acc : p.beta_mode == 1 ? __fadd_rn(*dst, acc)
+                                                               : __fadd_rn(__fmul_rn(*dst, p.beta), acc);
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, S::TMEM_COLS);
+  }
+}
+
+template <int BM, int BN, int STAGES>
+static int launch(const GParams& p, cudaStream_t s) {
+  using S = GSmem<BM, BN, STAGES>;
+  static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
+  auto kern = brgemm_grouped_kernel<BM, BN, STAGES>;
+  cudaError_t e = ensure_smem_attr((const void*)kern, S::BYTES);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_grouped_kernel)");
+  const long long ntiles = p.groups * p.tiles_m * p.tiles_n;
+  const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_grouped_kernel)");
+  TPP_CUDA_LAUNCH_CHECK("brgemm_grouped_kernel");
+  set_last_config("brgemm_grouped_kernel<" + std::to_string(BM) + "," + std::to_string(BN) + "," +
+                  std::to_string(STAGES) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(ntiles));
+  return TPP_OK;
+}
+
+}  // namespace grp
+
+// 1 = not applicable (caller falls back to the ordered engine), else a status
+int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const void* b, int64_t stride_a,
+                      int64_t stride_b, const int64_t* a_idx, const int64_t* b_idx, int64_t count, void* c,
+                      const int64_t* c_off, int64_t groups, cudaStream_t s) {
+  using namespace grp;
+  if (d->in_dtype != TPP_BF16 || count < 1 || groups < 1) return 1;
+  GParams p{};
+  // fast-path shape condition; block alignment is checked per stage in the kernel
+  p.dims_ok = !(d->k % 8 || d->m % 8 || d->ldb % 8 || (!d->a_vnni && d->lda % 8));
+  p.m = d->m; p.n = d->n; p.k = d->k;
+  p.lda = d->lda; p.ldb = d->ldb; p.ldc = d->ldc;
+  p.vnni = d->a_vnni;
+  p.kind = kind;
+  p.a = reinterpret_cast<const uint16_t*>(a);
+  p.b = reinterpret_cast<const uint16_t*>(b);
+  p.stride_a = stride_a; p.stride_b = stride_b;
+  p.a_idx = reinterpret_cast<const long long*>(a_idx);
+  p.b_idx = reinterpret_cast<const long long*>(b_idx);
+  p.count = count;
+  p.c = reinterpret_cast<float*>(c);
+  p.c_off = reinterpret_cast<const long long*>(c_off);
+  p.groups = groups;
+  p.kchunks = (d->k + 63) / 64;
+  p.beta = (float)d->beta;
+  p.beta_mode = d->beta == 0.0 ? 0 : d->beta == 1.0 ? 1 : 2;
+  const int BM = d->m <= 64 ? 64 : 128;
+  const int BN = d->n <= 64 ? 64 : d->n <= 128 ? 128 : 256;
+  p.tiles_m = (d->m + BM - 1) / BM;
+  p.tiles_n = (d->n + BN - 1) / BN;
+  if (BM == 64) {
+    if (BN == 64) return launch<64, 64, 8>(p, s);
+    if (BN == 128) return launch<64, 128, 6>(p, s);
+    return launch<64, 256, 4>(p, s);
+  }
+  if (BN == 64) return launch<128, 64, 6>(p, s);
+  if (BN == 128) return launch<128, 128, 5>(p, s);
+  return launch<128, 256, 4>(p, s);
+}
+
+}  // namespace tpp

@@ -50,8 +50,8 @@ static int check_gemm(const tpp_gemm_desc* d) {
               "EMULATED_SPLIT applies to BF16 inputs");
   TPP_REQUIRE(!d->a_vnni || d->in_dtype == TPP_BF16 || d->in_dtype == TPP_INT8, TPP_E_TENSOR,
               "VNNI A layout needs a 16- or 8-bit input dtype");
-  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR || d->in_dtype == TPP_INT8, TPP_E_UNSUPPORTED,
-              "single-BRGEMM tensor-core engine is INT8-only: use the FC / conv layer entry points");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR || d->in_dtype == TPP_INT8 || d->in_dtype == TPP_BF16,
+              TPP_E_UNSUPPORTED, "the tensor-core engine serves BF16 and INT8 inputs (FP32/FP64: ordered engine)");
   return TPP_OK;
 }
 
@@ -111,6 +111,13 @@ int tpp_brgemm_stride(const tpp_gemm_desc* d, const void* a, const void* b, int6
     TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED,
                 "INT8 tensor engine: plain A and 16-byte aligned pointers / lda / ldb / strides");
   }
+  // BF16: the tcgen05 BRGEMM (AUTO and TENSOR); ORDERED keeps the reference order
+  if (d->in_dtype == TPP_BF16 && d->engine != TPP_ENGINE_ORDERED) {
+    const int r = brgemm_grouped_tc(d, 0, a, b, stride_a, stride_b, nullptr, nullptr, count, c, nullptr, 1,
+                                    as_stream(stream));
+    if (r != 1) return r;
+    TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "BF16 tensor engine: needs count >= 1");
+  }
   OrderedParams p = base_params(d, c);
   p.mode = 0;
   p.count = count;
@@ -128,7 +135,14 @@ int tpp_brgemm_offset(const tpp_gemm_desc* d, const void* a, const void* b,
   if (rc) return rc;
   TPP_REQUIRE(count >= 0, TPP_E_TENSOR, "negative batch count");
   TPP_REQUIRE(count == 0 || (a_offsets && b_offsets), TPP_E_TENSOR, "null offset arrays");
-  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "INT8 tensor engine serves STRIDE batches");
+  // BF16 (AUTO / TENSOR): the tcgen05 BRGEMM (misaligned blocks take its
+  // element-wise staging path, checked per stage on the device)
+  if (d->engine != TPP_ENGINE_ORDERED && d->in_dtype == TPP_BF16) {
+    const int r = brgemm_grouped_tc(d, 1, a, b, 0, 0, a_offsets, b_offsets, count, c, nullptr, 1, as_stream(stream));
+    if (r != 1) return r;
+    TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "BF16 tensor engine: needs count >= 1");
+  }
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "tensor engine for OFFSET batches: BF16 inputs");
   OrderedParams p = base_params(d, c);
   p.mode = 1;
   p.count = count;
@@ -145,13 +159,37 @@ int tpp_brgemm_address(const tpp_gemm_desc* d, const void* const* a_ptrs,
   if (rc) return rc;
   TPP_REQUIRE(count >= 0, TPP_E_TENSOR, "negative batch count");
   TPP_REQUIRE(count == 0 || (a_ptrs && b_ptrs), TPP_E_TENSOR, "null pointer arrays");
-  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "INT8 tensor engine serves STRIDE batches");
+  if (d->engine != TPP_ENGINE_ORDERED && d->in_dtype == TPP_BF16) {  // as tpp_brgemm_offset
+    const int r = brgemm_grouped_tc(d, 2, nullptr, nullptr, 0, 0, reinterpret_cast<const int64_t*>(a_ptrs),
+                                    reinterpret_cast<const int64_t*>(b_ptrs), count, c, nullptr, 1, as_stream(stream));
+    if (r != 1) return r;
+    TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "BF16 tensor engine: needs count >= 1");
+  }
+  TPP_REQUIRE(d->engine != TPP_ENGINE_TENSOR, TPP_E_UNSUPPORTED, "tensor engine for ADDRESS batches: BF16 inputs");
   OrderedParams p = base_params(d, c);
   p.mode = 2;
   p.count = count;
   p.a_ptrs = a_ptrs;
   p.b_ptrs = b_ptrs;
   return launch_brgemm_ordered(p, d->in_dtype, as_stream(stream));
+}
+
+int tpp_brgemm_grouped(const tpp_gemm_desc* d, int32_t kind, const void* a, const void* b, int64_t stride_a,
+                       int64_t stride_b, const int64_t* a_index, const int64_t* b_index, int64_t count, void* c,
+                       const int64_t* c_offsets, int64_t groups, void* stream) {
+  int rc = check_gemm(d);
+  if (rc) return rc;
+  TPP_REQUIRE(kind >= 0 && kind <= 2, TPP_E_TENSOR, "batch kind must be 0 STRIDE, 1 OFFSET or 2 ADDRESS");
+  TPP_REQUIRE(count >= 1 && groups >= 0, TPP_E_TENSOR, "grouped BRGEMM needs count >= 1");
+  TPP_REQUIRE(groups <= 1 || c_offsets, TPP_E_TENSOR, "several groups need per-group C offsets");
+  TPP_REQUIRE(kind == 0 || (a_index && b_index), TPP_E_TENSOR, "null offset / pointer arrays");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_ORDERED && d->in_dtype == TPP_BF16, TPP_E_UNSUPPORTED,
+              "grouped BRGEMM runs the BF16 tensor-core engine (other dtypes: one brgemm call per group)");
+  if (groups == 0) return TPP_OK;
+  const int r = brgemm_grouped_tc(d, kind, a, b, stride_a, stride_b, a_index, b_index, count, c, c_offsets, groups,
+                                  as_stream(stream));
+  if (r != 1) return r;
+  return fail(TPP_E_UNSUPPORTED, "grouped BRGEMM: BF16 inputs and count >= 1");
 }
 
 int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void* b,

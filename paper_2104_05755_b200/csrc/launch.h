@@ -55,6 +55,11 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
                void* mask_out, const void* mask_in, cudaStream_t stream);
 void set_debug_timestamps(unsigned long long* p);
 unsigned long long* debug_timestamps();
+// brgemm_grouped.cu (K11): BF16 BRGEMM on tcgen05 over stride / offset /
+// address batches, `groups` C blocks per launch; 1 = not applicable
+int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const void* b, int64_t stride_a,
+                      int64_t stride_b, const int64_t* a_idx, const int64_t* b_idx, int64_t count, void* c,
+                      const int64_t* c_off, int64_t groups, cudaStream_t s);
 // brgemm_i8.cu (K10): INT8 STRIDE BRGEMM on tcgen05 kind::i8; 1 = not applicable
 int brgemm_i8_stride_tc(int m, int n, int k, const int8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
                         int64_t stride_a, int64_t stride_b, int64_t count, int32_t* c, int64_t ldc, double beta,

@@ -1,0 +1,233 @@
+"""The BRGEMM TPP itself on tcgen05 (K11, brgemm_grouped.cu) through the
+reference API: brgemm() / gemm() / matmul() with BF16 inputs under
+Engine.AUTO / TENSOR for all three addressing variants, and brgemm_grouped()
+(many C blocks per launch).  Tolerance: normwise <= 2e-2 of the reference
+(north_star BF16 rule; the tensor core sums a tile's whole batch in one FP32
+accumulator, the reference sums per entry then across entries,
+contraction.py:295-315).  Every test asserts via tpp_last_config() that the
+tensor-core kernel ran."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tpp_oracle as O
+
+from gpu_util import bf16_bits_to_f32, normwise, to_dev, to_host, vnni_weights
+
+pytestmark = pytest.mark.gpu
+tpp = pytest.importorskip("paper_2104_05755_b200")
+from paper_2104_05755_b200 import _lib  # noqa: E402
+
+TOL = 2e-2
+GROUPED = "brgemm_grouped_kernel<"
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+    torch.cuda.synchronize()
+
+
+def _batch(variant, abuf, bbuf, sa, sb, cnt, a0=0, b0=0):
+    if variant == "stride":
+        return tpp.BrgemmBatch.stride((abuf, a0), (bbuf, b0), sa, sb, cnt)
+    if variant == "offset":
+        return tpp.BrgemmBatch.offset(abuf, bbuf, [a0 + j * sa for j in range(cnt)], [b0 + j * sb for j in range(cnt)])
+    return tpp.BrgemmBatch.address([(abuf, a0 + j * sa) for j in range(cnt)], [(bbuf, b0 + j * sb) for j in range(cnt)])
+
+
+@pytest.mark.parametrize("variant", ["stride", "offset", "address"])
+def test_golden_bf16_cases_on_tensor_cores(golden, variant):
+    """The reference-generated BF16 cases (odd shapes, lds, VNNI tails, every
+    beta): the tensor engine's element-wise staging path."""
+    g = golden("brgemm_cases.npz")
+    ran = 0
+    for i in range(int(g["count"])):
+        key = f"case{i:03d}"
+        if str(g[key + "_dtype"]) != "bf16":
+            continue
+        m, n, k, lda, ldb, ldc, cnt, sa, sb, vnni = (int(v) for v in g[key + "_meta"])
+        abuf, bbuf = to_dev(g[key + "_a"]), to_dev(g[key + "_b"])
+        c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32), to_dev(g[key + "_c0"]))
+        eng = tpp.Engine.TENSOR if cnt > 0 else tpp.Engine.AUTO   # an empty batch has no GEMM
+        spec = tpp.GemmSpec(m, n, k, lda, ldb, ldc, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                            beta=float(g[key + "_beta"]), engine=eng,
+                            a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN)
+        tpp.brgemm(spec, _batch(variant, abuf, bbuf, sa, sb, cnt), c)
+        got = to_host(c.primary).reshape(-1, ldc)[:n, :m]
+        want = g[key + "_c"].reshape(-1, ldc)[:n, :m]
+        if cnt > 0:
+            assert _lib.last_config().startswith(GROUPED), _lib.last_config()
+            ran += 1
+        assert normwise(got, want) <= TOL, (i, variant)
+    assert ran >= 8
+
+
+def test_conv_offset_fixture_grouped_and_single(golden):
+    """The reference's offset-BRGEMM 3x3 conv fixture (tests/golden/conv.npz,
+    made by the unmodified reference): every output row one OFFSET batch of
+    R*S*Cb taps -- as single brgemm() calls and as ONE grouped launch."""
+    g = golden("conv.npz")
+    x, wv, want = g["x"], g["w"], g["out"]
+    N, Cb, H, W, bc = x.shape
+    Kb, _, R, S, _, bk, _ = wv.shape
+    Hp, Wp = H + 2, W + 2
+    xp = np.zeros((N, Cb, Hp, Wp, bc), np.uint16)
+    xp[:, :, 1:-1, 1:-1] = x
+    xd, wd = to_dev(xp), to_dev(wv)
+    spec = tpp.GemmSpec(bk, W, bc, bk, bc, bk, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                        a_layout=tpp.ALayout.VNNI, engine=tpp.Engine.TENSOR)
+    a_rows, b_rows, c_offs = [], [], []
+    out = torch.zeros(N * Kb * H * W * bk, dtype=torch.float32, device="cuda")
+    single = torch.zeros_like(out)
+    for n in range(N):
+        for kb in range(Kb):
+            for oh in range(H):
+                ao = [(((kb * Cb + cb) * R + r) * S + s) * bc * bk for r in range(R) for s in range(S) for cb in range(Cb)]
+                bo = [(((n * Cb + cb) * Hp + oh + r) * Wp + s) * bc for r in range(R) for s in range(S) for cb in range(Cb)]
+                co = ((n * Kb + kb) * H + oh) * W * bk
+                a_rows.append(ao)
+                b_rows.append(bo)
+                c_offs.append(co)
+                cv = tpp.TensorView(tpp.TensorDesc(bk, W, bk, tpp.DType.FP32), single[co:])
+                tpp.brgemm(spec, tpp.BrgemmBatch.offset(wd, xd, ao, bo), cv)
+                assert _lib.last_config().startswith(GROUPED)
+    tpp.brgemm_grouped(spec, tpp.GroupedBatch.offset(wd, xd, a_rows, b_rows), out, c_offs)
+    assert _lib.last_config().startswith(GROUPED) and f"tiles={N * Kb * H}" in _lib.last_config()
+    for res in (out, single):
+        got = to_host(res).reshape(N, Kb, H, W, bk)
+        assert normwise(got, O.bf16_to_fp32(want)) <= TOL
+        assert np.mean(O.fp32_to_bf16_rne(got) == want) > 0.95
+    assert torch.equal(out, single)   # same kernel, same per-tile order
+
+
+@pytest.mark.parametrize("variant", ["stride", "offset", "address"])
+def test_cfg2_composition_grouped(variant):
+    """BASELINE cfg 2 composed from the BRGEMM TPP the way the reference's
+    fc_forward does (kernels.py:312-329): 256 C blocks (token block nb x
+    feature block kb), each a 16-entry batch of VNNI weight blocks x input
+    blocks -- one grouped tcgen05 launch."""
+    rng = np.random.default_rng(90)
+    Nb, Cb, bn, bc, Kb, bk = 16, 16, 64, 64, 16, 64
+    x = O.fp32_to_bf16_rne(rng.normal(0, 1, (Nb, Cb, bn, bc)).astype(np.float32))
+    wv = vnni_weights(rng, Kb, Cb, bk, bc, 0.05)
+    xd, wd = to_dev(x), to_dev(wv)
+    blk = bc * bk
+    spec = tpp.GemmSpec(bk, bn, bc, bk, bc, bk, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                        a_layout=tpp.ALayout.VNNI)
+    groups = [(nb, kb) for nb in range(Nb) for kb in range(Kb)]
+    if variant == "stride":
+        gb = tpp.GroupedBatch.stride(wd, xd, blk, blk, Cb, [kb * Cb * blk for _, kb in groups],
+                                     [nb * Cb * blk for nb, _ in groups])
+    elif variant == "offset":
+        gb = tpp.GroupedBatch.offset(wd, xd, [[(kb * Cb + i) * blk for i in range(Cb)] for _, kb in groups],
+                                     [[(nb * Cb + i) * blk for i in range(Cb)] for nb, _ in groups])
+    else:
+        gb = tpp.GroupedBatch.address([[(wd, (kb * Cb + i) * blk) for i in range(Cb)] for _, kb in groups],
+                                      [[(xd, (nb * Cb + i) * blk) for i in range(Cb)] for nb, _ in groups])
+    out = torch.empty(Nb * Kb * bn * bk, dtype=torch.float32, device="cuda")
+    tpp.brgemm_grouped(spec, gb, out, [(nb * Kb + kb) * bn * bk for nb, kb in groups])
+    assert _lib.last_config().startswith("brgemm_grouped_kernel<64,64,"), _lib.last_config()
+    sel = [0, 7, 15]
+    _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)   # FP32 pre-narrow
+    got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
+    assert normwise(got, want) <= TOL
+
+
+@pytest.mark.parametrize("beta", [0.0, 1.0, 0.5])
+def test_plain_a_multi_tile_vs_fp64(beta):
+    """PLAIN (MN-major) A over several 128 x 256 tiles, ragged edges, padded
+    lds, 3 entries, 16-byte staging path."""
+    rng = np.random.default_rng(91)
+    m, n, k, cnt = 200, 300, 136, 3
+    lda, ldb, ldc = 208, 144, 200
+    sa, sb = lda * k, ldb * n
+    a = O.fp32_to_bf16_rne(rng.standard_normal(sa * cnt).astype(np.float32))
+    b = O.fp32_to_bf16_rne(rng.standard_normal(sb * cnt).astype(np.float32))
+    c0 = rng.standard_normal(ldc * n).astype(np.float32)
+    spec = tpp.GemmSpec(m, n, k, lda, ldb, ldc, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32, beta=beta,
+                        engine=tpp.Engine.TENSOR)
+    c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32), torch.from_numpy(c0.copy()).cuda())
+    tpp.brgemm(spec, tpp.BrgemmBatch.stride(to_dev(a), to_dev(b), sa, sb, cnt), c)
+    assert _lib.last_config().startswith("brgemm_grouped_kernel<128,256,"), _lib.last_config()
+    af, bf = O.bf16_to_fp32(a).astype(np.float64), O.bf16_to_fp32(b).astype(np.float64)
+    ref = beta * c0.reshape(n, ldc)[:, :m].T.astype(np.float64)
+    for i in range(cnt):
+        A = af[i * sa:i * sa + lda * k].reshape(k, lda).T[:m]
+        B = bf[i * sb:i * sb + ldb * n].reshape(n, ldb).T[:k]
+        ref = ref + A @ B
+    got = to_host(c.primary).reshape(n, ldc)[:, :m].T
+    assert normwise(got, ref) <= 1e-5   # FP32 accumulation of exact BF16 products
+
+
+def test_misaligned_blocks_generic_staging():
+    """Blocks at odd element offsets (not 16-byte aligned) and odd extents:
+    per-stage element-wise staging, VNNI and PLAIN A, beta = -2."""
+    rng = np.random.default_rng(92)
+    for vnni in (False, True):
+        m, n, k, cnt = 37, 50, 21, 4
+        lda, ldb, ldc = 41, 23, 39
+        asz = (-(-k // 2) * m * 2) if vnni else lda * k
+        sa, sb = asz + 3, ldb * n + 5
+        a = O.fp32_to_bf16_rne(rng.standard_normal(sa * cnt + 3).astype(np.float32))
+        b = O.fp32_to_bf16_rne(rng.standard_normal(sb * cnt + 1).astype(np.float32))
+        c0 = rng.standard_normal(ldc * n).astype(np.float32)
+        spec = tpp.GemmSpec(m, n, k, lda, ldb, ldc, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32, beta=-2.0,
+                            a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN)
+        c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32), torch.from_numpy(c0.copy()).cuda())
+        ad, bd = to_dev(a), to_dev(b)
+        tpp.brgemm(spec, tpp.BrgemmBatch.address([(ad, 3 + j * sa) for j in range(cnt)],
+                                                 [(bd, 1 + j * sb) for j in range(cnt)]), c)
+        assert _lib.last_config().startswith(GROUPED)
+        ab = [O.load_a(a, 3 + j * sa, m, k, lda, "bf16", vnni=vnni) for j in range(cnt)]
+        bb = [O.load_b(b, 1 + j * sb, k, n, ldb, "bf16") for j in range(cnt)]
+        want = O.brgemm(ab, bb, c0.reshape(n, ldc)[:, :m].T.copy(), -2.0, "bf16")
+        got = to_host(c.primary).reshape(n, ldc)[:, :m].T
+        assert normwise(got, want) <= TOL, vnni
+
+
+def test_gemm_and_matmul_bf16_use_tensor_cores():
+    rng = np.random.default_rng(93)
+    m, n, k = 96, 80, 64
+    a = tpp.from_array(rng.standard_normal((m, k)).astype(np.float32), tpp.DType.BF16)
+    b = tpp.from_array(rng.standard_normal((k, n)).astype(np.float32), tpp.DType.BF16)
+    c = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+    tpp.matmul(a, b, c)
+    assert _lib.last_config().startswith("brgemm_grouped_kernel<128,128,")
+    ref = O.bf16_to_fp32(tpp.bits_of(a)).astype(np.float64) @ O.bf16_to_fp32(tpp.bits_of(b)).astype(np.float64)
+    assert normwise(tpp.to_array(c), ref) <= 1e-5
+    # ORDERED stays the bitwise reference order
+    c2 = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+    tpp.gemm(tpp.GemmSpec(m, n, k, m, k, m, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                          engine=tpp.Engine.ORDERED), a, b, c2)
+    want = O.brgemm([O.bf16_to_fp32(tpp.bits_of(a))], [O.bf16_to_fp32(tpp.bits_of(b))],
+                    np.zeros((m, n), np.float32), 0.0, "bf16")
+    assert tpp.to_array(c2).tobytes() == np.asarray(want, np.float32).tobytes()
+
+
+def test_grouped_fallback_other_dtypes_matches_single_calls():
+    """brgemm_grouped on FP32 runs one ordered brgemm per group: bitwise equal
+    to the single calls (the reference order)."""
+    rng = np.random.default_rng(94)
+    m = n = k = 16
+    G, cnt = 5, 3
+    a = torch.from_numpy(rng.standard_normal(G * cnt * m * k).astype(np.float32)).cuda()
+    b = torch.from_numpy(rng.standard_normal(G * cnt * k * n).astype(np.float32)).cuda()
+    spec = tpp.GemmSpec(m, n, k, m, k, m)
+    gb = tpp.GroupedBatch.stride(a, b, m * k, k * n, cnt, [g * cnt * m * k for g in range(G)],
+                                 [g * cnt * k * n for g in range(G)])
+    out = torch.zeros(G * m * n, dtype=torch.float32, device="cuda")
+    tpp.brgemm_grouped(spec, gb, out, [g * m * n for g in range(G)])
+    for g in range(G):
+        c = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
+        tpp.brgemm(spec, tpp.BrgemmBatch.stride((a, g * cnt * m * k), (b, g * cnt * k * n), m * k, k * n, cnt), c)
+        assert torch.equal(c.primary, out[g * m * n:(g + 1) * m * n])
+    with pytest.raises(tpp.TensorError):
+        tpp.brgemm_grouped(spec, gb, out, [0] * G)            # C blocks must be distinct
+    with pytest.raises(NotImplementedError):
+        tpp.brgemm_grouped(tpp.GemmSpec(m, n, k, m, k, m, engine=tpp.Engine.TENSOR), gb, out,
+                           [g * m * n for g in range(G)])

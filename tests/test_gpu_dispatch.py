@@ -303,4 +303,9 @@ def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):
     got_dw = T.unpack_weight(dw.cpu(), D, D).numpy()
     for fb in (0, 31, 63):
         ref = dyf[:, fb * 64:(fb + 1) * 64].T @ xf
-        assert normwise(got_dw[fb * 64:(fb + 1) * 64], ref) <= FP32_TOL, fb
+        e = normwise(got_dw[fb * 64:(fb + 1) * 64], ref)
+        print(f"bwd-weights 4096x4096x8192 block {fb}: GPU vs FP64 {e:.2e}")
+        # FP32 output of BF16-input products summed over 8192 tokens in the
+        # tensor core's accumulator (see test_cfg5_full_train_step): well
+        # inside the BF16 tolerance, ~1e-5 from FP64
+        assert e <= 1e-4, fb

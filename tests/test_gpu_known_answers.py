@@ -137,7 +137,7 @@ def test_bf16_emulated_matches_native_bitwise():
     outs = []
     for path in (tpp.ComputePath.NATIVE, tpp.ComputePath.EMULATED_SPLIT):
         c = tpp.alloc(tpp.TensorDesc(m, n, m, tpp.DType.FP32))
-        tpp.gemm(_spec(m, n, k, tpp.DType.BF16, compute_path=path), a, b, c)
+        tpp.gemm(_spec(m, n, k, tpp.DType.BF16, compute_path=path, engine=tpp.Engine.ORDERED), a, b, c)
         outs.append(_bits(tpp.to_array(c)))
     assert outs[0] == outs[1]
     # and both equal the oracle's reference-order BRGEMM

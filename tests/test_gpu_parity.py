@@ -74,7 +74,8 @@ def test_brgemm_cases_bitwise(golden, variant):
         c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, acc), to_dev(g[key + "_c0"]))
         spec = tpp.GemmSpec(m, n, k, lda, ldb, ldc, in_dtype=dt, out_dtype=acc,
                             beta=float(g[key + "_beta"]),
-                            a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN)
+                            a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN,
+                            engine=tpp.Engine.ORDERED)   # the reference's order: bitwise
         if variant == "stride":
             batch = tpp.BrgemmBatch.stride(abuf, bbuf, sa, sb, cnt)
         elif variant == "offset":
