@@ -283,7 +283,7 @@ int conv_backward_weights_tc(int N, int Cb, int Kb, int H, int W, int R, int S, 
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
   cfg.attrs = at;
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, mx, md, p);

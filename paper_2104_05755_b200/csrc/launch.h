@@ -14,6 +14,13 @@
 
 namespace tpp {
 
+// programmatic dependent launch (PDL) for the library's kernels; TPP_NO_PDL=1
+// switches it off (experiments: A/B of the launch overlap)
+inline int pdl_allowed() {
+  static const int v = getenv("TPP_NO_PDL") ? 0 : 1;
+  return v;
+}
+
 // cudaFuncSetAttribute(max dynamic shared memory) once per (kernel, device):
 // thread-safe, and a second device used by the same process gets its own
 // opt-in (the attribute is per device)

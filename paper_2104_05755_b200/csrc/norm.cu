@@ -601,7 +601,7 @@ int launch_layernorm_blocked(int n_b, int m_b, int bn, int bm, int dtype, const 
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
     cfg.attrs = at;
     cfg.numAttrs = 1;
     static const int ln_spin = getenv("TPP_LN_SPIN") ? atoi(getenv("TPP_LN_SPIN")) : 0;  // diagnostics
