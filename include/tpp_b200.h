@@ -134,7 +134,8 @@ int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void*
  * BF16 runs tcgen05 with the epilogue TPPs fused into the GEMM tail. */
 enum tpp_act { TPP_ACT_NONE = 0, TPP_ACT_RELU = 1, TPP_ACT_GELU = 2 };
 enum tpp_fc_flags { TPP_FC_BIAS = 1, TPP_FC_RESIDUAL = 2, TPP_FC_RELU_MASK = 4,
-                    TPP_FC_OUT_FP32 = 8, TPP_FC_BIAS_FP32 = 16, TPP_FC_RELU_INV = 32 };
+                    TPP_FC_OUT_FP32 = 8, TPP_FC_BIAS_FP32 = 16, TPP_FC_RELU_INV = 32,
+                    TPP_FC_SGD = 64 };
 
 typedef struct {
   int32_t m_b, n_b, k_b, bm, bn, bk;
@@ -173,6 +174,16 @@ int tpp_fc_backward_data(const tpp_fc_desc* d, const void* w_packed, const void*
                          const void* relu_mask_in, void* din, void* stream);
 int tpp_fc_backward_weights(const tpp_fc_desc* d, const void* dout, const void* x, void* dw,
                             void* stream);
+/* Backward-weights with the split-SGD update fused into the GEMM epilogue
+ * (kernels.py:235-251, single rank: no gradient exchange in between): the
+ * FP32 dW tile is never stored; each element updates the split FP32 master
+ * in place, W = hi:lo, W - dW*fp32(lr), re-split into w_hi (BF16 bits, the
+ * packed weights the GEMMs read) and w_lo.  Bitwise equal to
+ * tpp_fc_backward_weights (FP32) followed by tpp_split_sgd.  w_hi / w_lo:
+ * [m_b][k_b][bm][bk], 16-byte aligned; no other GEMM may read w_hi while
+ * this runs (issue the layer's backward-data first). */
+int tpp_fc_backward_weights_sgd(const tpp_fc_desc* d, const void* dout, const void* x, uint16_t* w_hi,
+                                uint16_t* w_lo, float lr, void* stream);
 /* Softmax cross-entropy gradient on blocked FP32 logits [n_b][m_b][bn][bm]
  * (tokens x classes): per token the reference softmax (kernels.py:84-99 with
  * exp_taylor, approx.py:190-218), then dlogits = (p - onehot(target)) * scale

@@ -22,7 +22,7 @@ FP64, FP32, BF16, INT32, INT16, INT8, BIT = range(7)
 BCAST_NONE, BCAST_ROW, BCAST_COL, BCAST_SCALAR = range(4)
 ENGINE_AUTO, ENGINE_ORDERED, ENGINE_TENSOR = range(3)
 ACT_NONE, ACT_RELU, ACT_GELU = range(3)
-FC_BIAS, FC_RESIDUAL, FC_RELU_MASK, FC_OUT_FP32, FC_BIAS_FP32, FC_RELU_INV = 1, 2, 4, 8, 16, 32
+FC_BIAS, FC_RESIDUAL, FC_RELU_MASK, FC_OUT_FP32, FC_BIAS_FP32, FC_RELU_INV, FC_SGD = 1, 2, 4, 8, 16, 32, 64
 
 
 class TppUnavailableError(RuntimeError):
@@ -74,6 +74,7 @@ _SIGS = {
     "tpp_fc_forward": (C.c_int, [C.POINTER(FcDescC), _P, _P, _P, _P, _P, _P, _P]),
     "tpp_fc_backward_data": (C.c_int, [C.POINTER(FcDescC), _P, _P, _P, _P, _P]),
     "tpp_fc_backward_weights": (C.c_int, [C.POINTER(FcDescC), _P, _P, _P, _P]),
+    "tpp_fc_backward_weights_sgd": (C.c_int, [C.POINTER(FcDescC), _P, _P, _P, _P, C.c_float, _P]),
     "tpp_softmax_xent_blocked": (C.c_int, [_I32, _I32, _I32, _I32, _P, _P, C.c_float, _P, _P, _P]),
     "tpp_conv_packed_weight_bytes": (C.c_int64, [C.POINTER(ConvDescC)]),
     "tpp_conv_pack_weights": (C.c_int, [C.POINTER(ConvDescC), _P, _P, _I32, _P]),

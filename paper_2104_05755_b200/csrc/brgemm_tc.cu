@@ -99,6 +99,8 @@ struct Params {
   int dbg_mode;  // experiments: bit0 skip epilogue math, bit1 skip MMAs
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
   int cv_rows;              // conv: output rows per tile (2, or 4 for RES = 3)
+  uint16_t* sgd_lo;         // TPP_FC_SGD: lo halves of the split FP32 master (out = hi halves)
+  float sgd_lr;
 };
 
 // RES = 1: the B operand (conv weights, J = R*S*C_b tap blocks of BN x 64)
@@ -534,7 +536,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       // Index arithmetic (integer divisions) is done while the accumulator is
       // still being computed; the empty asm pins it before the wait.
       // token coordinates only for the paths that address rows themselves
-      const bool need_rows = !p.tma_store || (p.flags & (TPP_FC_RELU_INV | TPP_FC_RESIDUAL | TPP_FC_OUT_FP32)) ||
+      const bool need_rows = !p.tma_store || (p.flags & (TPP_FC_RELU_INV | TPP_FC_RESIDUAL | TPP_FC_OUT_FP32 | TPP_FC_SGD)) ||
                              (p.act == TPP_ACT_RELU && (p.flags & TPP_FC_RELU_MASK));
       int t = 0, nb = 0, n_in = 0;
       if (need_rows) {
@@ -644,7 +646,34 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             }
           }
         }
-        if (p.flags & TPP_FC_OUT_FP32) {
+        if (p.flags & TPP_FC_SGD) {
+          // split-SGD on the FP32 master, in place (kernels.py:235-251; the
+          // split_sgd_vec_kernel arithmetic): w = hi:lo, w - g*lr, re-split
+          uint4* hp = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
+          uint4* lp = reinterpret_cast<uint4*>(p.sgd_lo + row_off * p.o_bm + m_in);
+          uint4 hv[4], lv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            hv[i] = hp[i];
+            lv[i] = lp[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t hw[4] = {hv[i].x, hv[i].y, hv[i].z, hv[i].w}, lw[4] = {lv[i].x, lv[i].y, lv[i].z, lv[i].w};
+            uint32_t oh[4], ol[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float w0 = __uint_as_float((hw[q] << 16) | (lw[q] & 0xFFFFu));
+              const float w1 = __uint_as_float((hw[q] & 0xFFFF0000u) | (lw[q] >> 16));
+              const uint32_t r0 = __float_as_uint(__fsub_rn(w0, __fmul_rn(x[8 * i + 2 * q], p.sgd_lr)));
+              const uint32_t r1 = __float_as_uint(__fsub_rn(w1, __fmul_rn(x[8 * i + 2 * q + 1], p.sgd_lr)));
+              oh[q] = (r0 >> 16) | (r1 & 0xFFFF0000u);
+              ol[q] = (r0 & 0xFFFFu) | (r1 << 16);
+            }
+            hp[i] = make_uint4(oh[0], oh[1], oh[2], oh[3]);
+            lp[i] = make_uint4(ol[0], ol[1], ol[2], ol[3]);
+          }
+        } else if (p.flags & TPP_FC_OUT_FP32) {
           float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + row_off * p.o_bm + m_in);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -1039,7 +1068,7 @@ int run_gemm(const Operand& A, const Operand& B, const void* a_ptr, const void* 
   if (rc) return rc;
   // BF16 outputs leave through smem staging + TMA stores: output tensor
   // [ntb][o_mb][o_bn][o_bm], box = 32 tokens x 32 features, 64B swizzle
-  p.tma_store = !env_no_tma_store() && !(p.flags & TPP_FC_OUT_FP32) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
+  p.tma_store = !env_no_tma_store() && !(p.flags & (TPP_FC_OUT_FP32 | TPP_FC_SGD)) && p.o_bn % 32 == 0 && p.o_bm % 32 == 0 &&
                 reinterpret_cast<uintptr_t>(p.out) % 16 == 0;
   mc = ma;
   if (p.tma_store) {
@@ -1065,10 +1094,12 @@ unsigned long long* debug_timestamps() { return g_dbg_ts; }
 
 int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
                const void* x_for_dw, const void* bias, const void* residual, void* out,
-               void* mask_out, const void* mask_in, cudaStream_t stream) {
+               void* mask_out, const void* mask_in, cudaStream_t stream, uint16_t* sgd_lo, float sgd_lr) {
   using namespace tc;
   const int m_b = d->m_b, n_b = d->n_b, k_b = d->k_b, bm = d->bm, bn = d->bn, bk = d->bk;
   Params p{};
+  p.sgd_lo = sgd_lo;
+  p.sgd_lr = sgd_lr;
   p.mode = FEED_FC;
   p.act = d->activation;
   p.flags = d->flags;

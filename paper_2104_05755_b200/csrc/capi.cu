@@ -251,6 +251,22 @@ int tpp_fc_backward_weights(const tpp_fc_desc* d, const void* dout, const void* 
   return fc_gemm_tc(2, d, nullptr, dout, x, nullptr, nullptr, dw, nullptr, nullptr, as_stream(stream));
 }
 
+int tpp_fc_backward_weights_sgd(const tpp_fc_desc* d, const void* dout, const void* x, uint16_t* w_hi,
+                                uint16_t* w_lo, float lr, void* stream) {
+  int rc = check_fc(d);
+  if (rc) return rc;
+  TPP_REQUIRE(d->in_dtype == TPP_BF16, TPP_E_SPEC_DTYPE, "FC backward runs on BF16 operands");
+  TPP_REQUIRE(dout && x && w_hi && w_lo, TPP_E_TENSOR, "null FC operand");
+  TPP_REQUIRE(w_hi != w_lo, TPP_E_TENSOR, "hi and lo halves must be distinct buffers");
+  TPP_REQUIRE(reinterpret_cast<uintptr_t>(w_hi) % 16 == 0 && reinterpret_cast<uintptr_t>(w_lo) % 16 == 0,
+              TPP_E_TENSOR, "split-master halves must be 16-byte aligned");
+  TPP_REQUIRE(!(d->flags & ~(TPP_FC_OUT_FP32 | TPP_FC_SGD)) && d->activation == TPP_ACT_NONE, TPP_E_SPEC_FLAG,
+              "backward-weights-SGD takes no epilogue flags");
+  tpp_fc_desc dd = *d;
+  dd.flags = TPP_FC_OUT_FP32 | TPP_FC_SGD;
+  return fc_gemm_tc(2, &dd, nullptr, dout, x, nullptr, nullptr, w_hi, nullptr, nullptr, as_stream(stream), w_lo, lr);
+}
+
 int tpp_softmax_xent_blocked(int32_t n_b, int32_t m_b, int32_t bn, int32_t bm, const float* logits,
                              const int32_t* targets, float scale, void* dlogits, float* loss,
                              void* stream) {

@@ -59,7 +59,8 @@ int fc_forward_tc(const tpp_fc_desc* d, const void* w_packed, const void* x, con
                   const void* residual, void* out, void* mask, cudaStream_t stream);
 int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const void* x_or_dy,
                const void* x_for_dw, const void* bias, const void* residual, void* out,
-               void* mask_out, const void* mask_in, cudaStream_t stream);
+               void* mask_out, const void* mask_in, cudaStream_t stream, uint16_t* sgd_lo = nullptr,
+               float sgd_lr = 0.0f);
 void set_debug_timestamps(unsigned long long* p);
 unsigned long long* debug_timestamps();
 // brgemm_grouped.cu (K11): BF16 BRGEMM on tcgen05 over stride / offset /

@@ -783,7 +783,9 @@ softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __res
                             uint16_t* __restrict__ dlog, float* __restrict__ loss) {
   extern __shared__ __align__(16) uint8_t xsm[];
   const int F = m_b * bm;
-  const int pitch = F + 1;  // odd pitch: per-token row walks are conflict-free
+  // row pitch F + 4 floats: 16-byte aligned rows (the serial sum reads
+  // float4s), 4-bank skew between consecutive tokens
+  const int pitch = F + 4;
   float* rows = reinterpret_cast<float*>(xsm);
   float* mxs = rows + kXentTok * pitch;
   float* rcp = mxs + kXentTok;
@@ -792,7 +794,26 @@ softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __res
   const int n0 = (blockIdx.x % chunks_per_blk) * kXentTok;
   const int T_ = min(kXentTok, bn - n0);
   const int tid = threadIdx.x;
-  if (bm % 4 == 0 && (T_ * bm) % 4 == 0) {
+  if (bm == 64 && T_ == kXentTok && blockDim.x == 256) {
+    // the cfg-5 shape: each feature block's 16 x 64 sub-tile is 256 float4,
+    // one per thread (token t = tid / 16, float4 m4 = tid % 16): no index
+    // arithmetic per element, all 16 blocks' loads in flight at once
+    const int t = tid >> 4, m4 = tid & 15;
+    const float4* src = reinterpret_cast<const float4*>(logits + ((int64_t)nb * m_b * bn + n0) * 64) + tid;
+    float* d = rows + t * pitch + m4 * 4;
+    for (int mb0 = 0; mb0 < m_b; mb0 += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (mb0 + u < m_b) v[u] = __ldg(src + (int64_t)(mb0 + u) * bn * 16);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (mb0 + u < m_b) {
+          float* q = d + (mb0 + u) * 64;
+          q[0] = v[u].x; q[1] = v[u].y; q[2] = v[u].z; q[3] = v[u].w;
+        }
+    }
+  } else if (bm % 4 == 0 && (T_ * bm) % 4 == 0) {
     // 16-byte loads, 8 in flight per thread (the logits are read once from HBM)
     const int n4 = T_ * bm / 4, bm4 = bm / 4;
     for (int base = 0; base < m_b * n4; base += 8 * blockDim.x) {
@@ -862,6 +883,23 @@ softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __res
     const float* r = rows + tid * pitch;
     float tot = 0.0f;
     int f = 0;
+    if (F % 16 == 0 && F >= 16) {
+      // float4 reads one 16-float chunk ahead of the dependent add chain
+      const float4* r4 = reinterpret_cast<const float4*>(r);
+      float4 a0 = r4[0], a1 = r4[1], a2 = r4[2], a3 = r4[3];
+      for (; f < F; f += 16) {
+        float4 n0 = a0, n1 = a1, n2 = a2, n3 = a3;
+        if (f + 16 < F) {
+          const float4* q = r4 + (f + 16) / 4;
+          n0 = q[0]; n1 = q[1]; n2 = q[2]; n3 = q[3];
+        }
+        const float v[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                             a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+#pragma unroll
+        for (int u = 0; u < 16; ++u) tot = __fadd_rn(tot, v[u]);
+        a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+      }
+    }
     for (; f + 8 <= F; f += 8) {
       float v[8];
 #pragma unroll
@@ -877,7 +915,26 @@ softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __res
   }
   __syncthreads();
   // dlogits: 16 threads per token, 4 consecutive features each (8-byte stores)
-  if (bm % 64 == 0) {
+  if (bm == 64 && T_ == kXentTok && blockDim.x == 256) {
+    // same mapping as the load: per feature block one 8-byte store per thread,
+    // a warp writes two token rows of 128 contiguous bytes
+    const int t = tid >> 4, m4 = tid & 15;
+    const float rc = rcp[t];
+    const int tg = targets[(int64_t)nb * bn + n0 + t];
+    const float* r = rows + t * pitch + m4 * 4;
+    uint2* dst = reinterpret_cast<uint2*>(dlog + ((int64_t)nb * m_b * bn + n0) * 64) + tid;
+#pragma unroll 4
+    for (int mb = 0; mb < m_b; ++mb) {
+      const int f = mb * 64 + m4 * 4;
+      float g[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        g[u] = __fmul_rn(__fsub_rn(__fmul_rn(r[mb * 64 + u], rc), f + u == tg ? 1.0f : 0.0f), scale);
+      uint32_t w[2];
+      pack_bf16_ref_n<2>(g, w);   // hardware RNE, one rarely-taken branch for the NaN rule
+      dst[(int64_t)mb * bn * 16] = make_uint2(w[0], w[1]);
+    }
+  } else if (bm % 64 == 0) {
     const int t = tid >> 4, k = tid & 15;
     if (t < T_) {
       const float rc = rcp[t];
@@ -914,7 +971,7 @@ int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* l
                                 const int32_t* targets, float scale, void* dlogits, float* loss,
                                 cudaStream_t s) {
   const int F = m_b * bm;
-  const size_t smem = (size_t)kXentTok * (F + 1) * sizeof(float) + 2 * kXentTok * sizeof(float);
+  const size_t smem = (size_t)kXentTok * (F + 4) * sizeof(float) + 2 * kXentTok * sizeof(float);
   TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "softmax_xent: class dimension too long for smem");
   const int blocks = n_b * ((bn + kXentTok - 1) / kXentTok);
   if (blocks == 0) return TPP_OK;

@@ -208,6 +208,26 @@ class FcLayer:
         return out
 
 
+    def backward_weights_sgd(self, dout: torch.Tensor, x: torch.Tensor, n_b: int, bn: int, w_lo: torch.Tensor,
+                             lr: float, stream=None) -> None:
+        """dW = sum over tokens of dout^T x applied at once as split-SGD on the
+        FP32 master whose hi halves are this layer's packed weights
+        (``w_packed``) and lo halves ``w_lo`` (kernels.py:235-251): the FP32
+        dW never leaves the chip.  Bitwise equal to ``backward_weights`` +
+        ``split_sgd_flat``.  Issue the layer's backward-data first: it reads
+        the weights this call updates."""
+        if dout.dtype != torch.bfloat16 or x.dtype != torch.bfloat16:
+            raise TensorError("dout and x must be BF16")
+        n_w = self.m_b * self.k_b * self.bm * self.bk
+        if w_lo.numel() < n_w or w_lo.element_size() != 2:
+            raise TensorError("w_lo must hold the 16-bit lo halves of every weight")
+        lib = _lib.load()
+        d = _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16, _lib.ACT_NONE, 0, self.block_n)
+        _lib.check(lib.tpp_fc_backward_weights_sgd(C.byref(d), dout.data_ptr(), x.data_ptr(),
+                                                   self.w_packed.data_ptr(), w_lo.data_ptr(), float(lr),
+                                                   _lib.stream_ptr(stream)), "FcLayer.backward_weights_sgd")
+
+
 def softmax_xent_blocked(logits: torch.Tensor, targets: torch.Tensor, n_b: int, m_b: int, bn: int,
                          bm: int, scale: float, dlogits: Optional[torch.Tensor] = None,
                          loss: Optional[torch.Tensor] = None, stream=None):

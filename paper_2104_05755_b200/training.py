@@ -57,12 +57,16 @@ class BlockedMLP:
     def __init__(self, dims: Sequence[int], tokens: int, bn: int = 64, lr: float = 0.01,
                  global_batch: Optional[int] = None, init_std: float = 0.02, seed: int = 0,
                  device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None,
-                 grad_dtype: str = "fp32", reduce_fn=None):
+                 grad_dtype: str = "fp32", reduce_fn=None, fuse_sgd: Optional[bool] = None):
         """``grad_dtype``: "fp32" (dW written and applied in FP32) or "bf16"
         (dW written as BF16 by the backward-weights epilogue, exchanged as
         BF16 — half the allreduce bytes — and applied by split-SGD, which
         accepts BF16 gradients like the reference's, kernels.py:235-251).
-        ``reduce_fn`` replaces the dW collective (rank emulation in tests)."""
+        ``reduce_fn`` replaces the dW collective (rank emulation in tests).
+        ``fuse_sgd`` (default: on when there is no gradient exchange and dW is
+        FP32): each layer's split-SGD runs inside its backward-weights GEMM
+        epilogue, so dW is never written (``self.dw`` stays unused); results
+        are bitwise those of the unfused step."""
         if grad_dtype not in ("fp32", "bf16"):
             raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         if any(d % BLK for d in dims) or tokens % bn or bn % BLK:
@@ -101,6 +105,11 @@ class BlockedMLP:
         self.dw = [torch.empty(dims[l + 1] * dims[l], dtype=dwt, device=dev) for l in range(self.nl)]
         self.loss = torch.empty(tokens, dtype=torch.float32, device=dev)
         self.sync = GradSync(group, reduce_fn=reduce_fn, device=dev)
+        if fuse_sgd is None:
+            fuse_sgd = not self.sync.active and grad_dtype == "fp32"
+        if fuse_sgd and (self.sync.active or grad_dtype != "fp32"):
+            raise ValueError("fused split-SGD needs FP32 gradients and no gradient exchange")
+        self.fuse_sgd = fuse_sgd
         # optional per-launch hook (label) called right after each main-stream
         # launch -- bench.py records CUDA events there for the step breakdown
         self.trace = None
@@ -130,6 +139,18 @@ class BlockedMLP:
                                1.0 / self.global_batch, dlogits=self.g[nl - 1], loss=self.loss)
         if tr:
             tr("xent")
+        if self.fuse_sgd:
+            for l in range(nl - 1, -1, -1):
+                layer = self.layers[l]
+                if l > 0:   # the last reader of the layer's weights goes first
+                    layer.backward_data(self.g[l], self.n_b, self.bn, relu_mask_in=self.mask[l],
+                                        out=self.g[l - 1])
+                    if tr:
+                        tr(f"dx{l}")
+                layer.backward_weights_sgd(self.g[l], self.h[l], self.n_b, self.bn, self.lo[l], self.lr)
+                if tr:
+                    tr(f"dw{l}")
+            return
         for l in range(nl - 1, -1, -1):
             layer = self.layers[l]
             layer.backward_weights(self.g[l], self.h[l], self.n_b, self.bn, out=self.dw[l])

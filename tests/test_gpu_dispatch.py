@@ -194,7 +194,8 @@ def test_cfg5_full_train_step(monkeypatch):
     ws = [rng.standard_normal((dims[l + 1], dims[l]), dtype=np.float32) * np.float32(0.02) for l in range(nl)]
     x = O.fp32_to_bf16_rne(rng.standard_normal((Tk, dims[0]), dtype=np.float32))
     tg = rng.integers(0, dims[-1], Tk).astype(np.int32)
-    mlp = tpp.BlockedMLP(dims, Tk, bn=bn, lr=lr, global_batch=Tk, weights=[torch.from_numpy(w) for w in ws])
+    mlp = tpp.BlockedMLP(dims, Tk, bn=bn, lr=lr, global_batch=Tk, weights=[torch.from_numpy(w) for w in ws],
+                         fuse_sgd=False)   # materialise dW so every kernel can be checked
     xb = x.reshape(n_b, bn, dims[0] // 64, 64).transpose(0, 2, 1, 3).copy()
     loss = mlp.train_step(to_dev(xb), to_dev(tg))
     torch.cuda.synchronize()
@@ -272,6 +273,19 @@ def test_cfg5_full_train_step(monkeypatch):
         want = O.split_sgd_step(ws[l], dws[l], lr)
         got = mlp.master_weight(l).cpu().numpy()
         assert got.tobytes() == np.asarray(want, np.float32).tobytes(), l
+    # ---- the benchmarked step fuses split-SGD into the backward-weights
+    # epilogue (dW never stored): bitwise the same weights and loss ----
+    del mlp
+    torch.cuda.empty_cache()
+    rec.log.clear()
+    fused = tpp.BlockedMLP(dims, Tk, bn=bn, lr=lr, global_batch=Tk, weights=[torch.from_numpy(w) for w in ws])
+    assert fused.fuse_sgd
+    fl = fused.train_step(to_dev(xb), to_dev(tg))
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(fl), to_host(loss))
+    for l in range(nl):
+        assert fused.master_weight(l).cpu().numpy().tobytes() == np.asarray(
+            O.split_sgd_step(ws[l], dws[l], lr), np.float32).tobytes(), l
 
 
 def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):

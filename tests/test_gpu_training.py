@@ -98,7 +98,7 @@ def test_mlp_train_step_vs_oracle():
     x = _bf16(rng, (T_, dims[0]), 1.0)
     tg = rng.integers(0, dims[-1], T_).astype(np.int32)
     mlp = tpp.BlockedMLP(dims, T_, bn=64, lr=0.5, global_batch=T_,
-                         weights=[torch.from_numpy(w) for w in ws])
+                         weights=[torch.from_numpy(w) for w in ws], fuse_sgd=False)
     loss = mlp.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
     torch.cuda.synchronize()
     new_ref, dws_ref, loss_ref = O.mlp_train_step(x, ws, tg, 0.5, T_)
@@ -108,6 +108,14 @@ def test_mlp_train_step_vs_oracle():
         assert normwise(dw, dws_ref[l]) <= TOL, l
         got_w = mlp.master_weight(l).cpu().numpy()
         assert normwise(got_w - ws[l], new_ref[l] - ws[l]) <= TOL, l
+    # split-SGD fused into the backward-weights epilogue: bitwise the same step
+    fused = tpp.BlockedMLP(dims, T_, bn=64, lr=0.5, global_batch=T_, weights=[torch.from_numpy(w) for w in ws])
+    assert fused.fuse_sgd
+    fused.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
+    torch.cuda.synchronize()
+    for l in range(3):
+        assert torch.equal(fused.hi[l].view(torch.int16), mlp.hi[l].view(torch.int16)), l
+        assert torch.equal(fused.lo[l], mlp.lo[l]), l
 
 
 # ---------------------------------------------------------------------------
@@ -132,11 +140,11 @@ def test_sharded_step_equals_global_step_emulated(grad_dtype):
     dims, T_, ws, x, tg = _mlp_case()
     lr = 0.5
     wt = [torch.from_numpy(w) for w in ws]
-    full = tpp.BlockedMLP(dims, T_, bn=64, lr=lr, global_batch=T_, weights=wt)
+    full = tpp.BlockedMLP(dims, T_, bn=64, lr=lr, global_batch=T_, weights=wt, fuse_sgd=False)
     full.train_step(to_dev(_blocked(x, 64)), to_dev(tg))
     half = T_ // 2
-    shards = [tpp.BlockedMLP(dims, half, bn=64, lr=lr, global_batch=T_, weights=wt, grad_dtype=grad_dtype)
-              for _ in range(2)]
+    shards = [tpp.BlockedMLP(dims, half, bn=64, lr=lr, global_batch=T_, weights=wt, grad_dtype=grad_dtype,
+                             fuse_sgd=False) for _ in range(2)]
     for r, m in enumerate(shards):
         m.forward(to_dev(_blocked(x[r * half:(r + 1) * half], 64)))
         m.backward(to_dev(tg[r * half:(r + 1) * half]))
