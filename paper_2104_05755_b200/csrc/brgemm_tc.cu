@@ -101,6 +101,45 @@ struct Params {
   int cv_rows;              // conv: output rows per tile (2, or 4 for RES = 3)
   uint16_t* sgd_lo;         // TPP_FC_SGD: lo halves of the split FP32 master (out = hi halves)
   float sgd_lr;
+  // stream-K tail (FC mode): work items [0, sk_dp) are whole tiles handed out
+  // round-robin; the remaining items' stages (sk_stages in total) are split
+  // evenly over the workers.  A tile cut between workers is finished by the
+  // worker holding its first stage, which adds the other workers' FP32
+  // partials (sk_ws slots, sk_flag handshake) in k order before the epilogue.
+  int sk_dp, sk_stages;
+  float* sk_ws;
+  unsigned* sk_flag;
+};
+
+// One worker's walk over its segments: (work item, first stage, end stage)
+struct Seg {
+  int tile, k0, k1;
+};
+struct SegWalk {
+  int w, P, dp, S, i, pos, end;
+  __device__ __forceinline__ static int sk_begin(const Params& p, int w, int P) {
+    return (int)(((long long)w * p.sk_stages) / P);
+  }
+  __device__ __forceinline__ void start(const Params& p, int w_, int P_, int S_) {
+    w = w_; P = P_; S = S_; dp = p.sk_dp; i = 0;
+    pos = p.sk_stages ? sk_begin(p, w, P) : 0;
+    end = p.sk_stages ? sk_begin(p, w + 1, P) : 0;
+  }
+  __device__ __forceinline__ bool next(Seg& sg) {
+    const int t = w + i * P;
+    if (t < dp) {
+      sg.tile = t; sg.k0 = 0; sg.k1 = S;
+      ++i;
+      return true;
+    }
+    if (pos >= end) return false;
+    const int tr = pos / S;
+    sg.tile = dp + tr;
+    sg.k0 = pos - tr * S;
+    sg.k1 = min(S, end - tr * S);
+    pos = tr * S + sg.k1;
+    return true;
+  }
 };
 
 // RES = 1: the B operand (conv weights, J = R*S*C_b tap blocks of BN x 64)
@@ -346,9 +385,13 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const int pid = warp == 0 ? 0 : 1;
     if (lane == 0) {
       FeedIter f;
-      if (cl_id < num_tiles) {
+      SegWalk walk;
+      walk.start(p, cl_id, n_cl, nstages);
+      Seg sg;
+      bool have = walk.next(sg);
+      if (have) {
         int tm, tn;
-        tile_mn(cl_id, tm, tn);
+        tile_mn(sg.tile, tm, tn);
         if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
         else f.start(p, tm, tn);
       }
@@ -371,14 +414,16 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       uint32_t it = 0;
       // pair: completion bytes of both CTAs count on the leader's full[s]
       const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
-      for (int tile = cl_id; tile < num_tiles; tile += n_cl) {
-        if (tile != cl_id) {  // the first tile's feed was set up before the wait
+      bool first = true;
+      for (; have; have = walk.next(sg), first = false) {
+        if (!first) {  // the first segment's feed was set up before the wait
           int tm, tn;
-          tile_mn(tile, tm, tn);
+          tile_mn(sg.tile, tm, tn);
           if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
           else f.start(p, tm, tn);
         }
-        for (int j = 0; j < nstages; ++j, ++it) {
+        for (int j = 0; j < sg.k0; ++j) f.next();  // stream-K: a segment may start mid-tile
+        for (int j = sg.k0; j < sg.k1; ++j, ++it) {
           if (NPROD == 1 || (int)(it % NPROD) == pid) {
             mbar_wait(&empty[s], ph ^ 1);
             uint8_t* sa = smem + s * S::STAGE_BYTES;
@@ -424,7 +469,11 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       if (RES) mbar_wait(bres, 0);
       int s = 0;
       uint32_t ph = 0, tcount = 0;
-      for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
+      SegWalk walk;
+      walk.start(p, cl_id, n_cl, nstages);
+      Seg sg;
+      for (; walk.next(sg); ++tcount) {
+        const int j0 = sg.k0;
         const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32, 240 + tcount, gtimer());
@@ -432,7 +481,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 321 + (tcount == 30) * 2, gtimer());
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * (BN * CT::NACC);
-        for (int j = 0; j < nstages; ++j) {
+        for (int j = j0; j < sg.k1; ++j) {
           mbar_wait(&full[s], ph);
           TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0, 2, gtimer());
           TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32 && j == 0, 16 + 4 * tcount, gtimer());
@@ -459,7 +508,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                   for (int kk = 0; kk < BK / 16; ++kk)
                     if (!(TPP_DBG_MODE & 2))
                       umma_f16_warp(tmem_d + h * BN, ad + 2 * kk, bd + 2 * kk, idesc,
-                                    (j > 0 || tap > 0 || kk > 0) ? 1u : 0u);
+                                    (j > j0 || tap > 0 || kk > 0) ? 1u : 0u);
                 }
               }
             } else {
@@ -472,7 +521,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
                       umma_f16_warp(tmem_d + h * BN, ad + 2 * kk, bd + 2 * kk, idesc,
-                                    (j > 0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
+                                    (j > j0 || rr > 0 || ss > 0 || kk > 0) ? 1u : 0u);
                   }
                 }
               }
@@ -486,10 +535,10 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                 if (TPP_DBG_MODE & 2) continue;
                 if (PAIR)
                   umma_f16_pair_warp(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk, idesc,
-                                (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                                (j > j0 || kb > 0 || kk > 0) ? 1u : 0u);
                 else
                   umma_f16_warp(tmem_d, adesc0 + soff + asub * kb + astep * kk, bd + bstep * kk,
-                           idesc, (j > 0 || kb > 0 || kk > 0) ? 1u : 0u);
+                           idesc, (j > j0 || kb > 0 || kk > 0) ? 1u : 0u);
               }
             }
           }
@@ -515,10 +564,24 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     uint8_t* stg0 = smem + S::STG_OFF + ew * 2048 * S::STG_BUFS;  // 32 rows x 64 B, 64B-swizzled
     uint32_t nstore = 0;
     uint32_t tcount = 0;
-    for (int tile = cl_id; tile < num_tiles; tile += n_cl, ++tcount) {
+    SegWalk walk;
+    walk.start(p, cl_id, n_cl, nstages);
+    Seg sg;
+    for (; walk.next(sg); ++tcount) {
+      const int tile = sg.tile;
       int tm, tn;
       tile_mn(tile, tm, tn);
       if (PAIR) tm = 2 * tm + (int)rank;
+      // stream-K roles: a segment without the tile's first stage only parks
+      // its FP32 partial; the one with it (k0 == 0) adds the partials of the
+      // workers that hold the rest of the tile (k order) before the epilogue
+      const bool sk_part = sg.k0 > 0;
+      const int sk_w0 = cl_id + 1;
+      int sk_w1 = sk_w0;  // partial sources [sk_w0, sk_w1)
+      if (!sk_part && sg.k1 < nstages) {
+        const int tile_end = (tile - p.sk_dp + 1) * nstages;
+        while (sk_w1 < n_cl && SegWalk::sk_begin(p, sk_w1, n_cl) < tile_end) ++sk_w1;
+      }
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       float* bs = bias_s + as * 256;
       if (p.flags & TPP_FC_BIAS) {
@@ -587,6 +650,17 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
       };
       if (nch <= 0) release();
+      if (sk_w1 > sk_w0) {  // the partials of this tile's later k ranges must have landed
+        if (lane == 0)
+          for (int w2 = sk_w0; w2 < sk_w1; ++w2) {
+            const unsigned* fl = p.sk_flag + w2 * CG + (int)rank;
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+            } while (v == 0);
+          }
+        __syncwarp();
+      }
 #pragma unroll 1
       for (int ch = 0; ch < nch; ++ch) {
         const int col = chunk_col(ch);
@@ -598,6 +672,22 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         // the next chunk's TMEM load overlaps this chunk's math and stores
         if (ch + 1 < nch) tmem_ld32(tacc + chunk_acc(ch + 1) * BN + chunk_col(ch + 1), v);
         else release();
+        if (sk_part) {  // stream-K: park this worker's FP32 partial (slot [128 rows][BN])
+          float4* dst = reinterpret_cast<float4*>(p.sk_ws + ((size_t)(cl_id * CG + (int)rank) * BM + r) * BN + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) __stcg(dst + i, make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]));
+          continue;
+        }
+        for (int w2 = sk_w0; w2 < sk_w1; ++w2) {  // later k ranges, in k order
+          const float4* src =
+              reinterpret_cast<const float4*>(p.sk_ws + ((size_t)(w2 * CG + (int)rank) * BM + r) * BN + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 q4 = __ldcg(src + i);
+            x[4 * i] = __fadd_rn(x[4 * i], q4.x); x[4 * i + 1] = __fadd_rn(x[4 * i + 1], q4.y);
+            x[4 * i + 2] = __fadd_rn(x[4 * i + 2], q4.z); x[4 * i + 3] = __fadd_rn(x[4 * i + 3], q4.w);
+          }
+        }
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0, 7, gtimer());
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 0, clock64());
         const int f0 = tn * BN + col;
@@ -715,6 +805,20 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
+      if (sk_part || sk_w1 > sk_w0) {
+        // publish this worker's partial / recycle the consumed flags (every
+        // epilogue thread's stores are fenced before the barrier)
+        if (sk_part) __threadfence();
+        named_bar_sync(2, kEpiWarps * 32);
+        if (ew == 0 && lane == 0) {
+          if (sk_part) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + cl_id * CG + (int)rank), "r"(1u)
+                         : "memory");
+          } else {
+            for (int w2 = sk_w0; w2 < sk_w1; ++w2) p.sk_flag[w2 * CG + (int)rank] = 0u;
+          }
+        }
+      }
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 8, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 5, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 19 + 4 * tcount, gtimer());
@@ -783,6 +887,53 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
   return TPP_OK;
 }
 
+// The stream-K tail is OFF by default: measured on the cfg-5 GEMMs it was
+// slower than whole tiles (fwd 8192x4096->1024: 78 vs 56 us; dW 4096^2 over
+// 8192 tokens: 223 vs 215 us; dW 1024x4096: 86 vs 78 us, tools/sk_probe.py) —
+// segments that start mid-K break the lock-step K sweep the concurrent tiles
+// share in L2, and the finisher's partial reads sit on the critical path.
+// TPP_STREAMK=1 enables it (experiments; tests/test_gpu_dispatch.py checks
+// its numerics when set).
+static bool env_no_streamk() {
+  static const bool v = getenv("TPP_STREAMK") == nullptr;
+  return v;
+}
+
+// Stream-K partial slots + flags, one buffer per device, allocated on first
+// use outside a CUDA-graph capture (inside a capture without it the GEMM runs
+// without the stream-K tail).  The flags are reset by their consumers, so the
+// buffer is reusable by every later launch; stream-K GEMMs of one device must
+// not run concurrently on two streams.
+static float* sk_workspace(cudaStream_t stream, size_t floats, unsigned** flags) {
+  static std::mutex mu;
+  static std::unordered_map<int, std::pair<float*, size_t>> bufs;
+  constexpr size_t kFlagBytes = 4096;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = bufs.find(dev);
+  if (it == bufs.end() || it->second.second < floats) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (it != bufs.end()) {
+      cudaDeviceSynchronize();
+      cudaFree(it->second.first);
+      bufs.erase(it);
+    }
+    const size_t want = floats < ((size_t)19 << 20) / 4 ? ((size_t)19 << 20) / 4 : floats;
+    void* ptr = nullptr;
+    if (cudaMalloc(&ptr, kFlagBytes + want * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    cudaMemset(ptr, 0, kFlagBytes);
+    cudaDeviceSynchronize();
+    it = bufs.emplace(dev, std::make_pair(reinterpret_cast<float*>(static_cast<char*>(ptr) + kFlagBytes), want)).first;
+  }
+  *flags = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(it->second.first) - kFlagBytes);
+  return it->second.first;
+}
+
 template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1, int MC = 1>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       const Params& p, cudaStream_t stream) {
@@ -816,6 +967,26 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   });
   const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * (p.tiles_n / MC);
   const int grid = CL * (units < max_clusters ? units : max_clusters);
+  Params pk = p;
+  pk.sk_dp = units;   // default: every work item whole, round-robin
+  pk.sk_stages = 0;
+  {
+    // stream-K tail: when the last wave of work items would leave workers
+    // idle, spread the last (partial + one full) wave's stages evenly
+    const int workers = grid / CL;
+    const int S = p.kblocks / KPS;
+    if (RES == 0 && MC == 1 && p.mode == FEED_FC && units > workers && units % workers != 0 &&
+        (units % workers) * 10 < workers * 9 && S >= 4 && !env_no_streamk()) {
+      unsigned* flags = nullptr;
+      float* ws = sk_workspace(stream, (size_t)workers * CG * BM * BN, &flags);
+      if (ws) {
+        pk.sk_dp = (units / workers - 1) * workers;
+        pk.sk_stages = (units - pk.sk_dp) * S;
+        pk.sk_ws = ws;
+        pk.sk_flag = flags;
+      }
+    }
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -828,13 +999,15 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   attr[1].val.clusterDim.x = CL; attr[1].val.clusterDim.y = 1; attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = CL > 1 ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, pk);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_tc_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_tc_kernel");
   set_last_config("brgemm_tc_kernel<" + std::to_string(BN) + "," + std::to_string(STAGES) + "," +
                   std::to_string(KPS) + "," + std::to_string(RES) + "," + std::to_string(CG) + "," +
                   std::to_string(MC) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(p.tiles_m) +
-                  "x" + std::to_string(p.tiles_n));
+                  "x" + std::to_string(p.tiles_n) +
+                  (pk.sk_stages ? " streamk=" + std::to_string(units - pk.sk_dp) + "/" + std::to_string(units)
+                                : std::string()));
   return TPP_OK;
 }
 

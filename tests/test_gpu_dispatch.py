@@ -18,6 +18,8 @@ instantiation really ran, and check the results against the CPU oracle
 * the softmax-CE gradient and the split-SGD update bitwise (same order).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -306,6 +308,8 @@ def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):
     assert rec.log[-1][1].startswith(PAIR256), rec.log[-1]
     dw = layer.backward_weights(dyd, xd, n_b, bn)
     assert rec.log[-1][1].startswith(PAIR256), rec.log[-1]
+    if os.environ.get("TPP_STREAMK"):  # opt-in: the last 1.46 waves of the 256 pair tiles as a stream-K tail
+        assert "streamk=108/256" in rec.log[-1][1], rec.log[-1]
     torch.cuda.synchronize()
     wf = O.bf16_to_fp32(w).astype(np.float64)
     dyf = O.bf16_to_fp32(dy).astype(np.float64)
