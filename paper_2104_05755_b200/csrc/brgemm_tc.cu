@@ -126,9 +126,9 @@ struct SegWalk {
     end = p.sk_stages ? sk_begin(p, w + 1, P) : 0;
   }
   __device__ __forceinline__ bool next(Seg& sg) {
-    const int t = w + i * P;
-    if (t < dp) {
-      sg.tile = t; sg.k0 = 0; sg.k1 = S;
+    const int u = w + i * P;
+    if (u < dp) {
+      sg.tile = u; sg.k0 = 0; sg.k1 = S;
       ++i;
       return true;
     }
@@ -572,15 +572,22 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       int tm, tn;
       tile_mn(tile, tm, tn);
       if (PAIR) tm = 2 * tm + (int)rank;
-      // stream-K roles: a segment without the tile's first stage only parks
-      // its FP32 partial; the one with it (k0 == 0) adds the partials of the
-      // workers that hold the rest of the tile (k order) before the epilogue
-      const bool sk_part = sg.k0 > 0;
-      const int sk_w0 = cl_id + 1;
-      int sk_w1 = sk_w0;  // partial sources [sk_w0, sk_w1)
-      if (!sk_part && sg.k1 < nstages) {
-        const int tile_end = (tile - p.sk_dp + 1) * nstages;
-        while (sk_w1 < n_cl && SegWalk::sk_begin(p, sk_w1, n_cl) < tile_end) ++sk_w1;
+      // partial bookkeeping: `park` stores this segment's FP32 partial in
+      // slot park_slot and skips the epilogue; otherwise nsrc parked partials
+      // (slots src_base + j * src_step, k order) are added before it
+      bool park = false;
+      int park_slot = 0, nsrc = 0, src_base = 0, src_step = 1;
+      if (p.sk_stages) {  // stream-K tail: the worker with the first stage finishes
+        if (sg.k0 > 0) {
+          park = true;
+          park_slot = cl_id;
+        } else if (sg.k1 < nstages) {
+          const int tile_end = (tile - p.sk_dp + 1) * nstages;
+          int w1 = cl_id + 1;
+          while (w1 < n_cl && SegWalk::sk_begin(p, w1, n_cl) < tile_end) ++w1;
+          nsrc = w1 - cl_id - 1;
+          src_base = cl_id + 1;
+        }
       }
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       float* bs = bias_s + as * 256;
@@ -650,10 +657,10 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
       };
       if (nch <= 0) release();
-      if (sk_w1 > sk_w0) {  // the partials of this tile's later k ranges must have landed
+      if (nsrc > 0) {  // the parked partials of this tile must have landed
         if (lane == 0)
-          for (int w2 = sk_w0; w2 < sk_w1; ++w2) {
-            const unsigned* fl = p.sk_flag + w2 * CG + (int)rank;
+          for (int j = 0; j < nsrc; ++j) {
+            const unsigned* fl = p.sk_flag + (src_base + j * src_step) * CG + (int)rank;
             unsigned v;
             do {
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
@@ -672,18 +679,23 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         // the next chunk's TMEM load overlaps this chunk's math and stores
         if (ch + 1 < nch) tmem_ld32(tacc + chunk_acc(ch + 1) * BN + chunk_col(ch + 1), v);
         else release();
-        if (sk_part) {  // stream-K: park this worker's FP32 partial (slot [128 rows][BN])
-          float4* dst = reinterpret_cast<float4*>(p.sk_ws + ((size_t)(cl_id * CG + (int)rank) * BM + r) * BN + col);
+        if (park) {  // park this segment's FP32 partial (slot [128 rows][BN])
+          // slot layout [BN/4][128 rows][4]: a warp's 32 rows of one column quad
+          // are 512 contiguous bytes (coalesced stores and loads)
+          float4* dst = reinterpret_cast<float4*>(p.sk_ws + (size_t)(park_slot * CG + (int)rank) * BM * BN) +
+                        (col / 4) * BM + r;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) __stcg(dst + i, make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]));
+          for (int i = 0; i < 8; ++i)
+            __stcg(dst + i * BM, make_float4(x[4 * i], x[4 * i + 1], x[4 * i + 2], x[4 * i + 3]));
           continue;
         }
-        for (int w2 = sk_w0; w2 < sk_w1; ++w2) {  // later k ranges, in k order
+        for (int j = 0; j < nsrc; ++j) {  // the other k ranges, in slot order
           const float4* src =
-              reinterpret_cast<const float4*>(p.sk_ws + ((size_t)(w2 * CG + (int)rank) * BM + r) * BN + col);
+              reinterpret_cast<const float4*>(p.sk_ws + (size_t)((src_base + j * src_step) * CG + (int)rank) * BM * BN) +
+              (col / 4) * BM + r;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 q4 = __ldcg(src + i);
+            const float4 q4 = __ldcg(src + i * BM);
             x[4 * i] = __fadd_rn(x[4 * i], q4.x); x[4 * i + 1] = __fadd_rn(x[4 * i + 1], q4.y);
             x[4 * i + 2] = __fadd_rn(x[4 * i + 2], q4.z); x[4 * i + 3] = __fadd_rn(x[4 * i + 3], q4.w);
           }
@@ -805,17 +817,17 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
-      if (sk_part || sk_w1 > sk_w0) {
-        // publish this worker's partial / recycle the consumed flags (every
+      if (park || nsrc > 0) {
+        // publish the parked partial / recycle the consumed flags (every
         // epilogue thread's stores are fenced before the barrier)
-        if (sk_part) __threadfence();
+        if (park) __threadfence();
         named_bar_sync(2, kEpiWarps * 32);
         if (ew == 0 && lane == 0) {
-          if (sk_part) {
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + cl_id * CG + (int)rank), "r"(1u)
+          if (park) {
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.sk_flag + park_slot * CG + (int)rank), "r"(1u)
                          : "memory");
           } else {
-            for (int w2 = sk_w0; w2 < sk_w1; ++w2) p.sk_flag[w2 * CG + (int)rank] = 0u;
+            for (int j = 0; j < nsrc; ++j) p.sk_flag[(src_base + j * src_step) * CG + (int)rank] = 0u;
           }
         }
       }
@@ -907,7 +919,7 @@ static bool env_no_streamk() {
 static float* sk_workspace(cudaStream_t stream, size_t floats, unsigned** flags) {
   static std::mutex mu;
   static std::unordered_map<int, std::pair<float*, size_t>> bufs;
-  constexpr size_t kFlagBytes = 4096;
+  constexpr size_t kFlagBytes = 64 * 1024;   // 16K slot flags
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> g(mu);
@@ -966,17 +978,20 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     }
   });
   const int units = (CG > 1 ? (p.tiles_m + 1) / 2 : p.tiles_m) * (p.tiles_n / MC);
-  const int grid = CL * (units < max_clusters ? units : max_clusters);
+  int grid = CL * (units < max_clusters ? units : max_clusters);
   Params pk = p;
   pk.sk_dp = units;   // default: every work item whole, round-robin
   pk.sk_stages = 0;
-  {
-    // stream-K tail: when the last wave of work items would leave workers
-    // idle, spread the last (partial + one full) wave's stages evenly
-    const int workers = grid / CL;
+  if (RES == 0 && MC == 1 && p.mode == FEED_FC) {
     const int S = p.kblocks / KPS;
-    if (RES == 0 && MC == 1 && p.mode == FEED_FC && units > workers && units % workers != 0 &&
-        (units % workers) * 10 < workers * 9 && S >= 4 && !env_no_streamk()) {
+    // (split-K of every tile into 2-4 K parts, part-major, was measured
+    // slower on every cfg-5 shape -- the FP32 partial round trip costs more
+    // than the idle tail it removes: fwd 8192x4096->1024 92 vs 56 us, dW
+    // 4096^2 219 vs 215 us, dW 1024x4096 93 vs 78 us -- and is not built)
+    // stream-K tail (opt-in, TPP_STREAMK=1)
+    const int workers = grid / CL;
+    if (units > workers && units % workers != 0 && (units % workers) * 10 < workers * 9 &&
+        S >= 4 && !env_no_streamk()) {
       unsigned* flags = nullptr;
       float* ws = sk_workspace(stream, (size_t)workers * CG * BM * BN, &flags);
       if (ws) {
