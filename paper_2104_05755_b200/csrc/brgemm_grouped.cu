@@ -1,5 +1,5 @@
 // K11: the BRGEMM TPP itself on tcgen05 — brgemm() over STRIDE / OFFSET /
-// ADDRESS batches of arbitrary (aligned) BF16 blocks, many C blocks per launch.
+// ADDRESS batches of arbitrary BF16 blocks, many C blocks per launch.
 //
 // Reference semantics (contraction.py:261-322): for every group g (one C
 // block; a single brgemm() call is one group)
@@ -9,16 +9,17 @@
 // block (ldb), C an m x n FP32 column-major block (ldc).  The blocks live at
 // arbitrary (16-byte aligned) addresses — the batch is an address / offset /
 // stride list, not a tensor — so operands cannot come through a TMA tensor
-// map.  Instead 4 producer warps move each (entry i, 64-deep k chunk) stage
+// map.  Instead 8 producer warps move each (entry i, 64-deep k chunk) stage
 // from global memory straight into the UMMA-canonical 128B-swizzled smem
 // layouts:
 //   B        K-major (k contiguous per column): 16-byte cp.async per chunk
 //   A PLAIN  MN-major (m contiguous per k):     16-byte cp.async per chunk
-//   A VNNI   K-major: a 32-bit word transpose in registers — 4 x 16-byte
-//            loads of (4 k-pairs x 4 rows) become 4 x 16-byte row chunks
-// (zero fill past m, n, k), several stages in flight (cp.async groups + a
-// one-stage register lookahead for VNNI), then fence.proxy.async and an
-// mbarrier arrive hand the stage to the MMA warp.  The MMA warp issues
+//   A VNNI   K-major: 4 x 16-byte cp.async of (4 k-pairs x 4 rows) into a raw
+//            area, then a 32-bit word transpose into 4 x 16-byte row chunks
+// (zero fill past m, n, k), STAGES - 2 stages in flight per thread (cp.async
+// groups; VNNI A lands raw and each thread transposes its own words once its
+// group completed), then fence.proxy.async and an mbarrier arrive hand the
+// stage to the MMA warp.  The MMA warp issues
 // tcgen05.mma kind::f16 (M = 64 when the C block has <= 64 rows, else 128;
 // N = 64/128/256) into a double-buffered TMEM accumulator — the whole batch
 // of a tile accumulates on chip — and 4 epilogue warps apply beta and store
@@ -38,11 +39,11 @@ using namespace sm100;
 namespace grp {
 
 constexpr int kEpiWarps = 4;    // warps 0-3: epilogue (TMEM lane quarter = warp)
-constexpr int kProdWarp0 = 4;   // warps 4-7: producers
-constexpr int kProd = 128;
-constexpr int kMmaWarp = 8;     // MMA issue + TMEM allocation
-constexpr int kThreads = 32 * 9;
-constexpr int kLag = 2;         // cp.async groups in flight per producer thread
+constexpr int kProdWarp0 = 4;   // warps 4-11: producers
+constexpr int kProdWarps = 8;
+constexpr int kProd = 32 * kProdWarps;
+constexpr int kMmaWarp = kProdWarp0 + kProdWarps;  // MMA issue + TMEM allocation
+constexpr int kThreads = 32 * (kMmaWarp + 1);
 
 struct GParams {
   int m, n, k, lda, ldb, ldc;
@@ -67,7 +68,8 @@ template <int BM, int BN, int STAGES>
 struct GSmem {
   static constexpr int A_BYTES = BM * 128;  // BM rows x 64 k (bf16)
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int RAW_BYTES = BM * 128;  // VNNI A as loaded, before the word transpose
+  static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE;
   static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * BN;
@@ -102,7 +104,8 @@ __device__ __forceinline__ const uint16_t* op_ptr(int kind, const uint16_t* base
 
 // the producer's walk over (work item, batch entry, k chunk)
 struct StageIt {
-  long long tile, i;
+  int tile;
+  long long i;
   int kc;
 };
 
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const long long ntiles = p.groups * p.tiles_m * p.tiles_n;
+  const int ntiles = (int)(p.groups * p.tiles_m * p.tiles_n);   // < 2^31 (checked by the host)
   const long long per_tile = p.count * p.kchunks;
 
   if (threadIdx.x == 0) {
@@ -139,17 +142,48 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  if (warp >= kProdWarp0 && warp < kProdWarp0 + 4) {
+  if (warp >= kProdWarp0 && warp < kProdWarp0 + kProdWarps) {
     // ============================ producers ============================
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int t = threadIdx.x - kProdWarp0 * 32;
-    constexpr int AU = BM * 2 / kProd;  // VNNI units (4 k-pairs x 4 rows) per thread: 8 * BM/4 / 128
-    auto tile_coords = [&](long long tile, long long& g, int& tm, int& tn) {
-      const long long per_g = (long long)p.tiles_m * p.tiles_n;
+    // ---- per-thread chunk assignments, fixed for the whole kernel (the
+    // fast path's per-stage work is then a few adds per 16-byte copy) ----
+    // B (K-major, BN rows x 8 chunks): rows br0 + BRS j, chunk bq
+    constexpr int BRS = kProd / 8, BJ = BN / BRS;
+    const int br0 = t >> 3, bq = t & 7;
+    const uint32_t b_soff = (br0 >> 3) * 1024 + (br0 & 7) * 128 + ((bq ^ (br0 & 7)) << 4);  // + j * BRS * 128
+    // A PLAIN (MN-major, 64 k rows x BM/8 chunks): k rows akk0 + AKS j, chunk ach
+    constexpr int CPR = BM / 8, AKS = kProd / CPR, AJ = 64 / AKS;
+    const int akk0 = t / CPR, ach = t % CPR;
+    const uint32_t a_soff = (ach >> 3) * 8192 + (akk0 >> 3) * 1024 + (akk0 & 7) * 128 +
+                            (((ach & 7) ^ (akk0 & 7)) << 4);  // + j * AKS * 128
+    // A VNNI: units (k-pair quad pq, row quad mq) = t + u * 128
+    constexpr int AU = (BM * 2 + kProd - 1) / kProd;   // units of 4 k-pairs x 4 rows: 8 * BM / 4 in all
+    constexpr int NUNITS = BM * 2;
+    // ---- per-tile state, refreshed when the walk reaches a new tile ----
+    int cur_tile = -1, tm = 0, tn = 0;
+    long long g = 0;
+    long long b_toff = 0, a_toff = 0;   // element offsets of this thread's first chunk in a block
+    uint32_t b_rows_ok = 0;             // bit j: B row br0 + 16 j exists
+    bool a_rows_ok = false;             // PLAIN: rows tm*BM + ach*8 .. +7 exist
+    uint32_t v_rows_ok = 0;             // VNNI: bit u: rows of unit u exist
+    auto set_tile = [&](int tile) {
+      const int per_g = p.tiles_m * p.tiles_n;
       g = tile / per_g;
-      const int rem = (int)(tile - g * per_g);
+      const int rem = tile - (int)g * per_g;
       tm = rem / p.tiles_n;
       tn = rem - tm * p.tiles_n;
+      b_toff = (long long)(tn * BN + br0) * p.ldb + bq * 8;
+      b_rows_ok = 0;
+#pragma unroll
+      for (int jj = 0; jj < BJ; ++jj) b_rows_ok |= (uint32_t)(tn * BN + br0 + BRS * jj < p.n) << jj;
+      a_toff = tm * BM + ach * 8 + (long long)akk0 * p.lda;
+      a_rows_ok = tm * BM + ach * 8 < p.m;
+      v_rows_ok = 0;
+#pragma unroll
+      for (int u = 0; u < AU; ++u)
+        v_rows_ok |= (uint32_t)(t + u * kProd < NUNITS && tm * BM + ((t + u * kProd) % (BM / 4)) * 4 < p.m) << u;
+      cur_tile = tile;
     };
     auto advance = [&](StageIt& s) {
       if (++s.kc == p.kchunks) {
@@ -160,49 +194,54 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         }
       }
     };
-    // A stage takes the fast path (16-byte cp.async / vector loads) when the
-    // problem's extents and strides are multiples of 8 elements and both
-    // block addresses are 16-byte aligned; otherwise every 16-byte smem chunk
-    // is assembled from 2-byte loads (any shape, any alignment).
-    auto stage_ptrs = [&](const StageIt& st, long long& g, int& tm, int& tn, const uint16_t*& ap,
-                          const uint16_t*& bp) -> bool {
-      tile_coords(st.tile, g, tm, tn);
+    // A stage takes the fast path (16-byte cp.async) when the problem's
+    // extents and strides are multiples of 8 elements and both block
+    // addresses are 16-byte aligned; otherwise every 16-byte smem chunk is
+    // assembled from 2-byte loads (any shape, any alignment).
+    auto stage_ptrs = [&](const StageIt& st, const uint16_t*& ap, const uint16_t*& bp) -> bool {
+      if ((int)st.tile != cur_tile) set_tile((int)st.tile);
       ap = op_ptr(p.kind, p.a, p.a_idx, p.stride_a, p.count, g, st.i);
       bp = op_ptr(p.kind, p.b, p.b_idx, p.stride_b, p.count, g, st.i);
       return p.dims_ok && ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(bp)) & 15) == 0;
     };
-    // VNNI A: (k-pair quad pq, row quad mq) units; 4 x 16 B loads = words (p, m..m+3) for 4 k-pairs
-    auto load_vnni = [&](const StageIt& st, uint4 (&r)[AU][4]) {
-      long long g;
-      int tm, tn;
-      const uint16_t *ap, *bp;
-      if (!stage_ptrs(st, g, tm, tn, ap, bp)) return;  // generic stage: assembled at store time
+    // VNNI A fast path: each unit is 4 x 16 B cp.async of words (p, m..m+3)
+    // for 4 consecutive k-pairs into this thread's own 64 B of the stage's
+    // raw area; once they land (the thread's own cp.async group) the thread
+    // word-transposes them into 4 16-byte K-major row chunks of the A tile
+    auto issue_vnni = [&](int kc, const uint16_t* ap, uint32_t sRaw) {
 #pragma unroll
       for (int u = 0; u < AU; ++u) {
         const int unit = t + u * kProd;
+        if (unit >= NUNITS) break;
         const int pq = unit / (BM / 4), mq = unit % (BM / 4);
-        const int mrow = tm * BM + mq * 4;
-        const int k0 = st.kc * 64 + pq * 8;
-        const bool ok = mrow < p.m && k0 < p.k;
+        const int k0 = kc * 64 + pq * 8;
+        const bool ok = ((v_rows_ok >> u) & 1u) && k0 < p.k;
+        const uint16_t* src = ap + (long long)(k0 >> 1) * 2 * p.m + 2 * (tm * BM + mq * 4);
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp) {
-          const long long pr = (long long)(k0 >> 1) + pp;
-          r[u][pp] = ok ? ldg_nc16(ap + pr * 2 * p.m + 2 * mrow) : make_uint4(0, 0, 0, 0);
-        }
+        for (int pp = 0; pp < 4; ++pp)
+          cp_async16(sRaw + (unit * 4 + pp) * 16, ok ? (const void*)(src + (long long)pp * 2 * p.m) : (const void*)ap,
+                     ok ? 16 : 0);
       }
     };
-    auto store_vnni = [&](uint32_t sA, const uint4 (&r)[AU][4]) {
+    auto transpose_vnni = [&](uint32_t sRaw, uint32_t sA) {
 #pragma unroll
       for (int u = 0; u < AU; ++u) {
         const int unit = t + u * kProd;
+        if (unit >= NUNITS) break;
         const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+        uint4 r[4];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp)
+          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(r[pp].x), "=r"(r[pp].y), "=r"(r[pp].z), "=r"(r[pp].w)
+                       : "r"(sRaw + (unit * 4 + pp) * 16));
 #pragma unroll
         for (int mm = 0; mm < 4; ++mm) {
           const int row = mq * 4 + mm;
-          const uint32_t w0 = mm == 0 ? r[u][0].x : mm == 1 ? r[u][0].y : mm == 2 ? r[u][0].z : r[u][0].w;
-          const uint32_t w1 = mm == 0 ? r[u][1].x : mm == 1 ? r[u][1].y : mm == 2 ? r[u][1].z : r[u][1].w;
-          const uint32_t w2 = mm == 0 ? r[u][2].x : mm == 1 ? r[u][2].y : mm == 2 ? r[u][2].z : r[u][2].w;
-          const uint32_t w3 = mm == 0 ? r[u][3].x : mm == 1 ? r[u][3].y : mm == 2 ? r[u][3].z : r[u][3].w;
+          const uint32_t w0 = mm == 0 ? r[0].x : mm == 1 ? r[0].y : mm == 2 ? r[0].z : r[0].w;
+          const uint32_t w1 = mm == 0 ? r[1].x : mm == 1 ? r[1].y : mm == 2 ? r[1].z : r[1].w;
+          const uint32_t w2 = mm == 0 ? r[2].x : mm == 1 ? r[2].y : mm == 2 ? r[2].z : r[2].w;
+          const uint32_t w3 = mm == 0 ? r[3].x : mm == 1 ? r[3].y : mm == 2 ? r[3].z : r[3].w;
           sts16(sA + (row >> 3) * 1024 + (row & 7) * 128 + ((pq ^ (row & 7)) << 4), make_uint4(w0, w1, w2, w3));
         }
       }
@@ -213,31 +252,30 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       return v;
     };
     // fast path: cp.async for B (K-major) and PLAIN A (MN-major)
-    auto issue_fast = [&](int tm, int tn, int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA,
-                          uint32_t sB) {
+    auto issue_fast = [&](int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA, uint32_t sB) {
       const int kb = kc * 64;
-      for (int c = t; c < BN * 8; c += kProd) {
-        const int r = c >> 3, q = c & 7;
-        const int nn = tn * BN + r, kk = kb + q * 8;
-        const bool ok = nn < p.n && kk < p.k;
-        cp_async16(sB + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4),
-                   ok ? (const void*)(bp + (long long)nn * p.ldb + kk) : (const void*)bp, ok ? 16 : 0);
+      {
+        const bool kok = kb + bq * 8 < p.k;
+        const uint16_t* src = bp + b_toff + kb;
+        const long long step = (long long)BRS * p.ldb;
+#pragma unroll
+        for (int jj = 0; jj < BJ; ++jj) {
+          const bool ok = kok && ((b_rows_ok >> jj) & 1u);
+          cp_async16(sB + b_soff + jj * BRS * 128, ok ? (const void*)(src + jj * step) : (const void*)bp, ok ? 16 : 0);
+        }
       }
       if (!p.vnni) {
-        constexpr int CPR = BM / 8;  // 16-byte chunks per k row
-        for (int c = t; c < 64 * CPR; c += kProd) {
-          const int kk = c / CPR, ch = c % CPR;
-          const int j = ch >> 3, cc = ch & 7;
-          const int mrow = tm * BM + ch * 8, kg = kb + kk;
-          const bool ok = mrow < p.m && kg < p.k;
-          cp_async16(sA + j * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((cc ^ (kk & 7)) << 4),
-                     ok ? (const void*)(ap + mrow + (long long)kg * p.lda) : (const void*)ap, ok ? 16 : 0);
+        const uint16_t* src = ap + a_toff + (long long)kb * p.lda;
+        const long long step = (long long)AKS * p.lda;
+#pragma unroll
+        for (int jj = 0; jj < AJ; ++jj) {
+          const bool ok = a_rows_ok && kb + akk0 + AKS * jj < p.k;
+          cp_async16(sA + a_soff + jj * AKS * 128, ok ? (const void*)(src + jj * step) : (const void*)ap, ok ? 16 : 0);
         }
       }
     };
     // generic path: every chunk from 2-byte loads, bounds per element
-    auto issue_generic = [&](int tm, int tn, int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA,
-                             uint32_t sB) {
+    auto issue_generic = [&](int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA, uint32_t sB) {
       const int kb = kc * 64;
       for (int c = t; c < BN * 8; c += kProd) {  // B: column nn, k = kk .. kk+7
         const int r = c >> 3, q = c & 7;
@@ -281,49 +319,48 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         }
       }
     };
+    // LAG stages in flight per thread: stage it's cp.async group is waited
+    // for (and, for VNNI A, transposed) LAG stages later, then handed over
+    constexpr int LAG = STAGES - 2;
     StageIt cur{blockIdx.x, 0, 0};
-    StageIt pre = cur;
-    uint4 ra[AU][4], rb[AU][4];
-    if (p.vnni && pre.tile < ntiles) {
-      load_vnni(pre, ra);
-      advance(pre);
-    }
     uint32_t it = 0;
-    auto one = [&](uint4 (&mine)[AU][4], uint4 (&next)[AU][4]) -> bool {
-      if (cur.tile >= ntiles) return false;
+    uint32_t vmask = 0;   // bit (stage % 32): that stage still needs its VNNI transpose
+    auto finish = [&](uint32_t j) {
+      const int sj = j % STAGES;
+      if ((vmask >> (j & 31)) & 1u) {
+        const uint32_t base = smem_u32(smem + sj * S::STAGE);
+        transpose_vnni(base + S::A_BYTES + S::B_BYTES, base);
+        vmask &= ~(1u << (j & 31));
+      }
+      fence_async_smem();
+      mbar_arrive(&full[sj]);
+    };
+    while (cur.tile < ntiles) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
-      if (p.vnni && pre.tile < ntiles) {  // one stage of register lookahead
-        load_vnni(pre, next);
-        advance(pre);
-      }
-      long long g;
-      int tm, tn;
       const uint16_t *ap, *bp;
-      const bool fast = stage_ptrs(cur, g, tm, tn, ap, bp);
+      const bool fast = stage_ptrs(cur, ap, bp);
       mbar_wait(&empty[s], ph ^ 1);
       const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
       if (fast) {
-        issue_fast(tm, tn, cur.kc, ap, bp, sA, sB);
-        if (p.vnni) store_vnni(sA, mine);
+        issue_fast(cur.kc, ap, bp, sA, sB);
+        if (p.vnni) {
+          issue_vnni(cur.kc, ap, sB + S::B_BYTES);
+          vmask |= 1u << (it & 31);
+        }
       } else {
-        issue_generic(tm, tn, cur.kc, ap, bp, sA, sB);
+        issue_generic(cur.kc, ap, bp, sA, sB);
       }
       cp_async_commit();
-      if (it >= (uint32_t)kLag) {
-        cp_async_wait<kLag>();
-        fence_async_smem();
-        mbar_arrive(&full[(it - kLag) % STAGES]);
+      if (it >= (uint32_t)LAG) {
+        cp_async_wait<LAG>();
+        finish(it - LAG);
       }
       advance(cur);
       ++it;
-      return true;
-    };
-    while (one(ra, rb) && one(rb, ra)) {
     }
     cp_async_wait<0>();
-    fence_async_smem();
-    for (uint32_t j = it > (uint32_t)kLag ? it - kLag : 0; j < it; ++j) mbar_arrive(&full[j % STAGES]);
+    for (uint32_t j = it > (uint32_t)LAG ? it - LAG : 0; j < it; ++j) finish(j);
   } else if (warp == kMmaWarp) {
     // ============================ MMA issue ============================
     const uint32_t idesc = idesc_bf16_f32(BM, BN, p.vnni ? 0 : 1, 0);
@@ -331,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     const uint64_t b0 = sw128_kmajor_desc(smem_u32(smem + S::A_BYTES));
     const uint32_t astep = p.vnni ? (32 >> 4) : (2048 >> 4);
     uint32_t it = 0, tcount = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       mbar_wait(&tempty[as], aph ^ 1);
       tc_fence_after();
@@ -357,10 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     const int lrow = BM == 128 ? q * 32 + lane : q * 16 + lane;
     const bool lane_ok = BM == 128 || lane < 16;
     uint32_t tcount = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
-      const long long per_g = (long long)p.tiles_m * p.tiles_n;
-      const long long g = tile / per_g;
-      const int rem = (int)(tile - g * per_g);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+      const int per_g = p.tiles_m * p.tiles_n;
+      const int g = tile / per_g;
+      const int rem = tile - g * per_g;
       const int tm = rem / p.tiles_n, tn = rem - tm * p.tiles_n;
       float* cg = p.c + (p.c_off ? p.c_off[g] : 0);
       const int row = tm * BM + lrow;
@@ -458,17 +495,22 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.beta = (float)d->beta;
   p.beta_mode = d->beta == 0.0 ? 0 : d->beta == 1.0 ? 1 : 2;
   const int BM = d->m <= 64 ? 64 : 128;
-  const int BN = d->n <= 64 ? 64 : d->n <= 128 ? 128 : 256;
+  // widest N tile that still gives every SM a tile (one C block of a
+  // single brgemm() call is otherwise only a handful of work items)
+  const long long tm_all = groups * ((d->m + BM - 1) / BM);
+  int BN = d->n <= 64 ? 64 : d->n <= 128 ? 128 : 256;
+  while (BN > 64 && tm_all * ((d->n + BN - 1) / BN) < num_sms()) BN /= 2;
   p.tiles_m = (d->m + BM - 1) / BM;
   p.tiles_n = (d->n + BN - 1) / BN;
+  TPP_REQUIRE(groups * p.tiles_m * p.tiles_n < (1LL << 31), TPP_E_UNSUPPORTED, "grouped BRGEMM: too many tiles");
   if (BM == 64) {
     if (BN == 64) return launch<64, 64, 8>(p, s);
     if (BN == 128) return launch<64, 128, 6>(p, s);
     return launch<64, 256, 4>(p, s);
   }
-  if (BN == 64) return launch<128, 64, 6>(p, s);
-  if (BN == 128) return launch<128, 128, 5>(p, s);
-  return launch<128, 256, 4>(p, s);
+  if (BN == 64) return launch<128, 64, 5>(p, s);
+  if (BN == 128) return launch<128, 128, 4>(p, s);
+  return launch<128, 256, 3>(p, s);
 }
 
 }  // namespace tpp
