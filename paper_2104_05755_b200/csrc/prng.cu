@@ -328,6 +328,143 @@ __global__ void __launch_bounds__(256) dropout_mask_kernel(const uint32_t* __res
   }
 }
 
+// DROPOUT fused (dense BF16 / FP32 column-major views, rows % 64 == 0): the
+// keep draws and the scaled copy in ONE pass.  Lane = column for the draws
+// (warp = 32 columns x a run of `run` rows, one jump, as
+// dropout_mask_kernel); the data moves coalesced instead: per 64-row slab the
+// warp's 32 x 64 block is read as 8 passes of 4 columns x 64 rows (8 lanes
+// per column, 16 contiguous bytes each), issued BEFORE the slab's draws so
+// the HBM reads are in flight while the ALU runs the xorshift steps (BF16:
+// one slab ahead); each lane fetches its columns' keep byte from the drawing
+// lane with a shuffle, applies keep ? x * scale : 0 (the DROPOUT_INV rule,
+// FP32 math, RNE + the reference NaN rule for BF16) and stores 16 bytes; the
+// drawing lane stores its 8-byte mask word.  Bitwise the mask kernel +
+// DROPOUT_INV.
+template <typename TI>
+struct SlabPart;
+template <>
+struct SlabPart<uint16_t> {  // 8 rows of BF16 = 16 B per lane per pass
+  static constexpr int N = 1;
+  uint4 v[8];
+  __device__ __forceinline__ void load(const uint16_t* p, int64_t col_stride, bool ok) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+      v[it] = ok ? __ldg(reinterpret_cast<const uint4*>(p + it * 4 * col_stride)) : make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void get(int it, float (&x)[8]) const {
+    const uint32_t w[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[2 * q] = __uint_as_float(w[q] << 16);
+      x[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+    }
+  }
+};
+template <>
+struct SlabPart<float> {  // 8 rows of FP32 = 32 B per lane per pass
+  float4 v[16];
+  __device__ __forceinline__ void load(const float* p, int64_t col_stride, bool ok) {
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const float4* q = reinterpret_cast<const float4*>(p + it * 4 * col_stride);
+      v[2 * it] = ok ? __ldg(q) : make_float4(0, 0, 0, 0);
+      v[2 * it + 1] = ok ? __ldg(q + 1) : make_float4(0, 0, 0, 0);
+    }
+  }
+  __device__ __forceinline__ void get(int it, float (&x)[8]) const {
+    const float4 a = v[2 * it], b = v[2 * it + 1];
+    x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+  }
+};
+
+template <typename TO>
+__device__ __forceinline__ void store8_vec(TO* op, const float (&r)[8]) {
+  if constexpr (sizeof(TO) == 2) {
+    uint32_t u[4];
+    pack_bf16_ref_n<4>(r, u);
+    *reinterpret_cast<uint4*>(op) = make_uint4(u[0], u[1], u[2], u[3]);
+  } else {
+    reinterpret_cast<float4*>(op)[0] = make_float4(r[0], r[1], r[2], r[3]);
+    reinterpret_cast<float4*>(op)[1] = make_float4(r[4], r[5], r[6], r[7]);
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) dropout_fused_kernel(const uint32_t* __restrict__ st_in,
+                                                            uint32_t* __restrict__ st_out, uint32_t thr24,
+                                                            const TI* __restrict__ in, TO* __restrict__ out,
+                                                            uint8_t* __restrict__ mask_out, int rows, int cols,
+                                                            int run, float scale, const uint4* __restrict__ tab) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * kTileCols;
+  const int j = j0 + lane;
+  const int64_t rs64 = ((int64_t)blockIdx.y * kWarps + w) * run;
+  if (rs64 >= rows) return;                  // warp-uniform
+  const int rs = (int)rs64;
+  const int nslab = min(run, rows - rs) / kSub;
+  const bool draws = j < cols;
+  // data role: pass it covers columns j0 + 4 it + lane / 8, rows (lane % 8) * 8 .. + 7 of the slab
+  const int dc = lane >> 3, dr = (lane & 7) * 8;
+  const int64_t col_stride = rows;
+  const int64_t d0 = (int64_t)(j0 + dc) * col_stride + rs + dr;
+  const int valid_cols = min(kTileCols, cols - j0);
+  uint64_t* mb = reinterpret_cast<uint64_t*>(mask_out + (int64_t)j * (rows >> 3) + (rs >> 3));
+  SlabPart<TI> cur;
+  const bool full_group = valid_cols == kTileCols;
+  if (full_group) cur.load(in + d0, col_stride, true);
+  Xs128 s{0u, 0u, 0u, 1u};
+  if (draws) s = start_state(st_in, cols, j, rs, tab);
+#pragma unroll 1
+  for (int q = 0; q < nslab; ++q) {
+    SlabPart<TI> nxt;
+    if (sizeof(TI) == 2 && full_group && q + 1 < nslab) nxt.load(in + d0 + (q + 1) * kSub, col_stride, true);
+    uint64_t bits = 0;
+    if (draws) bits = draw_keep64(s, thr24, kSub);
+    const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int c = 4 * it + dc;                       // column (within the group) this lane moves
+      const uint32_t wl = __shfl_sync(0xffffffffu, lo, c), wh = __shfl_sync(0xffffffffu, hi, c);
+      const uint32_t byte = ((dr < 32 ? wl : wh) >> (dr & 31)) & 0xFFu;
+      if (c < valid_cols) {
+        float x[8];
+        if (full_group) {
+          cur.get(it, x);
+        } else {  // ragged last column group: this lane's 8 values directly
+          const TI* src = in + d0 + (int64_t)4 * it * col_stride + q * kSub;
+          if constexpr (sizeof(TI) == 2) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+            const uint32_t ww[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[2 * e] = __uint_as_float(ww[e] << 16);
+              x[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+            }
+          } else {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(src)), b = __ldg(reinterpret_cast<const float4*>(src) + 1);
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+          }
+        }
+        float r[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[e] = ((byte >> e) & 1u) ? __fmul_rn(x[e], scale) : 0.0f;
+        store8_vec<TO>(out + d0 + (int64_t)4 * it * col_stride + q * kSub, r);
+      }
+    }
+    if (draws) mb[q] = bits;
+    if (full_group && q + 1 < nslab) {
+      if (sizeof(TI) == 2) cur = nxt;                      // BF16: loaded one slab ahead
+      else cur.load(in + d0 + (q + 1) * kSub, col_stride, true);
+    }
+  }
+  if (draws && rs + nslab * kSub == rows) {  // this thread drew the column's last row
+    st_out[j] = s.x;
+    st_out[cols + j] = s.y;
+    st_out[2 * cols + j] = s.z;
+    st_out[3 * cols + j] = s.w;
+  }
+}
+
 // PRNG fill (ops.py:416-427): FP32 uniforms.  Item = blockIdx.x: column group
 // item / parts, row part item % parts; warp w draws `run` contiguous rows, 64
 // at a time into shared memory, and the CTA streams each 32 x (8 x 64) slab.
@@ -430,6 +567,11 @@ static int sm_count() {
   return n;
 }
 
+static bool dropout_unfused() {  // experiments: TPP_DROPOUT_UNFUSED=1 keeps mask kernel + DROPOUT_INV
+  static const bool v = getenv("TPP_DROPOUT_UNFUSED") != nullptr;
+  return v;
+}
+
 int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t* st_out, double p,
                      void* out, int out_dtype, int out_ld, uint8_t* mask_out, int rows, int cols, bool f64,
                      cudaStream_t s) {
@@ -461,6 +603,39 @@ int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t*
   // 1) keep mask.  keep <=> (float)(w >> 8) * 2^-24 >= float32(p) <=> (w >> 8) >= ceil(float32(p) * 2^24)
   const double thr = std::ceil((double)(float)p * 16777216.0);
   const uint32_t thr24 = (uint32_t)thr;  // <= 2^24; 2^24 means "never keep"
+  // dense column-major BF16 / FP32 views with whole 64-row slabs: draws and
+  // the scaled copy fused into one pass
+  if (!f64 && rows % kSub == 0 && in.ld == rows && out_ld == rows && in.bcast == TPP_BCAST_NONE &&
+      (in.dtype == TPP_BF16 || in.dtype == TPP_FP32) && (out_dtype == TPP_BF16 || out_dtype == TPP_FP32) &&
+      ((uintptr_t)in.p & 15) == 0 && ((uintptr_t)out & 15) == 0 && ((uintptr_t)mask_out & 7) == 0 &&
+      !dropout_unfused()) {
+    const int64_t target_threads = (int64_t)sm_count() * 1024;
+    int64_t run64 = ((int64_t)rows * cols + target_threads - 1) / target_threads;
+    run64 = (run64 + kSub - 1) / kSub * kSub;
+    if (run64 < kSub) run64 = kSub;
+    if (run64 > rows) run64 = rows;
+    const int run = (int)run64;
+    const int64_t segs = ((int64_t)rows + run - 1) / run;
+    const int64_t gy = (segs + kWarps - 1) / kWarps;
+    if (gy <= 65535 && cgroups <= 0x7fffffff) {
+      const float scale = compute_scale<float>(p);
+      const dim3 grid((unsigned)cgroups, (unsigned)gy);
+      if (in.dtype == TPP_BF16 && out_dtype == TPP_BF16)
+        dropout_fused_kernel<uint16_t, uint16_t><<<grid, kWarps * 32, 0, s>>>(
+            st_in, st_out, thr24, (const uint16_t*)in.p, (uint16_t*)out, mask_out, rows, cols, run, scale, tab);
+      else if (in.dtype == TPP_BF16)
+        dropout_fused_kernel<uint16_t, float><<<grid, kWarps * 32, 0, s>>>(
+            st_in, st_out, thr24, (const uint16_t*)in.p, (float*)out, mask_out, rows, cols, run, scale, tab);
+      else if (out_dtype == TPP_BF16)
+        dropout_fused_kernel<float, uint16_t><<<grid, kWarps * 32, 0, s>>>(
+            st_in, st_out, thr24, (const float*)in.p, (uint16_t*)out, mask_out, rows, cols, run, scale, tab);
+      else
+        dropout_fused_kernel<float, float><<<grid, kWarps * 32, 0, s>>>(
+            st_in, st_out, thr24, (const float*)in.p, (float*)out, mask_out, rows, cols, run, scale, tab);
+      TPP_CUDA_LAUNCH_CHECK("dropout_fused_kernel");
+      return TPP_OK;
+    }
+  }
   // runs sized for ~32 resident warps per SM (a jump costs ~32 L1 loads)
   const int64_t target_threads = (int64_t)sm_count() * 1024;
   int64_t run64 = ((int64_t)rows * cols + target_threads - 1) / target_threads;
