@@ -683,6 +683,27 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
         del a, b, cs
     except Exception as e:
         out["int8_brgemm_tc"] = {"error": str(e)[:200]}
+    # ---- 1-D dilated conv at the paper's ATACworks scale (address/stride BRGEMM user) ----
+    try:
+        C_, K_, S_, d_, Q_ = 15, 15, 51, 8, 60000
+        W_ = Q_ + (S_ - 1) * d_
+        spec_d = tpp.DilatedConvSpec(C_, K_, W_, Q_, S_, d_)
+        inp = tpp.TensorView(tpp.TensorDesc(C_, W_, C_, tpp.DType.FP32),
+                             torch.randn(C_ * W_, generator=gen, device=dev))
+        wv = tpp.TensorView(tpp.TensorDesc(C_ * S_, K_, C_ * S_, tpp.DType.FP32),
+                            torch.randn(C_ * S_ * K_, generator=gen, device=dev))
+        outd = tpp.alloc(tpp.TensorDesc(K_, Q_, K_, tpp.DType.FP32), device=dev)
+        g = graph_of(torch, [lambda: tpp.dilated_conv1d_forward(spec_d, inp, wv, outd)] * 5)
+        ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.3)) / 5
+        fl = 2 * C_ * K_ * S_ * Q_
+        simt = 148 * 128 * 2 * 1.965e9 / 1e12   # FP32 SIMT peak (TFLOP/s), SURVEY §8(d)
+        out["dilated_conv1d_atacworks"] = {
+            "shape": "W=60400, Q=60000, C=K=15, S=51, d=8, FP32 (PAPER.md:819)", "us": round(ms * 1e3, 2),
+            "GFLOP/s": round(fl / ms / 1e6, 1), "frac_fp32_simt_peak": round(fl / ms / 1e9 / simt, 4),
+            "parity": "bitwise vs the reference order (tests/test_gpu_parity.py)"}
+        del inp, wv, outd
+    except Exception as e:
+        out["dilated_conv1d_atacworks"] = {"error": str(e)[:200]}
     # ---- cfg 1: FP32 BRGEMM 16 x 64^3, beta = 1, reference order (bitwise) ------
     try:
         m = n = k = 64

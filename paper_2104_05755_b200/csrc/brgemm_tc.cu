@@ -23,6 +23,7 @@
 // The batch-reduce loop accumulates on chip: C is written exactly once.
 
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -873,10 +874,41 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // 5-D bf16 map, dims innermost first, strides in bytes for dims 1..4
+// Encoded maps are cached per thread (the same layer calls encode the same
+// three maps every time; cuTensorMapEncodeTiled costs ~2-3 us of host time
+// per map, more than a small layer's kernel): key = every encode argument.
+struct MapKey {
+  const void* base;
+  uint64_t dims[5], strides[4];
+  uint32_t box[5];
+  int swz, dt;
+  bool operator==(const MapKey& o) const { return memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapCache {
+  static constexpr int N = 48;
+  MapKey key[N];
+  CUtensorMap map[N];
+  int used = 0, next = 0;
+};
+
 static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
                        const uint64_t strides[4], const uint32_t box[5],
                        CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B,
                        CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16) {
+  thread_local MapCache cache;
+  MapKey k;
+  memset(&k, 0, sizeof(k));
+  k.base = base;
+  memcpy(k.dims, dims, sizeof(k.dims));
+  memcpy(k.strides, strides, sizeof(k.strides));
+  memcpy(k.box, box, sizeof(k.box));
+  k.swz = (int)swz;
+  k.dt = (int)dt;
+  for (int i = 0; i < cache.used; ++i)
+    if (cache.key[i] == k) {
+      *m = cache.map[i];
+      return TPP_OK;
+    }
   auto enc = get_encode();
   if (!enc) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (reinterpret_cast<uintptr_t>(base) % 16) return fail(TPP_E_TENSOR, "TMA base not 16B aligned");
@@ -896,6 +928,9 @@ static int make_map_5d(CUtensorMap* m, const void* base, const uint64_t dims[5],
                    es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TPP_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  const int slot = cache.used < MapCache::N ? cache.used++ : (cache.next++ % MapCache::N);
+  cache.key[slot] = k;
+  cache.map[slot] = *m;
   return TPP_OK;
 }
 

@@ -944,3 +944,20 @@ def test_fc_gelu_epilogue_special_values():
     got = to_host(out).reshape(Nb, 1, bn, 64)
     want, _, _ = O.fc_forward_bf16(xb, wv, None, activation="gelu")
     assert bf16_equal(got.reshape(-1), np.asarray(want).reshape(-1))
+
+
+def test_dilated_conv1d_atacworks_scale_bitwise():
+    """The paper's ATACworks layer: W = 60400, Q = 60000,
+    C = K = 15, S = 51, d = 8, FP32 — bitwise the reference order."""
+    rng = np.random.default_rng(300)
+    C_, K_, S_, d_, Q_ = 15, 15, 51, 8, 60000
+    W_ = Q_ + (S_ - 1) * d_ + 0   # 60400
+    x = rng.standard_normal((C_, W_)).astype(np.float32)
+    wt = rng.standard_normal((C_ * S_, K_)).astype(np.float32)
+    spec = tpp.DilatedConvSpec(C_, K_, W_, Q_, S_, d_)
+    inp = tpp.TensorView(tpp.TensorDesc(C_, W_, C_, tpp.DType.FP32), to_dev(x.T.reshape(-1)))
+    wv = tpp.TensorView(tpp.TensorDesc(C_ * S_, K_, C_ * S_, tpp.DType.FP32), to_dev(wt.T.reshape(-1)))
+    out = tpp.alloc(tpp.TensorDesc(K_, Q_, K_, tpp.DType.FP32))
+    tpp.dilated_conv1d_forward(spec, inp, wv, out)
+    want = O.dilated_conv1d(x, wt, C_, K_, S_, d_, Q_)
+    assert bits(tpp.to_array(out)) == bits(want)
