@@ -100,6 +100,8 @@ struct Params {
   int dbg_mode;  // experiments: bit0 skip epilogue math, bit1 skip MMAs
   int tma_store;            // BF16 output through smem staging + TMA (map_c)
   int cv_rows;              // conv: output rows per tile (2, or 4 for RES = 3)
+  int cv_wq;                // conv strips (RES = 4): position-space row stride W + pad
+  int stage_tx;             // conv strips: bytes one halo box lands (HR x Wq x 128)
   uint16_t* sgd_lo;         // TPP_FC_SGD: lo halves of the split FP32 master (out = hi halves)
   float sgd_lr;
   // stream-K tail (FC mode): work items [0, sk_dp) are whole tiles handed out
@@ -154,12 +156,23 @@ constexpr int kHaloRows = 4;   // 2 output rows + R - 1 (R <= 3)
 // weight tap, 6 halo rows per stage): per output row 1.5 halo rows cross L2->smem
 // instead of 2, and the per-tile handoff (commit, accumulator wait, stage wait)
 // is paid once per 4 rows
+// RES = 4 (conv strips): output positions p = oy * Wq + ox with Wq = W + pad
+// -- the right pad of input row y is the left pad of row y + 1, so the halo
+// is ONE TMA box of rows Wq pixels wide (x from -pad, OOB zero fill) and tap
+// (r, s) of position p reads halo row p + r * Wq + s: a uniform shift across
+// row boundaries.  A tile is 256 consecutive positions (two M = 128
+// accumulators) regardless of row ends, so only the pad column per row
+// (1/57 at W = 56) is wasted instead of 64 - W columns of a 64-wide row, and
+// the epilogue stores straight from registers (no smem staging on the port
+// the MMAs read operands through).
 template <int RES> struct ConvTile {
   static constexpr bool HALO = RES >= 2;
-  static constexpr int ROWS = RES == 3 ? 4 : 2;  // output rows per tile
+  static constexpr bool STRIP = RES == 4;
+  static constexpr int ROWS = RES >= 3 ? 4 : 2;  // output rows per tile (RES 3)
   static constexpr int NACC = ROWS / 2;           // M = 128 accumulators per tile
-  static constexpr int HROWS = ROWS + 2;          // input rows per halo (R <= 3)
+  static constexpr int HROWS = ROWS + 2;          // input rows per halo (R <= 3, RES 2/3)
 };
+constexpr int kStripHaloBytes = 66 * 1024;  // >= (Wq - 1 + 256 + 2 Wq + 2 + Wq) pixels x 128 B for Wq <= 64
 
 // CG = 2: CTA pair (cluster of 2, tcgen05 cta_group::2).  The pair computes a
 // 256 x BN tile: each CTA stages its own 128 rows of A and HALF of the B rows
@@ -168,22 +181,28 @@ template <int RES> struct ConvTile {
 // smem reads) drops by a quarter (BN=256: 48 KB -> 32 KB per 64-deep block).
 template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1>
 struct Smem {
-  static constexpr int A_BYTES = ConvTile<RES>::HALO ? ConvTile<RES>::HROWS * 64 * BK * 2 : KPS * BM * BK * 2;
+  static constexpr int A_BYTES = ConvTile<RES>::STRIP ? kStripHaloBytes
+                                 : ConvTile<RES>::HALO ? ConvTile<RES>::HROWS * 64 * BK * 2 : KPS * BM * BK * 2;
   static constexpr int B_BYTES = RES ? 0 : KPS * (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN * ConvTile<RES>::NACC;
+  // TMEM accumulator buffers: as many as fit in the 512 columns (<= 4).  A
+  // tile's tcgen05.ld is served behind the MMAs already queued on the tensor
+  // pipe, so with only two buffers the MMAs of tile t + 2 wait for an epilogue
+  // that itself waited for tile t + 1's MMAs; 4 buffers let them run on.
+  static constexpr int NBUF = 512 / (BN * ConvTile<RES>::NACC) >= 4 ? 4 : 2;
+  static constexpr int TMEM_COLS = NBUF * BN * ConvTile<RES>::NACC;
   static constexpr int RES_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = RES_OFF + (RES ? kResMaxBytes : 0);
-  // barriers: full[S], empty[S], tfull[2], tempty[2], bres; then tmem base +
+  // barriers: full[S], empty[S], tfull[NBUF], tempty[NBUF], bres; then tmem base +
   // gelu table (float4 x 512: one entry per 9-bit |x| exponent prefix)
-  static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 15) & ~15;
+  static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 2 * NBUF + 1) * 8 + 16 + 15) & ~15;
   // the conv (RES = 2) epilogue has no bias / GELU: no table, no bias staging
   static constexpr int BIAS_OFF = TAB_OFF + (RES >= 2 ? 0 : 512 * 16);    // float [2][256]
   // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
   // when the smem budget allows (a chunk's store need not have left the
   // buffer before the next chunk is staged)
   static constexpr int STG_OFF = (BIAS_OFF + (RES >= 2 ? 0 : 2 * 256 * 4) + 1023) & ~1023;
-  static constexpr int STG_BUFS = STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1;
+  static constexpr int STG_BUFS = ConvTile<RES>::STRIP ? 0 : (STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1);
   static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 * STG_BUFS + 1024;
 };
 
@@ -227,7 +246,9 @@ struct FeedIter {
       cb_n = p.cv_Cb; s_n = p.cv_S; pad = p.cv_pad;
       const int n = tm / p.cv_tiles_per_img, pr = tm % p.cv_tiles_per_img;
       s = 0;
-      ai.c[0] = 0; ai.c[1] = -pad; ai.c[2] = p.cv_rows * pr - pad; ai.c[3] = 0; ai.c[4] = n;
+      // strips: the halo starts at the input row of the tile's first position
+      const int y0 = p.cv_wq ? (pr * 2 * BM) / p.cv_wq : p.cv_rows * pr;
+      ai.c[0] = 0; ai.c[1] = -pad; ai.c[2] = y0 - pad; ai.c[3] = 0; ai.c[4] = n;
     }
   }
   __device__ __forceinline__ void next() {
@@ -310,8 +331,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* bres = tempty + 2;
+  uint64_t* tempty = tfull + S::NBUF;
+  uint64_t* bres = tempty + S::NBUF;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
@@ -344,7 +365,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], MC);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < S::NBUF; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);
     }
@@ -436,7 +457,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             } else if ((TPP_DBG_MODE & 4) && it >= STAGES) {
               mbar_arrive(&full[s]);  // diagnostics: reuse the resident stage, no TMA traffic
             } else {
-              mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+              mbar_arrive_expect_tx(&full[s], CT::STRIP ? (uint32_t)p.stage_tx : (uint32_t)S::STAGE_BYTES);
               // halo conv: the input box at (cb = j) covering all taps
               if (!MCAST)
                 tma_load_5d(sa, &map_a, &full[s], f.ai.c[0], f.ai.c[1], f.ai.c[2], CT::HALO ? j : f.ai.c[3], f.ai.c[4]);
@@ -475,13 +496,18 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       Seg sg;
       for (; walk.next(sg); ++tcount) {
         const int j0 = sg.k0;
-        const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
+        const uint32_t as = tcount % S::NBUF, aph = (tcount / S::NBUF) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount < 32, 240 + tcount, gtimer());
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 320 + (tcount == 30) * 2, clock64());
         TPP_STAMP(blockIdx.x == 0 && lane == 0 && (tcount == 4 || tcount == 30), 321 + (tcount == 30) * 2, gtimer());
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + as * (BN * CT::NACC);
+        uint64_t strip_off = 0;  // strips: halo row of the tile's first position, 16-byte units
+        if (CT::STRIP) {
+          const int p0 = (sg.tile % p.cv_tiles_per_img) * 2 * BM;
+          strip_off = (uint64_t)((p0 - (p0 / p.cv_wq) * p.cv_wq) * 8);
+        }
         for (int j = j0; j < sg.k1; ++j) {
           mbar_wait(&full[s], ph);
           TPP_STAMP(blockIdx.x == 0 && lane == 0 && tcount == p.dbg_tile && j == 0, 2, gtimer());
@@ -496,7 +522,23 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
             const uint64_t a0 = adesc0 + soff;
             const uint64_t b0 = bres0 + (uint64_t)((j * BN * BK * 2) >> 4);
             const uint64_t btap = (uint64_t)((p.cv_Cb * BN * BK * 2) >> 4);
-            if (p.cv_R == 3 && p.cv_S == 3) {
+            if (CT::STRIP) {
+              // tap (r, s), accumulator h: halo row off + h * 128 + r * Wq + s
+              const uint64_t a1 = a0 + strip_off;
+              const uint64_t wq8 = (uint64_t)p.cv_wq * 8;
+#pragma unroll
+              for (int tap = 0; tap < 9; ++tap) {
+                const uint64_t bd = b0 + btap * tap;
+                const uint64_t at = a1 + wq8 * (tap / 3) + 8 * (tap % 3);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                  for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_f16_warp(tmem_d + h * BN, at + (uint64_t)(h * BM * 8) + 2 * kk, bd + 2 * kk, idesc,
+                                  (j > j0 || tap > 0 || kk > 0) ? 1u : 0u);
+                }
+              }
+            } else if (p.cv_R == 3 && p.cv_S == 3) {
               // 3x3: every descriptor offset is an immediate (the single
               // issuing thread must keep pace with 48-cycle N=64 MMAs)
 #pragma unroll
@@ -590,8 +632,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           src_base = cl_id + 1;
         }
       }
-      const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
-      float* bs = bias_s + as * 256;
+      const uint32_t as = tcount % S::NBUF, aph = (tcount / S::NBUF) & 1;
+      float* bs = bias_s + (tcount & 1) * 256;
       if (p.flags & TPP_FC_BIAS) {
         // stage this tile's bias (COL broadcast) in smem while the MMAs run
         for (int i = ew * 32 + lane; i < BN; i += kEpiWarps * 32) {
@@ -703,6 +745,22 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch == 0, 7, gtimer());
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 0, clock64());
+        if (CT::STRIP) {
+          // position p0 + hacc * 128 + r of image n -> output pixel (oy, ox);
+          // the pad column (ox >= Q) and positions past the image are dropped
+          const int img = tm / p.cv_tiles_per_img;
+          const int pos = (tm - img * p.cv_tiles_per_img) * 2 * BM + hacc * BM + r;
+          const int oy = pos / p.cv_wq, ox = pos - oy * p.cv_wq;
+          if (ox < p.cv_Q && oy < p.cv_P) {
+            uint32_t w[16];
+            pack_bf16_ref_n<16>(x, w);
+            uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) +
+                                                 ((((int64_t)img * p.o_mb + tn) * p.cv_P + oy) * p.cv_Q + ox) * 64 + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+          }
+          continue;
+        }
         const int f0 = tn * BN + col;
         if (TPP_DBG_MODE & 1) continue;
         if (f0 >= p.feats || (!p.tma_store && t < 0)) continue;
@@ -1122,6 +1180,11 @@ static int launch(int bn_tile, int kps, int cg, const CUtensorMap& ma, const CUt
     switch (bn_tile) {
       case 64: return launch_cfg<64, 2, 1, 3>(ma, mb, mc, p, s);
     }
+  } else if (kps == -4) {
+    // strips: 256 consecutive Wq-stride positions per tile, one halo box
+    switch (bn_tile) {
+      case 64: return launch_cfg<64, 2, 1, 4>(ma, mb, mc, p, s);
+    }
   }
   return fail(TPP_E_UNSUPPORTED, "no kernel instantiation for this tile width / stage depth");
 }
@@ -1424,8 +1487,19 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   const bool res_ok = BN == 64 && feats / BN == 1 && (int64_t)p.kblocks * BN * 128 <= tc::kResMaxBytes;
   const bool halo_ok = res_ok && 2 + R - 1 <= tc::kHaloRows && W + S - 1 <= 64;
   const bool rows4 = halo_ok && !two_row && reinterpret_cast<uintptr_t>(out) % 16 == 0 && !env_no_tma_store();
+  // strips (RES 4): 3x3, pad 1, Wq = W + 1 <= 64, 16-byte aligned output
+  static const bool no_strip = getenv("TPP_CONV_ROWS") != nullptr;  // experiments: the row tiles
+  const int wq = W + pad;
+  const int strip_hr = (wq - 1 + 2 * BM + (R - 1) * wq + (S - 1) + wq - 1) / wq;
+  const bool strip = res_ok && !no_strip && R == 3 && S == 3 && pad == 1 && wq <= 64 &&
+                     strip_hr * wq * 128 <= tc::kStripHaloBytes && reinterpret_cast<uintptr_t>(out) % 16 == 0;
   p.cv_rows = rows4 ? 4 : 2;
   p.cv_tiles_per_img = (P + p.cv_rows - 1) / p.cv_rows;
+  if (strip) {
+    p.cv_wq = wq;
+    p.cv_tiles_per_img = (P * wq + 2 * BM - 1) / (2 * BM);
+    p.stage_tx = strip_hr * wq * 128;
+  }
   p.tiles_m = N * p.cv_tiles_per_img;
   p.tiles_n = feats / BN;
   p.feats = feats;
@@ -1444,12 +1518,17 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Cb, (uint64_t)N};
     const uint64_t str[4] = {128, (uint64_t)W * 128, (uint64_t)H * W * 128, (uint64_t)Cb * H * W * 128};
-    const uint32_t box[5] = {64, 64, halo ? (uint32_t)(p.cv_rows + 2) : 2u, 1, 1};
+    uint32_t box[5] = {64, 64, halo ? (uint32_t)(p.cv_rows + 2) : 2u, 1, 1};
+    if (strip) {  // rows of Wq pixels from x = -pad: adjacent rows share the pad column
+      box[1] = (uint32_t)wq;
+      box[2] = (uint32_t)strip_hr;
+    }
     int rc = make_map_5d(&ma, x, dims, str, box);
     if (rc) return rc;
   }
   // output [N][K_b][H][W][64] through TMA stores: box 32 channels x 32 pixels
-  p.tma_store = reinterpret_cast<uintptr_t>(out) % 16 == 0 && !env_no_tma_store();
+  // (strips store from registers)
+  p.tma_store = !strip && reinterpret_cast<uintptr_t>(out) % 16 == 0 && !env_no_tma_store();
   mc = ma;
   if (p.tma_store) {
     const uint64_t dims[5] = {64, (uint64_t)W, (uint64_t)H, (uint64_t)Kb, (uint64_t)N};
@@ -1465,7 +1544,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
     int rc = make_map_5d(&mb, w_packed, wb.dims, wb.strides, wb.box);
     if (rc) return rc;
   }
-  return launch(BN, halo ? (rows4 ? -3 : -2) : (res ? -1 : 1), 1, ma, mb, mc, p, stream);
+  return launch(BN, strip ? -4 : halo ? (rows4 ? -3 : -2) : (res ? -1 : 1), 1, ma, mb, mc, p, stream);
 }
 
 }  // namespace tpp
