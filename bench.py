@@ -279,6 +279,8 @@ def count_kernels(torch, fn):
                 n = e.name.split("(")[0]
                 if n.startswith("void "):
                     n = n[5:]
+                if not n.startswith("tpp::"):  # only this library's kernels (not copies / collectives)
+                    continue
                 names[n] = names.get(n, 0) + 1
         return names
     except Exception as ex:  # profiler unavailable: caller falls back to the static count
@@ -437,6 +439,7 @@ def run_ours(args, rank, world, dist):
     if world > 1:
         comm = {"backend": dist.get_backend(), "nranks": dist.get_world_size(),
                 "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                "one_gpu_functional_check": os.environ.get("TPP_BENCH_ONE_GPU") == "1",
                 "high_priority_streams": True, "nccl_init_log": _nccl_init_lines()}
     if rank == 0:
         line = {
@@ -984,7 +987,7 @@ def main():
         if not args.dry_run and args.impl == "ours":
             import torch
             have = torch.cuda.device_count()
-            if have < args.gpus:
+            if have < args.gpus and os.environ.get("TPP_BENCH_ONE_GPU") != "1":
                 print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but {have} visible GPUs",
                                   "n_gpus": args.gpus}), flush=True)
                 sys.exit(2)
@@ -999,7 +1002,11 @@ def main():
         return
     import torch
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # TPP_BENCH_BACKEND=gloo + TPP_BENCH_ONE_GPU=1: every rank on cuda:0 over
+    # gloo -- a functional check of the N-rank path on a single-GPU box (not
+    # a measurement: the ranks share one GPU)
+    one_gpu = os.environ.get("TPP_BENCH_ONE_GPU") == "1"
+    torch.cuda.set_device(0 if one_gpu else local)
     dist = None
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -1008,7 +1015,7 @@ def main():
         import torch.distributed as dist_mod
 
         from paper_2104_05755_b200 import parallel
-        parallel.init_from_env("nccl")
+        parallel.init_from_env(os.environ.get("TPP_BENCH_BACKEND", "nccl"))
         dist = dist_mod
     run_ours(args, rank, world, dist)
     if dist is not None:

@@ -183,7 +183,8 @@ def init_from_env(backend: Optional[str] = None):
         kw = {}
         if backend == "nccl":
             local = int(os.environ.get("LOCAL_RANK", "0"))
-            torch.cuda.set_device(local)
+            if os.environ.get("TPP_BENCH_ONE_GPU") != "1":
+                torch.cuda.set_device(local)
             kw["device_id"] = torch.device("cuda", local)
             try:
                 kw["pg_options"] = dist.ProcessGroupNCCL.Options(is_high_priority_stream=True)

@@ -961,3 +961,19 @@ def test_dilated_conv1d_atacworks_scale_bitwise():
     tpp.dilated_conv1d_forward(spec, inp, wv, out)
     want = O.dilated_conv1d(x, wt, C_, K_, S_, d_, Q_)
     assert bits(tpp.to_array(out)) == bits(want)
+
+
+@pytest.mark.parametrize("n", [4096 * 8, 1000])
+def test_split_sgd_bf16_grads_bitwise(n):
+    """split_sgd_step with BF16 gradients (kernels.py:235-251 accepts them;
+    the data-parallel step exchanges BF16 dW buckets): the 16-byte vector
+    kernel (n % 8 == 0) and the scalar one, bitwise the reference."""
+    from paper_2104_05755_b200 import training as T
+    rng = np.random.default_rng(400 + n)
+    w = rng.standard_normal(n).astype(np.float32)
+    g = O.fp32_to_bf16_rne((rng.standard_normal(n) * 1e-2).astype(np.float32))
+    hi, lo = T.split_master(torch.from_numpy(w).cuda())
+    tpp.split_sgd_flat(hi, lo, to_dev(g), 0.05)
+    got = T.pack_master(hi, lo).cpu().numpy()
+    want = O.split_sgd_step(w, O.bf16_to_fp32(g), 0.05)
+    assert bits(got) == bits(np.asarray(want, np.float32))
