@@ -39,10 +39,12 @@ using namespace sm100;
 namespace grp {
 
 constexpr int kEpiWarps = 4;    // warps 0-3: epilogue (TMEM lane quarter = warp)
-constexpr int kProdWarp0 = 4;   // warps 4-11: producers
-constexpr int kProdWarps = 8;
+constexpr int kProdWarp0 = 4;   // warps 4-7: issue the stage copies, never wait for data
+constexpr int kProdWarps = 4;
 constexpr int kProd = 32 * kProdWarps;
-constexpr int kMmaWarp = kProdWarp0 + kProdWarps;  // MMA issue + TMEM allocation
+constexpr int kFinWarp0 = kProdWarp0 + kProdWarps;  // warps 8-11: land a stage (VNNI transpose, proxy fence)
+constexpr int kFinWarps = 4;
+constexpr int kMmaWarp = kFinWarp0 + kFinWarps;     // MMA issue + TMEM allocation
 constexpr int kThreads = 32 * (kMmaWarp + 1);
 
 struct GParams {
@@ -71,7 +73,7 @@ struct GSmem {
   static constexpr int RAW_BYTES = BM * 128;  // VNNI A as loaded, before the word transpose
   static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* landed = tempty + 2;   // a stage's copies are in smem (issue warps -> finisher warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(landed + STAGES);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int ntiles = (int)(p.groups * p.tiles_m * p.tiles_n);   // < 2^31 (checked by the host)
@@ -126,8 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], kProd);
+      mbar_init(&full[s], 32 * kFinWarps);
       mbar_init(&empty[s], 1);
+      mbar_init(&landed[s], kProd);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -223,29 +227,6 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
                      ok ? 16 : 0);
       }
     };
-    auto transpose_vnni = [&](uint32_t sRaw, uint32_t sA) {
-#pragma unroll
-      for (int u = 0; u < AU; ++u) {
-        const int unit = t + u * kProd;
-        if (unit >= NUNITS) break;
-        const int pq = unit / (BM / 4), mq = unit % (BM / 4);
-        uint4 r[4];
-#pragma unroll
-        for (int pp = 0; pp < 4; ++pp)
-          asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(r[pp].x), "=r"(r[pp].y), "=r"(r[pp].z), "=r"(r[pp].w)
-                       : "r"(sRaw + (unit * 4 + pp) * 16));
-#pragma unroll
-        for (int mm = 0; mm < 4; ++mm) {
-          const int row = mq * 4 + mm;
-          const uint32_t w0 = mm == 0 ? r[0].x : mm == 1 ? r[0].y : mm == 2 ? r[0].z : r[0].w;
-          const uint32_t w1 = mm == 0 ? r[1].x : mm == 1 ? r[1].y : mm == 2 ? r[1].z : r[1].w;
-          const uint32_t w2 = mm == 0 ? r[2].x : mm == 1 ? r[2].y : mm == 2 ? r[2].z : r[2].w;
-          const uint32_t w3 = mm == 0 ? r[3].x : mm == 1 ? r[3].y : mm == 2 ? r[3].z : r[3].w;
-          sts16(sA + (row >> 3) * 1024 + (row & 7) * 128 + ((pq ^ (row & 7)) << 4), make_uint4(w0, w1, w2, w3));
-        }
-      }
-    };
     auto ld16 = [](const uint16_t* q) -> uint32_t {
       unsigned short v;
       asm volatile("ld.global.nc.u16 %0, [%1];" : "=h"(v) : "l"(q));
@@ -303,38 +284,34 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           sts16(sA + j * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((cc ^ (kk & 7)) << 4),
                 make_uint4(w[0], w[1], w[2], w[3]));
         }
-      } else {  // A VNNI, K-major chunks: one row at 8 k
-        for (int c = t; c < BM * 8; c += kProd) {
-          const int r = c >> 3, q = c & 7;
-          const int mrow = tm * BM + r, kk = kb + q * 8;
-          uint32_t w[4] = {0, 0, 0, 0};
-          if (mrow < p.m) {
+      } else {  // A VNNI: the raw unit layout of the fast path (the finisher transposes)
+        const uint32_t sRaw = sB + S::B_BYTES;
+        for (int unit = t; unit < NUNITS; unit += kProd) {
+          const int pq = unit / (BM / 4), mq = unit % (BM / 4);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int ke = kk + e;
-              if (ke < p.k) w[e >> 1] |= ld16(ap + (long long)(ke >> 1) * 2 * p.m + 2 * mrow + (ke & 1)) << (16 * (e & 1));
+          for (int pp = 0; pp < 4; ++pp) {
+            const int ke = kb + pq * 8 + 2 * pp;   // k of the pair's even element
+            uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+              const int mrow = tm * BM + mq * 4 + mm;
+              if (mrow < p.m) {
+                const uint16_t* q = ap + (long long)(ke >> 1) * 2 * p.m + 2 * mrow;
+                if (ke < p.k) w[mm] |= ld16(q);
+                if (ke + 1 < p.k) w[mm] |= ld16(q + 1) << 16;
+              }
             }
+            sts16(sRaw + (unit * 4 + pp) * 16, make_uint4(w[0], w[1], w[2], w[3]));
           }
-          sts16(sA + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
         }
       }
     };
-    // LAG stages in flight per thread: stage it's cp.async group is waited
-    // for (and, for VNNI A, transposed) LAG stages later, then handed over
-    constexpr int LAG = STAGES - 2;
-    StageIt cur{blockIdx.x, 0, 0};
+    // issue warps: never wait for data.  A stage's copies arrive on landed[s]
+    // as they complete (cp.async.mbarrier.arrive.noinc); the element-wise
+    // path writes synchronously, fences and arrives.  Up to STAGES stages in
+    // flight, bounded only by the MMA consuming slots.
+    StageIt cur{(int)blockIdx.x, 0, 0};
     uint32_t it = 0;
-    uint32_t vmask = 0;   // bit (stage % 32): that stage still needs its VNNI transpose
-    auto finish = [&](uint32_t j) {
-      const int sj = j % STAGES;
-      if ((vmask >> (j & 31)) & 1u) {
-        const uint32_t base = smem_u32(smem + sj * S::STAGE);
-        transpose_vnni(base + S::A_BYTES + S::B_BYTES, base);
-        vmask &= ~(1u << (j & 31));
-      }
-      fence_async_smem();
-      mbar_arrive(&full[sj]);
-    };
     while (cur.tile < ntiles) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
@@ -344,23 +321,57 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
       if (fast) {
         issue_fast(cur.kc, ap, bp, sA, sB);
-        if (p.vnni) {
-          issue_vnni(cur.kc, ap, sB + S::B_BYTES);
-          vmask |= 1u << (it & 31);
-        }
+        if (p.vnni) issue_vnni(cur.kc, ap, sB + S::B_BYTES);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&landed[s])) : "memory");
       } else {
         issue_generic(cur.kc, ap, bp, sA, sB);
-      }
-      cp_async_commit();
-      if (it >= (uint32_t)LAG) {
-        cp_async_wait<LAG>();
-        finish(it - LAG);
+        fence_async_smem();
+        mbar_arrive(&landed[s]);
       }
       advance(cur);
       ++it;
     }
-    cp_async_wait<0>();
-    for (uint32_t j = it > (uint32_t)LAG ? it - LAG : 0; j < it; ++j) finish(j);
+  } else if (warp >= kFinWarp0 && warp < kFinWarp0 + kFinWarps) {
+    // ============================ finishers ============================
+    // per landed stage: VNNI A's word transpose (raw -> K-major A tile), then
+    // the generic -> async proxy fence the tensor core's operand reads need,
+    // then full[s] for the MMA warp
+    const int t = threadIdx.x - kFinWarp0 * 32;
+    constexpr int AU = (BM * 2 + 32 * kFinWarps - 1) / (32 * kFinWarps);
+    constexpr int NUNITS = BM * 2;
+    const int per_tile = (int)(p.count * p.kchunks);
+    const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    const long long nst = (long long)my_tiles * per_tile;
+    for (long long it = 0; it < nst; ++it) {
+      const int s = (int)(it % STAGES);
+      mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
+      if (p.vnni) {
+        const uint32_t sA = smem_u32(smem + s * S::STAGE), sRaw = sA + S::A_BYTES + S::B_BYTES;
+#pragma unroll
+        for (int u = 0; u < AU; ++u) {
+          const int unit = t + u * 32 * kFinWarps;
+          if (unit >= NUNITS) break;
+          const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+          uint4 r[4];
+#pragma unroll
+          for (int pp = 0; pp < 4; ++pp)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r[pp].x), "=r"(r[pp].y), "=r"(r[pp].z), "=r"(r[pp].w)
+                         : "r"(sRaw + (unit * 4 + pp) * 16));
+#pragma unroll
+          for (int mm = 0; mm < 4; ++mm) {
+            const int row = mq * 4 + mm;
+            const uint32_t w0 = mm == 0 ? r[0].x : mm == 1 ? r[0].y : mm == 2 ? r[0].z : r[0].w;
+            const uint32_t w1 = mm == 0 ? r[1].x : mm == 1 ? r[1].y : mm == 2 ? r[1].z : r[1].w;
+            const uint32_t w2 = mm == 0 ? r[2].x : mm == 1 ? r[2].y : mm == 2 ? r[2].z : r[2].w;
+            const uint32_t w3 = mm == 0 ? r[3].x : mm == 1 ? r[3].y : mm == 2 ? r[3].z : r[3].w;
+            sts16(sA + (row >> 3) * 1024 + (row & 7) * 128 + ((pq ^ (row & 7)) << 4), make_uint4(w0, w1, w2, w3));
+          }
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(&full[s]);
+    }
   } else if (warp == kMmaWarp) {
     // ============================ MMA issue ============================
     const uint32_t idesc = idesc_bf16_f32(BM, BN, p.vnni ? 0 : 1, 0);
