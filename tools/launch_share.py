@@ -19,21 +19,20 @@ for r in rows[hi + 1:]:
         name = r[ki].split("(")[0].replace("void ", "")
         if "tpp::" in r[ki] or "tc::" in name or "brgemm" in name:
             seq.append((name, float(r[mi].replace(",", ""))))
-# split into steps of the 16 library launches (4 fwd, xent, 4 dW, 3 dX, 4 SGD)
-steps, cur = [], []
-for name, ns in seq:
-    cur.append((name, ns))
-    if "split_sgd" in name and sum("split_sgd" in n for n, _ in cur) == 4:
-        steps.append(cur)
-        cur = []
-steps = [s for s in steps if len(s) == 16]
+# a step = 4 forward GEMMs, the softmax-CE kernel, then per layer (last first)
+# backward-data + backward-weights (split-SGD fused at one rank): 12 launches
+# anchored on the softmax_xent kernel
+NB, NA = 4, 7
+labels = ["fwd0", "fwd1", "fwd2", "fwd3", "xent", "dx3", "dw3", "dx2", "dw2", "dx1", "dw1", "dw0"]
+steps = []
+for k, (name, _) in enumerate(seq):
+    if "softmax_xent" in name and k >= NB and k + NA < len(seq):
+        steps.append(seq[k - NB:k + NA + 1])
 print(f"# ncu launch list ({sys.argv[1]}): {len(seq)} library launches, {len(steps)} complete training steps")
 print("# cold-cache, serialised per-launch times (ncu --metrics gpu__time_duration.sum --clock-control none):")
 print("# compare SHARES with bench.py's live breakdown, not absolutes")
 if steps:
-    labels = ["fwd0", "fwd1", "fwd2", "fwd3", "xent", "dw3", "dx3", "dw2", "dx2", "dw1", "dx1", "dw0",
-              "sgd3", "sgd2", "sgd1", "sgd0"]
-    med = [statistics.median(s[i][1] for s in steps) for i in range(16)]
+    med = [statistics.median(s[i][1] for s in steps) for i in range(len(labels))]
     tot = sum(med)
     print(f"median step (sum of launches): {tot / 1e3:.1f} us")
     for lab, (name, _), v in zip(labels, steps[-1], med):
