@@ -703,6 +703,8 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
         out["dilated_conv1d_atacworks"] = {
             "shape": "W=60400, Q=60000, C=K=15, S=51, d=8, FP32 (PAPER.md:819)", "us": round(ms * 1e3, 2),
             "GFLOP/s": round(fl / ms / 1e6, 1), "frac_fp32_simt_peak": round(fl / ms / 1e9 / simt, 4),
+            "frac_no_fma_bound": round(2 * fl / ms / 1e9 / simt, 4),
+            "kernel": "K1w brgemm_ordered_window_kernel (bitwise order: separate mul + add, so half the FMA peak)",
             "parity": "bitwise vs the reference order (tests/test_gpu_parity.py)"}
         del inp, wv, outd
     except Exception as e:

@@ -13,6 +13,7 @@
 // TN accumulation chains are independent, which is the ILP this kernel has
 // (the per-element chain itself is inherently serial — that is the order).
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -367,8 +368,267 @@ static int launch_t(const OrderedParams& p, cudaStream_t s) {
 }
 
 // zero-count batches only apply the beta rule (contraction.py:300-315)
+// Narrow-and-long FP32 BRGEMMs (m, k <= 16, many columns): the dilated
+// conv1d's shape (kernels.py:350-378: C = K = 15 channels, S = 51 taps,
+// Q = 60000 positions).  One thread per C column owns all m accumulators (the
+// m independent per-row chains are the ILP).  Per CTA of kColN columns:
+//   * the A blocks of kColChunk entries are staged in shared memory as
+//     [entry][k][16] (zero-padded rows), read back as float4 broadcasts;
+//   * each entry's B window (kColN columns x k values, contiguous when
+//     ldb == k) is staged by coalesced 4-byte cp.async into a [col][k|1]
+//     tile (odd pitch: conflict-free column reads), kColStages entries ahead.
+// Per element the order is the reference's: part = +0; part += a*b over k
+// ascending; acc += part over entries ascending (separately rounded).
+constexpr int kColM = 16, kColK = 16, kColN = 64, kColChunk = 8, kColStages = 4;
+constexpr int kColRows = 8;  // rows per thread: m > 8 takes two row groups per column
+
+template <int KC>  // KC = p.k (compile-time: the inner loop carries no bounds checks)
+__global__ void __launch_bounds__(2 * kColN) brgemm_ordered_cols_kernel(OrderedParams p) {
+  __shared__ __align__(16) float As[kColChunk][KC][kColM];
+  __shared__ __align__(16) float Bs[kColStages][(kColN * (KC | 1) + 3) & ~3];
+  constexpr int pitch = KC | 1;
+  const int n0 = blockIdx.x * kColN, ncols = min(kColN, (int)(p.n - n0));
+  const int t = threadIdx.x, nthr = blockDim.x;
+  const int col = t % kColN, r0 = (t / kColN) * kColRows;  // row group: warp-uniform
+  const bool live = col < ncols;
+  float* c = reinterpret_cast<float*>(p.c);
+  float acc[kColRows];
+#pragma unroll
+  for (int mm = 0; mm < kColRows; ++mm) {
+    float v = 0.f;
+    if (live && r0 + mm < p.m && p.beta != 0.0) {
+      v = c[r0 + mm + (int64_t)(n0 + col) * p.ldc];
+      if (p.beta != 1.0) v = __fmul_rn(v, (float)p.beta);
+    }
+    acc[mm] = v;
+  }
+  // Staging walk: element e = col * k + kk of the window, e = t, t + nthr, ...
+  // advanced incrementally (no per-element division).
+  const int tile_elems = ncols * p.k;
+  const int col0 = t / p.k, kk0 = t - col0 * p.k;
+  const int dcol = nthr / p.k, dkk = nthr - dcol * p.k;
+  // Contiguous windows (ldb == k, k odd: the dilated conv's case) are copied
+  // as-is -- [col][k] with an odd pitch is already conflict-free -- with
+  // 16-byte cp.async when the window start is 16-byte aligned.
+  const bool contig = p.ldb == KC && (KC & 1);
+  auto stage_b = [&](int64_t entry, int slot) {
+    if (entry < p.count && contig) {
+      const float* win = batch_b<float>(p, 0, entry) + (int64_t)n0 * KC;
+      float* dst = Bs[slot];
+      if ((reinterpret_cast<uintptr_t>(win) & 15) == 0) {
+        const int v4 = tile_elems >> 2;
+        for (int e = t; e < v4; e += nthr) cp_async16(dst + 4 * e, win + 4 * e);
+        for (int e = 4 * v4 + t; e < tile_elems; e += nthr) stage_elem<float>(dst + e, win + e);
+      } else {
+        for (int e = t; e < tile_elems; e += nthr) stage_elem<float>(dst + e, win + e);
+      }
+    } else if (entry < p.count) {
+      const float* src = batch_b<float>(p, 0, entry) + (int64_t)n0 * p.ldb + (int64_t)col0 * p.ldb + kk0;
+      float* dst = Bs[slot] + col0 * pitch + kk0;
+      int kk = kk0;
+      for (int e = t; e < tile_elems; e += nthr) {
+        stage_elem<float>(dst, src);
+        kk += dkk;
+        src += (int64_t)dcol * p.ldb + dkk;
+        dst += dcol * pitch + dkk;
+        if (kk >= p.k) { kk -= p.k; src += p.ldb - p.k; dst += pitch - p.k; }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int st = 0; st < kColStages - 1; ++st) stage_b(st, st);
+  for (int64_t i0 = 0; i0 < p.count; i0 += kColChunk) {
+    const int cnt = (int)min((int64_t)kColChunk, p.count - i0);
+    __syncthreads();  // previous chunk's A reads done
+    for (int e = t; e < cnt * KC * kColM; e += nthr) {
+      const int bi = e / (KC * kColM), kk = (e / kColM) % KC, mm = e % kColM;
+      float v = 0.f;
+      if (mm < p.m) v = batch_a<float>(p, 0, i0 + bi)[mm + (int64_t)kk * p.lda];
+      As[bi][kk][mm] = v;
+    }
+    for (int bi = 0; bi < cnt; ++bi) {
+      const int64_t i = i0 + bi;
+      asm volatile("cp.async.wait_group %0;" ::"n"(kColStages - 2) : "memory");
+      __syncthreads();  // entry i's B tile (and, at bi == 0, the A chunk) visible; slot of i-1 free
+      stage_b(i + kColStages - 1, (int)((i + kColStages - 1) % kColStages));
+      if (live) {
+        const float* bs = Bs[i % kColStages] + col * pitch;
+        float part[kColRows];
+#pragma unroll
+        for (int mm = 0; mm < kColRows; ++mm) part[mm] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+          const float bv = bs[kk];
+          const float4* ar = reinterpret_cast<const float4*>(&As[bi][kk][r0]);
+#pragma unroll
+          for (int q = 0; q < kColRows / 4; ++q) {
+            const float4 av = ar[q];
+            part[4 * q + 0] = __fadd_rn(part[4 * q + 0], __fmul_rn(av.x, bv));
+            part[4 * q + 1] = __fadd_rn(part[4 * q + 1], __fmul_rn(av.y, bv));
+            part[4 * q + 2] = __fadd_rn(part[4 * q + 2], __fmul_rn(av.z, bv));
+            part[4 * q + 3] = __fadd_rn(part[4 * q + 3], __fmul_rn(av.w, bv));
+          }
+        }
+#pragma unroll
+        for (int mm = 0; mm < kColRows; ++mm) acc[mm] = __fadd_rn(acc[mm], part[mm]);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (live) {
+#pragma unroll
+    for (int mm = 0; mm < kColRows; ++mm)
+      if (r0 + mm < p.m) c[r0 + mm + (int64_t)(n0 + col) * p.ldc] = acc[mm];
+  }
+}
+
+// Sliding-window variant: STRIDE batches whose B blocks are column windows
+// of one contiguous matrix (ldb == k, stride_b = sh columns) -- the dilated
+// conv's taps, entry s reading input columns q + s*d.  A CTA covers ncb
+// columns; the union of its windows (ncb + (count-1)*sh columns) and every
+// entry's A block are staged ONCE (cp.async), then the entry loop is pure
+// shared-memory reads + arithmetic with no barrier.  One CTA per SM with the
+// columns split evenly (ncb = n / #SMs rounded up to a warp), so the single
+// wave is balanced.  Same per-element order as the kernels above.
+template <int KC>
+__global__ void __launch_bounds__(512, 1) brgemm_ordered_window_kernel(OrderedParams p, int ncb, int sh) {
+  extern __shared__ __align__(16) float wsm[];
+  float* As = wsm;                                   // [count][KC][16], rows >= m zero
+  float* Bu = wsm + (size_t)p.count * KC * kColM;    // [U][KC] window union
+  const int n0 = blockIdx.x * ncb, ncols = min(ncb, (int)(p.n - n0));
+  if (ncols <= 0) return;
+  const int t = threadIdx.x, nthr = blockDim.x;
+  const int ucols = ncols + (int)(p.count - 1) * sh;
+  {
+    const float* win = reinterpret_cast<const float*>(p.b) + (int64_t)n0 * KC;
+    const int elems = ucols * KC;
+    int done = 0;
+    if ((reinterpret_cast<uintptr_t>(win) & 15) == 0) {
+      done = elems & ~3;
+      for (int e = 4 * t; e < done; e += 4 * nthr) cp_async16(Bu + e, win + e);
+    }
+    for (int e = done + t; e < elems; e += nthr) stage_elem<float>(Bu + e, win + e);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* a = reinterpret_cast<const float*>(p.a);
+    for (int e = t; e < (int)p.count * KC * kColM; e += nthr) {
+      const int mm = e % kColM, kk = (e / kColM) % KC, bi = e / (KC * kColM);
+      As[e] = mm < p.m ? a[(int64_t)bi * p.stride_a + mm + (int64_t)kk * p.lda] : 0.f;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+  }
+  // Thread -> (row group, columns col and col + ncb/2): every A broadcast
+  // feeds two columns' products.  (A warp straddling two row groups reads two
+  // A addresses per LDS -- harmless.)
+  const int half = ncb / 2;
+  const int g = t / half, col = t - g * half;
+  const int r0 = g * kColRows;
+  if (col >= ncols) return;
+  const bool two = col + half < ncols;
+  float* c0 = reinterpret_cast<float*>(p.c) + (int64_t)(n0 + col) * p.ldc + r0;
+  float* c1 = c0 + (int64_t)half * p.ldc;
+  float acc0[kColRows], acc1[kColRows];
+#pragma unroll
+  for (int mm = 0; mm < kColRows; ++mm) {
+    float v0 = 0.f, v1 = 0.f;
+    if (r0 + mm < p.m && p.beta != 0.0) {
+      v0 = c0[mm];
+      if (two) v1 = c1[mm];
+      if (p.beta != 1.0) v0 = __fmul_rn(v0, (float)p.beta), v1 = __fmul_rn(v1, (float)p.beta);
+    }
+    acc0[mm] = v0;
+    acc1[mm] = v1;
+  }
+  const float* bs = Bu + col * KC;  // column col + half is half * KC further (inside the union)
+  const float* as = As + r0;
+  for (int i = 0; i < (int)p.count; ++i, bs += sh * KC, as += KC * kColM) {
+    float part0[kColRows], part1[kColRows];
+#pragma unroll
+    for (int mm = 0; mm < kColRows; ++mm) part0[mm] = 0.f, part1[mm] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      const float b0 = bs[kk], b1 = bs[half * KC + kk];
+      const float4* ar = reinterpret_cast<const float4*>(as + kk * kColM);
+#pragma unroll
+      for (int q = 0; q < kColRows / 4; ++q) {
+        const float4 av = ar[q];
+        part0[4 * q + 0] = __fadd_rn(part0[4 * q + 0], __fmul_rn(av.x, b0));
+        part0[4 * q + 1] = __fadd_rn(part0[4 * q + 1], __fmul_rn(av.y, b0));
+        part0[4 * q + 2] = __fadd_rn(part0[4 * q + 2], __fmul_rn(av.z, b0));
+        part0[4 * q + 3] = __fadd_rn(part0[4 * q + 3], __fmul_rn(av.w, b0));
+        part1[4 * q + 0] = __fadd_rn(part1[4 * q + 0], __fmul_rn(av.x, b1));
+        part1[4 * q + 1] = __fadd_rn(part1[4 * q + 1], __fmul_rn(av.y, b1));
+        part1[4 * q + 2] = __fadd_rn(part1[4 * q + 2], __fmul_rn(av.z, b1));
+        part1[4 * q + 3] = __fadd_rn(part1[4 * q + 3], __fmul_rn(av.w, b1));
+      }
+    }
+#pragma unroll
+    for (int mm = 0; mm < kColRows; ++mm) {
+      acc0[mm] = __fadd_rn(acc0[mm], part0[mm]);
+      acc1[mm] = __fadd_rn(acc1[mm], part1[mm]);
+    }
+  }
+#pragma unroll
+  for (int mm = 0; mm < kColRows; ++mm) {
+    if (r0 + mm < p.m) {
+      c0[mm] = acc0[mm];
+      if (two) c1[mm] = acc1[mm];
+    }
+  }
+}
+
+// Window-path plan: 0 = not applicable, else fills ncb / sh / smem bytes.
+static bool window_plan(const OrderedParams& p, int* ncb, int* sh, int* smem) {
+  if (p.mode != 0 || (p.k & 1) == 0 || p.ldb != p.k || p.stride_b < 0 || p.stride_b % p.k != 0) return false;
+  const int64_t groups = (p.m + kColRows - 1) / kColRows;
+  int64_t cols = (p.n + num_sms() - 1) / num_sms();
+  cols = (cols + 1) & ~int64_t(1);
+  cols = std::min<int64_t>(cols, 512 / groups * 2);  // threads = groups * cols / 2 <= 512
+  const int64_t shift = p.stride_b / p.k;
+  // (the last CTA's threads whose second column lies past n still read --
+  // and ignore -- union slots up to column cols - 1 + (count - 1) * shift)
+  const int64_t bytes = p.count * p.k * kColM * 4 + (cols + (p.count - 1) * shift) * p.k * 4;
+  if (bytes > 200 * 1024 || shift > (1 << 20)) return false;
+  *ncb = (int)cols;
+  *sh = (int)shift;
+  *smem = (int)bytes;
+  return true;
+}
+
 int launch_brgemm_ordered(const OrderedParams& p, int in_dtype, cudaStream_t s) {
   if (p.m == 0 || p.n == 0 || p.instances == 0) return TPP_OK;
+  static const bool no_cols = getenv("TPP_ORDERED_NO_COLS") != nullptr;  // experiments
+  if (in_dtype == TPP_FP32 && !p.vnni && p.instances == 1 && p.m <= kColM && p.k >= 1 && p.k <= kColK && p.n >= 2048 &&
+      p.count > 0 && !no_cols) {
+    static const bool no_window = getenv("TPP_ORDERED_NO_WINDOW") != nullptr;  // experiments
+    int ncb = 0, sh = 0, smem = 0;
+    if (!no_window && window_plan(p, &ncb, &sh, &smem)) {
+      const int wthreads = ncb / 2 * ((p.m + kColRows - 1) / kColRows);
+      const int wblocks = (int)((p.n + ncb - 1) / ncb);
+      switch (p.k) {
+#define TPP_WIN_K(K)                                                                                  \
+  case K:                                                                                             \
+    if (ensure_smem_attr((const void*)brgemm_ordered_window_kernel<K>, smem) != cudaSuccess) break;  \
+    brgemm_ordered_window_kernel<K><<<wblocks, wthreads, smem, s>>>(p, ncb, sh);                       \
+    TPP_CUDA_LAUNCH_CHECK("brgemm_ordered_window_kernel");                                             \
+    return TPP_OK;
+        TPP_WIN_K(1) TPP_WIN_K(3) TPP_WIN_K(5) TPP_WIN_K(7) TPP_WIN_K(9) TPP_WIN_K(11) TPP_WIN_K(13) TPP_WIN_K(15)
+#undef TPP_WIN_K
+      }
+    }
+    const int blocks = (int)((p.n + kColN - 1) / kColN);
+    const int threads = kColN * ((p.m + kColRows - 1) / kColRows);
+    switch (p.k) {
+#define TPP_COLS_K(K) case K: brgemm_ordered_cols_kernel<K><<<blocks, threads, 0, s>>>(p); break;
+      TPP_COLS_K(1) TPP_COLS_K(2) TPP_COLS_K(3) TPP_COLS_K(4) TPP_COLS_K(5) TPP_COLS_K(6) TPP_COLS_K(7)
+      TPP_COLS_K(8) TPP_COLS_K(9) TPP_COLS_K(10) TPP_COLS_K(11) TPP_COLS_K(12) TPP_COLS_K(13)
+      TPP_COLS_K(14) TPP_COLS_K(15) TPP_COLS_K(16)
+#undef TPP_COLS_K
+    }
+    TPP_CUDA_LAUNCH_CHECK("brgemm_ordered_cols_kernel");
+    return TPP_OK;
+  }
   switch (in_dtype) {
     case TPP_FP32: return launch_t<float, float>(p, s);
     case TPP_FP64: return launch_t<double, double>(p, s);

@@ -7,6 +7,7 @@
 #include <stdlib.h>
 
 #include <mutex>
+#include <map>
 #include <set>
 #include <utility>
 
@@ -21,19 +22,21 @@ inline int pdl_allowed() {
   return v;
 }
 
-// cudaFuncSetAttribute(max dynamic shared memory) once per (kernel, device):
-// thread-safe, and a second device used by the same process gets its own
-// opt-in (the attribute is per device)
+// cudaFuncSetAttribute(max dynamic shared memory) per (kernel, device),
+// raised whenever a launch needs more than the opt-in so far (kernels with a
+// data-dependent footprint): thread-safe, and a second device used by the
+// same process gets its own opt-in (the attribute is per device)
 inline cudaError_t ensure_smem_attr(const void* kern, int bytes) {
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, int> done;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
-  if (done.count({kern, dev})) return cudaSuccess;
+  auto it = done.find({kern, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done.insert({kern, dev});
+  if (e == cudaSuccess) done[{kern, dev}] = bytes;
   return e;
 }
 

@@ -111,6 +111,66 @@ def test_brgemm_fp32_stride_staging_paths(m, n, k, count, beta):
     assert bits(got) == bits(np.asarray(want, dtype=np.float32)), (m, n, k, count)
 
 
+@pytest.mark.parametrize("m,n,k,count,beta,variant", [
+    (15, 4096, 15, 51, 0.0, "stride"), (16, 2500, 16, 33, 1.0, "stride"),
+    (3, 2048, 7, 5, 0.5, "offset"), (9, 3000, 1, 64, 1.0, "address")])
+def test_brgemm_fp32_narrow_column_kernel(m, n, k, count, beta, variant):
+    """Narrow-and-long FP32 BRGEMMs (m, k <= 16, n >= 2048: the dilated conv's
+    shape) take the one-thread-per-column ordered kernel: entries staged in
+    chunks of 32 (ragged last chunk), padded lda / ldb / ldc, every batch
+    addressing mode; bitwise vs the reference order."""
+    rng = np.random.default_rng(7 * m + k + count)
+    lda, ldb, ldc = m + 1, k + 2, m + 3
+    sa, sb = lda * k + 5, ldb * n + 3
+    af = rng.standard_normal(sa * count).astype(np.float32)
+    bf = rng.standard_normal(sb * count).astype(np.float32)
+    c0 = rng.standard_normal((ldc, n)).astype(np.float32)
+    a_blocks = [af[i * sa: i * sa + lda * k].reshape(k, lda).T[:m, :] for i in range(count)]
+    b_blocks = [bf[i * sb: i * sb + ldb * n].reshape(n, ldb).T[:k, :] for i in range(count)]
+    want = O.brgemm(a_blocks, b_blocks, c0[:m, :], beta)
+    c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32),
+                       torch.from_numpy(c0.T.reshape(-1).copy()).cuda())
+    sp = tpp.GemmSpec(m, n, k, lda, ldb, ldc, beta=beta)
+    ad, bd = torch.from_numpy(af).cuda(), torch.from_numpy(bf).cuda()
+    if variant == "stride":
+        batch = tpp.BrgemmBatch.stride(ad, bd, sa, sb, count)
+    elif variant == "offset":
+        batch = tpp.BrgemmBatch.offset(ad, bd, [i * sa for i in range(count)], [i * sb for i in range(count)])
+    else:
+        batch = tpp.BrgemmBatch.address([(ad, i * sa) for i in range(count)], [(bd, i * sb) for i in range(count)])
+    tpp.brgemm(sp, batch, c)
+    got = tpp.to_array(c)
+    assert bits(got) == bits(np.asarray(want, dtype=np.float32)), (m, n, k, count, variant)
+
+
+@pytest.mark.parametrize("m,n,k,count,sh,beta", [
+    (15, 5000, 15, 51, 8, 0.0), (5, 2048, 3, 9, 0, 0.5), (16, 2049, 7, 20, 3, 1.0), (9, 70001, 15, 4, 1, 1.0)])
+def test_brgemm_fp32_sliding_window_kernel(m, n, k, count, sh, beta):
+    """STRIDE batches whose B blocks are overlapping column windows of one
+    matrix (ldb == k odd, stride_b = sh columns: the dilated conv's taps) take
+    the window kernel that stages the union once per CTA: evenly split
+    columns (ragged last CTA), one or two row groups, sh = 0 (every entry the
+    same window); bitwise vs the reference order."""
+    rng = np.random.default_rng(11 * m + k + sh)
+    lda, ldc = m + 2, m + 1
+    sa = lda * k + 3
+    af = rng.standard_normal(sa * count).astype(np.float32)
+    wcols = n + (count - 1) * sh
+    bf = rng.standard_normal(k * wcols).astype(np.float32)
+    c0 = rng.standard_normal((ldc, n)).astype(np.float32)
+    bm = bf.reshape(wcols, k).T
+    a_blocks = [af[i * sa: i * sa + lda * k].reshape(k, lda).T[:m, :] for i in range(count)]
+    b_blocks = [bm[:, i * sh: i * sh + n] for i in range(count)]
+    want = O.brgemm(a_blocks, b_blocks, c0[:m, :], beta)
+    c = tpp.TensorView(tpp.TensorDesc(m, n, ldc, tpp.DType.FP32),
+                       torch.from_numpy(c0.T.reshape(-1).copy()).cuda())
+    sp = tpp.GemmSpec(m, n, k, lda, k, ldc, beta=beta)
+    tpp.brgemm(sp, tpp.BrgemmBatch.stride(torch.from_numpy(af).cuda(), torch.from_numpy(bf).cuda(),
+                                          sa, sh * k, count), c)
+    got = tpp.to_array(c)
+    assert bits(got) == bits(np.asarray(want, dtype=np.float32)), (m, n, k, count, sh)
+
+
 def test_brgemm_cancellation_and_doubling():
     """test_gemm.py:117-137 properties on the GPU (FP64, exact)."""
     rng = np.random.default_rng(3)
