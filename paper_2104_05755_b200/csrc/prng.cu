@@ -32,7 +32,9 @@
 // rounded once into the output dtype.
 
 #include "common.cuh"
+#include "sm100.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <mutex>
 
@@ -40,6 +42,16 @@ namespace tpp {
 
 namespace {
 
+#ifndef TPP_DRAW_UNROLL
+#define TPP_DRAW_UNROLL 8
+#endif
+#ifndef TPP_DROP_DIAG
+#define TPP_DROP_DIAG 0
+#endif
+#ifndef TPP_DROP_MINB
+#define TPP_DROP_MINB 1
+#endif
+constexpr int kDrawUnroll = TPP_DRAW_UNROLL;
 constexpr int kSub = 64;                    // rows per draw slab (one keep word)
 constexpr int kWarps = 8;
 constexpr int kTileCols = 32;
@@ -254,7 +266,7 @@ __device__ __forceinline__ uint32_t xs_step_fast(Xs128& s) {
 // first row in the MSB, so the word is bit-reversed at the end.
 __device__ __forceinline__ uint32_t draw_keep32(Xs128& s, uint32_t nthr) {
   uint32_t lo = 0;
-#pragma unroll
+#pragma unroll kDrawUnroll
   for (int i = 0; i < 32; ++i) {
     const uint32_t w = xs_step_fast(s);
     asm("{ .reg .u32 d; add.cc.u32 d, %1, %2; addc.u32 %0, %0, %0; }" : "+r"(lo) : "r"(w), "r"(nthr));
@@ -390,7 +402,7 @@ __device__ __forceinline__ void store8_vec(TO* op, const float (&r)[8]) {
 }
 
 template <typename TI, typename TO>
-__global__ void __launch_bounds__(256) dropout_fused_kernel(const uint32_t* __restrict__ st_in,
+__global__ void __launch_bounds__(256, TPP_DROP_MINB) dropout_fused_kernel(const uint32_t* __restrict__ st_in,
                                                             uint32_t* __restrict__ st_out, uint32_t thr24,
                                                             const TI* __restrict__ in, TO* __restrict__ out,
                                                             uint8_t* __restrict__ mask_out, int rows, int cols,
@@ -419,7 +431,15 @@ __global__ void __launch_bounds__(256) dropout_fused_kernel(const uint32_t* __re
     SlabPart<TI> nxt;
     if (sizeof(TI) == 2 && full_group && q + 1 < nslab) nxt.load(in + d0 + (q + 1) * kSub, col_stride, true);
     uint64_t bits = 0;
+#if TPP_DROP_DIAG == 1
+    bits = 0xF7F7F7F7F7F7F7F7ull ^ (uint64_t)q;
+#else
     if (draws) bits = draw_keep64(s, thr24, kSub);
+#endif
+#if TPP_DROP_DIAG == 2
+    if (draws) mb[q] = bits;
+    continue;
+#endif
     const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -463,6 +483,204 @@ __global__ void __launch_bounds__(256) dropout_fused_kernel(const uint32_t* __re
     st_out[2 * cols + j] = s.z;
     st_out[3 * cols + j] = s.w;
   }
+}
+
+// Two streams at once: the xorshift chain of one stream is latency-bound
+// (each step waits on the previous w), so a lane advances two independent
+// row runs of its column with the steps interleaved.
+__device__ __forceinline__ void draw_keep64x2(Xs128& a, Xs128& b, uint32_t thr24, uint64_t& ra, uint64_t& rb) {
+  if (thr24 >= (1u << 24) || thr24 == 0) {
+    ra = draw_keep64(a, thr24, kSub);
+    rb = draw_keep64(b, thr24, kSub);
+    return;
+  }
+  const uint32_t nthr = 0u - (thr24 << 8);
+  uint32_t h[4];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t la = 0, lb = 0;
+#pragma unroll kDrawUnroll
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t wa = xs_step_fast(a), wb = xs_step_fast(b);
+      asm("{ .reg .u32 d; add.cc.u32 d, %1, %2; addc.u32 %0, %0, %0; }" : "+r"(la) : "r"(wa), "r"(nthr));
+      asm("{ .reg .u32 d; add.cc.u32 d, %1, %2; addc.u32 %0, %0, %0; }" : "+r"(lb) : "r"(wb), "r"(nthr));
+    }
+    h[2 * half] = __brev(la);
+    h[2 * half + 1] = __brev(lb);
+  }
+  ra = (uint64_t)h[0] | ((uint64_t)h[2] << 32);
+  rb = (uint64_t)h[1] | ((uint64_t)h[3] << 32);
+}
+
+template <typename TO, int N>
+__device__ __forceinline__ void store_vec_n(TO* op, const float (&r)[N]) {
+  if constexpr (sizeof(TO) == 2) {
+    uint32_t u[N / 2];
+    pack_bf16_ref_n<N / 2>(r, u);
+    if constexpr (N == 8) *reinterpret_cast<uint4*>(op) = make_uint4(u[0], u[1], u[2], u[3]);
+    else *reinterpret_cast<uint2*>(op) = make_uint2(u[0], u[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q)
+      reinterpret_cast<float4*>(op)[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+  }
+}
+
+// DROPOUT fused, TMA-fed (dense column-major BF16 / FP32 views, rows % 64
+// == 0).  Warp = 32 consecutive columns x one run of `run` rows (a multiple
+// of 128) split into two halves A / B that the lanes draw as two interleaved
+// streams (lane = column, one jump per stream).  The warp's 32 x 64-row input
+// slabs arrive by TMA into a private kDropStages-deep shared-memory ring (the
+// HBM reads stay in flight without holding registers), in the order A0 B0
+// A1 B1 ...; per slab each lane takes 16-byte chunks (8 lanes per column:
+// conflict-free), fetches the chunk's keep bits from the drawing lane with a
+// shuffle, applies keep ? x * scale : 0 (DROPOUT_INV's rule, FP32 math; RNE +
+// the reference NaN rule for BF16 out) and stores coalesced; the drawing lane
+// stores the slab's 8-byte mask word.  Bitwise the same draws, mask and
+// values as the other DROPOUT paths (ops.py:430-444).
+constexpr int kDropWarps = 4;
+template <typename TI> struct DropTma {
+  static constexpr int kStages = 3;
+  static constexpr int kSlab = 32 * kSub * (int)sizeof(TI);  // bytes per warp slab
+  static constexpr int kSmem = kDropWarps * kStages * kSlab + kDropWarps * kStages * 8;
+};
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(kDropWarps * 32) dropout_tma_kernel(
+    const __grid_constant__ CUtensorMap tin, const uint32_t* __restrict__ st_in, uint32_t* __restrict__ st_out,
+    uint32_t thr24, TO* __restrict__ out, int64_t out_ld, uint8_t* __restrict__ mask_out, int rows, int cols,
+    int run, float scale, const uint4* __restrict__ tab) {
+  using namespace sm100;
+  constexpr int E = sizeof(TI), S = DropTma<TI>::kStages, SLAB = DropTma<TI>::kSlab;
+  constexpr int EPC = 16 / E;      // elements per 16-byte chunk
+  constexpr int CPC = kSub / EPC;  // chunks per column of a slab (= passes per slab)
+  extern __shared__ __align__(128) uint8_t dsm[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // item = (column group, row run), flattened so the grid fits one wave
+  const int64_t item = (int64_t)blockIdx.x * kDropWarps + w;
+  const int segs = (rows + run - 1) / run;
+  const int64_t cg = item / segs;
+  if (cg * 32 >= cols) return;  // warp-uniform; barriers and ring are private to the warp
+  const int64_t rs64 = (item - cg * segs) * run;
+  uint8_t* ring = dsm + (size_t)w * S * SLAB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (size_t)kDropWarps * S * SLAB) + w * S;
+  const int j0 = (int)cg * 32, j = j0 + lane;
+  const int rs = (int)rs64, half = run / 2;
+  const int nA = min(half, rows - rs) / kSub;
+  const int nB = max(0, min(half, rows - rs - half)) / kSub;
+  const int T = nA + nB;
+  auto slab_row = [&](int k) { return k < 2 * nB ? rs + (k & 1) * half + (k >> 1) * kSub : rs + (k - nB) * kSub; };
+  auto issue = [&](int k) {
+    const int st = k % S;
+    mbar_arrive_expect_tx(&bars[st], SLAB);
+    tma_load_5d(ring + st * SLAB, &tin, &bars[st], slab_row(k) * E / 2, j0, 0, 0, 0);
+  };
+  if (lane == 0) {
+    for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
+    fence_mbar_init();
+    for (int k = 0; k < min(S, T); ++k) issue(k);
+  }
+  __syncwarp();
+  const bool draws = j < cols;
+  const int valid_cols = min(32, cols - j0);
+  Xs128 sa{0u, 0u, 0u, 1u}, sb{0u, 0u, 0u, 1u};
+  if (draws) {
+#if TPP_DROP_DIAG == 3
+    sa = Xs128{st_in[j], st_in[cols + j], 1u, 2u};
+    sb = Xs128{st_in[j] ^ 5u, st_in[cols + j], 3u, 4u};
+#else
+    // run is a power-of-two multiple of 128 rows, so rs / 64 has few set
+    // bits (popcount(item's run index) jumps) and stream B is ONE jump from
+    // stream A's start (half / 64 is a power of two: one jump level)
+    sa = start_state(st_in, cols, j, rs, tab);
+    if (nB > 0) sb = jump(sa, tab + (31 - __clz(half / kSub)) * kNibs * 16);
+#endif
+  }
+  uint8_t* mcol = mask_out + (int64_t)j * (rows >> 3);
+  // apply-phase mapping: pass p, lane -> column p * CPP + lane / CPC of the
+  // group, rows b0 .. b0 + EPC - 1 of the slab (b0 fixed per lane)
+  constexpr int CPP = 32 / CPC;  // columns per pass
+  const int lane_c = lane / CPC, b0 = (lane % CPC) * EPC;
+  const int lane_smem = lane_c * kSub * E + (lane % CPC) * 16;
+  TO* const obase = out + (int64_t)(j0 + lane_c) * out_ld + b0;
+  const int64_t ostride = (int64_t)CPP * out_ld;
+  int k = 0;
+#pragma unroll 1
+  for (int q = 0; q < nA; ++q) {
+    const bool both = q < nB;
+    uint64_t bw0 = 0ull, bw1 = 0ull;
+#if TPP_DROP_DIAG == 1
+    bw0 = 0xF7F7F7F7F7F7F7F7ull ^ (uint64_t)q;
+    bw1 = ~bw0;
+#else
+    if (draws) {
+      if (both) draw_keep64x2(sa, sb, thr24, bw0, bw1);
+      else bw0 = draw_keep64(sa, thr24, kSub);
+    }
+#endif
+#pragma unroll 1
+    for (int part = 0; part < (both ? 2 : 1); ++part, ++k) {
+      const uint64_t bits = part ? bw1 : bw0;
+      const int row0 = rs + part * half + q * kSub;
+      const int st = k % S;
+      mbar_wait(&bars[st], (uint32_t)(k / S) & 1u);
+      const uint8_t* sl = ring + st * SLAB + lane_smem;
+      TO* o = obase + row0;
+      const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
+#pragma unroll
+      for (int pass = 0; pass < (TPP_DROP_DIAG == 2 ? 0 : CPC); ++pass) {
+        const int c = pass * CPP + lane_c;  // column (within the group) of this lane's chunk
+        const uint32_t wl = __shfl_sync(0xffffffffu, lo, c), wh = __shfl_sync(0xffffffffu, hi, c);
+        const uint32_t kb = ((b0 < 32 ? wl : wh) >> (b0 & 31)) & ((1u << EPC) - 1u);
+        if (c < valid_cols) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sl + pass * CPP * kSub * E);
+          float x[EPC];
+          if constexpr (E == 2) {
+            const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              x[2 * e] = __uint_as_float(ww[e] << 16);
+              x[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+            }
+          } else {
+            x[0] = __uint_as_float(v.x); x[1] = __uint_as_float(v.y);
+            x[2] = __uint_as_float(v.z); x[3] = __uint_as_float(v.w);
+          }
+          float r[EPC];
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) r[e] = ((kb >> e) & 1u) ? __fmul_rn(x[e], scale) : 0.0f;
+          store_vec_n<TO, EPC>(o + pass * ostride, r);
+        }
+      }
+      if (draws) *reinterpret_cast<uint64_t*>(mcol + (row0 >> 3)) = bits;
+      __syncwarp();  // every lane's reads of this stage are done before TMA refills it
+      if (lane == 0 && k + S < T) issue(k + S);
+    }
+  }
+  if (draws) {
+    const bool b_last = nB > 0 && rs + half + nB * kSub == rows;
+    const bool a_last = nB == 0 && rs + nA * kSub == rows;
+    if (a_last || b_last) {
+      const Xs128 f = b_last ? sb : sa;
+      st_out[j] = f.x;
+      st_out[cols + j] = f.y;
+      st_out[2 * cols + j] = f.z;
+      st_out[3 * cols + j] = f.w;
+    }
+  }
+}
+
+template <typename TI, typename TO>
+static int launch_dropout_tma(const CUtensorMap& m, const uint32_t* st_in, uint32_t* st_out, uint32_t thr24, void* out,
+                              int64_t out_ld, uint8_t* mask_out, int rows, int cols, int run, float scale,
+                              const uint4* tab, dim3 grid, cudaStream_t s) {
+  constexpr int smem = DropTma<TI>::kSmem;
+  cudaError_t e = ensure_smem_attr((const void*)dropout_tma_kernel<TI, TO>, smem);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(dropout_tma_kernel)");
+  dropout_tma_kernel<TI, TO><<<grid, kDropWarps * 32, smem, s>>>(m, st_in, st_out, thr24, reinterpret_cast<TO*>(out),
+                                                                  out_ld, mask_out, rows, cols, run, scale, tab);
+  TPP_CUDA_LAUNCH_CHECK("dropout_tma_kernel");
+  return TPP_OK;
 }
 
 // PRNG fill (ops.py:416-427): FP32 uniforms.  Item = blockIdx.x: column group
@@ -603,8 +821,52 @@ int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t*
   // 1) keep mask.  keep <=> (float)(w >> 8) * 2^-24 >= float32(p) <=> (w >> 8) >= ceil(float32(p) * 2^24)
   const double thr = std::ceil((double)(float)p * 16777216.0);
   const uint32_t thr24 = (uint32_t)thr;  // <= 2^24; 2^24 means "never keep"
+  // TPP_DROPOUT_FUSED=2: the register-staged fused kernel below instead of
+  // the TMA-fed one (experiments)
+  static const int fused_mode = [] {
+    const char* e = getenv("TPP_DROPOUT_FUSED");
+    return e ? atoi(e) : 0;
+  }();
   // dense column-major BF16 / FP32 views with whole 64-row slabs: draws and
-  // the scaled copy fused into one pass
+  // the scaled copy fused into one pass -- TMA-fed (dropout_tma_kernel)
+  static const bool no_tma = fused_mode == 2;  // experiments
+  const int esz = in.dtype == TPP_BF16 ? 2 : 4;
+  if (!f64 && !no_tma && rows % kSub == 0 && in.bcast == TPP_BCAST_NONE &&
+      (in.dtype == TPP_BF16 || in.dtype == TPP_FP32) && (out_dtype == TPP_BF16 || out_dtype == TPP_FP32) &&
+      ((uintptr_t)in.p & 15) == 0 && ((int64_t)in.ld * esz) % 16 == 0 && in.ld >= rows &&
+      ((uintptr_t)out & 15) == 0 && out_ld >= rows && out_ld % 8 == 0 && ((uintptr_t)mask_out & 7) == 0 &&
+      !dropout_unfused()) {
+    const int per_sm = esz == 2 ? 4 : 2;  // CTAs resident per SM (shared-memory ring)
+    const int64_t warps = (int64_t)sm_count() * per_sm * kDropWarps;
+    // run: the smallest power-of-two multiple of 128 rows whose items fit one wave
+    int64_t run64 = 2 * kSub;
+    while (cgroups * (((int64_t)rows + run64 - 1) / run64) > warps && run64 < rows) run64 *= 2;
+    const int run = (int)run64;
+    const int64_t segs = ((int64_t)rows + run - 1) / run;
+    const int64_t ctas = (cgroups * segs + kDropWarps - 1) / kDropWarps;
+    if (ctas <= 0x7fffffff) {
+      CUtensorMap m;
+      const uint64_t dims[5] = {(uint64_t)rows * esz / 2, (uint64_t)cols, 1, 1, 1};
+      const uint64_t str[4] = {(uint64_t)in.ld * esz, (uint64_t)in.ld * esz * cols, (uint64_t)in.ld * esz * cols,
+                               (uint64_t)in.ld * esz * cols};
+      const uint32_t box[5] = {(uint32_t)(kSub * esz / 2), 32, 1, 1, 1};
+      int mrc = make_tma_map_5d(&m, in.p, dims, str, box, 0);
+      if (mrc != TPP_OK) return mrc;
+      const float scale = compute_scale<float>(p);
+      const dim3 grid((unsigned)ctas);
+      if (in.dtype == TPP_BF16 && out_dtype == TPP_BF16)
+        return launch_dropout_tma<uint16_t, uint16_t>(m, st_in, st_out, thr24, out, out_ld, mask_out, rows, cols, run,
+                                                      scale, tab, grid, s);
+      if (in.dtype == TPP_BF16)
+        return launch_dropout_tma<uint16_t, float>(m, st_in, st_out, thr24, out, out_ld, mask_out, rows, cols, run,
+                                                   scale, tab, grid, s);
+      if (out_dtype == TPP_BF16)
+        return launch_dropout_tma<float, uint16_t>(m, st_in, st_out, thr24, out, out_ld, mask_out, rows, cols, run,
+                                                   scale, tab, grid, s);
+      return launch_dropout_tma<float, float>(m, st_in, st_out, thr24, out, out_ld, mask_out, rows, cols, run, scale,
+                                              tab, grid, s);
+    }
+  }
   if (!f64 && rows % kSub == 0 && in.ld == rows && out_ld == rows && in.bcast == TPP_BCAST_NONE &&
       (in.dtype == TPP_BF16 || in.dtype == TPP_FP32) && (out_dtype == TPP_BF16 || out_dtype == TPP_FP32) &&
       ((uintptr_t)in.p & 15) == 0 && ((uintptr_t)out & 15) == 0 && ((uintptr_t)mask_out & 7) == 0 &&

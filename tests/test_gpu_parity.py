@@ -803,6 +803,13 @@ def test_dropout_bitwise(golden):
     (130, 5, 130, 0.25, "fp64"),
     (64, 3, 64, 0.99999999, "fp32"),    # float32(p) == 1.0: nothing kept
     (4100, 40, 4100, 0.0, "bf16"),      # p = 0: everything kept, scale 1
+    # TMA-fed fused kernel (rows % 64 == 0): two interleaved streams per lane
+    (8192, 1024, 8192, 0.1, "bf16"),    # 2 + 2 slabs per warp
+    (1984, 45, 2000, 0.3, "bf16"),      # last warp: stream A only; ragged columns, padded ld
+    (4096, 70, 4104, 0.5, "fp32"),
+    (640, 33, 640, 0.2, "fp32"),
+    (16384, 8, 16384, 0.1, "bf16"),     # one column group, many warps
+    (16384, 2048, 16384, 0.1, "bf16"),  # TMA fused: 4 + 4 slabs per warp, stream B one level-2 jump
 ])
 def test_dropout_matches_oracle(rows, cols, ld, p, dt):
     rng = np.random.default_rng(rows + cols)
