@@ -45,8 +45,11 @@ namespace {
 #ifndef TPP_DRAW_UNROLL
 #define TPP_DRAW_UNROLL 8
 #endif
-#ifndef TPP_DROP_DIAG
-#define TPP_DROP_DIAG 0
+#ifndef TPP_DROP_NS
+#define TPP_DROP_NS 2
+#endif
+#ifndef TPP_DROP_STAGES
+#define TPP_DROP_STAGES 3
 #endif
 #ifndef TPP_DROP_MINB
 #define TPP_DROP_MINB 1
@@ -431,15 +434,7 @@ __global__ void __launch_bounds__(256, TPP_DROP_MINB) dropout_fused_kernel(const
     SlabPart<TI> nxt;
     if (sizeof(TI) == 2 && full_group && q + 1 < nslab) nxt.load(in + d0 + (q + 1) * kSub, col_stride, true);
     uint64_t bits = 0;
-#if TPP_DROP_DIAG == 1
-    bits = 0xF7F7F7F7F7F7F7F7ull ^ (uint64_t)q;
-#else
     if (draws) bits = draw_keep64(s, thr24, kSub);
-#endif
-#if TPP_DROP_DIAG == 2
-    if (draws) mb[q] = bits;
-    continue;
-#endif
     const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
 #pragma unroll
     for (int it = 0; it < 8; ++it) {
@@ -526,21 +521,46 @@ __device__ __forceinline__ void store_vec_n(TO* op, const float (&r)[N]) {
   }
 }
 
+// Four streams at once (see draw_keep64x2).
+__device__ __forceinline__ void draw_keep64x4(Xs128 (&s)[4], uint32_t nthr, uint64_t (&r)[4]) {
+  uint32_t h[2][4];
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    uint32_t l[4] = {0u, 0u, 0u, 0u};
+#pragma unroll kDrawUnroll
+    for (int i = 0; i < 32; ++i) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t w = xs_step_fast(s[q]);
+        asm("{ .reg .u32 d; add.cc.u32 d, %1, %2; addc.u32 %0, %0, %0; }" : "+r"(l[q]) : "r"(w), "r"(nthr));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) h[hf][q] = __brev(l[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = (uint64_t)h[0][q] | ((uint64_t)h[1][q] << 32);
+}
+
 // DROPOUT fused, TMA-fed (dense column-major BF16 / FP32 views, rows % 64
-// == 0).  Warp = 32 consecutive columns x one run of `run` rows (a multiple
-// of 128) split into two halves A / B that the lanes draw as two interleaved
-// streams (lane = column, one jump per stream).  The warp's 32 x 64-row input
-// slabs arrive by TMA into a private kDropStages-deep shared-memory ring (the
-// HBM reads stay in flight without holding registers), in the order A0 B0
-// A1 B1 ...; per slab each lane takes 16-byte chunks (8 lanes per column:
-// conflict-free), fetches the chunk's keep bits from the drawing lane with a
-// shuffle, applies keep ? x * scale : 0 (DROPOUT_INV's rule, FP32 math; RNE +
-// the reference NaN rule for BF16 out) and stores coalesced; the drawing lane
-// stores the slab's 8-byte mask word.  Bitwise the same draws, mask and
-// values as the other DROPOUT paths (ops.py:430-444).
+// == 0).  Warp = 32 consecutive columns x one run of `run` rows split into NS
+// equal parts (NS = 4 for BF16 input, 2 for FP32; each part a power-of-two
+// multiple of 64 rows) that the lanes draw as NS interleaved streams -- the
+// xorshift chain is latency-bound, so the interleave is the ILP (lane =
+// column; part 0 jumps from the seed by popcount(run index) levels, the
+// others are one or two jumps from it).  The warp's 32 x 64-row input slabs
+// arrive by TMA into a private kStages-deep shared-memory ring (the HBM reads
+// stay in flight without holding registers), in the order (slab 0 of parts
+// 0..NS-1), (slab 1 ...), ...; per slab each lane takes 16-byte chunks (8 or
+// 16 lanes per column: conflict-free), fetches the chunk's keep bits from the
+// drawing lane with a shuffle, applies keep ? x * scale : 0 (DROPOUT_INV's
+// rule, FP32 math; RNE + the reference NaN rule for BF16 out) and stores
+// coalesced; the drawing lane stores the slab's 8-byte mask word.  Bitwise
+// the same draws, mask and values as the other DROPOUT paths (ops.py:430-444).
 constexpr int kDropWarps = 4;
 template <typename TI> struct DropTma {
-  static constexpr int kStages = 3;
+  static constexpr int kStreams = sizeof(TI) == 2 ? TPP_DROP_NS : 2;
+  static constexpr int kStages = sizeof(TI) == 2 ? TPP_DROP_STAGES : 3;
   static constexpr int kSlab = 32 * kSub * (int)sizeof(TI);  // bytes per warp slab
   static constexpr int kSmem = kDropWarps * kStages * kSlab + kDropWarps * kStages * 8;
 };
@@ -551,7 +571,7 @@ __global__ void __launch_bounds__(kDropWarps * 32) dropout_tma_kernel(
     uint32_t thr24, TO* __restrict__ out, int64_t out_ld, uint8_t* __restrict__ mask_out, int rows, int cols,
     int run, float scale, const uint4* __restrict__ tab) {
   using namespace sm100;
-  constexpr int E = sizeof(TI), S = DropTma<TI>::kStages, SLAB = DropTma<TI>::kSlab;
+  constexpr int E = sizeof(TI), S = DropTma<TI>::kStages, SLAB = DropTma<TI>::kSlab, NS = DropTma<TI>::kStreams;
   constexpr int EPC = 16 / E;      // elements per 16-byte chunk
   constexpr int CPC = kSub / EPC;  // chunks per column of a slab (= passes per slab)
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -561,40 +581,48 @@ __global__ void __launch_bounds__(kDropWarps * 32) dropout_tma_kernel(
   const int segs = (rows + run - 1) / run;
   const int64_t cg = item / segs;
   if (cg * 32 >= cols) return;  // warp-uniform; barriers and ring are private to the warp
-  const int64_t rs64 = (item - cg * segs) * run;
+  const int rs = (int)(item - cg * segs) * run, part = run / NS;
   uint8_t* ring = dsm + (size_t)w * S * SLAB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (size_t)kDropWarps * S * SLAB) + w * S;
   const int j0 = (int)cg * 32, j = j0 + lane;
-  const int rs = (int)rs64, half = run / 2;
-  const int nA = min(half, rows - rs) / kSub;
-  const int nB = max(0, min(half, rows - rs - half)) / kSub;
-  const int T = nA + nB;
-  auto slab_row = [&](int k) { return k < 2 * nB ? rs + (k & 1) * half + (k >> 1) * kSub : rs + (k - nB) * kSub; };
-  auto issue = [&](int k) {
-    const int st = k % S;
+  int n[NS];  // slabs per stream (non-increasing)
+#pragma unroll
+  for (int i = 0; i < NS; ++i) n[i] = max(0, min(part, rows - rs - i * part)) / kSub;
+  // TMA producer cursor (lane 0): slab q of stream i, streams inner
+  int pq = 0, pi = 0, issued = 0;
+  auto issue_next = [&]() {
+    const int st = issued % S;
     mbar_arrive_expect_tx(&bars[st], SLAB);
-    tma_load_5d(ring + st * SLAB, &tin, &bars[st], slab_row(k) * E / 2, j0, 0, 0, 0);
+    tma_load_5d(ring + st * SLAB, &tin, &bars[st], (rs + pi * part + pq * kSub) * E / 2, j0, 0, 0, 0);
+    ++issued;
+    ++pi;
+    int npi = 0;  // n[pi] without dynamic indexing (keeps n in registers)
+#pragma unroll
+    for (int i = 1; i < NS; ++i) npi = pi == i ? n[i] : npi;
+    if (pi == NS || pq >= npi) pi = 0, ++pq;
   };
+  int total = 0;
+#pragma unroll
+  for (int i = 0; i < NS; ++i) total += n[i];
   if (lane == 0) {
     for (int st = 0; st < S; ++st) mbar_init(&bars[st], 1);
     fence_mbar_init();
-    for (int k = 0; k < min(S, T); ++k) issue(k);
+    while (issued < min(S, total)) issue_next();
   }
   __syncwarp();
   const bool draws = j < cols;
   const int valid_cols = min(32, cols - j0);
-  Xs128 sa{0u, 0u, 0u, 1u}, sb{0u, 0u, 0u, 1u};
-  if (draws) {
-#if TPP_DROP_DIAG == 3
-    sa = Xs128{st_in[j], st_in[cols + j], 1u, 2u};
-    sb = Xs128{st_in[j] ^ 5u, st_in[cols + j], 3u, 4u};
-#else
-    // run is a power-of-two multiple of 128 rows, so rs / 64 has few set
-    // bits (popcount(item's run index) jumps) and stream B is ONE jump from
-    // stream A's start (half / 64 is a power of two: one jump level)
-    sa = start_state(st_in, cols, j, rs, tab);
-    if (nB > 0) sb = jump(sa, tab + (31 - __clz(half / kSub)) * kNibs * 16);
-#endif
+  Xs128 sv[NS];
+  {
+    const int lp = 31 - __clz(part / kSub);  // jump level of one part
+    sv[0] = draws ? start_state(st_in, cols, j, rs, tab) : Xs128{0u, 0u, 0u, 1u};
+    if constexpr (NS == 2) {
+      sv[1] = n[1] > 0 && draws ? jump(sv[0], tab + lp * kNibs * 16) : sv[0];
+    } else {
+      sv[1] = n[1] > 0 && draws ? jump(sv[0], tab + lp * kNibs * 16) : sv[0];
+      sv[2] = n[2] > 0 && draws ? jump(sv[0], tab + (lp + 1) * kNibs * 16) : sv[0];
+      sv[3] = n[3] > 0 && draws ? jump(sv[2], tab + lp * kNibs * 16) : sv[0];
+    }
   }
   uint8_t* mcol = mask_out + (int64_t)j * (rows >> 3);
   // apply-phase mapping: pass p, lane -> column p * CPP + lane / CPC of the
@@ -604,31 +632,35 @@ __global__ void __launch_bounds__(kDropWarps * 32) dropout_tma_kernel(
   const int lane_smem = lane_c * kSub * E + (lane % CPC) * 16;
   TO* const obase = out + (int64_t)(j0 + lane_c) * out_ld + b0;
   const int64_t ostride = (int64_t)CPP * out_ld;
+  const bool special = thr24 >= (1u << 24) || thr24 == 0;
   int k = 0;
 #pragma unroll 1
-  for (int q = 0; q < nA; ++q) {
-    const bool both = q < nB;
-    uint64_t bw0 = 0ull, bw1 = 0ull;
-#if TPP_DROP_DIAG == 1
-    bw0 = 0xF7F7F7F7F7F7F7F7ull ^ (uint64_t)q;
-    bw1 = ~bw0;
-#else
+  for (int q = 0; q < n[0]; ++q) {
+    uint64_t bw[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) bw[i] = 0ull;
     if (draws) {
-      if (both) draw_keep64x2(sa, sb, thr24, bw0, bw1);
-      else bw0 = draw_keep64(sa, thr24, kSub);
+      if (!special && q < n[NS - 1]) {
+        if constexpr (NS == 4) draw_keep64x4(sv, 0u - (thr24 << 8), bw);
+        else draw_keep64x2(sv[0], sv[1], thr24, bw[0], bw[1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NS; ++i)
+          if (q < n[i]) bw[i] = draw_keep64(sv[i], thr24, kSub);
+      }
     }
-#endif
-#pragma unroll 1
-    for (int part = 0; part < (both ? 2 : 1); ++part, ++k) {
-      const uint64_t bits = part ? bw1 : bw0;
-      const int row0 = rs + part * half + q * kSub;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      if (q >= n[i]) break;  // n is non-increasing
+      const uint64_t bits = bw[i];
+      const int row0 = rs + i * part + q * kSub;
       const int st = k % S;
       mbar_wait(&bars[st], (uint32_t)(k / S) & 1u);
       const uint8_t* sl = ring + st * SLAB + lane_smem;
       TO* o = obase + row0;
       const uint32_t lo = (uint32_t)bits, hi = (uint32_t)(bits >> 32);
 #pragma unroll
-      for (int pass = 0; pass < (TPP_DROP_DIAG == 2 ? 0 : CPC); ++pass) {
+      for (int pass = 0; pass < CPC; ++pass) {
         const int c = pass * CPP + lane_c;  // column (within the group) of this lane's chunk
         const uint32_t wl = __shfl_sync(0xffffffffu, lo, c), wh = __shfl_sync(0xffffffffu, hi, c);
         const uint32_t kb = ((b0 < 32 ? wl : wh) >> (b0 & 31)) & ((1u << EPC) - 1u);
@@ -654,14 +686,17 @@ __global__ void __launch_bounds__(kDropWarps * 32) dropout_tma_kernel(
       }
       if (draws) *reinterpret_cast<uint64_t*>(mcol + (row0 >> 3)) = bits;
       __syncwarp();  // every lane's reads of this stage are done before TMA refills it
-      if (lane == 0 && k + S < T) issue(k + S);
+      if (lane == 0 && issued < total) issue_next();
+      ++k;
     }
   }
-  if (draws) {
-    const bool b_last = nB > 0 && rs + half + nB * kSub == rows;
-    const bool a_last = nB == 0 && rs + nA * kSub == rows;
-    if (a_last || b_last) {
-      const Xs128 f = b_last ? sb : sa;
+  if (draws) {  // the stream that drew the column's last row hands the state on
+    bool last = false;
+    Xs128 f = sv[0];
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+      if (n[i] > 0 && rs + i * part + n[i] * kSub == rows) last = true, f = sv[i];
+    if (last) {
       st_out[j] = f.x;
       st_out[cols + j] = f.y;
       st_out[2 * cols + j] = f.z;
@@ -836,10 +871,11 @@ int launch_prng_tile(int mode, const DView& in, const uint32_t* st_in, uint32_t*
       ((uintptr_t)in.p & 15) == 0 && ((int64_t)in.ld * esz) % 16 == 0 && in.ld >= rows &&
       ((uintptr_t)out & 15) == 0 && out_ld >= rows && out_ld % 8 == 0 && ((uintptr_t)mask_out & 7) == 0 &&
       !dropout_unfused()) {
-    const int per_sm = esz == 2 ? 4 : 2;  // CTAs resident per SM (shared-memory ring)
+    // CTAs resident per SM (the shared-memory ring bounds it)
+    const int per_sm = std::max(1, (227 * 1024) / (esz == 2 ? DropTma<uint16_t>::kSmem : DropTma<float>::kSmem));
     const int64_t warps = (int64_t)sm_count() * per_sm * kDropWarps;
-    // run: the smallest power-of-two multiple of 128 rows whose items fit one wave
-    int64_t run64 = 2 * kSub;
+    // run: the smallest power-of-two multiple of (streams x 64) rows whose items fit one wave
+    int64_t run64 = (esz == 2 ? DropTma<uint16_t>::kStreams : DropTma<float>::kStreams) * kSub;
     while (cgroups * (((int64_t)rows + run64 - 1) / run64) > warps && run64 < rows) run64 *= 2;
     const int run = (int)run64;
     const int64_t segs = ((int64_t)rows + run - 1) / run;
