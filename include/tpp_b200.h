@@ -135,7 +135,11 @@ int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void*
 enum tpp_act { TPP_ACT_NONE = 0, TPP_ACT_RELU = 1, TPP_ACT_GELU = 2 };
 enum tpp_fc_flags { TPP_FC_BIAS = 1, TPP_FC_RESIDUAL = 2, TPP_FC_RELU_MASK = 4,
                     TPP_FC_OUT_FP32 = 8, TPP_FC_BIAS_FP32 = 16, TPP_FC_RELU_INV = 32,
-                    TPP_FC_SGD = 64 };
+                    TPP_FC_SGD = 64,
+                    /* draw this GEMM's tiles from a per-stream ticket counter instead of
+                     * the static round-robin walk: for GEMMs the caller runs side by
+                     * side on two streams (they fill each other's idle SMs) */
+                    TPP_FC_DYNAMIC_TILES = 128 };
 
 typedef struct {
   int32_t m_b, n_b, k_b, bm, bn, bk;
@@ -328,6 +332,12 @@ int tpp_split_sgd(int64_t n, uint16_t* hi, uint16_t* lo, const void* grad,
  * prologue done, first stage landed, last MMA issued, accumulator ready,
  * epilogue done, exit.  NULL disables.  Tools only. */
 int tpp_debug_phase_timestamps(uint64_t* dev_buf);
+/* Tile scheduling of the persistent tensor-core FC GEMMs: 0 = static
+ * round-robin except calls flagged TPP_FC_DYNAMIC_TILES (the default), 1 =
+ * dynamic for every call, 2 = static for every call (also TPP_STATIC_TILES=1
+ * at startup), other values query.  Returns the previous mode.  Results do
+ * not depend on it. */
+int tpp_set_tile_scheduling(int32_t mode);
 
 #ifdef __cplusplus
 }

@@ -23,6 +23,7 @@ BCAST_NONE, BCAST_ROW, BCAST_COL, BCAST_SCALAR = range(4)
 ENGINE_AUTO, ENGINE_ORDERED, ENGINE_TENSOR = range(3)
 ACT_NONE, ACT_RELU, ACT_GELU = range(3)
 FC_BIAS, FC_RESIDUAL, FC_RELU_MASK, FC_OUT_FP32, FC_BIAS_FP32, FC_RELU_INV, FC_SGD = 1, 2, 4, 8, 16, 32, 64
+FC_DYNAMIC_TILES = 128
 
 
 class TppUnavailableError(RuntimeError):
@@ -104,6 +105,7 @@ _SIGS = {
                               C.POINTER(TensorDescC), _P, _P]),
     "tpp_split_sgd": (C.c_int, [_I64, _P, _P, _P, _I32, C.c_float, _P]),
     "tpp_debug_phase_timestamps": (C.c_int, [_P]),
+    "tpp_set_tile_scheduling": (C.c_int, [C.c_int32]),
     "tpp_quantize": (C.c_int, [C.POINTER(TensorDescC), _P, _I32, C.c_double,
                                C.POINTER(TensorDescC), _P, _P, _P, _P]),
     "tpp_dequantize": (C.c_int, [C.POINTER(TensorDescC), _P, C.c_double,

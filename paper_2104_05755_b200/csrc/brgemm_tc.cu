@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 
@@ -112,7 +113,22 @@ struct Params {
   int sk_dp, sk_stages;
   float* sk_ws;
   unsigned* sk_flag;
+  // dynamic tile scheduling (FC mode): {ticket, done} counters, zero at
+  // launch and reset by the last worker; null = static round-robin
+  unsigned* dyn;
 };
+
+// Dynamic tile queue: the (pair) leader's producer draws work items from a
+// global ticket counter and publishes each to its CTA's (and the peer's)
+// consumers through a kTQ-deep smem ring (tile id + a full mbarrier per
+// slot).  Workers that start late -- e.g. behind a concurrent kernel on
+// another stream -- simply draw fewer tiles, so two GEMMs launched side by
+// side fill each other's wave-quantisation tails.  The ring needs no empty
+// barriers: the producer publishes item k + 1 when it starts loading item k,
+// it is at most STAGES items ahead of the MMA, which is at most NBUF items
+// ahead of the slowest epilogue warp (TMEM buffers), so a slot is rewritten
+// only after every consumer has read it when kTQ > STAGES + NBUF + 2.
+constexpr int kTQ = 32;
 
 // One worker's walk over its segments: (work item, first stage, end stage)
 struct Seg {
@@ -195,7 +211,9 @@ struct Smem {
   static constexpr int BAR_OFF = RES_OFF + (RES ? kResMaxBytes : 0);
   // barriers: full[S], empty[S], tfull[NBUF], tempty[NBUF], bres; then tmem base +
   // gelu table (float4 x 512: one entry per 9-bit |x| exponent prefix)
-  static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 2 * NBUF + 1) * 8 + 16 + 15) & ~15;
+  // + tile queue: tqf[kTQ] barriers, then the tmem slot (16 B), ids[kTQ]
+  static_assert(kTQ > STAGES + NBUF + 3, "tile queue shallower than the pipeline");
+  static constexpr int TAB_OFF = (BAR_OFF + (2 * STAGES + 2 * NBUF + 1 + kTQ) * 8 + 16 + kTQ * 4 + 15) & ~15;
   // the conv (RES = 2) epilogue has no bias / GELU: no table, no bias staging
   static constexpr int BIAS_OFF = TAB_OFF + (RES >= 2 ? 0 : 512 * 16);    // float [2][256]
   // TMA-store staging: 32 rows x 64 B per epilogue warp, double-buffered
@@ -333,7 +351,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + S::NBUF;
   uint64_t* bres = tempty + S::NBUF;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+  uint64_t* tqf = bres + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tqf + kTQ);
+  int* tq_ids = reinterpret_cast<int*>(tmem_slot + 4);
   float4* gelu_tab = reinterpret_cast<float4*>(smem + S::TAB_OFF);
 
   TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 0, 0, gtimer());
@@ -370,6 +390,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_init(&tempty[a], kEpiWarps * CG);
     }
     mbar_init(bres, 1);
+    for (int i = 0; i < kTQ; ++i) mbar_init(&tqf[i], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -399,6 +420,72 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   auto pdl_wait_after = [](int dep) { asm volatile("griddepcontrol.wait;" ::"r"(dep) : "memory"); };
 
+  // ---- dynamic tile queue (p.dyn: FC mode, RES 0, MC 1, no stream-K) ----
+  const bool dyn = p.dyn != nullptr;
+  const bool q_remote = PAIR && !leader;  // the peer's consumers: slots written by the leader CTA
+  // i-th queued work item (-1: none left); one thread per consumer
+  auto tq_pop = [&](uint32_t i) -> int {
+    const uint32_t slot = i % kTQ, par = (i / kTQ) & 1;
+    if (q_remote) mbar_wait_cluster(&tqf[slot], par);
+    else mbar_wait(&tqf[slot], par);
+    return *reinterpret_cast<volatile int*>(&tq_ids[slot]);
+  };
+  // the leader's producer: publish item i to both CTAs
+  auto tq_push = [&](uint32_t i, int t) {
+    const uint32_t slot = i % kTQ;
+    *reinterpret_cast<volatile int*>(&tq_ids[slot]) = t;
+    if (PAIR) {
+      st_shared_cluster_s32(mapa_shared(smem_u32(&tq_ids[slot]), 1), t);
+      mbar_arrive_cluster(mapa_shared(smem_u32(&tqf[slot]), 1));
+    }
+    mbar_arrive(&tqf[slot]);
+  };
+  // items cl_id and cl_id + n_cl are every worker's first two (static: no
+  // atomic round trip before the first loads); ticket k is item 2 n_cl + k
+  // draw returns the raw ticket; it is converted only where the item is
+  // published, a tile later, so the atomic's round trip never stalls the
+  // producer (its result register is not touched before then)
+  // (inline PTX: atomicAdd() gets warp-aggregated, with a shuffle of the
+  // result right behind the atomic -- exactly the stall this avoids)
+  auto tq_draw = [&]() -> unsigned {
+    unsigned t;
+    asm volatile("atom.global.relaxed.gpu.inc.u32 %0, [%1], 0x7fffffff;" : "=r"(t) : "l"(p.dyn) : "memory");  // +1 (tickets stay far below the wrap bound)
+    return t;
+  };
+  auto tq_item = [&](unsigned ticket) -> int {
+    const unsigned t = ticket + 2u * (unsigned)n_cl;
+    return t < (unsigned)num_tiles ? (int)t : -1;
+  };
+  // every worker draws exactly one ticket past the end; the last one to
+  // finish resets the counters for the next launch on this slot (stream order
+  // -- and griddepcontrol.wait before the first draw -- separates the launches)
+  auto tq_done = [&] {
+    __threadfence();
+    if (atomicAdd(p.dyn + 1, 1u) == (unsigned)n_cl - 1) {
+      atomicExch(p.dyn, 0u);
+      atomicExch(p.dyn + 1, 0u);
+    }
+  };
+  // a warp's work items: lane 0 pops, the id is broadcast.  Dynamic: the
+  // following item is popped in the middle of the current one (warp_ahead),
+  // so the tile boundary costs a register move, not a barrier round trip
+  // (item k + 1 is published when the producer starts item k: never waits)
+  auto warp_pop = [&](uint32_t& qi) -> int {
+    int t = 0;
+    if (lane == 0) t = tq_pop(qi++);
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  auto warp_next = [&](SegWalk& w, uint32_t& qi, int& ahead, Seg& sg) -> bool {
+    if (!dyn) return w.next(sg);
+    const int t = ahead == -2 ? warp_pop(qi) : ahead;  // -2: nothing popped ahead
+    ahead = -2;
+    sg.tile = t; sg.k0 = 0; sg.k1 = nstages;
+    return t >= 0;
+  };
+  auto warp_ahead = [&](uint32_t& qi, int& ahead, int cur) {
+    if (dyn && ahead == -2 && cur >= 0) ahead = warp_pop(qi);
+  };
+
   if (warp == 0 || (RES == 1 && warp == 3)) {
     // ===================== TMA producer(s) =====================
     // RES kernels run two issuing threads (warps 0 and 3) on alternate
@@ -410,15 +497,69 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       SegWalk walk;
       walk.start(p, cl_id, n_cl, nstages);
       Seg sg;
-      bool have = walk.next(sg);
-      if (have) {
-        int tm, tn;
-        tile_mn(sg.tile, tm, tn);
-        if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
-        else f.start(p, tm, tn);
+      // dynamic (leader): item k + 1 is published when item k starts and
+      // the ticket of item k + 2 drawn then, so neither the peer's producer
+      // nor the atomic's round trip ever waits at a tile boundary
+      uint32_t qi = 0;
+      int nxt = -1;
+      unsigned tk = 0;
+      bool ended = false;
+      auto next_seg = [&](Seg& g) -> bool {
+        if (!dyn) return walk.next(g);
+        int t;
+        if (!q_remote) {
+          t = nxt;
+          if (t >= 0 && !ended) {
+            const int item = tq_item(tk);
+            tq_push(qi++, item);
+            nxt = item;
+            if (item < 0) {
+              ended = true;  // tq_done() after the last loads are issued (its fence would stall them)
+            } else {
+              tk = tq_draw();
+            }
+          }
+        } else {
+          t = tq_pop(qi++);
+        }
+        g.tile = t; g.k0 = 0; g.k1 = nstages;
+        return t >= 0;
+      };
+      bool have;
+      if (!dyn || !q_remote) {
+        if (dyn) {  // the two static first items, published before the wait
+          const int a0 = cl_id < num_tiles ? cl_id : -1;
+          const int a1 = a0 >= 0 && cl_id + n_cl < num_tiles ? cl_id + n_cl : -1;
+          tq_push(qi++, a0);
+          if (a0 >= 0) tq_push(qi++, a1);
+          nxt = a1;
+          sg.tile = a0; sg.k0 = 0; sg.k1 = nstages;
+          have = a0 >= 0;
+        } else {
+          have = walk.next(sg);
+        }
+        if (have) {
+          int tm, tn;
+          tile_mn(sg.tile, tm, tn);
+          if (PAIR) f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
+          else f.start(p, tm, tn);
+        }
+        // dynamic: the ticket counter is reset by the previous launch on this slot
+        pdl_wait_after(f.ai.c[0] + f.ai.c[1] + f.ai.c[2] + f.ai.c[3] + f.ai.c[4] + f.bi.c[0] + f.bi.c[1] + f.bi.c[2] +
+                       f.bi.c[3] + f.bi.c[4] + nstages);
+        if (dyn) {
+          if (nxt >= 0) tk = tq_draw();
+          else ended = true;
+        }
+      } else {
+        have = next_seg(sg);  // the peer: the leader's first item
+        if (have) {
+          int tm, tn;
+          tile_mn(sg.tile, tm, tn);
+          f.start(p, 2 * tm + (int)rank, 2 * tn + (int)rank);
+        }
+        pdl_wait_after(f.ai.c[0] + f.bi.c[0] + nstages);
       }
-      pdl_wait_after(f.ai.c[0] + f.ai.c[1] + f.ai.c[2] + f.ai.c[3] + f.ai.c[4] + f.bi.c[0] + f.bi.c[1] + f.bi.c[2] +
-                     f.bi.c[3] + f.bi.c[4] + nstages);
       TPP_STAMP(blockIdx.x == 0 && pid == 0, 10, gtimer());
       if (RES && pid == 0) {
         // resident weights: every tap block once, on the bres barrier
@@ -437,7 +578,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       // pair: completion bytes of both CTAs count on the leader's full[s]
       const uint32_t full_cl = PAIR ? mapa_shared(smem_u32(full), 0) : 0;
       bool first = true;
-      for (; have; have = walk.next(sg), first = false) {
+      for (; have; have = next_seg(sg), first = false) {
         if (!first) {  // the first segment's feed was set up before the wait
           int tm, tn;
           tile_mn(sg.tile, tm, tn);
@@ -474,6 +615,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
       }
+      if (dyn && !q_remote) tq_done();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread; pair: the leader's) =====================
@@ -494,7 +636,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       SegWalk walk;
       walk.start(p, cl_id, n_cl, nstages);
       Seg sg;
-      for (; walk.next(sg); ++tcount) {
+      uint32_t qi = 0;
+      int ahead = -2;
+      for (; warp_next(walk, qi, ahead, sg); ++tcount) {
         const int j0 = sg.k0;
         const uint32_t as = tcount % S::NBUF, aph = (tcount / S::NBUF) & 1;
         mbar_wait(&tempty[as], aph ^ 1);
@@ -589,6 +733,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           else if (MCAST) umma_commit_mc_warp(&empty[s], (uint16_t)((1u << MC) - 1));
           else umma_commit_warp(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }
+          warp_ahead(qi, ahead, sg.tile);  // the MMAs of this stage are queued: slack
         }
         if (PAIR) umma_commit_pair_warp(&tfull[as], 3);
         else umma_commit_warp(&tfull[as]);
@@ -610,7 +755,9 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     SegWalk walk;
     walk.start(p, cl_id, n_cl, nstages);
     Seg sg;
-    for (; walk.next(sg); ++tcount) {
+    uint32_t qi = 0;
+    int ahead = -2;
+    for (; warp_next(walk, qi, ahead, sg); ++tcount) {
       const int tile = sg.tile;
       int tm, tn;
       tile_mn(tile, tm, tn);
@@ -673,6 +820,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
       }
       asm volatile("" ::"r"(t), "r"(nb), "r"(n_in), "r"(sc1), "r"(sc2), "r"(sc4), "r"((int)warp_rows));
       mbar_wait(&tfull[as], aph);
+      warp_ahead(qi, ahead, tile);
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 4, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 189, clock64());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount < 32, 18 + 4 * tcount, gtimer());
@@ -1039,6 +1187,77 @@ static float* sk_workspace(cudaStream_t stream, size_t floats, unsigned** flags)
   return it->second.first;
 }
 
+// Dynamic tile scheduling: FC-mode GEMMs flagged TPP_FC_DYNAMIC_TILES (the
+// overlapped backward of BlockedMLP), or all of them under
+// tpp_set_tile_scheduling(1).  Alone, a GEMM runs as fast either way
+// (tools/dyn_ab.py: within 1-3 %); side by side on two streams the dynamic
+// draw lets each fill the other's idle SMs.
+static std::atomic<int> g_tile_mode{-1};  // -1: not yet read from the environment
+static int tile_mode() {
+  int v = g_tile_mode.load(std::memory_order_relaxed);
+  if (v < 0) {
+    int want = getenv("TPP_STATIC_TILES") != nullptr ? 2 : 0, expect = -1;
+    g_tile_mode.compare_exchange_strong(expect, want);
+    v = g_tile_mode.load(std::memory_order_relaxed);
+  }
+  return v;
+}
+}  // namespace tc
+int set_tile_scheduling(int mode) {
+  const int prev = tc::tile_mode();
+  if (mode >= 0 && mode <= 2) tc::g_tile_mode.store(mode);
+  return prev;
+}
+namespace tc {
+
+// Ticket counters for dynamic tile scheduling: one 32-byte slot {ticket, done}
+// per (device, stream).  Launches on one stream are ordered (a PDL successor
+// draws only after griddepcontrol.wait, i.e. after its predecessor's reset),
+// so a slot is never shared by two running kernels; kernels on different
+// streams -- the concurrent GEMMs this exists for -- use different slots.  The
+// buffer is allocated and zeroed once per device, outside any graph capture
+// (a capture before first use runs the static walk).  A captured graph keeps
+// its capture streams' slots: it must not be replayed concurrently with other
+// work on those streams.
+static unsigned* dyn_counter(cudaStream_t stream) {
+  constexpr int kSlots = 4096, kStride = 8;
+  struct Dev {
+    unsigned* buf = nullptr;
+    std::unordered_map<cudaStream_t, int> slot;
+  };
+  static std::mutex mu;
+  static std::unordered_map<int, Dev> devs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  Dev& d = devs[dev];
+  if (!d.buf) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    void* ptr = nullptr;
+    if (cudaMalloc(&ptr, (size_t)kSlots * kStride * sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (cudaMemset(ptr, 0, (size_t)kSlots * kStride * sizeof(unsigned)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(ptr);
+      return nullptr;
+    }
+    d.buf = static_cast<unsigned*>(ptr);
+  }
+  auto it = d.slot.find(stream);
+  if (it == d.slot.end()) {
+    if ((int)d.slot.size() >= kSlots) return nullptr;
+    it = d.slot.emplace(stream, (int)d.slot.size()).first;
+  }
+  return d.buf + (size_t)it->second * kStride;
+}
+
 template <int BN, int STAGES, int KPS, int RES = 0, int CG = 1, int MC = 1>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       const Params& p, cudaStream_t stream) {
@@ -1095,6 +1314,10 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
       }
     }
   }
+  pk.dyn = nullptr;
+  if (RES == 0 && MC == 1 && p.mode == FEED_FC && pk.sk_stages == 0 && units > 1 &&
+      (tile_mode() == 1 || (tile_mode() == 0 && (p.flags & TPP_FC_DYNAMIC_TILES))))
+    pk.dyn = dyn_counter(stream);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -1115,7 +1338,8 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
                   std::to_string(MC) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(p.tiles_m) +
                   "x" + std::to_string(p.tiles_n) +
                   (pk.sk_stages ? " streamk=" + std::to_string(units - pk.sk_dp) + "/" + std::to_string(units)
-                                : std::string()));
+                                : std::string()) +
+                  (pk.dyn ? " dyn" : ""));
   return TPP_OK;
 }
 
@@ -1331,6 +1555,28 @@ int pick_cg(int BN, int tiles_m, int tiles_n, bool b_mn) {
   return (BN == 256 && (int64_t)((tiles_m + 1) / 2) * tiles_n >= num_sms() / 2) ? 2 : 1;
 }
 
+// Long GEMMs with less than a wave of pair tiles: one wave of 256-wide pair
+// tiles (the tensor pipe at its floor) can beat ~2 waves of 1-CTA tiles that
+// are shared-memory bound (128 x 128: both 4 KB operands per 64-cycle MMA; 128
+// x 256: 188 B/cycle; 128 x 64: 48-cycle MMAs).  Cost per SM ~ waves x the
+// SM's share of a tile / MMA efficiency; measured on the cfg-5 dW of the
+// 1024-wide layers (1024 x 4096 over 8192 tokens): 79 us as 64 pair tiles in
+// one wave vs 102 us as 256 1-CTA 128 x 128 tiles in 1.73 waves.
+void prefer_pairs(int feats, int tiles_m, int pref, int& BN, int& cg, int blk = 64) {
+  static const bool forced = getenv("TPP_BN") != nullptr || getenv("TPP_CG") != nullptr;
+  if (cg == 2 || pref || forced || feats % 256 != 0 || tiles_m < 2) return;
+  if (blk >= 256 ? blk % 256 != 0 : 256 % blk != 0) return;  // output blocks must tile the 256-wide tile
+  auto eff = [](int bn) { return bn == 256 ? 0.68 : bn == 128 ? 0.77 : 0.67; };
+  const int64_t sms = num_sms(), pairs = sms / 2;
+  const int64_t u1 = (int64_t)tiles_m * (feats / BN), w1 = (u1 + sms - 1) / sms;
+  const int64_t u2 = (int64_t)((tiles_m + 1) / 2) * (feats / 256), w2 = (u2 + pairs - 1) / pairs;
+  const double c1 = (double)w1 * 128.0 * BN / eff(BN), c2 = (double)w2 * 128.0 * 256.0;
+  if (c2 < c1) {
+    BN = 256;
+    cg = 2;
+  }
+}
+
 // A-multicast cluster size for forward FC (experiments: TPP_MC=2|4).  Off by
 // default: on cfg 2 (one 128x64 tile per CTA) clusters of 2 / 4 sharing the
 // activation boxes measured 6.96 / 7.12 us against 6.25 us without -- halving
@@ -1403,11 +1649,12 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     TPP_REQUIRE(bk % 64 == 0 && bm % 32 == 0, TPP_E_UNSUPPORTED, "tensor-core FC needs bk % 64 == 0, bm % 32 == 0");
     const int feats = m_b * bm, tokens = n_b * bn;
     const int tiles_m = (tokens + BM - 1) / BM;
-    const int BN = pick_bn(feats, tiles_m, d->block_n);
+    int BN = pick_bn(feats, tiles_m, d->block_n);
     TPP_REQUIRE(feats % BN == 0 && ((bm >= BN && bm % BN == 0) || (bm < BN && BN % bm == 0)),
                 TPP_E_UNSUPPORTED, "features must tile by the tile width");
     const int kblocks = k_b * (bk / 64);
-    const int cg = pick_cg(BN, tiles_m, feats / BN, false);
+    int cg = pick_cg(BN, tiles_m, feats / BN, false);
+    prefer_pairs(feats, tiles_m, d->block_n, BN, cg, bm);
     const int kps = pick_kps(BN, kblocks, bk == 64, cg);
     const int mc = pick_mc(BN, cg, kps, tiles_m, feats / BN);
     p.tokens = tokens; p.kblocks = kblocks;
@@ -1421,10 +1668,11 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
     TPP_REQUIRE(bk == 64 && bm % 64 == 0, TPP_E_UNSUPPORTED, "backward-data needs bk == 64, bm % 64 == 0");
     const int feats = k_b * bk, tokens = n_b * bn;
     const int tiles_m = (tokens + BM - 1) / BM;
-    const int BN = pick_bn(feats, tiles_m, d->block_n);
+    int BN = pick_bn(feats, tiles_m, d->block_n);
     TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
     const int kblocks = m_b * (bm / 64);
-    const int cg = pick_cg(BN, tiles_m, feats / BN, true);
+    int cg = pick_cg(BN, tiles_m, feats / BN, true);
+    prefer_pairs(feats, tiles_m, d->block_n, BN, cg);
     const int kps = pick_kps(BN, kblocks, bm == 64, cg);
     p.tokens = tokens; p.kblocks = kblocks;
     p.tiles_m = tiles_m; p.tiles_n = feats / BN; p.feats = feats; p.bn_tile = BN;
@@ -1438,10 +1686,11 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
               "backward-weights needs bm == bk == 64 and bn % 64 == 0");
   const int rows = m_b * bm, feats = k_b * bk;
   const int tiles_m = (rows + BM - 1) / BM;
-  const int BN = pick_bn(feats, tiles_m, d->block_n);
+  int BN = pick_bn(feats, tiles_m, d->block_n);
   TPP_REQUIRE(feats % BN == 0, TPP_E_UNSUPPORTED, "input features must tile by the tile width");
   const int kblocks = n_b * (bn / 64);
-  const int cg = pick_cg(BN, tiles_m, feats / BN, true);
+  int cg = pick_cg(BN, tiles_m, feats / BN, true);
+  prefer_pairs(feats, tiles_m, d->block_n, BN, cg);
   int kps = pick_kps(BN, kblocks, true, cg);
   while (kps > 1 && bn != 64 && bn % (64 * kps) != 0) kps /= 2;  // a box must not skip token rows
   p.tokens = rows; p.kblocks = kblocks;

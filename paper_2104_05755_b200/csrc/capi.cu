@@ -84,6 +84,7 @@ int tpp_debug_phase_timestamps(uint64_t* dev_buf) {
   set_debug_timestamps(reinterpret_cast<unsigned long long*>(dev_buf));
   return TPP_OK;
 }
+int tpp_set_tile_scheduling(int32_t mode) { return set_tile_scheduling(mode); }
 int tpp_version(void) { return 1; }
 int tpp_device_sm_count(void) {
   int dev = 0, n = 0;
@@ -246,8 +247,8 @@ int tpp_fc_backward_weights(const tpp_fc_desc* d, const void* dout, const void* 
   if (rc) return rc;
   TPP_REQUIRE(d->in_dtype == TPP_BF16, TPP_E_SPEC_DTYPE, "FC backward runs on BF16 operands");
   TPP_REQUIRE(dout && x && dw, TPP_E_TENSOR, "null FC operand");
-  TPP_REQUIRE(!(d->flags & ~TPP_FC_OUT_FP32) && d->activation == TPP_ACT_NONE, TPP_E_SPEC_FLAG,
-              "backward-weights takes only the FP32-output flag");
+  TPP_REQUIRE(!(d->flags & ~(TPP_FC_OUT_FP32 | TPP_FC_DYNAMIC_TILES)) && d->activation == TPP_ACT_NONE,
+              TPP_E_SPEC_FLAG, "backward-weights takes only the FP32-output flag");
   return fc_gemm_tc(2, d, nullptr, dout, x, nullptr, nullptr, dw, nullptr, nullptr, as_stream(stream));
 }
 
@@ -260,10 +261,10 @@ int tpp_fc_backward_weights_sgd(const tpp_fc_desc* d, const void* dout, const vo
   TPP_REQUIRE(w_hi != w_lo, TPP_E_TENSOR, "hi and lo halves must be distinct buffers");
   TPP_REQUIRE(reinterpret_cast<uintptr_t>(w_hi) % 16 == 0 && reinterpret_cast<uintptr_t>(w_lo) % 16 == 0,
               TPP_E_TENSOR, "split-master halves must be 16-byte aligned");
-  TPP_REQUIRE(!(d->flags & ~(TPP_FC_OUT_FP32 | TPP_FC_SGD)) && d->activation == TPP_ACT_NONE, TPP_E_SPEC_FLAG,
-              "backward-weights-SGD takes no epilogue flags");
+  TPP_REQUIRE(!(d->flags & ~(TPP_FC_OUT_FP32 | TPP_FC_SGD | TPP_FC_DYNAMIC_TILES)) && d->activation == TPP_ACT_NONE,
+              TPP_E_SPEC_FLAG, "backward-weights-SGD takes no epilogue flags");
   tpp_fc_desc dd = *d;
-  dd.flags = TPP_FC_OUT_FP32 | TPP_FC_SGD;
+  dd.flags = TPP_FC_OUT_FP32 | TPP_FC_SGD | (d->flags & TPP_FC_DYNAMIC_TILES);
   return fc_gemm_tc(2, &dd, nullptr, dout, x, nullptr, nullptr, w_hi, nullptr, nullptr, as_stream(stream), w_lo, lr);
 }
 

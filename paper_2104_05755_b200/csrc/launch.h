@@ -65,6 +65,7 @@ int fc_gemm_tc(int flavor, const tpp_fc_desc* d, const void* w_packed, const voi
                void* mask_out, const void* mask_in, cudaStream_t stream, uint16_t* sgd_lo = nullptr,
                float sgd_lr = 0.0f);
 void set_debug_timestamps(unsigned long long* p);
+int set_tile_scheduling(int mode);  // 0 flagged calls dynamic, 1 all, 2 none; other: query; returns the previous mode
 unsigned long long* debug_timestamps();
 // brgemm_grouped.cu (K11): BF16 BRGEMM on tcgen05 over stride / offset /
 // address batches, `groups` C blocks per launch; 1 = not applicable

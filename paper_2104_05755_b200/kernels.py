@@ -169,15 +169,17 @@ class FcLayer:
         return out
 
     def backward_data(self, dout: torch.Tensor, n_b: int, bn: int, relu_mask_in: Optional[torch.Tensor] = None,
-                      out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+                      out: Optional[torch.Tensor] = None, stream=None, dynamic_tiles: bool = False) -> torch.Tensor:
         """din = dout . W  ([n_b][k_b][bn][bk], BF16), optionally masked by the
-        forward input's ReLU bitmask (RELU_INV fused in the epilogue)."""
+        forward input's ReLU bitmask (RELU_INV fused in the epilogue).
+        ``dynamic_tiles``: tiles drawn dynamically (TPP_FC_DYNAMIC_TILES), for
+        a GEMM that runs beside another one on a second stream."""
         if dout.dtype != torch.bfloat16 or dout.numel() < n_b * self.m_b * bn * self.bm:
             raise TensorError("dout must be a BF16 [n_b][m_b][bn][bm] buffer")
         n_in = n_b * self.k_b * bn * self.bk
         if out is None:
             out = torch.empty(n_in, dtype=torch.bfloat16, device=dout.device)
-        flags = 0
+        flags = _lib.FC_DYNAMIC_TILES if dynamic_tiles else 0
         if relu_mask_in is not None:
             if relu_mask_in.numel() < n_b * self.k_b * bn * ((self.bk + 7) // 8):
                 raise TensorError("bitmask buffer too small")
@@ -209,7 +211,7 @@ class FcLayer:
 
 
     def backward_weights_sgd(self, dout: torch.Tensor, x: torch.Tensor, n_b: int, bn: int, w_lo: torch.Tensor,
-                             lr: float, stream=None) -> None:
+                             lr: float, stream=None, dynamic_tiles: bool = False) -> None:
         """dW = sum over tokens of dout^T x applied at once as split-SGD on the
         FP32 master whose hi halves are this layer's packed weights
         (``w_packed``) and lo halves ``w_lo`` (kernels.py:235-251): the FP32
@@ -222,7 +224,8 @@ class FcLayer:
         if w_lo.numel() < n_w or w_lo.element_size() != 2:
             raise TensorError("w_lo must hold the 16-bit lo halves of every weight")
         lib = _lib.load()
-        d = _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16, _lib.ACT_NONE, 0, self.block_n)
+        d = _lib.FcDescC(self.m_b, n_b, self.k_b, self.bm, bn, self.bk, _lib.BF16, _lib.ACT_NONE,
+                         _lib.FC_DYNAMIC_TILES if dynamic_tiles else 0, self.block_n)
         _lib.check(lib.tpp_fc_backward_weights_sgd(C.byref(d), dout.data_ptr(), x.data_ptr(),
                                                    self.w_packed.data_ptr(), w_lo.data_ptr(), float(lr),
                                                    _lib.stream_ptr(stream)), "FcLayer.backward_weights_sgd")

@@ -57,7 +57,8 @@ class BlockedMLP:
     def __init__(self, dims: Sequence[int], tokens: int, bn: int = 64, lr: float = 0.01,
                  global_batch: Optional[int] = None, init_std: float = 0.02, seed: int = 0,
                  device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None,
-                 grad_dtype: str = "fp32", reduce_fn=None, fuse_sgd: Optional[bool] = None):
+                 grad_dtype: str = "fp32", reduce_fn=None, fuse_sgd: Optional[bool] = None,
+                 overlap: bool = True):
         """``grad_dtype``: "fp32" (dW written and applied in FP32) or "bf16"
         (dW written as BF16 by the backward-weights epilogue, exchanged as
         BF16 — half the allreduce bytes — and applied by split-SGD, which
@@ -66,7 +67,13 @@ class BlockedMLP:
         ``fuse_sgd`` (default: on when there is no gradient exchange and dW is
         FP32): each layer's split-SGD runs inside its backward-weights GEMM
         epilogue, so dW is never written (``self.dw`` stays unused); results
-        are bitwise those of the unfused step."""
+        are bitwise those of the unfused step.
+        ``overlap`` (fused-SGD steps): each hidden layer's backward-weights
+        GEMM runs on a side stream, concurrently with the next layer's
+        backward-data GEMM (and layer 0's with layer 1's); the tensor-core
+        kernels draw their tiles dynamically, so the two fill each other's
+        wave-quantisation tails.  Results are bitwise those of the serial
+        order (the kernels are independent and deterministic per tile)."""
         if grad_dtype not in ("fp32", "bf16"):
             raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         if any(d % BLK for d in dims) or tokens % bn or bn % BLK:
@@ -110,6 +117,8 @@ class BlockedMLP:
         if fuse_sgd and (self.sync.active or grad_dtype != "fp32"):
             raise ValueError("fused split-SGD needs FP32 gradients and no gradient exchange")
         self.fuse_sgd = fuse_sgd
+        self.overlap = overlap and fuse_sgd
+        self._side = torch.cuda.Stream(device=dev) if self.overlap else None
         # optional per-launch hook (label) called right after each main-stream
         # launch -- bench.py records CUDA events there for the step breakdown
         self.trace = None
@@ -140,16 +149,30 @@ class BlockedMLP:
         if tr:
             tr("xent")
         if self.fuse_sgd:
+            # the per-launch trace (bench breakdown) times the serial order
+            main = torch.cuda.current_stream(self.device)
+            side = self._side if tr is None else None
+            dyn = side is not None   # the GEMMs that run side by side draw their tiles dynamically
             for l in range(nl - 1, -1, -1):
                 layer = self.layers[l]
                 if l > 0:   # the last reader of the layer's weights goes first
                     layer.backward_data(self.g[l], self.n_b, self.bn, relu_mask_in=self.mask[l],
-                                        out=self.g[l - 1])
+                                        out=self.g[l - 1], dynamic_tiles=dyn and l < nl - 1)
                     if tr:
                         tr(f"dx{l}")
-                layer.backward_weights_sgd(self.g[l], self.h[l], self.n_b, self.bn, self.lo[l], self.lr)
+                if side is not None and l > 0:
+                    # dW_l + SGD after dX_l (it rewrites W_l), beside dX_{l-1}
+                    side.wait_stream(main)
+                    with torch.cuda.stream(side):
+                        layer.backward_weights_sgd(self.g[l], self.h[l], self.n_b, self.bn, self.lo[l], self.lr,
+                                                   dynamic_tiles=True)
+                else:
+                    layer.backward_weights_sgd(self.g[l], self.h[l], self.n_b, self.bn, self.lo[l], self.lr,
+                                               dynamic_tiles=dyn)
                 if tr:
                     tr(f"dw{l}")
+            if side is not None:
+                main.wait_stream(side)
             return
         for l in range(nl - 1, -1, -1):
             layer = self.layers[l]

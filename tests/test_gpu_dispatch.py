@@ -210,7 +210,8 @@ def test_cfg5_full_train_step(monkeypatch):
     bwd_w = [c for k, c in rec.log if k == "backward_weights"]
     assert all(c.startswith(PAIR256) for c in fwd), fwd
     assert all(c.startswith(PAIR256) for c in bwd_d), bwd_d
-    assert bwd_w[1].startswith(PAIR256) and bwd_w[2].startswith(PAIR256), bwd_w  # layers 3 and 2 (4096 x 4096)
+    # dW of the 1024-wide layers too: one wave of pair tiles beats 1.73 waves of 1-CTA tiles (prefer_pairs)
+    assert all(c.startswith(PAIR256) for c in bwd_w), bwd_w
 
     wb = [O.bf16_to_fp32((w.view(np.uint32) >> 16).astype(np.uint16)) for w in ws]  # the hi halves the GEMMs read
     sel = [0, 97]
@@ -327,3 +328,70 @@ def test_pair_backward_at_cfg5_dims_vs_fp64(monkeypatch):
         # tensor core's accumulator (see test_cfg5_full_train_step): well
         # inside the BF16 tolerance, ~1e-5 from FP64
         assert e <= 1e-4, fb
+
+
+# ---------------------------------------------------------------------------
+# dynamic tile scheduling: ticket counters reset launch after launch, and two
+# GEMMs running side by side on two streams (the overlapped backward) draw
+# disjoint, complete tile sets
+# ---------------------------------------------------------------------------
+@pytest.fixture
+def _all_dynamic():
+    lib = _lib.load()
+    prev = lib.tpp_set_tile_scheduling(1)   # every FC GEMM draws its tiles dynamically
+    yield
+    lib.tpp_set_tile_scheduling(prev)
+
+
+def test_dynamic_tiles_concurrent_streams(_all_dynamic):
+    rng = np.random.default_rng(11)
+    T_, C_, F_ = 4096, 1024, 4096   # 16 x 16 = 256 pair tiles: 3.46 waves
+    n_b, bn = T_ // 64, 64
+    x = to_dev(O.fp32_to_bf16_rne(rng.standard_normal(T_ * C_, dtype=np.float32)))
+    w = to_dev(vnni_weights(rng, F_ // 64, C_ // 64, 64, 64, 0.02))
+    layer = tpp.FcLayer(F_ // 64, C_ // 64, 64, 64, w, activation=tpp.UnaryKind.RELU)
+    ref = layer.forward(x, n_b, bn)
+    torch.cuda.synchronize()
+    assert _lib.last_config().startswith(PAIR256) and _lib.last_config().endswith(" dyn"), _lib.last_config()
+    want = to_host(ref)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty_like(ref) for _ in range(24)]
+    for o in outs:
+        o.fill_(float("nan"))
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        with torch.cuda.stream(s1 if i % 2 == 0 else s2):
+            layer.forward(x, n_b, bn, out=o)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        assert np.array_equal(to_host(o), want), i
+    # and a 1-CTA shape (cfg 2 dims): 128 tiles, one wave
+    x2 = to_dev(O.fp32_to_bf16_rne(rng.standard_normal(1024 * 1024, dtype=np.float32)))
+    w2 = to_dev(vnni_weights(rng, 16, 16, 64, 64, 0.02))
+    l2 = tpp.FcLayer(16, 16, 64, 64, w2)
+    r2 = to_host(l2.forward(x2, 16, 64))
+    for _ in range(3):
+        assert np.array_equal(to_host(l2.forward(x2, 16, 64)), r2)
+    assert _lib.last_config().startswith("brgemm_tc_kernel<64,") and _lib.last_config().endswith(" dyn"), \
+        _lib.last_config()
+
+
+def test_overlapped_step_equals_serial_step():
+    """The fused-SGD step with the overlapped backward (dW_l on a side stream
+    beside dX_{l-1}, tiles drawn dynamically) is bitwise the serial step."""
+    rng = np.random.default_rng(5)
+    dims, Tk, bn = [1024, 4096, 4096, 4096, 1024], 8192, 64
+    ws = [torch.from_numpy(rng.standard_normal((dims[l + 1], dims[l]), dtype=np.float32) * np.float32(0.02))
+          for l in range(len(dims) - 1)]
+    x = to_dev(O.fp32_to_bf16_rne(rng.standard_normal(Tk * dims[0], dtype=np.float32)))
+    tg = to_dev(rng.integers(0, dims[-1], Tk).astype(np.int32))
+    a = tpp.BlockedMLP(dims, Tk, bn=bn, lr=0.01, global_batch=Tk, weights=ws, overlap=True)
+    b = tpp.BlockedMLP(dims, Tk, bn=bn, lr=0.01, global_batch=Tk, weights=ws, overlap=False)
+    assert a.overlap and not b.overlap
+    for _ in range(3):
+        la = to_host(a.train_step(x, tg))
+        lb = to_host(b.train_step(x, tg))
+        torch.cuda.synchronize()
+        assert np.array_equal(la, lb)
+    for l in range(len(dims) - 1):
+        assert torch.equal(a.hi[l], b.hi[l]) and torch.equal(a.lo[l], b.lo[l]), l
