@@ -204,6 +204,25 @@ __device__ __forceinline__ float exp_taylor(float x) {
   return out;
 }
 
+// exp_taylor restricted to x <= 0 or NaN (softmax: x = v - max): bitwise the
+// same results -- the x > 88 overflow branch and the upper exponent clamp
+// cannot fire, and a NaN x gives NaN through q either way -- in 3 fewer
+// instructions
+__device__ __forceinline__ float exp_taylor_nonpos(float x) {
+  const float log2e = __uint_as_float(0x3FB8AA3Bu);
+  const float c1 = __uint_as_float(0x3F316F7Du);
+  const float c2 = __uint_as_float(0x3E781EEEu);
+  const float c3 = __uint_as_float(0x3D656460u);
+  float r = __fmul_rn(x, log2e);
+  float n = rintf(r);
+  float y = __fsub_rn(r, n);
+  float q = __fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(__fadd_rn(__fmul_rn(c3, y), c2), y), c1), y), 1.0f);
+  int ni = (int)fmaxf(n, -126.0f);
+  float out = __fmul_rn(q, __int_as_float((ni + 127) << 23));
+  if (x < -87.0f) out = 0.0f;
+  return out;
+}
+
 // Logical element (i, j) of a column-major view with ROW/COL/SCALAR broadcast
 // (tensor.py:207-217), widened exactly; stores narrow once (RNE for BF16).
 template <typename T>

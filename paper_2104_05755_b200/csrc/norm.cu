@@ -11,6 +11,7 @@
 // consecutive rows) or from shared memory (blocked layout), never from
 // scattered HBM.
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -1002,10 +1003,196 @@ softmax_xent_blocked_kernel(int n_b, int m_b, int bn, int bm, const float* __res
   }
 }
 
+// ---- softmax-CE with every token of an SM resident -------------------------
+// The reference's per-token sum is a 1024-long dependent FADD chain (~4k
+// cycles).  In the 16-token kernel above every other warp of the CTA waits at
+// a barrier while 16 lanes run it (ncu: 28 % of the warp samples on that
+// barrier, 1.15 waves of 3 CTAs per SM, DRAM 13 % busy).  Here one CTA per SM
+// owns <= 56 consecutive tokens, all resident in smem at once (56 x 4 KB):
+//   warps 2-15  copy every token's logits into smem at once (cp.async, each
+//               thread the 16-byte quads it reads later: the whole SM share
+//               in flight); per token (a half warp, 16 float4 per lane in
+//               registers): max (16-lane shuffle), exp_taylor, exponentials
+//               back to smem -- tokens 0-27 first, so their sums overlap the
+//               second round's exponentials; then each round's dlogits once
+//               its sums are done
+//   warps 0, 1  the serial sums of tokens 0-27 / 28-55 (lane = token).
+// (256-byte TMA bulk copies per token row measured slower: 58 vs 38 us.)
+// Same arithmetic and order as the kernel above (bitwise).
+constexpr int kXpThreads = 512;
+constexpr int kXpWorkers = kXpThreads - 64;       // 14 warps = 28 token rows per round
+constexpr int kXpRound = kXpWorkers / 16;          // 28
+constexpr int kXpMaxTok = 2 * kXpRound;            // 56
+
+__global__ void __launch_bounds__(kXpThreads, 1)
+softmax_xent_resident_kernel(int n_tok, int m_b, int bn, const float* __restrict__ logits,
+                             const int32_t* __restrict__ targets, float scale, uint16_t* __restrict__ dlog,
+                             float* __restrict__ loss) {
+  using namespace sm100;
+  extern __shared__ __align__(16) uint8_t xsm[];
+  const int F = m_b * 64;
+  const int pitch = F + 4;  // floats; 16-byte aligned rows, 4-bank skew per token
+  float* rows = reinterpret_cast<float*>(xsm);
+  float* rcs = rows + kXpMaxTok * pitch;
+  uint64_t* exp_ready = reinterpret_cast<uint64_t*>(rcs + kXpMaxTok);  // [2] round's exponentials written
+  uint64_t* sum_ready = exp_ready + 2;                                // [2] round's sums done
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t_begin = (int)(((int64_t)n_tok * blockIdx.x) / gridDim.x);
+  const int ntok = (int)(((int64_t)n_tok * (blockIdx.x + 1)) / gridDim.x) - t_begin;   // <= 56
+  const int nr0 = min(ntok, kXpRound), nr1 = ntok - nr0;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 2; ++c) {
+      mbar_init(&exp_ready[c], c == 0 ? max(nr0, 1) : max(nr1, 1));  // one arrival per token
+      mbar_init(&sum_ready[c], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp <= 1) {
+    // ===== the reference's ascending sums: round `warp`, one lane per token =====
+    const int c = warp, nrc = c == 0 ? nr0 : nr1;
+    if (nrc > 0) {
+      mbar_wait_sleep(&exp_ready[c], 0);   // sleeping: the workers need the issue slots
+      if (lane < nrc) {
+        const int t = c * kXpRound + lane;
+        const float* r = rows + t * pitch;
+        float tot = 0.0f;
+        const float4* r4 = reinterpret_cast<const float4*>(r);
+        float4 a0 = r4[0], a1 = r4[1], a2 = r4[2], a3 = r4[3];
+        for (int f = 0; f < F; f += 16) {   // F % 64 == 0: float4 reads one 16-float chunk ahead
+          float4 n0 = a0, n1 = a1, n2 = a2, n3 = a3;
+          if (f + 16 < F) {
+            const float4* q = r4 + (f + 16) / 4;
+            n0 = q[0]; n1 = q[1]; n2 = q[2]; n3 = q[3];
+          }
+          const float v[16] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w,
+                               a2.x, a2.y, a2.z, a2.w, a3.x, a3.y, a3.z, a3.w};
+#pragma unroll
+          for (int u = 0; u < 16; ++u) tot = __fadd_rn(tot, v[u]);
+          a0 = n0; a1 = n1; a2 = n2; a3 = n3;
+        }
+        const float rc = __fdiv_rn(1.0f, tot);
+        rcs[t] = rc;
+        const int tok = t_begin + t;
+        if (loss) loss[tok] = -logf(__fmul_rn(r[targets[tok]], rc));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sum_ready[c]);
+    }
+    return;
+  }
+  // ===== workers: half warp = one token row, lane m4 = feature quad m4 of every block =====
+  const int wt = threadIdx.x - 64;
+  const int tr = wt >> 4, m4 = wt & 15;
+  // the whole SM share in flight at once: each thread copies (cp.async, 16 B)
+  // exactly the quads it later reads -- its token of each round -- so its own
+  // wait_group is the only synchronisation a round's loads need
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int t = c * kXpRound + tr;
+    if (t < ntok) {
+      const int tok = t_begin + t, nb = tok / bn, nin = tok - nb * bn;
+      const float* src = logits + ((int64_t)nb * m_b * bn + nin) * 64 + 4 * m4;
+      const uint32_t dst = smem_u32(rows + t * pitch + 4 * m4);
+      for (int mb = 0; mb < m_b; ++mb)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + mb * 256),
+                     "l"(src + (int64_t)mb * bn * 64)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int c = 0; c < 2; ++c) {
+    const int t = c * kXpRound + tr;
+    const bool valid = t < ntok;
+    float4 v[16];
+    float mx = -__int_as_float(0x7F800000);
+    bool nan = false;
+    if (c == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (valid) {
+      const float* row = rows + t * pitch + 4 * m4;
+#pragma unroll
+      for (int mb = 0; mb < 16; ++mb)
+        if (mb < m_b) v[mb] = *reinterpret_cast<const float4*>(row + mb * 64);
+#pragma unroll
+      for (int mb = 0; mb < 16; ++mb)
+        if (mb < m_b) {
+          nan |= (v[mb].x != v[mb].x) | (v[mb].y != v[mb].y) | (v[mb].z != v[mb].z) | (v[mb].w != v[mb].w);
+          mx = fmaxf(fmaxf(mx, v[mb].x), fmaxf(v[mb].y, fmaxf(v[mb].z, v[mb].w)));
+        }
+    }
+    // (a warp holds two token rows: both halves shuffle even when one is past the end)
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+      nan |= __shfl_xor_sync(0xFFFFFFFFu, (int)nan, o) != 0;
+    }
+    if (nan) mx = __int_as_float(0x7FC00000);
+    if (valid) {
+      float* row = rows + t * pitch + 4 * m4;
+#pragma unroll
+      for (int mb = 0; mb < 16; ++mb)
+        if (mb < m_b) {
+          float4 e;
+          e.x = exp_taylor_nonpos(__fsub_rn(v[mb].x, mx));
+          e.y = exp_taylor_nonpos(__fsub_rn(v[mb].y, mx));
+          e.z = exp_taylor_nonpos(__fsub_rn(v[mb].z, mx));
+          e.w = exp_taylor_nonpos(__fsub_rn(v[mb].w, mx));
+          *reinterpret_cast<float4*>(row + mb * 64) = e;
+        }
+    }
+    __syncwarp();
+    if (valid && m4 == 0) mbar_arrive(&exp_ready[c]);   // one arrival per token (after its 16 lanes' writes)
+  }
+  // dlogits of each round once its sums are done
+  for (int c = 0; c < 2; ++c) {
+    const int t = c * kXpRound + tr;
+    if ((c == 0 ? nr0 : nr1) == 0) break;
+    mbar_wait_sleep(&sum_ready[c], 0);
+    if (t < ntok) {
+      const int tok = t_begin + t, nb = tok / bn, nin = tok - nb * bn;
+      const float rc = rcs[t];
+      const int tg = targets[tok];
+      const float* row = rows + t * pitch + 4 * m4;
+      uint2* dst = reinterpret_cast<uint2*>(dlog) + ((int64_t)nb * m_b * bn + nin) * 16 + m4;
+#pragma unroll 4
+      for (int mb = 0; mb < m_b; ++mb) {
+        const float4 x = *reinterpret_cast<const float4*>(row + mb * 64);
+        const int f = mb * 64 + 4 * m4;
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+        float g[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          g[u] = __fmul_rn(__fsub_rn(__fmul_rn(xv[u], rc), f + u == tg ? 1.0f : 0.0f), scale);
+        uint32_t w[2];
+        pack_bf16_ref_n<2>(g, w);
+        dst[(int64_t)mb * bn * 16] = make_uint2(w[0], w[1]);
+      }
+    }
+  }
+}
+
 int launch_softmax_xent_blocked(int n_b, int m_b, int bn, int bm, const float* logits,
                                 const int32_t* targets, float scale, void* dlogits, float* loss,
                                 cudaStream_t s) {
   const int F = m_b * bm;
+  // every token of an SM resident (bm = 64, <= 16 feature blocks, <= 56 tokens per CTA)
+  {
+    const int64_t n_tok = (int64_t)n_b * bn;
+    static const bool legacy = getenv("TPP_XENT_LEGACY") != nullptr;  // A/B: the 16-token kernel
+    const int64_t grid = std::max<int64_t>(num_sms(), (n_tok + kXpMaxTok - 1) / kXpMaxTok);
+    if (!legacy && bm == 64 && m_b <= 16 && n_tok >= num_sms() && grid < 65536 &&
+        reinterpret_cast<uintptr_t>(logits) % 16 == 0 && reinterpret_cast<uintptr_t>(dlogits) % 8 == 0) {
+      const size_t smem = (size_t)kXpMaxTok * (F + 4) * sizeof(float) + kXpMaxTok * sizeof(float) +
+                          4 * sizeof(uint64_t);
+      cudaError_t e = ensure_smem_attr((const void*)softmax_xent_resident_kernel, (int)smem);
+      if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(softmax_xent_resident)");
+      softmax_xent_resident_kernel<<<(unsigned)grid, kXpThreads, smem, s>>>(
+          (int)n_tok, m_b, bn, logits, targets, scale, reinterpret_cast<uint16_t*>(dlogits), loss);
+      TPP_CUDA_LAUNCH_CHECK("softmax_xent_resident_kernel");
+      return TPP_OK;
+    }
+  }
   const size_t smem = (size_t)kXentTok * (F + 4) * sizeof(float) + 2 * kXentTok * sizeof(float);
   TPP_REQUIRE(smem <= 227 * 1024, TPP_E_UNSUPPORTED, "softmax_xent: class dimension too long for smem");
   const int blocks = n_b * ((bn + kXentTok - 1) / kXentTok);
