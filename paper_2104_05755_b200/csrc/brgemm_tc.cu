@@ -902,10 +902,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           if (ox < p.cv_Q && oy < p.cv_P) {
             uint32_t w[16];
             pack_bf16_ref_n<16>(x, w);
-            uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) +
-                                                 ((((int64_t)img * p.o_mb + tn) * p.cv_P + oy) * p.cv_Q + ox) * 64 + col);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            // two 256-bit stores: full 32-byte sectors (a warp's 32 positions
+            // are 32 different lines; 16-byte pieces cost twice the L1 wavefronts)
+            uint16_t* op = reinterpret_cast<uint16_t*>(p.out) +
+                           ((((int64_t)img * p.o_mb + tn) * p.cv_P + oy) * p.cv_Q + ox) * 64 + col;
+            st_global_v8(op, w);
+            st_global_v8(op + 16, w + 8);
           }
           continue;
         }
@@ -1741,7 +1743,7 @@ int conv_forward_tc(int N, int Cb, int Kb, int H, int W, int R, int S, int pad,
   const int wq = W + pad;
   const int strip_hr = (wq - 1 + 2 * BM + (R - 1) * wq + (S - 1) + wq - 1) / wq;
   const bool strip = res_ok && !no_strip && R == 3 && S == 3 && pad == 1 && wq <= 64 &&
-                     strip_hr * wq * 128 <= tc::kStripHaloBytes && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+                     strip_hr * wq * 128 <= tc::kStripHaloBytes && reinterpret_cast<uintptr_t>(out) % 32 == 0;
   p.cv_rows = rows4 ? 4 : 2;
   p.cv_tiles_per_img = (P + p.cv_rows - 1) / p.cv_rows;
   if (strip) {

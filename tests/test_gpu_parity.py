@@ -556,6 +556,10 @@ def test_conv_multi_wave_shapes():
     assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
     err_f, err_b = _conv_case(rng, 12, 1, 1, 28, 20, n_sel=[4, 7])    # 14 per image, ragged width: pairs
     assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+    # W = 64 (the widest tile row), a one-row image, a 2-pixel-wide image
+    for n, h, w in ((2, 7, 64), (3, 1, 5), (2, 9, 2)):
+        err_f, err_b = _conv_case(rng, n, 1, 1, h, w)
+        assert err_f <= BF16_TOL and err_b <= BF16_TOL, (n, h, w, err_f, err_b)
 
 
 # ---------------------------------------------------------------------------
