@@ -27,6 +27,7 @@
 //
 // Persistent CTAs walk work items (group, row tile, column tile).
 
+#include <cstdlib>
 #include <cuda.h>
 
 #include <mutex>
@@ -64,7 +65,10 @@ struct GParams {
   int dims_ok;      // m, k, ldb (lda for PLAIN A) multiples of 8: 16-byte chunks never straddle an edge
   float beta;
   int beta_mode;    // 0: beta == 0, 1: beta == 1, 2: general
+  int dbg;          // experiments (TPP_GRP_DBG): 1 no MMAs, 2 no copies, 4 no VNNI transpose
 };
+
+constexpr int kIdxChunk = 256;   // batch entries whose indices sit in smem at a time
 
 template <int BM, int BN, int STAGES>
 struct GSmem {
@@ -72,7 +76,8 @@ struct GSmem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int RAW_BYTES = BM * 128;  // VNNI A as loaded, before the word transpose
   static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int IDX_OFF = STAGES * STAGE;                 // batch index chunk [2][kIdxChunk]
+  static constexpr int BAR_OFF = IDX_OFF + 2 * kIdxChunk * 8;
   static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * BN;
 };
@@ -95,13 +100,6 @@ __device__ __forceinline__ uint4 ldg_nc16(const void* p) {
 __device__ __forceinline__ void sts16(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
-}
-
-__device__ __forceinline__ const uint16_t* op_ptr(int kind, const uint16_t* base, const long long* idx,
-                                                  long long stride, long long count, long long g, long long i) {
-  if (kind == 0) return base + (idx ? idx[g] : 0) + i * stride;
-  if (kind == 1) return base + idx[g * count + i];
-  return reinterpret_cast<const uint16_t*>(idx[g * count + i]);
 }
 
 // the producer's walk over (work item, batch entry, k chunk)
@@ -202,10 +200,47 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     // extents and strides are multiples of 8 elements and both block
     // addresses are 16-byte aligned; otherwise every 16-byte smem chunk is
     // assembled from 2-byte loads (any shape, any alignment).
+    // The batch's index values (STRIDE: the group's base offsets; OFFSET: the
+    // entries' offsets; ADDRESS: their pointers) are staged in shared memory
+    // by the producer warps together, kIdxChunk entries at a time (at a tile's
+    // first stage and every kIdxChunk entries): a stage then reads them from
+    // smem.  A global load per stage whose result the same stage consumes was
+    // the producers' critical path -- one L2 round trip per stage, ~0.5 us,
+    // with the copies, MMAs and transposes all switched off.
+    long long* sidx = reinterpret_cast<long long*>(smem + S::IDX_OFF);   // [2][kIdxChunk]: a, b
+    auto refill = [&](const StageIt& st) {
+      named_bar_sync(2, kProd);   // every producer is done with the previous chunk
+      const long long gg = st.tile / (p.tiles_m * p.tiles_n);
+      if (p.kind == 0) {
+        if (t == 0) {
+          sidx[0] = p.a_idx ? __ldg(p.a_idx + gg) : 0;
+          sidx[kIdxChunk] = p.b_idx ? __ldg(p.b_idx + gg) : 0;
+        }
+      } else {
+        const long long base = gg * p.count + st.i;
+        for (int e = t; e < kIdxChunk && st.i + e < p.count; e += kProd) {
+          sidx[e] = __ldg(p.a_idx + base + e);
+          sidx[kIdxChunk + e] = __ldg(p.b_idx + base + e);
+        }
+      }
+      named_bar_sync(2, kProd);
+    };
     auto stage_ptrs = [&](const StageIt& st, const uint16_t*& ap, const uint16_t*& bp) -> bool {
       if ((int)st.tile != cur_tile) set_tile((int)st.tile);
-      ap = op_ptr(p.kind, p.a, p.a_idx, p.stride_a, p.count, g, st.i);
-      bp = op_ptr(p.kind, p.b, p.b_idx, p.stride_b, p.count, g, st.i);
+      if (st.kc == 0 && (st.i == 0 || (p.kind != 0 && st.i % kIdxChunk == 0))) refill(st);
+      if (p.kind == 0) {
+        ap = p.a + sidx[0] + st.i * p.stride_a;
+        bp = p.b + sidx[kIdxChunk] + st.i * p.stride_b;
+      } else {
+        const int e = (int)(st.i % kIdxChunk);
+        if (p.kind == 1) {
+          ap = p.a + sidx[e];
+          bp = p.b + sidx[kIdxChunk + e];
+        } else {
+          ap = reinterpret_cast<const uint16_t*>(sidx[e]);
+          bp = reinterpret_cast<const uint16_t*>(sidx[kIdxChunk + e]);
+        }
+      }
       return p.dims_ok && ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(bp)) & 15) == 0;
     };
     // VNNI A fast path: each unit is 4 x 16 B cp.async of words (p, m..m+3)
@@ -317,9 +352,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       const uint32_t ph = (it / STAGES) & 1;
       const uint16_t *ap, *bp;
       const bool fast = stage_ptrs(cur, ap, bp);
-      mbar_wait(&empty[s], ph ^ 1);
+      if (p.dbg & 8) mbar_wait_sleep(&empty[s], ph ^ 1); else mbar_wait(&empty[s], ph ^ 1);
       const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
-      if (fast) {
+      if (p.dbg & 2) {
+        mbar_arrive(&landed[s]);
+      } else if (fast) {
         issue_fast(cur.kc, ap, bp, sA, sB);
         if (p.vnni) issue_vnni(cur.kc, ap, sB + S::B_BYTES);
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&landed[s])) : "memory");
@@ -344,8 +381,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     const long long nst = (long long)my_tiles * per_tile;
     for (long long it = 0; it < nst; ++it) {
       const int s = (int)(it % STAGES);
-      mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
-      if (p.vnni) {
+      if (p.dbg & 8) mbar_wait_sleep(&landed[s], (uint32_t)((it / STAGES) & 1)); else mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
+      if (p.vnni && !(p.dbg & 4)) {
         const uint32_t sA = smem_u32(smem + s * S::STAGE), sRaw = sA + S::A_BYTES + S::B_BYTES;
 #pragma unroll
         for (int u = 0; u < AU; ++u) {
@@ -369,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           }
         }
       }
-      fence_async_smem();
+      if (!(p.dbg & 32)) fence_async_smem();
       mbar_arrive(&full[s]);
     }
   } else if (warp == kMmaWarp) {
@@ -391,8 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         const uint64_t soff = (uint64_t)((s * S::STAGE) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_f16_warp(tmem_d, a0 + soff + astep * kk, b0 + soff + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit_warp(&empty[s]);
+          if (!(p.dbg & 1))
+            umma_f16_warp(tmem_d, a0 + soff + astep * kk, b0 + soff + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+        if (p.dbg & 16) {
+          if (lane == 0) mbar_arrive(&empty[s]);
+        } else {
+          umma_commit_warp(&empty[s]);
+        }
       }
       umma_commit_warp(&tfull[as]);
     }
@@ -414,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       const int row = tm * BM + lrow;
       const bool row_ok = lane_ok && row < p.m;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
-      mbar_wait(&tfull[as], aph);
+      if (p.dbg & 8) mbar_wait_sleep(&tfull[as], aph); else mbar_wait(&tfull[as], aph);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       uint32_t v[32];
@@ -505,6 +547,8 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.kchunks = (d->k + 63) / 64;
   p.beta = (float)d->beta;
   p.beta_mode = d->beta == 0.0 ? 0 : d->beta == 1.0 ? 1 : 2;
+  static const int dbg = getenv("TPP_GRP_DBG") ? atoi(getenv("TPP_GRP_DBG")) : 0;
+  p.dbg = dbg;
   const int BM = d->m <= 64 ? 64 : 128;
   // widest N tile that still gives every SM a tile (one C block of a
   // single brgemm() call is otherwise only a handful of work items)
