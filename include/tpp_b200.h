@@ -206,11 +206,19 @@ typedef struct {
 } tpp_conv_desc;
 int64_t tpp_conv_packed_weight_bytes(const tpp_conv_desc* d);
 /* bwd_data=0: pack for forward; 1: flip taps and swap C/K (VNNI_TO_VNNIT per
- * tap) for backward-data, which is then a forward conv of dO. */
+ * tap) for backward-data, which is then a forward conv of dO; 2: the same
+ * flipped / swapped weights kept in the reference VNNI layout
+ * [C_b][K_b][R][S][bk/2][bc][2] (the generic offset-BRGEMM path's A blocks). */
 int tpp_conv_pack_weights(const tpp_conv_desc* d, const void* w_vnni, void* w_packed,
                           int32_t bwd_data, void* stream);
 int tpp_conv_forward(const tpp_conv_desc* d, const void* w_packed, const void* x,
                      void* out, void* stream);
+/* Explicit zero padding / zero insertion of a blocked activation (the padded
+ * input the reference's offset-BRGEMM convolution reads, kernels.py-style
+ * composition): out[N][C_b][ho][wo][64](y, x) = in[N][C_b][hi][wi][64]
+ * ((y - top) / dil, (x - left) / dil) when both divide and fall inside, else 0. */
+int tpp_conv_pad(int32_t n, int32_t c_b, int32_t hi, int32_t wi, int32_t ho, int32_t wo, int32_t top,
+                 int32_t left, int32_t dil, const void* in, void* out, void* stream);
 /* dI[N][C_b][H][W][bc] from dO[N][K_b][P][Q][bk] with bwd-packed weights */
 int tpp_conv_backward_data(const tpp_conv_desc* d, const void* w_packed_bwd,
                            const void* dout, void* din, void* stream);

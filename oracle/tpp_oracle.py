@@ -597,14 +597,16 @@ def fc_forward_bf16(x_bits, w_vnni_bits, bias_bits=None, activation=None,
     return fp32_to_bf16_rne(c), mask, c
 
 
-def conv2d_fwd_bf16(x_bits, w_vnni_bits, pad: int = 1, n_sel=None):
+def conv2d_fwd_bf16(x_bits, w_vnni_bits, pad: int = 1, n_sel=None, stride: int = 1):
     """Direct 2-D convolution as an OFFSET-addressed BRGEMM over the R*S taps
     (contraction.py:152-160), on an explicitly zero-padded
     input; FP32 accumulation then BF16 RNE.  Per output row the batch entries
-    are the taps in (r, s) order with the Cb input-channel blocks inner.
+    are the taps in (r, s) order with the Cb input-channel blocks inner; with
+    a stride the B block of a tap is every stride-th padded column (ldb =
+    stride * bc) of padded row oh * stride + r.
 
     x_bits: [N][Cb][H][W][bc], w_vnni_bits: [Kb][Cb][R][S][bc/2][bk][2].
-    Returns out_bits [N'][Kb][H][W][bk] (stride 1, 'same' padding).
+    Returns out_bits [N'][Kb][P][Q][bk], P = (H + 2 pad - R) // stride + 1.
     """
     x_bits = np.asarray(x_bits)
     if n_sel is not None:
@@ -617,18 +619,42 @@ def conv2d_fwd_bf16(x_bits, w_vnni_bits, pad: int = 1, n_sel=None):
     # logical A (bk x bc) per (kb, cb, r, s)
     a_l = bf16_to_fp32(np.asarray(w_vnni_bits).transpose(0, 1, 2, 3, 5, 4, 6)
                        .reshape(Kb, Cb, R, S, bk, bc))
-    OH, OW = H + 2 * pad - R + 1, W + 2 * pad - S + 1
+    OH, OW = (H + 2 * pad - R) // stride + 1, (W + 2 * pad - S) // stride + 1
     out = np.zeros((N, Kb, OH, OW, bk), dtype=np.float32)
     # batch entries ordered (r, s, cb) — every entry: B block = input row slice
     a_stack = np.stack([a_l[:, cb, r, s] for r in range(R) for s in range(S)
                         for cb in range(Cb)], axis=1)        # [Kb, I, bk, bc]
     for oh in range(OH):
-        b_stack = np.stack([xf[:, cb, oh + r, s:s + OW, :].transpose(0, 2, 1)
+        b_stack = np.stack([xf[:, cb, oh * stride + r, s:s + stride * (OW - 1) + 1:stride, :].transpose(0, 2, 1)
                             for r in range(R) for s in range(S) for cb in range(Cb)],
                            axis=1)                             # [N, I, bc, OW]
         acc = brgemm_blocked(a_stack[None], b_stack[:, None])  # [N, Kb, bk, OW]
         out[:, :, oh] = acc.transpose(0, 1, 3, 2)
     return fp32_to_bf16_rne(out), out
+
+
+def conv2d_bwd_data_fp64(dout_bits, w_vnni_bits, h: int, w: int, pad: int, stride: int):
+    """FP64 restatement of the convolution's adjoint (the forward above is
+    out[oh][ow] = sum_{r,s} xpad[oh*stride + r][ow*stride + s] W[r][s]):
+    dI[h][w] = sum over (r, s, oh, ow) with oh*stride + r - pad = h,
+    ow*stride + s - pad = w of dO[oh][ow] W[r][s].  dout_bits
+    [N][Kb][P][Q][bk], weights VNNI [Kb][Cb][R][S][bc/2][bk][2]; returns
+    [N][Cb][H][W][bc] float64."""
+    do = bf16_to_fp32(np.asarray(dout_bits)).astype(np.float64)
+    N, Kb, P, Q, bk = do.shape
+    wv = np.asarray(w_vnni_bits)
+    _, Cb, R, S, bc2, _, _ = wv.shape
+    bc = 2 * bc2
+    wl = bf16_to_fp32(wv.transpose(0, 1, 2, 3, 5, 4, 6).reshape(Kb, Cb, R, S, bk, bc)).astype(np.float64)
+    hp, wpd = h + 2 * pad + stride, w + 2 * pad + stride
+    dip = np.zeros((N, Cb, hp, wpd, bc), dtype=np.float64)
+    for r in range(R):
+        for s in range(S):
+            # contribution of tap (r, s): dip[oh*stride + r][ow*stride + s] += dO[oh][ow] . W[r][s]
+            t = np.einsum("nkpqa,kcab->ncpqb", do.reshape(N, Kb, P, Q, bk),
+                          wl[:, :, r, s])                       # [N, Cb, P, Q, bc]
+            dip[:, :, r:r + stride * (P - 1) + 1:stride, s:s + stride * (Q - 1) + 1:stride] += t
+    return dip[:, :, pad:pad + h, pad:pad + w]
 
 
 def conv_weights_bwd_data(w_vnni_bits):

@@ -80,6 +80,7 @@ _SIGS = {
     "tpp_conv_packed_weight_bytes": (C.c_int64, [C.POINTER(ConvDescC)]),
     "tpp_conv_pack_weights": (C.c_int, [C.POINTER(ConvDescC), _P, _P, _I32, _P]),
     "tpp_conv_forward": (C.c_int, [C.POINTER(ConvDescC), _P, _P, _P, _P]),
+    "tpp_conv_pad": (C.c_int, [_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "tpp_conv_backward_data": (C.c_int, [C.POINTER(ConvDescC), _P, _P, _P, _P]),
     "tpp_conv_backward_weights_workspace_bytes": (C.c_int64, [C.POINTER(ConvDescC)]),
     "tpp_conv_backward_weights": (C.c_int, [C.POINTER(ConvDescC), _P, _P, _P, _P, _P]),

@@ -370,8 +370,20 @@ int tpp_conv_pack_weights(const tpp_conv_desc* d, const void* w_vnni, void* w_pa
                                         (int64_t)d->k_b * d->c_b * d->r * d->s, rm,
                                         as_stream(stream));
   }
+  if (bwd_data == 2)
+    return launch_pack_conv_bwd_vnni(w_vnni, w_packed, d->k_b, d->c_b, d->r, d->s, d->bc, d->bk, as_stream(stream));
   return launch_pack_conv_bwd(w_vnni, w_packed, d->k_b, d->c_b, d->r, d->s, d->bc, d->bk,
                               as_stream(stream));
+}
+
+int tpp_conv_pad(int32_t n, int32_t c_b, int32_t hi, int32_t wi, int32_t ho, int32_t wo, int32_t top,
+                 int32_t left, int32_t dil, const void* in, void* out, void* stream) {
+  TPP_REQUIRE(n >= 0 && c_b >= 0 && hi >= 1 && wi >= 1 && ho >= 0 && wo >= 0 && top >= 0 && left >= 0 && dil >= 1,
+              TPP_E_TENSOR, "bad conv padding extents");
+  TPP_REQUIRE(in && out, TPP_E_TENSOR, "null operand");
+  TPP_REQUIRE(reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0,
+              TPP_E_TENSOR, "conv padding needs 16-byte aligned buffers");
+  return launch_conv_pad(in, out, (int64_t)n * c_b, hi, wi, ho, wo, top, left, dil, as_stream(stream));
 }
 
 int tpp_conv_forward(const tpp_conv_desc* d, const void* w_packed, const void* x, void* out,

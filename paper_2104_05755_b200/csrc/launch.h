@@ -99,6 +99,10 @@ int launch_word_transpose_blocks(const void* src, void* dst, int rows, int cols,
                                  BlockRemap remap, cudaStream_t s);
 int launch_pack_conv_bwd(const void* src, void* dst, int Kb, int Cb, int R, int S, int bc, int bk,
                          cudaStream_t s);
+int launch_pack_conv_bwd_vnni(const void* src, void* dst, int Kb, int Cb, int R, int S, int bc, int bk,
+                              cudaStream_t s);
+int launch_conv_pad(const void* in, void* out, int64_t planes, int hi, int wi, int ho, int wo, int top, int left,
+                    int dil, cudaStream_t s);
 // kind: 0 TRANSPOSE, 1 VNNI, 2 VNNI_TO_VNNIT, 3 COPY
 int launch_transform(int kind, int esize, const void* in, int in_ld, void* out, int out_rows,
                      int out_cols, int out_ld, int alpha, int alpha_out, int lrows, int lcols,

@@ -92,6 +92,83 @@ int launch_pack_conv_bwd(const void* src, void* dst, int Kb, int Cb, int R, int 
   return TPP_OK;
 }
 
+// Backward-data weights in the reference VNNI layout (the generic conv path
+// runs them as offset-BRGEMM A blocks): block (cb, kb, r', s') =
+// VNNI_TO_VNNIT of forward block (kb, cb, R-1-r', S-1-s') -- logical (c x k),
+// stored [k/2][c][2] (ops.py:556-565 on a spatial flip; the oracle's
+// conv_weights_bwd_data).
+__global__ void pack_conv_bwd_vnni_kernel(const uint16_t* __restrict__ src, uint16_t* __restrict__ dst,
+                                          int Kb, int Cb, int R, int S, int bc, int bk) {
+  const int64_t total = (int64_t)Kb * Cb * R * S * bc * bk;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int pb = (int)(e & 1);
+    int64_t t = e >> 1;
+    const int c = (int)(t % bc);
+    t /= bc;
+    const int k = 2 * (int)(t % (bk / 2)) + pb;
+    t /= bk / 2;
+    const int sf = (int)(t % S);
+    t /= S;
+    const int rf = (int)(t % R);
+    t /= R;
+    const int kb = (int)(t % Kb);
+    const int cb = (int)(t / Kb);
+    const int64_t blk = (((int64_t)kb * Cb + cb) * R + (R - 1 - rf)) * S + (S - 1 - sf);
+    dst[e] = src[blk * bc * bk + (int64_t)(c >> 1) * bk * 2 + k * 2 + (c & 1)];
+  }
+}
+
+int launch_pack_conv_bwd_vnni(const void* src, void* dst, int Kb, int Cb, int R, int S, int bc, int bk,
+                              cudaStream_t s) {
+  const int64_t total = (int64_t)Kb * Cb * R * S * bc * bk;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 65536) blocks = 65536;
+  pack_conv_bwd_vnni_kernel<<<(unsigned)blocks, threads, 0, s>>>(
+      reinterpret_cast<const uint16_t*>(src), reinterpret_cast<uint16_t*>(dst), Kb, Cb, R, S, bc, bk);
+  TPP_CUDA_LAUNCH_CHECK("pack_conv_bwd_vnni_kernel");
+  return TPP_OK;
+}
+
+// Explicit zero padding (and zero insertion) of a blocked activation
+// [N][C_b][Hi][Wi][64] into [N][C_b][Ho][Wo][64]: output pixel (y, x) is input
+// ((y - top) / dil, (x - left) / dil) when both divide evenly and land inside
+// the input, else 0 -- the padded input the reference's offset-BRGEMM
+// convolution reads (dil > 1: the zero-inserted dO of a strided conv's
+// backward-data).  16 bytes (8 channels) per thread.
+__global__ void conv_pad_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, int64_t planes, int hi,
+                                int wi, int ho, int wo, int top, int left, int dil) {
+  const int64_t total = planes * ho * wo * 8;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e & 7);
+    int64_t t = e >> 3;
+    const int x = (int)(t % wo);
+    t /= wo;
+    const int y = (int)(t % ho);
+    const int64_t pl = t / ho;
+    const int yy = y - top, xx = x - left;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (yy >= 0 && xx >= 0 && yy % dil == 0 && xx % dil == 0 && yy / dil < hi && xx / dil < wi)
+      v = in[((pl * hi + yy / dil) * wi + xx / dil) * 8 + q];
+    out[e] = v;
+  }
+}
+
+int launch_conv_pad(const void* in, void* out, int64_t planes, int hi, int wi, int ho, int wo, int top, int left,
+                    int dil, cudaStream_t s) {
+  const int64_t total = planes * ho * wo * 8;
+  if (total == 0) return TPP_OK;
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  conv_pad_kernel<<<(unsigned)blocks, threads, 0, s>>>(reinterpret_cast<const uint4*>(in), reinterpret_cast<uint4*>(out),
+                                                       planes, hi, wi, ho, wo, top, left, dil);
+  TPP_CUDA_LAUNCH_CHECK("conv_pad_kernel");
+  return TPP_OK;
+}
+
 // ---- transform TPP (ops.py:537-570) on column-major views -----------------
 // Elements are moved as raw bits of `esize` bytes.
 template <typename T>

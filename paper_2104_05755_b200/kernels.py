@@ -10,8 +10,10 @@ plus the B200 layer objects the paper's drivers become on a GPU:
   (+bitmask) / GELU, residual and BF16 RNE narrowing fused into the epilogue.
 * ``layernorm_blocked`` — the LayerNorm equation TPP on the blocked
   activation layout FC produces, bitwise to the reference.
-* ``Conv2d`` — 3x3 direct convolution as an offset-addressed BRGEMM over the
-  taps (PAPER.md:655), forward and backward-data.
+* ``Conv2d`` — direct convolution as an offset-addressed BRGEMM over the
+  taps, forward and backward-data (any R x S, stride, padding:
+  fused halo kernels for stride-1 'same' shapes, the reference composition on
+  the grouped tcgen05 BRGEMM otherwise) and backward-weights (fused shapes).
 """
 
 from __future__ import annotations
@@ -378,9 +380,15 @@ def split_sgd_flat(hi: torch.Tensor, lo: torch.Tensor, grad: torch.Tensor, lr: f
 
 @dataclass(frozen=True)
 class ConvSpec:
-    """3x3-style direct convolution, stride 1, 'same' padding.
-    input [N][C_b][H][W][bc], weights VNNI [K_b][C_b][R][S][bc/2][bk][2],
-    output [N][K_b][H][W][bk]."""
+    """Direct 2-D convolution on blocked BF16 activations: input
+    [N][C_b][H][W][bc], weights VNNI [K_b][C_b][R][S][bc/2][bk][2], output
+    [N][K_b][P][Q][bk] with P = (H + 2 pad - R) // stride + 1 (Q likewise).
+    ``stride`` = 1 and 'same' padding (2 pad = R - 1 = S - 1) with W <= 64 run
+    the fused tcgen05 halo kernel; every other shape runs the reference's own
+    formulation on the tensor cores: an explicitly zero-padded input and one
+    OFFSET-addressed BRGEMM batch over the (r, s, c_b) taps per output row
+    (K11, one grouped launch for all rows), FP32 accumulation,
+    then BF16 RNE."""
     n: int
     c_b: int
     k_b: int
@@ -391,19 +399,101 @@ class ConvSpec:
     pad: int = 1
     bc: int = 64
     bk: int = 64
+    stride: int = 1
+
+    def __post_init__(self):
+        if min(self.n, self.c_b, self.k_b, self.h, self.w, self.r, self.s, self.stride) < 1 or self.pad < 0:
+            raise TensorError("conv extents must be positive (pad >= 0)")
+        if self.h + 2 * self.pad < self.r or self.w + 2 * self.pad < self.s:
+            raise TensorError("the filter is larger than the padded input")
 
     def c(self) -> _lib.ConvDescC:
         return _lib.ConvDescC(self.n, self.c_b, self.k_b, self.h, self.w, self.r, self.s, self.pad,
                               self.bc, self.bk, 0, 0)
 
     @property
+    def p(self) -> int:
+        return (self.h + 2 * self.pad - self.r) // self.stride + 1
+
+    @property
+    def q(self) -> int:
+        return (self.w + 2 * self.pad - self.s) // self.stride + 1
+
+    @property
+    def fused(self) -> bool:
+        """The shapes the fused halo kernels (K2 forward / backward-data, K7
+        backward-weights) take; the rest run the offset-BRGEMM composition."""
+        return (self.stride == 1 and 2 * self.pad == self.r - 1 and 2 * self.pad == self.s - 1
+                and self.w <= 64 and self.bc == 64 and self.bk == 64)
+
+    @property
     def flops(self) -> int:
-        return 2 * self.n * self.h * self.w * self.c_b * self.bc * self.k_b * self.bk * self.r * self.s
+        return 2 * self.n * self.p * self.q * self.c_b * self.bc * self.k_b * self.bk * self.r * self.s
+
+
+class _OffsetConv:
+    """One offset-BRGEMM convolution (the reference composition) on the
+    tensor cores: groups = output rows (n, kb, oh), each C block the bk x Q
+    FP32 row at [n][kb][oh] (ldc = bk); batch entries = taps (r, s) x input
+    channel blocks cb, in that order: A = VNNI weight block (kb, cb, r, s),
+    B = the bc x Q input slice of padded row oh*stride + r from column s,
+    column stride stride*bc (ldb).  Index arrays built once, on the device."""
+
+    def __init__(self, n, ci_b, co_b, hp, wp, p, q, r, s, stride, device):
+        import numpy as np
+        from .contraction import GemmSpec
+        from .contraction import ALayout
+        blk = 64 * 64
+        self.groups = n * co_b * p
+        self.count = r * s * ci_b
+        self.spec = GemmSpec(64, q, 64, 64, stride * 64, 64, in_dtype=DType.BF16, out_dtype=DType.FP32,
+                             a_layout=ALayout.VNNI, beta=0.0)
+        nn, kb, oh = np.meshgrid(np.arange(n), np.arange(co_b), np.arange(p), indexing="ij")
+        rr, ss, cb = np.meshgrid(np.arange(r), np.arange(s), np.arange(ci_b), indexing="ij")
+        rr, ss, cb = rr.reshape(-1), ss.reshape(-1), cb.reshape(-1)
+        kbg, ng, ohg = kb.reshape(-1, 1), nn.reshape(-1, 1), oh.reshape(-1, 1)
+        a_off = ((kbg * ci_b + cb) * (r * s) + rr * s + ss) * blk
+        b_off = ((ng * ci_b + cb) * hp + ohg * stride + rr) * (wp * 64) + ss * 64
+        c_off = ((nn * co_b + kb) * p + oh).reshape(-1) * (q * 64)
+        # every block inside its buffer (the grouped kernel trusts the indices)
+        assert a_off.min() >= 0 and a_off.max() + blk <= co_b * ci_b * r * s * blk
+        last_col = b_off + (q - 1) * stride * 64 + 64
+        assert b_off.min() >= 0 and last_col.max() <= n * ci_b * hp * wp * 64
+        self.a_idx = torch.from_numpy(np.ascontiguousarray(a_off.reshape(-1), dtype=np.int64)).to(device)
+        self.b_idx = torch.from_numpy(np.ascontiguousarray(b_off.reshape(-1), dtype=np.int64)).to(device)
+        self.c_off = torch.from_numpy(np.ascontiguousarray(c_off, dtype=np.int64)).to(device)
+        self.out_elems = n * co_b * p * q * 64
+
+    def run(self, w_vnni: torch.Tensor, xpad: torch.Tensor, out_bf16: torch.Tensor, stream=None) -> None:
+        lib = _lib.load()
+        acc = torch.empty(self.out_elems, dtype=torch.float32, device=xpad.device)
+        d = self.spec.c()
+        d.engine = _lib.ENGINE_TENSOR
+        s = _lib.stream_ptr(stream)
+        _lib.check(lib.tpp_brgemm_grouped(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
+                                          self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
+                                          acc.data_ptr(), self.c_off.data_ptr(), self.groups, s),
+                   "conv (offset BRGEMM)")
+        # FP32 accumulators -> BF16 RNE (dtypes.py:82-97)
+        cols = self.out_elems // 64
+        din = _lib.TensorDescC(64, cols, 64, DType.FP32.code, 0)
+        dout = _lib.TensorDescC(64, cols, 64, DType.BF16.code, 0)
+        _lib.check(lib.tpp_convert(C.byref(din), acc.data_ptr(), C.byref(dout), out_bf16.data_ptr(), s),
+                   "conv (RNE)")
+
+
+def _conv_pad(x: torch.Tensor, n, cb, hi, wi, ho, wo, top, left, dil, stream=None) -> torch.Tensor:
+    out = torch.empty(n * cb * ho * wo * 64, dtype=torch.bfloat16, device=x.device)
+    _lib.check(_lib.load().tpp_conv_pad(n, cb, hi, wi, ho, wo, top, left, dil, x.data_ptr(), out.data_ptr(),
+                                        _lib.stream_ptr(stream)), "conv_pad")
+    return out
 
 
 class Conv2d:
     """Weights packed once for forward ([K_b][R][S][C_b][bk][bc], K-major
-    per tap) and for backward-data (taps flipped, C/K swapped)."""
+    per tap) and for backward-data (taps flipped, C/K swapped); shapes outside
+    the fused kernels keep the VNNI weights (forward) and the flipped,
+    transposed VNNI weights (backward-data) as offset-BRGEMM A blocks."""
 
     def __init__(self, spec: ConvSpec, w_vnni: torch.Tensor, stream=None):
         if w_vnni.dtype != torch.bfloat16 or not w_vnni.is_cuda:
@@ -411,45 +501,83 @@ class Conv2d:
         need = spec.k_b * spec.c_b * spec.r * spec.s * spec.bc * spec.bk
         if w_vnni.numel() < need:
             raise TensorError("weight buffer too small")
+        if spec.bc != 64 or spec.bk != 64:
+            raise NotImplementedError("tensor-core conv needs bc = bk = 64")
         self.spec = spec
         lib = _lib.load()
         d = spec.c()
-        self.w_fwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
-        self.w_bwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
         s = _lib.stream_ptr(stream)
-        _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_fwd.data_ptr(), 0, s),
-                   "conv_pack_weights")
-        _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_bwd.data_ptr(), 1, s),
-                   "conv_pack_weights(bwd)")
+        if spec.fused:
+            self.w_fwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
+            self.w_bwd = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
+            _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_fwd.data_ptr(), 0, s),
+                       "conv_pack_weights")
+            _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_bwd.data_ptr(), 1, s),
+                       "conv_pack_weights(bwd)")
+        else:
+            self.w_vnni = w_vnni[:need].clone()
+            self.w_bwd_vnni = torch.empty(need, dtype=torch.bfloat16, device=w_vnni.device)
+            _lib.check(lib.tpp_conv_pack_weights(C.byref(d), w_vnni.data_ptr(), self.w_bwd_vnni.data_ptr(), 2, s),
+                       "conv_pack_weights(bwd, VNNI)")
+            self._fwd_plan = None
+            self._bwd_plan = None
 
     def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         sp = self.spec
         n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
-        n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
+        n_out = sp.n * sp.k_b * sp.p * sp.q * sp.bk
         if x.dtype != torch.bfloat16 or x.numel() < n_in:
             raise TensorError("conv input must be a bf16 [N][C_b][H][W][bc] buffer")
         if out is None:
             out = torch.empty(n_out, dtype=torch.bfloat16, device=x.device)
+        elif out.dtype != torch.bfloat16 or out.numel() < n_out:
+            raise TensorError("conv output must be a bf16 [N][K_b][P][Q][bk] buffer")
         lib = _lib.load()
-        d = sp.c()
-        _lib.check(lib.tpp_conv_forward(C.byref(d), self.w_fwd.data_ptr(), x.data_ptr(),
-                                        out.data_ptr(), _lib.stream_ptr(stream)), "conv_forward")
+        if sp.fused:
+            d = sp.c()
+            _lib.check(lib.tpp_conv_forward(C.byref(d), self.w_fwd.data_ptr(), x.data_ptr(),
+                                            out.data_ptr(), _lib.stream_ptr(stream)), "conv_forward")
+            return out
+        hp, wp = sp.h + 2 * sp.pad, sp.w + 2 * sp.pad
+        if self._fwd_plan is None:
+            self._fwd_plan = _OffsetConv(sp.n, sp.c_b, sp.k_b, hp, wp, sp.p, sp.q, sp.r, sp.s, sp.stride, x.device)
+        xp = _conv_pad(x, sp.n, sp.c_b, sp.h, sp.w, hp, wp, sp.pad, sp.pad, 1, stream)
+        self._fwd_plan.run(self.w_vnni, xp, out, stream)
         return out
 
     def backward_data(self, dout: torch.Tensor, din: Optional[torch.Tensor] = None,
                       stream=None) -> torch.Tensor:
+        """dI = the forward conv's adjoint: for stride s, dO zero-inserted
+        (s - 1 zeros between pixels) and padded by R - 1 - pad (plus the rows /
+        columns the forward's floor division dropped), convolved at stride 1
+        with the flipped, C/K-swapped weights."""
         sp = self.spec
         n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
-        n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
+        n_out = sp.n * sp.k_b * sp.p * sp.q * sp.bk
         if dout.dtype != torch.bfloat16 or dout.numel() < n_out:
-            raise TensorError("dO must be a bf16 [N][K_b][H][W][bk] buffer")
+            raise TensorError("dO must be a bf16 [N][K_b][P][Q][bk] buffer")
         if din is None:
             din = torch.empty(n_in, dtype=torch.bfloat16, device=dout.device)
+        elif din.dtype != torch.bfloat16 or din.numel() < n_in:
+            raise TensorError("dI must be a bf16 [N][C_b][H][W][bc] buffer")
         lib = _lib.load()
-        d = sp.c()
-        _lib.check(lib.tpp_conv_backward_data(C.byref(d), self.w_bwd.data_ptr(), dout.data_ptr(),
-                                              din.data_ptr(), _lib.stream_ptr(stream)),
-                   "conv_backward_data")
+        if sp.fused:
+            d = sp.c()
+            _lib.check(lib.tpp_conv_backward_data(C.byref(d), self.w_bwd.data_ptr(), dout.data_ptr(),
+                                                  din.data_ptr(), _lib.stream_ptr(stream)),
+                       "conv_backward_data")
+            return din
+        if sp.pad > sp.r - 1 or sp.pad > sp.s - 1:
+            raise NotImplementedError("conv backward-data with pad > R - 1 (the adjoint crops its input)")
+        # dI[h][w] = sum_{r', s'} Zp[h + r'][w + s'] Wflip[r'][s'] with Zp the
+        # zero-inserted dO shifted by R - 1 - pad: a stride-1 'valid' conv of
+        # H x W outputs over an (H + R - 1) x (W + S - 1) buffer
+        top, left = sp.r - 1 - sp.pad, sp.s - 1 - sp.pad
+        hz, wz = sp.h + sp.r - 1, sp.w + sp.s - 1
+        if self._bwd_plan is None:
+            self._bwd_plan = _OffsetConv(sp.n, sp.k_b, sp.c_b, hz, wz, sp.h, sp.w, sp.r, sp.s, 1, dout.device)
+        dz = _conv_pad(dout, sp.n, sp.k_b, sp.p, sp.q, hz, wz, top, left, sp.stride, stream)
+        self._bwd_plan.run(self.w_bwd_vnni, dz, din, stream)
         return din
 
     def backward_weights(self, x: torch.Tensor, dout: torch.Tensor, dw: Optional[torch.Tensor] = None,
@@ -459,6 +587,9 @@ class Conv2d:
         all taps' partial sums in TMEM over its rows; a second kernel adds the
         per-CTA partials in a fixed order."""
         sp = self.spec
+        if not sp.fused:
+            raise NotImplementedError("conv backward-weights runs the fused kernel only (stride 1, 'same' "
+                                      "padding, W <= 64)")
         n_in = sp.n * sp.c_b * sp.h * sp.w * sp.bc
         n_out = sp.n * sp.k_b * sp.h * sp.w * sp.bk
         if x.dtype != torch.bfloat16 or x.numel() < n_in:

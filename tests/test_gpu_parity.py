@@ -562,6 +562,46 @@ def test_conv_multi_wave_shapes():
         assert err_f <= BF16_TOL and err_b <= BF16_TOL, (n, h, w, err_f, err_b)
 
 
+def _conv_generic_case(rng, N, Cb, Kb, H, W, R, S, pad, stride):
+    """Shapes outside the fused halo kernels: the reference composition (padded
+    input, OFFSET BRGEMM over the (r, s, cb) taps per output row) on the
+    grouped tcgen05 BRGEMM; forward against the oracle composition, backward-
+    data against an FP64 restatement of the adjoint."""
+    from paper_2104_05755_b200 import _lib
+    x = O.fp32_to_bf16_rne(rng.random((N, Cb, H, W, 64)).astype(np.float32))
+    wl = O.fp32_to_bf16_rne(rng.normal(0, np.sqrt(2 / (R * S * 64 * Cb)), (Kb, Cb, R, S, 64, 64)).astype(np.float32))
+    wv = wl.reshape(Kb, Cb, R, S, 64, 32, 2).transpose(0, 1, 2, 3, 5, 4, 6).copy()
+    spec = tpp.ConvSpec(N, Cb, Kb, H, W, r=R, s=S, pad=pad, stride=stride)
+    assert not spec.fused
+    conv = tpp.Conv2d(spec, to_dev(wv))
+    out = conv.forward(to_dev(x))
+    torch.cuda.synchronize()
+    assert _lib.last_config().startswith("brgemm_grouped_kernel"), _lib.last_config()
+    P, Q = spec.p, spec.q
+    got = bf16_bits_to_f32(to_host(out).reshape(N, Kb, P, Q, 64))
+    want_bits, _ = O.conv2d_fwd_bf16(x, wv, pad=pad, stride=stride)
+    assert want_bits.shape == (N, Kb, P, Q, 64)
+    err_f = normwise(got, O.bf16_to_fp32(want_bits))
+    dout = O.fp32_to_bf16_rne(rng.normal(0, 1, (N, Kb, P, Q, 64)).astype(np.float32))
+    din = conv.backward_data(to_dev(dout))
+    got_b = bf16_bits_to_f32(to_host(din).reshape(N, Cb, H, W, 64))
+    err_b = normwise(got_b, O.conv2d_bwd_data_fp64(dout, wv, H, W, pad, stride))
+    return err_f, err_b
+
+
+@pytest.mark.parametrize("N,Cb,Kb,H,W,R,S,pad,stride", [
+    (2, 1, 1, 9, 11, 3, 3, 1, 2),     # ResNet 3x3 stride-2 downsampling
+    (1, 2, 2, 8, 8, 1, 1, 0, 2),      # 1x1 stride-2 projection shortcut
+    (1, 1, 2, 13, 13, 7, 7, 3, 2),    # the 7x7 stride-2 stem
+    (1, 1, 1, 5, 70, 3, 3, 1, 1),     # W > 64
+    (2, 2, 1, 6, 7, 3, 3, 0, 1),      # 'valid' padding
+])
+def test_conv_generic_shapes(N, Cb, Kb, H, W, R, S, pad, stride):
+    rng = np.random.default_rng(43 + R + stride)
+    err_f, err_b = _conv_generic_case(rng, N, Cb, Kb, H, W, R, S, pad, stride)
+    assert err_f <= BF16_TOL and err_b <= BF16_TOL, (err_f, err_b)
+
+
 # ---------------------------------------------------------------------------
 # 1-D dilated conv (kernels.py:336-378): stride BRGEMM over taps, bitwise
 # ---------------------------------------------------------------------------
