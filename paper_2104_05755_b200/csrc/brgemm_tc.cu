@@ -1019,11 +1019,17 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile && ch < 8, 150 + 4 * ch + 3, clock64());
           }
         } else {
-          uint4* op = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in);
+          uint16_t* op = reinterpret_cast<uint16_t*>(p.out) + row_off * p.o_bm + m_in;
           uint32_t w[16];
           pack_bf16_ref_n<16>(x, w);
+          if ((reinterpret_cast<uintptr_t>(op) & 31) == 0) {  // full 32-byte sectors
+            st_global_v8(op, w);
+            st_global_v8(op + 16, w + 8);
+          } else {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) op[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+            for (int i = 0; i < 4; ++i)
+              reinterpret_cast<uint4*>(op)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+          }
         }
       }
       if (park || nsrc > 0) {
