@@ -116,6 +116,7 @@ struct Params {
   // dynamic tile scheduling (FC mode): {ticket, done} counters, zero at
   // launch and reset by the last worker; null = static round-robin
   unsigned* dyn;
+  int sleep_waits;   // producer / epilogue waits with a suspend-time hint (experiments: TPP_SLEEP_WAITS)
 };
 
 // Dynamic tile queue: the (pair) leader's producer draws work items from a
@@ -588,7 +589,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int j = 0; j < sg.k0; ++j) f.next();  // stream-K: a segment may start mid-tile
         for (int j = sg.k0; j < sg.k1; ++j, ++it) {
           if (NPROD == 1 || (int)(it % NPROD) == pid) {
-            mbar_wait(&empty[s], ph ^ 1);
+            if (p.sleep_waits) mbar_wait_sleep(&empty[s], ph ^ 1);
+            else mbar_wait(&empty[s], ph ^ 1);
             uint8_t* sa = smem + s * S::STAGE_BYTES;
             if (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
@@ -819,7 +821,8 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
         warp_rows = p.tma_store && sc2 < p.cv_P && sc1 < p.cv_Q;
       }
       asm volatile("" ::"r"(t), "r"(nb), "r"(n_in), "r"(sc1), "r"(sc2), "r"(sc4), "r"((int)warp_rows));
-      mbar_wait(&tfull[as], aph);
+      if (p.sleep_waits) mbar_wait_sleep(&tfull[as], aph);
+      else mbar_wait(&tfull[as], aph);
       warp_ahead(qi, ahead, tile);
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 4, gtimer());
       TPP_STAMP(blockIdx.x == 0 && threadIdx.x == 128 && tcount == p.dbg_tile, 189, clock64());
@@ -1322,6 +1325,8 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
       }
     }
   }
+  static const int sleep_waits = getenv("TPP_SLEEP_WAITS") ? atoi(getenv("TPP_SLEEP_WAITS")) : 0;
+  pk.sleep_waits = sleep_waits;
   pk.dyn = nullptr;
   if (RES == 0 && MC == 1 && p.mode == FEED_FC && pk.sk_stages == 0 && units > 1 &&
       (tile_mode() == 1 || (tile_mode() == 0 && (p.flags & TPP_FC_DYNAMIC_TILES))))
