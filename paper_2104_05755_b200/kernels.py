@@ -433,40 +433,51 @@ class ConvSpec:
 
 class _OffsetConv:
     """One offset-BRGEMM convolution (the reference composition) on the
-    tensor cores: groups = output rows (n, kb, oh), each C block the bk x Q
-    FP32 row at [n][kb][oh] (ldc = bk); batch entries = taps (r, s) x input
-    channel blocks cb, in that order: A = VNNI weight block (kb, cb, r, s),
-    B = the bc x Q input slice of padded row oh*stride + r from column s,
-    column stride stride*bc (ldb).  Index arrays built once, on the device."""
+    tensor cores.  Batch entries = taps (r, s) x input channel blocks cb, in
+    that order; A = the VNNI weight block (kb, cb, r, s); B = a bc x n slice
+    of the padded input with column stride stride*bc (ldb).  A C block covers
+    RB whole output rows in the padded-width position space: virtual column
+    v = row * Wp + ow reads padded pixel (row*stride + r, ow*stride + s) at
+    element stride*bc*v from the tap's base, uniformly across row ends, so one
+    block of n = RB*Wp <= 256 columns (RB the largest divisor of P that fits)
+    is one BRGEMM; the Wp - Q columns past each row's end are computed and
+    dropped by the strided FP32 -> BF16 RNE pass.  Index arrays are built once
+    and live on the device."""
 
     def __init__(self, n, ci_b, co_b, hp, wp, p, q, r, s, stride, device):
         import numpy as np
-        from .contraction import GemmSpec
-        from .contraction import ALayout
+        from .contraction import ALayout, GemmSpec
         blk = 64 * 64
-        self.groups = n * co_b * p
+        rb = max(d for d in range(1, p + 1) if p % d == 0 and (d * wp <= 256 or d == 1))
+        ncols = rb * wp
+        self.p, self.q, self.wp, self.rows_per_block = p, q, wp, rb
+        self.groups = n * co_b * (p // rb)
         self.count = r * s * ci_b
-        self.spec = GemmSpec(64, q, 64, 64, stride * 64, 64, in_dtype=DType.BF16, out_dtype=DType.FP32,
+        self.spec = GemmSpec(64, ncols, 64, 64, stride * 64, 64, in_dtype=DType.BF16, out_dtype=DType.FP32,
                              a_layout=ALayout.VNNI, beta=0.0)
-        nn, kb, oh = np.meshgrid(np.arange(n), np.arange(co_b), np.arange(p), indexing="ij")
+        nn, kb, ob = np.meshgrid(np.arange(n), np.arange(co_b), np.arange(p // rb), indexing="ij")
         rr, ss, cb = np.meshgrid(np.arange(r), np.arange(s), np.arange(ci_b), indexing="ij")
         rr, ss, cb = rr.reshape(-1), ss.reshape(-1), cb.reshape(-1)
-        kbg, ng, ohg = kb.reshape(-1, 1), nn.reshape(-1, 1), oh.reshape(-1, 1)
+        kbg, ng, obg = kb.reshape(-1, 1), nn.reshape(-1, 1), ob.reshape(-1, 1)
         a_off = ((kbg * ci_b + cb) * (r * s) + rr * s + ss) * blk
-        b_off = ((ng * ci_b + cb) * hp + ohg * stride + rr) * (wp * 64) + ss * 64
-        c_off = ((nn * co_b + kb) * p + oh).reshape(-1) * (q * 64)
-        # every block inside its buffer (the grouped kernel trusts the indices)
+        # rows of the padded input the blocks reach (virtual columns past the
+        # last row's end read on into the following rows): the caller pads to it
+        self.rows_needed = int(((p // rb - 1) * rb * stride + (r - 1)) + ((ncols - 1) * stride + (s - 1)) // wp + 1)
+        self.hp = max(hp, self.rows_needed)
+        b_off = ((ng * ci_b + cb) * self.hp + obg * rb * stride + rr) * (wp * 64) + ss * 64
+        c_off = ((nn * co_b + kb) * p + ob * rb).reshape(-1) * (wp * 64)
         assert a_off.min() >= 0 and a_off.max() + blk <= co_b * ci_b * r * s * blk
-        last_col = b_off + (q - 1) * stride * 64 + 64
-        assert b_off.min() >= 0 and last_col.max() <= n * ci_b * hp * wp * 64
+        last = b_off + (ncols - 1) * stride * 64 + 64
+        assert b_off.min() >= 0 and last.max() <= n * ci_b * self.hp * wp * 64
         self.a_idx = torch.from_numpy(np.ascontiguousarray(a_off.reshape(-1), dtype=np.int64)).to(device)
         self.b_idx = torch.from_numpy(np.ascontiguousarray(b_off.reshape(-1), dtype=np.int64)).to(device)
         self.c_off = torch.from_numpy(np.ascontiguousarray(c_off, dtype=np.int64)).to(device)
-        self.out_elems = n * co_b * p * q * 64
+        self.planes = n * co_b
+        self.acc_elems = n * co_b * p * wp * 64
 
     def run(self, w_vnni: torch.Tensor, xpad: torch.Tensor, out_bf16: torch.Tensor, stream=None) -> None:
         lib = _lib.load()
-        acc = torch.empty(self.out_elems, dtype=torch.float32, device=xpad.device)
+        acc = torch.empty(self.acc_elems, dtype=torch.float32, device=xpad.device)
         d = self.spec.c()
         d.engine = _lib.ENGINE_TENSOR
         s = _lib.stream_ptr(stream)
@@ -474,10 +485,12 @@ class _OffsetConv:
                                           self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
                                           acc.data_ptr(), self.c_off.data_ptr(), self.groups, s),
                    "conv (offset BRGEMM)")
-        # FP32 accumulators -> BF16 RNE (dtypes.py:82-97)
-        cols = self.out_elems // 64
-        din = _lib.TensorDescC(64, cols, 64, DType.FP32.code, 0)
-        dout = _lib.TensorDescC(64, cols, 64, DType.BF16.code, 0)
+        # FP32 accumulators -> BF16 RNE (dtypes.py:82-97), dropping the
+        # columns past each row's end: rows = Q*64 valid elements of a padded-
+        # width row (ld Wp*64), one column per output row
+        cols = self.planes * self.p
+        din = _lib.TensorDescC(self.q * 64, cols, self.wp * 64, DType.FP32.code, 0)
+        dout = _lib.TensorDescC(self.q * 64, cols, self.q * 64, DType.BF16.code, 0)
         _lib.check(lib.tpp_convert(C.byref(din), acc.data_ptr(), C.byref(dout), out_bf16.data_ptr(), s),
                    "conv (RNE)")
 
@@ -541,7 +554,7 @@ class Conv2d:
         hp, wp = sp.h + 2 * sp.pad, sp.w + 2 * sp.pad
         if self._fwd_plan is None:
             self._fwd_plan = _OffsetConv(sp.n, sp.c_b, sp.k_b, hp, wp, sp.p, sp.q, sp.r, sp.s, sp.stride, x.device)
-        xp = _conv_pad(x, sp.n, sp.c_b, sp.h, sp.w, hp, wp, sp.pad, sp.pad, 1, stream)
+        xp = _conv_pad(x, sp.n, sp.c_b, sp.h, sp.w, self._fwd_plan.hp, wp, sp.pad, sp.pad, 1, stream)
         self._fwd_plan.run(self.w_vnni, xp, out, stream)
         return out
 
@@ -576,7 +589,7 @@ class Conv2d:
         hz, wz = sp.h + sp.r - 1, sp.w + sp.s - 1
         if self._bwd_plan is None:
             self._bwd_plan = _OffsetConv(sp.n, sp.k_b, sp.c_b, hz, wz, sp.h, sp.w, sp.r, sp.s, 1, dout.device)
-        dz = _conv_pad(dout, sp.n, sp.k_b, sp.p, sp.q, hz, wz, top, left, sp.stride, stream)
+        dz = _conv_pad(dout, sp.n, sp.k_b, sp.p, sp.q, self._bwd_plan.hp, wz, top, left, sp.stride, stream)
         self._bwd_plan.run(self.w_bwd_vnni, dz, din, stream)
         return din
 
