@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32 * kFinWarps);
+      mbar_init(&full[s], kFinWarps);   // one arrival per finisher warp
       mbar_init(&empty[s], 1);
       mbar_init(&landed[s], kProd);
     }
@@ -406,8 +406,12 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           }
         }
       }
+      // every thread orders its own transposed chunks for the async proxy, then
+      // one elected arrival per warp (128 arrivals on one mbarrier word per
+      // stage serialise in shared memory)
       if (!(p.dbg & 32)) fence_async_smem();
-      mbar_arrive(&full[s]);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&full[s]);
     }
   } else if (warp == kMmaWarp) {
     // ============================ MMA issue ============================
