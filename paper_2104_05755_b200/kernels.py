@@ -466,9 +466,11 @@ class _OffsetConv:
         self.hp = max(hp, self.rows_needed)
         b_off = ((ng * ci_b + cb) * self.hp + obg * rb * stride + rr) * (wp * 64) + ss * 64
         c_off = ((nn * co_b + kb) * p + ob * rb).reshape(-1) * (wp * 64)
-        assert a_off.min() >= 0 and a_off.max() + blk <= co_b * ci_b * r * s * blk
+        # the grouped kernel trusts its indices: every block inside its buffer
         last = b_off + (ncols - 1) * stride * 64 + 64
-        assert b_off.min() >= 0 and last.max() <= n * ci_b * self.hp * wp * 64
+        if (a_off.min() < 0 or a_off.max() + blk > co_b * ci_b * r * s * blk or b_off.min() < 0
+                or last.max() > n * ci_b * self.hp * wp * 64):
+            raise TensorError("conv offset plan out of bounds (internal)")
         self.a_idx = torch.from_numpy(np.ascontiguousarray(a_off.reshape(-1), dtype=np.int64)).to(device)
         self.b_idx = torch.from_numpy(np.ascontiguousarray(b_off.reshape(-1), dtype=np.int64)).to(device)
         self.c_off = torch.from_numpy(np.ascontiguousarray(c_off, dtype=np.int64)).to(device)
