@@ -356,6 +356,51 @@ def gen_conv():
     save("conv.npz", x=x, w=wv, out=out)
 
 
+def gen_conv_strided():
+    """Strided / non-'same' conv through the same composition: OFFSET BRGEMM
+    over (r, s, cb) taps on an explicitly padded input, the tap's B block
+    every stride-th padded column (ldb = stride * bc) of padded row
+    oh * stride + r.  BF16 in, FP32 acc, BF16 out."""
+    rng = np.random.default_rng(17)
+    cases = {}
+    for name, (N, Cb, H, W, bc, Kb, bk, R, S, pad, st) in {
+            "s2_3x3": (2, 2, 7, 9, 8, 2, 8, 3, 3, 1, 2),
+            "s2_1x1": (1, 2, 6, 6, 8, 1, 8, 1, 1, 0, 2),
+            "s1_valid": (1, 1, 5, 6, 8, 2, 8, 3, 3, 0, 1)}.items():
+        x = fp32_to_bf16_rne(rng.random((N, Cb, H, W, bc)).astype(np.float32))
+        wl = fp32_to_bf16_rne(rng.normal(0, 0.3, size=(Kb, Cb, R, S, bk, bc)).astype(np.float32))
+        wv = np.zeros((Kb, Cb, R, S, bc // 2, bk, 2), dtype=np.uint16)
+        for kb_ in range(Kb):
+            for cb in range(Cb):
+                for r in range(R):
+                    for s in range(S):
+                        wv[kb_, cb, r, s] = tp.vnni_pack_a(wl[kb_, cb, r, s], 2).reshape(bc // 2, bk, 2)
+        Hp, Wp = H + 2 * pad, W + 2 * pad
+        P, Q = (Hp - R) // st + 1, (Wp - S) // st + 1
+        xp = np.zeros((N, Cb, Hp, Wp, bc), dtype=np.uint16)
+        xp[:, :, pad:pad + H, pad:pad + W] = x
+        xflat, wflat = xp.reshape(-1), wv.reshape(-1)
+        out = np.zeros((N, Kb, P, Q, bk), dtype=np.uint16)
+        gspec = tp.GemmSpec(bk, Q, bc, bk, st * bc, bk, in_dtype=tp.DType.BF16,
+                            out_dtype=tp.DType.FP32, beta=0.0, a_layout=tp.ALayout.VNNI)
+        for n in range(N):
+            for kb_ in range(Kb):
+                for oh in range(P):
+                    a_offs, b_offs = [], []
+                    for r in range(R):
+                        for s in range(S):
+                            for cb in range(Cb):
+                                a_offs.append((((kb_ * Cb + cb) * R + r) * S + s) * bc * bk)
+                                b_offs.append((((n * Cb + cb) * Hp + oh * st + r) * Wp + s) * bc)
+                    cblk = tp.alloc(tp.TensorDesc(bk, Q, bk, tp.DType.FP32))
+                    tp.brgemm(gspec, tp.BrgemmBatch.offset(wflat, xflat, a_offs, b_offs), cblk)
+                    ob = tp.convert(cblk, tp.DType.BF16)
+                    out[n, kb_, oh] = np.array(ob.primary).reshape(Q, bk)
+        cases.update({f"{name}_x": x, f"{name}_w": wv, f"{name}_out": out,
+                      f"{name}_geom": np.array([pad, st], dtype=np.int64)})
+    save("conv_strided.npz", **cases)
+
+
 def gen_dilated():
     """1-D dilated conv (kernels.py:336-378) through the reference's own
     address-based BRGEMM driver: the reference test's shape and a wider
@@ -472,6 +517,10 @@ def gen_quant():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:   # only the named generators, e.g. `make_golden.py gen_conv_strided`
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+        sys.exit(0)
     gen_dtypes()
     gen_cfg1()
     gen_brgemm_cases()
@@ -481,6 +530,7 @@ if __name__ == "__main__":
     gen_softmax_sgd()
     gen_fc()
     gen_conv()
+    gen_conv_strided()
     gen_dilated()
     gen_prng()
     gen_quant()

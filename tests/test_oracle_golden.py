@@ -152,6 +152,32 @@ def test_conv_offset_composition(golden):
     assert np.array_equal(out, g["out"])
 
 
+def test_conv_strided_composition(golden):
+    """Strided / 'valid' conv through the reference's own offset BRGEMM
+    (fixture from tests/golden/make_golden.py gen_conv_strided), bitwise."""
+    g = golden("conv_strided.npz")
+    for name in ("s2_3x3", "s2_1x1", "s1_valid"):
+        pad, st = (int(v) for v in g[f"{name}_geom"])
+        out, _ = O.conv2d_fwd_bf16(g[f"{name}_x"], g[f"{name}_w"], pad=pad, stride=st)
+        assert np.array_equal(out, g[f"{name}_out"]), name
+
+
+def test_conv_bwd_data_adjoint(golden):
+    """The FP64 backward-data restatement is the forward's adjoint:
+    <conv(x), y> == <x, conv_bwd(y)> on the strided fixture shapes."""
+    g = golden("conv_strided.npz")
+    rng = np.random.default_rng(5)
+    for name in ("s2_3x3", "s2_1x1", "s1_valid"):
+        pad, st = (int(v) for v in g[f"{name}_geom"])
+        x, w = g[f"{name}_x"], g[f"{name}_w"]
+        _, acc = O.conv2d_fwd_bf16(x, w, pad=pad, stride=st)
+        y = O.fp32_to_bf16_rne(rng.standard_normal(acc.shape).astype(np.float32))
+        dx = O.conv2d_bwd_data_fp64(y, w, x.shape[2], x.shape[3], pad, st)
+        lhs = float((acc.astype(np.float64) * O.bf16_to_fp32(y)).sum())
+        rhs = float((O.bf16_to_fp32(x).astype(np.float64) * dx).sum())
+        assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), 1e-30), (name, lhs, rhs)
+
+
 def test_dilated_conv1d(golden):
     """The address-BRGEMM dilated conv of the reference, bitwise (kernels.py:350-378)."""
     g = golden("dilated.npz")
