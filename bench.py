@@ -212,9 +212,10 @@ def time_graph(torch, dist, g, reps_min=5, min_seconds=1.0):
     return times
 
 
-def time_eager(torch, dist, fn, K, reps=5):
+def time_eager(torch, dist, fn, K, reps=5, tail=None):
     """K eager calls per timed region (barrier + sync both sides, CUDA events
-    on the current stream, max over ranks)."""
+    on the current stream, max over ranks); ``tail`` (e.g. joining deferred
+    updates) runs inside the region after the K calls."""
     times = []
     for _ in range(reps):
         if dist is not None:
@@ -225,6 +226,8 @@ def time_eager(torch, dist, fn, K, reps=5):
         e0.record()
         for _ in range(K):
             fn()
+        if tail is not None:
+            tail()
         e1.record()
         torch.cuda.synchronize()
         times.append(_max_over_ranks(torch, dist, e0.elapsed_time(e1)))
@@ -333,6 +336,7 @@ def run_e2e(torch, tpp, mlp, dist, K, W, graph: bool):
             s_in.wait_stream(cap)
             for i in range(K):
                 step(i, cap, capturing=True)
+            mlp.sync_updates()
             cap.wait_stream(s_in)
         torch.cuda.synchronize()
         for _ in range(3):
@@ -346,7 +350,7 @@ def run_e2e(torch, tpp, mlp, dist, K, W, graph: bool):
             step(ctr[0], torch.cuda.current_stream())
             ctr[0] += 1
 
-        times = time_eager(torch, dist, one, K, reps=5)
+        times = time_eager(torch, dist, one, K, reps=5, tail=mlp.sync_updates)
     return statistics.median(times) / K, n_x * 2 + tokens * 4, tokens * 4
 
 
@@ -361,8 +365,11 @@ def run_ours(args, rank, world, dist):
     peaks = _peaks()
     tokens = GLOBAL_TOKENS // world
     grad_dtype = args.grad_dtype or ("fp32" if world == 1 else "bf16")
+    # one rank: the backward overlaps dW_l with dX_{l-1} on a side stream and
+    # the next step's layer-0 GEMM runs beside the last updates (defer_join);
+    # every timed region ends by joining them (sync_updates)
     mlp = tpp.BlockedMLP(DIMS, tokens, bn=TOK_BLOCK, lr=LR, global_batch=GLOBAL_TOKENS, seed=7, device=dev,
-                         grad_dtype=grad_dtype)
+                         grad_dtype=grad_dtype, defer_join=True)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     x = torch.randn(tokens * DIMS[0], generator=gen, device=dev).to(torch.bfloat16)
@@ -376,12 +383,12 @@ def run_ours(args, rank, world, dist):
     use_graph = world == 1 and not args.eager
     with ClockSampler(torch.cuda.current_device()) as cs:
         if use_graph:
-            g = graph_of(torch, [step] * K)
+            g = graph_of(torch, [step] * K + [mlp.sync_updates])
             g.replay()
             torch.cuda.synchronize()
             times = time_graph(torch, None, g, reps_min=5, min_seconds=1.0)
         else:
-            times = time_eager(torch, dist, step, K, reps=max(5, args.reps))
+            times = time_eager(torch, dist, step, K, reps=max(5, args.reps), tail=mlp.sync_updates)
     clocks = cs.summary()
     ms_step = statistics.median(times) / K
     value = FLOPS_CFG5 / (ms_step * 1e-3) / 1e12

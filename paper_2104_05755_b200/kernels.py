@@ -135,7 +135,7 @@ class FcLayer:
 
     def forward(self, x: torch.Tensor, n_b: int, bn: int, out: Optional[torch.Tensor] = None,
                 residual: Optional[torch.Tensor] = None, relu_mask: Optional[torch.Tensor] = None,
-                out_fp32: bool = False, stream=None) -> torch.Tensor:
+                out_fp32: bool = False, stream=None, dynamic_tiles: bool = False) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or not x.is_cuda:
             raise TensorError("FC input must be a CUDA bfloat16 buffer")
         if x.numel() < n_b * self.k_b * bn * self.bk:
@@ -145,7 +145,7 @@ class FcLayer:
             out = torch.empty(n_out, dtype=torch.float32 if out_fp32 else torch.bfloat16, device=x.device)
         if out.numel() < n_out:
             raise TensorError("output buffer too small")
-        flags = 0
+        flags = _lib.FC_DYNAMIC_TILES if dynamic_tiles else 0
         if self.bias is not None:
             flags |= _lib.FC_BIAS | (_lib.FC_BIAS_FP32 if self.bias.dtype == torch.float32 else 0)
         if residual is not None:

@@ -58,7 +58,7 @@ class BlockedMLP:
                  global_batch: Optional[int] = None, init_std: float = 0.02, seed: int = 0,
                  device=None, weights: Optional[Sequence[torch.Tensor]] = None, group=None,
                  grad_dtype: str = "fp32", reduce_fn=None, fuse_sgd: Optional[bool] = None,
-                 overlap: bool = True):
+                 overlap: bool = True, defer_join: bool = False):
         """``grad_dtype``: "fp32" (dW written and applied in FP32) or "bf16"
         (dW written as BF16 by the backward-weights epilogue, exchanged as
         BF16 — half the allreduce bytes — and applied by split-SGD, which
@@ -73,7 +73,13 @@ class BlockedMLP:
         backward-data GEMM (and layer 0's with layer 1's); the tensor-core
         kernels draw their tiles dynamically, so the two fill each other's
         wave-quantisation tails.  Results are bitwise those of the serial
-        order (the kernels are independent and deterministic per tile)."""
+        order (the kernels are independent and deterministic per tile).
+        ``defer_join`` (with ``overlap``): ``step()`` leaves the side stream's
+        last updates in flight -- the next forward's layer-0 GEMM runs beside
+        them and only its layer 1 waits (layer 0's output alternates between
+        two buffers, since the in-flight dW_1 still reads the previous one).
+        Call ``sync_updates()`` (or synchronize the device) before reading the
+        weights or ending a timed region."""
         if grad_dtype not in ("fp32", "bf16"):
             raise ValueError("grad_dtype must be 'fp32' or 'bf16'")
         if any(d % BLK for d in dims) or tokens % bn or bn % BLK:
@@ -119,6 +125,9 @@ class BlockedMLP:
         self.fuse_sgd = fuse_sgd
         self.overlap = overlap and fuse_sgd
         self._side = torch.cuda.Stream(device=dev) if self.overlap else None
+        self.defer_join = bool(defer_join) and self.overlap and self.nl >= 2
+        self._pending = None          # event on the side stream: the deferred updates
+        self._h1_alt = torch.empty_like(self.h[1]) if self.defer_join else None
         # optional per-launch hook (label) called right after each main-stream
         # launch -- bench.py records CUDA events there for the step breakdown
         self.trace = None
@@ -127,9 +136,16 @@ class BlockedMLP:
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         """x: BF16 blocked [n_b][d0/64][bn][64]; returns FP32 logits (blocked)."""
         self.h[0] = x
+        deferred = self._pending is not None
+        if self.defer_join:   # the previous step's dW_1 may still read h[1]
+            self.h[1], self._h1_alt = self._h1_alt, self.h[1]
         for l, layer in enumerate(self.layers):
+            if l == 1 and self._pending is not None:
+                torch.cuda.current_stream(self.device).wait_event(self._pending)
+                self._pending = None
             if l < self.nl - 1:
-                layer.forward(self.h[l], self.n_b, self.bn, out=self.h[l + 1], relu_mask=self.mask[l + 1])
+                layer.forward(self.h[l], self.n_b, self.bn, out=self.h[l + 1], relu_mask=self.mask[l + 1],
+                              dynamic_tiles=deferred and l == 0)
             else:
                 layer.forward(self.h[l], self.n_b, self.bn, out=self.logits, out_fp32=True)
             if self.trace:
@@ -172,7 +188,12 @@ class BlockedMLP:
                 if tr:
                     tr(f"dw{l}")
             if side is not None:
-                main.wait_stream(side)
+                if self.defer_join:
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                    self._pending = ev
+                else:
+                    main.wait_stream(side)
             return
         for l in range(nl - 1, -1, -1):
             layer = self.layers[l]
@@ -194,10 +215,19 @@ class BlockedMLP:
 
     def step(self) -> None:
         """Complete the step: every layer's exchange and split-SGD update is
-        ordered before whatever the caller issues next."""
+        ordered before whatever the caller issues next (with ``defer_join``:
+        except the side stream's last updates, see ``sync_updates``)."""
         self.sync.finish()
+        if not self.defer_join:
+            self.sync_updates()
         if self.trace:
             self.trace("step")
+
+    def sync_updates(self) -> None:
+        """Order every deferred weight update before the caller's next work."""
+        if self._pending is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._pending)
+            self._pending = None
 
     def train_step(self, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         self.forward(x)
@@ -208,6 +238,7 @@ class BlockedMLP:
     # ------------------------------------------------------------------
     def master_weight(self, l: int) -> torch.Tensor:
         """FP32 master weight of layer l as a logical [out, in] matrix."""
+        self.sync_updates()
         return unpack_weight(pack_master(self.hi[l], self.lo[l]), self.dims[l + 1], self.dims[l])
 
     def gemm_flops(self, label: str) -> int:

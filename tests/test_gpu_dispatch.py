@@ -387,11 +387,18 @@ def test_overlapped_step_equals_serial_step():
     tg = to_dev(rng.integers(0, dims[-1], Tk).astype(np.int32))
     a = tpp.BlockedMLP(dims, Tk, bn=bn, lr=0.01, global_batch=Tk, weights=ws, overlap=True)
     b = tpp.BlockedMLP(dims, Tk, bn=bn, lr=0.01, global_batch=Tk, weights=ws, overlap=False)
-    assert a.overlap and not b.overlap
+    # deferred join: the next step's layer 0 beside the previous step's last updates
+    c = tpp.BlockedMLP(dims, Tk, bn=bn, lr=0.01, global_batch=Tk, weights=ws, overlap=True, defer_join=True)
+    assert a.overlap and not b.overlap and c.defer_join
     for _ in range(3):
         la = to_host(a.train_step(x, tg))
         lb = to_host(b.train_step(x, tg))
+        lc = c.train_step(x, tg)
         torch.cuda.synchronize()
         assert np.array_equal(la, lb)
+        assert np.array_equal(to_host(lc), lb)
+    c.sync_updates()
+    torch.cuda.synchronize()
     for l in range(len(dims) - 1):
         assert torch.equal(a.hi[l], b.hi[l]) and torch.equal(a.lo[l], b.lo[l]), l
+        assert torch.equal(c.hi[l], b.hi[l]) and torch.equal(c.lo[l], b.lo[l]), l

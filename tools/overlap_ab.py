@@ -24,16 +24,20 @@ x = torch.randn(8192 * 1024, generator=gen, device=dev).to(torch.bfloat16)
 tg = torch.randint(0, 1024, (8192,), generator=gen, device=dev, dtype=torch.int32)
 graphs = {}
 keep = []  # the graphs read the models' buffers
-for ov in (True, False):
-    mlp = tpp.BlockedMLP(bench.DIMS, 8192, bn=64, lr=0.01, global_batch=8192, seed=7, device=dev, overlap=ov)
+for mode in ("deferred", "overlap", "serial"):
+    mlp = tpp.BlockedMLP(bench.DIMS, 8192, bn=64, lr=0.01, global_batch=8192, seed=7, device=dev,
+                         overlap=mode != "serial", defer_join=mode == "deferred")
     keep.append(mlp)
     for dyn in (0, 2):   # 0: the default (overlapped GEMMs dynamic), 2: every GEMM static
+        if mode == "deferred" and dyn == 2:
+            continue
         lib.tpp_set_tile_scheduling(dyn)
         step = lambda m=mlp: m.train_step(x, tg)  # noqa: E731
         for _ in range(3):
             step()
+        mlp.sync_updates()
         torch.cuda.synchronize()
-        graphs[f"{'default' if dyn == 0 else 'static'}+{'overlap' if ov else 'serial'}"] = bench.graph_of(torch, [step] * K)
+        graphs[f"{'default' if dyn == 0 else 'static'}+{mode}"] = bench.graph_of(torch, [step] * K + [mlp.sync_updates])
 lib.tpp_set_tile_scheduling(0)
 res = {k: [] for k in graphs}
 for _ in range(R):
