@@ -328,6 +328,7 @@ def run_e2e(torch, tpp, mlp, dist, K, W, graph: bool):
 
     for i in range(max(W, 3)):
         step(i, comp0)
+    mlp.sync_updates()   # a capture must not depend on the eager steps' deferred updates
     torch.cuda.synchronize()
     if graph:
         gr = torch.cuda.CUDAGraph()
@@ -377,6 +378,7 @@ def run_ours(args, rank, world, dist):
     step = lambda: mlp.train_step(x, tg)  # noqa: E731
     for _ in range(W):
         step()
+    mlp.sync_updates()
     torch.cuda.synchronize()
 
     # ---- headline: K training steps per timed region -----------------------

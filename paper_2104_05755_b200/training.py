@@ -127,6 +127,7 @@ class BlockedMLP:
         self._side = torch.cuda.Stream(device=dev) if self.overlap else None
         self.defer_join = bool(defer_join) and self.overlap and self.nl >= 2
         self._pending = None          # event on the side stream: the deferred updates
+        self._pending_captured = False
         self._h1_alt = torch.empty_like(self.h[1]) if self.defer_join else None
         # optional per-launch hook (label) called right after each main-stream
         # launch -- bench.py records CUDA events there for the step breakdown
@@ -141,8 +142,7 @@ class BlockedMLP:
             self.h[1], self._h1_alt = self._h1_alt, self.h[1]
         for l, layer in enumerate(self.layers):
             if l == 1 and self._pending is not None:
-                torch.cuda.current_stream(self.device).wait_event(self._pending)
-                self._pending = None
+                self._join_pending()
             if l < self.nl - 1:
                 layer.forward(self.h[l], self.n_b, self.bn, out=self.h[l + 1], relu_mask=self.mask[l + 1],
                               dynamic_tiles=deferred and l == 0)
@@ -192,6 +192,7 @@ class BlockedMLP:
                     ev = torch.cuda.Event()
                     ev.record(side)
                     self._pending = ev
+                    self._pending_captured = torch.cuda.is_current_stream_capturing()
                 else:
                     main.wait_stream(side)
             return
@@ -226,8 +227,14 @@ class BlockedMLP:
     def sync_updates(self) -> None:
         """Order every deferred weight update before the caller's next work."""
         if self._pending is not None:
-            torch.cuda.current_stream(self.device).wait_event(self._pending)
-            self._pending = None
+            self._join_pending()
+
+    def _join_pending(self) -> None:
+        if torch.cuda.is_current_stream_capturing() and not self._pending_captured:
+            raise RuntimeError("BlockedMLP(defer_join=True): call sync_updates() before capturing a CUDA graph "
+                               "(the capture cannot wait on the eager steps' deferred updates)")
+        torch.cuda.current_stream(self.device).wait_event(self._pending)
+        self._pending = None
 
     def train_step(self, x: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         self.forward(x)
