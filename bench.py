@@ -536,6 +536,7 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
     """Other BASELINE configs, same timing method (CUDA graph of R steps,
     rotating buffers where the working set is smaller than L2)."""
     peak_bf16, peak_hbm = peaks["burst"], peaks["hbm"]
+    peak_sus = peaks["sustained"]   # the extras replay for >= 0.3 s: the clock settles under the power cap
     out = {}
     R = 20
     relu = tpp.UnaryKind.RELU
@@ -556,6 +557,7 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
         tf = FLOPS_CFG2 / ms / 1e9
         out["cfg2_fc_bias_relu"] = {"us": round(ms * 1e3, 3), "TFLOP/s": round(tf, 1),
                                     "frac_bf16_burst": round(tf / peak_bf16, 4),
+                                    "frac_bf16_sustained": round(tf / peak_sus, 4),
                                     "l2": f"{n_sets} rotating sets > 2x L2"}
         del sets, fns, g
     except Exception as e:
@@ -593,7 +595,7 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
             else:
                 tf = fl1 / ms / 1e9
                 res[name] = {"ms": round(ms, 5), "TFLOP/s": round(tf, 1),
-                             "frac_bf16": round(tf / peak_bf16, 4)}
+                             "frac_bf16": round(tf / peak_bf16, 4), "frac_bf16_sustained": round(tf / peak_sus, 4)}
         res["ffn_step_ms"] = round(total, 5)
         res["ffn_TFLOP/s"] = round(2 * fl1 / total / 1e9, 1)
         g = graph_of(torch, [lambda: tpp.layernorm_blocked(o2, nb, h, bn, 64, 1e-5, gam, bet, out=ln,
@@ -626,6 +628,7 @@ def run_extra(args, torch, tpp, dev, gen, peaks):
             ms = statistics.median(time_graph(torch, None, g, reps_min=5, min_seconds=0.3)) / 5
             tf = spec.flops / ms / 1e9
             res[name] = {"ms": round(ms, 5), "TFLOP/s": round(tf, 1), "frac_bf16": round(tf / peak_bf16, 4),
+                         "frac_bf16_sustained": round(tf / peak_sus, 4),
                          "GB/s": round(byts / ms / 1e6, 1), "frac_hbm": round(byts / ms / 1e6 / peak_hbm, 4)}
         out["cfg4_conv3x3"] = res
         del xin, yo, dO, dI, conv, dW
