@@ -118,6 +118,21 @@ int tpp_brgemm_grouped(const tpp_gemm_desc* d, int32_t kind, const void* a, cons
                        int64_t stride_a, int64_t stride_b, const int64_t* a_index,
                        const int64_t* b_index, int64_t count, void* c, const int64_t* c_offsets,
                        int64_t groups, void* stream);
+/* tpp_brgemm_grouped with the groups tiled in gangs: gang j is gang_m (1 or
+ * 2) x gang_n (1, 2, 4) groups where the groups of a gang row share their A
+ * lists and those of a gang column their B lists (e.g. every C block of one
+ * weight block row of an FC composition), so one tile loads each A and B
+ * block once and runs M = 64 gang_m x N = 64 gang_n (or n, gang_n = 1) MMAs.
+ * `gang` (device, int32) = rows [ngangs][gang_m] (a group whose A list feeds
+ * the row), cols [ngangs][gang_n] (a group whose B list feeds the column),
+ * cells [ngangs][gang_m][gang_n] (the group whose C a cell is), -1 = empty.
+ * Needs m <= 64 (and n <= 64 for gang_n > 1).  Same results as the ungrouped
+ * call (each C block is the same MMA chain over the same blocks). */
+int tpp_brgemm_grouped_gang(const tpp_gemm_desc* d, int32_t kind, const void* a, const void* b,
+                            int64_t stride_a, int64_t stride_b, const int64_t* a_index,
+                            const int64_t* b_index, int64_t count, void* c, const int64_t* c_offsets,
+                            int64_t groups, const int32_t* gang, int32_t ngangs, int32_t gang_m,
+                            int32_t gang_n, void* stream);
 /* Many independent stride-BRGEMMs in one launch (the GPU form of the
  * reference's `threads=` job loop over disjoint C tiles, contraction.py:317-322
  * and kernels.py:323-329): instance j uses a + j*inst_a, b + j*inst_b,

@@ -324,6 +324,7 @@ class GroupedBatch:
         self.a_goff, self.b_goff = a_goff, b_goff
         self._dev = None
         self._checked = set()   # (spec, C buffer, C offsets) combinations already validated
+        self._gang = {}         # (m, n, device) -> gang tiling (or None)
 
     @staticmethod
     def stride(a_base, b_base, stride_a: int, stride_b: int, count: int,
@@ -405,6 +406,45 @@ class GroupedBatch:
         if ev is not None and not torch.cuda.is_current_stream_capturing():
             (stream if stream is not None else torch.cuda.current_stream(device)).wait_event(ev)
         return a, b
+
+
+def _gang_table(keys_a, keys_b, m: int, n: int, device, sms: int):
+    """Gang tiling of a grouped BRGEMM whose groups form a full cross product
+    of A lists x B lists (the FC / conv compositions): returns (device int32
+    table, ngangs, gang_m, gang_n) or None.  Gang rows pair two A lists
+    (M = 128 MMAs) when m <= 64; gang columns take 2 or 4 B lists (N = 128 /
+    256) when n <= 64, as wide as still leaves one gang per SM."""
+    ia, ib = {}, {}
+    ga = [ia.setdefault(k, len(ia)) for k in keys_a]
+    gb = [ib.setdefault(k, len(ib)) for k in keys_b]
+    na, nb = len(ia), len(ib)
+    if m > 64 or na * nb != len(ga):
+        return None
+    cell = {}
+    for g, (x, y) in enumerate(zip(ga, gb)):
+        if (x, y) in cell:
+            return None
+        cell[(x, y)] = g
+    gm = 2 if na >= 2 else 1
+    gn = 1
+    if n <= 64:
+        for cand in (4, 2):
+            if -(-na // gm) * -(-nb // cand) >= sms:
+                gn = cand
+                break
+    if gm == 1 and gn == 1:
+        return None
+    rows, cols, cells = [], [], []
+    row_rep = {x: g for (x, _), g in cell.items()}
+    col_rep = {y: g for (_, y), g in cell.items()}
+    for x0 in range(0, na, gm):
+        for y0 in range(0, nb, gn):
+            rows += [row_rep.get(x0 + i, -1) for i in range(gm)]
+            cols += [col_rep.get(y0 + j, -1) for j in range(gn)]
+            cells += [cell.get((x0 + i, y0 + j), -1) for i in range(gm) for j in range(gn)]
+    ngangs = len(rows) // gm
+    table = torch.tensor(rows + cols + cells, dtype=torch.int32).pin_memory().to(device, non_blocking=True)
+    return table, ngangs, gm, gn
 
 
 class _COffsets:
@@ -496,9 +536,26 @@ def brgemm_grouped(spec: GemmSpec, gbatch: GroupedBatch, c, c_offsets: Sequence[
     else:
         (abuf, _), (bbuf, _) = gbatch.a_refs[0][0], gbatch.b_refs[0][0]
         a_ptr, b_ptr = abuf.data_ptr(), bbuf.data_ptr()
-    rc = lib.tpp_brgemm_grouped(C.byref(d), kind, a_ptr, b_ptr, gbatch.stride_a, gbatch.stride_b,
-                                ai.data_ptr(), bi.data_ptr(), gbatch.count, cbuf.data_ptr(), coff.data_ptr(),
-                                gbatch.groups, _lib.stream_ptr(stream))
+    gkey = ("gang", spec.m, spec.n, str(dev))
+    if gkey not in gbatch._gang:
+        # groups sharing A lists (rows) and B lists (columns): tiled together
+        if gbatch.kind is BatchKind.STRIDE:
+            ka, kb = list(gbatch.a_goff), list(gbatch.b_goff)
+        else:
+            ka = [tuple((id(buf), o) for buf, o in grp) for grp in gbatch.a_refs]
+            kb = [tuple((id(buf), o) for buf, o in grp) for grp in gbatch.b_refs]
+        gbatch._gang[gkey] = _gang_table(ka, kb, spec.m, spec.n, dev, int(lib.tpp_device_sm_count()))
+    gang = gbatch._gang[gkey]
+    if gang is not None:
+        table, ngangs, gm, gn = gang
+        rc = lib.tpp_brgemm_grouped_gang(C.byref(d), kind, a_ptr, b_ptr, gbatch.stride_a, gbatch.stride_b,
+                                         ai.data_ptr(), bi.data_ptr(), gbatch.count, cbuf.data_ptr(),
+                                         coff.data_ptr(), gbatch.groups, table.data_ptr(), ngangs, gm, gn,
+                                         _lib.stream_ptr(stream))
+    else:
+        rc = lib.tpp_brgemm_grouped(C.byref(d), kind, a_ptr, b_ptr, gbatch.stride_a, gbatch.stride_b,
+                                    ai.data_ptr(), bi.data_ptr(), gbatch.count, cbuf.data_ptr(), coff.data_ptr(),
+                                    gbatch.groups, _lib.stream_ptr(stream))
     _lib.check(rc, "brgemm_grouped")
 
 

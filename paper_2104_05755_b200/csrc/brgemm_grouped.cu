@@ -66,7 +66,19 @@ struct GParams {
   float beta;
   int beta_mode;    // 0: beta == 0, 1: beta == 1, 2: general
   int dbg;          // experiments (TPP_GRP_DBG): 1 no MMAs, 2 no copies, 4 no VNNI transpose
+  // Gangs (optional): a work item is gang_ma x gang_nb groups that share A
+  // lists along a row and B lists along a column (the reference's FC / conv
+  // compositions: every C block of one weight block row reuses its A blocks).
+  // A rows of sub-block ma come from group gang_rows[j][ma], B rows of
+  // sub-block nb from gang_cols[j][nb], C of (ma, nb) is group
+  // gang_cells[j][ma][nb]; -1 = empty (zero operands, no store).  Sub-blocks:
+  // 64 rows of A (m <= 64) and, when gang_nb > 1, 64 rows of B (n <= 64).
+  int gang_ma, gang_nb, ngangs;
+  const int* gang_rows;
+  const int* gang_cols;
+  const int* gang_cells;
 };
+constexpr int kGangMA = 2, kGangNB = 4;
 
 constexpr int kIdxChunk = 256;   // batch entries whose indices sit in smem at a time
 
@@ -76,8 +88,8 @@ struct GSmem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int RAW_BYTES = BM * 128;  // VNNI A as loaded, before the word transpose
   static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
-  static constexpr int IDX_OFF = STAGES * STAGE;                 // batch index chunk [2][kIdxChunk]
-  static constexpr int BAR_OFF = IDX_OFF + 2 * kIdxChunk * 8;
+  static constexpr int IDX_OFF = STAGES * STAGE;                 // batch index chunk [slots][kIdxChunk]
+  static constexpr int BAR_OFF = IDX_OFF + (kGangMA + kGangNB) * kIdxChunk * 8;
   static constexpr int BYTES = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * BN;
 };
@@ -122,7 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(landed + STAGES);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
-  const int ntiles = (int)(p.groups * p.tiles_m * p.tiles_n);   // < 2^31 (checked by the host)
+  // work items: gangs x column tiles, or groups x row tiles x column tiles (< 2^31, checked by the host)
+  const int ntiles = p.gang_cells ? p.ngangs * p.tiles_n : (int)(p.groups * p.tiles_m * p.tiles_n);
   const long long per_tile = p.count * p.kchunks;
 
   if (threadIdx.x == 0) {
@@ -163,28 +176,63 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     constexpr int AU = (BM * 2 + kProd - 1) / kProd;   // units of 4 k-pairs x 4 rows: 8 * BM / 4 in all
     constexpr int NUNITS = BM * 2;
     // ---- per-tile state, refreshed when the walk reaches a new tile ----
+    // A row r of the tile: sub-block ma = r / 64 of a gang (gang_ma == 2) or
+    // row tm*BM + r of the one group; B row r: sub-block nb = r / 64 of a gang
+    // (gang_nb > 1) or column tn*BN + r of the one group's B block
+    const bool asplit = p.gang_ma == 2, bsplit = p.gang_nb > 1;
     int cur_tile = -1, tm = 0, tn = 0;
-    long long g = 0;
+    int ga[kGangMA] = {-1, -1}, gb[kGangNB] = {-1, -1, -1, -1};  // groups feeding A / B sub-blocks
     long long b_toff = 0, a_toff = 0;   // element offsets of this thread's first chunk in a block
     uint32_t b_rows_ok = 0;             // bit j: B row br0 + 16 j exists
-    bool a_rows_ok = false;             // PLAIN: rows tm*BM + ach*8 .. +7 exist
+    bool a_rows_ok = false;             // PLAIN: rows of chunk ach exist
+    int a_ma = 0;                       // PLAIN: the A sub-block of chunk ach
     uint32_t v_rows_ok = 0;             // VNNI: bit u: rows of unit u exist
+    uint32_t v_ma = 0;                  // VNNI: bit u: unit u reads A sub-block 1
+    int v_row[AU];                      // VNNI: first row (within its A block) of unit u
     auto set_tile = [&](int tile) {
-      const int per_g = p.tiles_m * p.tiles_n;
-      g = tile / per_g;
-      const int rem = tile - (int)g * per_g;
-      tm = rem / p.tiles_n;
-      tn = rem - tm * p.tiles_n;
-      b_toff = (long long)(tn * BN + br0) * p.ldb + bq * 8;
+      if (p.gang_cells) {
+        const int j = tile / p.tiles_n;
+        tn = tile - j * p.tiles_n;
+        tm = 0;
+#pragma unroll
+        for (int ma = 0; ma < kGangMA; ++ma) ga[ma] = ma < p.gang_ma ? __ldg(p.gang_rows + j * p.gang_ma + ma) : -1;
+#pragma unroll
+        for (int nb = 0; nb < kGangNB; ++nb) gb[nb] = nb < p.gang_nb ? __ldg(p.gang_cols + j * p.gang_nb + nb) : -1;
+      } else {
+        const int per_g = p.tiles_m * p.tiles_n;
+        const int g = tile / per_g;
+        const int rem = tile - g * per_g;
+        tm = rem / p.tiles_n;
+        tn = rem - tm * p.tiles_n;
+        ga[0] = gb[0] = g;
+      }
+      b_toff = (long long)((bsplit ? 0 : tn * BN) + br0) * p.ldb + bq * 8;
       b_rows_ok = 0;
 #pragma unroll
-      for (int jj = 0; jj < BJ; ++jj) b_rows_ok |= (uint32_t)(tn * BN + br0 + BRS * jj < p.n) << jj;
-      a_toff = tm * BM + ach * 8 + (long long)akk0 * p.lda;
-      a_rows_ok = tm * BM + ach * 8 < p.m;
+      for (int jj = 0; jj < BJ; ++jj) {
+        const int row = br0 + BRS * jj;
+        const int nb = bsplit ? row >> 6 : 0;
+        const int rin = bsplit ? (row & 63) : tn * BN + row;
+        b_rows_ok |= (uint32_t)(rin < p.n && (nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3]) >= 0) << jj;
+      }
+      {
+        const int r = ach * 8;
+        a_ma = asplit ? r >> 6 : 0;
+        const int rin = asplit ? (r & 63) : tm * BM + r;
+        a_toff = rin + (long long)akk0 * p.lda;
+        a_rows_ok = rin < p.m && (a_ma ? ga[1] : ga[0]) >= 0;
+      }
       v_rows_ok = 0;
+      v_ma = 0;
 #pragma unroll
-      for (int u = 0; u < AU; ++u)
-        v_rows_ok |= (uint32_t)(t + u * kProd < NUNITS && tm * BM + ((t + u * kProd) % (BM / 4)) * 4 < p.m) << u;
+      for (int u = 0; u < AU; ++u) {
+        const int unit = t + u * kProd;
+        const int r = (unit % (BM / 4)) * 4;
+        const int ma = asplit ? r >> 6 : 0;
+        v_row[u] = asplit ? (r & 63) : tm * BM + r;
+        v_ma |= (uint32_t)ma << u;
+        v_rows_ok |= (uint32_t)(unit < NUNITS && v_row[u] < p.m && (ma ? ga[1] : ga[0]) >= 0) << u;
+      }
       cur_tile = tile;
     };
     auto advance = [&](StageIt& s) {
@@ -196,69 +244,84 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         }
       }
     };
-    // A stage takes the fast path (16-byte cp.async) when the problem's
-    // extents and strides are multiples of 8 elements and both block
-    // addresses are 16-byte aligned; otherwise every 16-byte smem chunk is
-    // assembled from 2-byte loads (any shape, any alignment).
-    // The batch's index values (STRIDE: the group's base offsets; OFFSET: the
+    // The batch's index values (STRIDE: the groups' base offsets; OFFSET: the
     // entries' offsets; ADDRESS: their pointers) are staged in shared memory
     // by the producer warps together, kIdxChunk entries at a time (at a tile's
-    // first stage and every kIdxChunk entries): a stage then reads them from
-    // smem.  A global load per stage whose result the same stage consumes was
-    // the producers' critical path -- one L2 round trip per stage, ~0.5 us,
-    // with the copies, MMAs and transposes all switched off.
-    long long* sidx = reinterpret_cast<long long*>(smem + S::IDX_OFF);   // [2][kIdxChunk]: a, b
+    // first stage and every kIdxChunk entries), one slot per A / B sub-block:
+    // a stage then reads them from smem.  A global load per stage whose result
+    // the same stage consumes was the producers' critical path -- one L2 round
+    // trip per stage, ~0.5 us, with the copies, MMAs and transposes all off.
+    long long* sidx = reinterpret_cast<long long*>(smem + S::IDX_OFF);   // [kGangMA + kGangNB][kIdxChunk]
     auto refill = [&](const StageIt& st) {
       named_bar_sync(2, kProd);   // every producer is done with the previous chunk
-      const long long gg = st.tile / (p.tiles_m * p.tiles_n);
-      if (p.kind == 0) {
-        if (t == 0) {
-          sidx[0] = p.a_idx ? __ldg(p.a_idx + gg) : 0;
-          sidx[kIdxChunk] = p.b_idx ? __ldg(p.b_idx + gg) : 0;
-        }
-      } else {
-        const long long base = gg * p.count + st.i;
-        for (int e = t; e < kIdxChunk && st.i + e < p.count; e += kProd) {
-          sidx[e] = __ldg(p.a_idx + base + e);
-          sidx[kIdxChunk + e] = __ldg(p.b_idx + base + e);
+#pragma unroll
+      for (int sl = 0; sl < kGangMA + kGangNB; ++sl) {
+        const bool is_a = sl < kGangMA;
+        const int g = is_a ? (sl == 0 ? ga[0] : ga[1])
+                           : (sl == 2 ? gb[0] : sl == 3 ? gb[1] : sl == 4 ? gb[2] : gb[3]);
+        if (g < 0) continue;
+        const long long* idx = is_a ? p.a_idx : p.b_idx;
+        long long* dst = sidx + sl * kIdxChunk;
+        if (p.kind == 0) {
+          if (t == 0) dst[0] = idx ? __ldg(idx + g) : 0;
+        } else {
+          const long long base = (long long)g * p.count + st.i;
+          for (int e = t; e < kIdxChunk && st.i + e < p.count; e += kProd) dst[e] = __ldg(idx + base + e);
         }
       }
       named_bar_sync(2, kProd);
     };
-    auto stage_ptrs = [&](const StageIt& st, const uint16_t*& ap, const uint16_t*& bp) -> bool {
+    // per stage: the A / B sub-block base pointers (unused sub-blocks: a valid
+    // dummy, their rows are masked)
+    const uint16_t* apv[kGangMA];
+    const uint16_t* bpv[kGangNB];
+    auto stage_ptrs = [&](const StageIt& st) -> bool {
       if ((int)st.tile != cur_tile) set_tile((int)st.tile);
       if (st.kc == 0 && (st.i == 0 || (p.kind != 0 && st.i % kIdxChunk == 0))) refill(st);
-      if (p.kind == 0) {
-        ap = p.a + sidx[0] + st.i * p.stride_a;
-        bp = p.b + sidx[kIdxChunk] + st.i * p.stride_b;
-      } else {
-        const int e = (int)(st.i % kIdxChunk);
-        if (p.kind == 1) {
-          ap = p.a + sidx[e];
-          bp = p.b + sidx[kIdxChunk + e];
-        } else {
-          ap = reinterpret_cast<const uint16_t*>(sidx[e]);
-          bp = reinterpret_cast<const uint16_t*>(sidx[kIdxChunk + e]);
+      const int e = p.kind == 0 ? 0 : (int)(st.i % kIdxChunk);
+      uintptr_t ormask = 0;
+      const uint16_t* any = nullptr;   // a real block address: the source of zero-size (masked) copies
+#pragma unroll
+      for (int sl = 0; sl < kGangMA + kGangNB; ++sl) {
+        const bool is_a = sl < kGangMA;
+        const int g = is_a ? (sl == 0 ? ga[0] : ga[1])
+                           : (sl == 2 ? gb[0] : sl == 3 ? gb[1] : sl == 4 ? gb[2] : gb[3]);
+        const uint16_t* ptr = nullptr;
+        if (g >= 0) {
+          const uint16_t* base = is_a ? p.a : p.b;
+          const long long v = sidx[sl * kIdxChunk + e];
+          if (p.kind == 0) ptr = base + v + st.i * (is_a ? p.stride_a : p.stride_b);
+          else if (p.kind == 1) ptr = base + v;
+          else ptr = reinterpret_cast<const uint16_t*>(v);
+          ormask |= reinterpret_cast<uintptr_t>(ptr);
+          any = ptr;
         }
+        if (is_a) apv[sl] = ptr;
+        else bpv[sl - kGangMA] = ptr;
       }
-      return p.dims_ok && ((reinterpret_cast<uintptr_t>(ap) | reinterpret_cast<uintptr_t>(bp)) & 15) == 0;
+#pragma unroll
+      for (int ma = 0; ma < kGangMA; ++ma) if (apv[ma] == nullptr) apv[ma] = any;
+#pragma unroll
+      for (int nb = 0; nb < kGangNB; ++nb) if (bpv[nb] == nullptr) bpv[nb] = any;
+      return p.dims_ok && (ormask & 15) == 0;
     };
     // VNNI A fast path: each unit is 4 x 16 B cp.async of words (p, m..m+3)
     // for 4 consecutive k-pairs into this thread's own 64 B of the stage's
     // raw area; once they land (the thread's own cp.async group) the thread
     // word-transposes them into 4 16-byte K-major row chunks of the A tile
-    auto issue_vnni = [&](int kc, const uint16_t* ap, uint32_t sRaw) {
+    auto issue_vnni = [&](int kc, uint32_t sRaw) {
 #pragma unroll
       for (int u = 0; u < AU; ++u) {
         const int unit = t + u * kProd;
         if (unit >= NUNITS) break;
-        const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+        const int pq = unit / (BM / 4);
         const int k0 = kc * 64 + pq * 8;
         const bool ok = ((v_rows_ok >> u) & 1u) && k0 < p.k;
-        const uint16_t* src = ap + (long long)(k0 >> 1) * 2 * p.m + 2 * (tm * BM + mq * 4);
+        const uint16_t* ab = ((v_ma >> u) & 1u) ? apv[1] : apv[0];
+        const uint16_t* src = ab + (long long)(k0 >> 1) * 2 * p.m + 2 * v_row[u];
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp)
-          cp_async16(sRaw + (unit * 4 + pp) * 16, ok ? (const void*)(src + (long long)pp * 2 * p.m) : (const void*)ap,
+          cp_async16(sRaw + (unit * 4 + pp) * 16, ok ? (const void*)(src + (long long)pp * 2 * p.m) : (const void*)ab,
                      ok ? 16 : 0);
       }
     };
@@ -268,39 +331,45 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       return v;
     };
     // fast path: cp.async for B (K-major) and PLAIN A (MN-major)
-    auto issue_fast = [&](int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA, uint32_t sB) {
+    auto issue_fast = [&](int kc, uint32_t sA, uint32_t sB) {
       const int kb = kc * 64;
       {
         const bool kok = kb + bq * 8 < p.k;
-        const uint16_t* src = bp + b_toff + kb;
         const long long step = (long long)BRS * p.ldb;
 #pragma unroll
         for (int jj = 0; jj < BJ; ++jj) {
+          // split B: rows br0 + 16 jj of sub-block jj / 4 (64 rows each)
+          const uint16_t* bb = bsplit ? bpv[(jj >> 2) & 3] : bpv[0];
+          const uint16_t* src = bb + b_toff + kb + (bsplit ? (jj & 3) : jj) * step;
           const bool ok = kok && ((b_rows_ok >> jj) & 1u);
-          cp_async16(sB + b_soff + jj * BRS * 128, ok ? (const void*)(src + jj * step) : (const void*)bp, ok ? 16 : 0);
+          cp_async16(sB + b_soff + jj * BRS * 128, ok ? (const void*)src : (const void*)bb, ok ? 16 : 0);
         }
       }
       if (!p.vnni) {
-        const uint16_t* src = ap + a_toff + (long long)kb * p.lda;
+        const uint16_t* ab = a_ma ? apv[1] : apv[0];
+        const uint16_t* src = ab + a_toff + (long long)kb * p.lda;
         const long long step = (long long)AKS * p.lda;
 #pragma unroll
         for (int jj = 0; jj < AJ; ++jj) {
           const bool ok = a_rows_ok && kb + akk0 + AKS * jj < p.k;
-          cp_async16(sA + a_soff + jj * AKS * 128, ok ? (const void*)(src + jj * step) : (const void*)ap, ok ? 16 : 0);
+          cp_async16(sA + a_soff + jj * AKS * 128, ok ? (const void*)(src + jj * step) : (const void*)ab, ok ? 16 : 0);
         }
       }
     };
     // generic path: every chunk from 2-byte loads, bounds per element
-    auto issue_generic = [&](int kc, const uint16_t* ap, const uint16_t* bp, uint32_t sA, uint32_t sB) {
+    auto issue_generic = [&](int kc, uint32_t sA, uint32_t sB) {
       const int kb = kc * 64;
       for (int c = t; c < BN * 8; c += kProd) {  // B: column nn, k = kk .. kk+7
         const int r = c >> 3, q = c & 7;
-        const int nn = tn * BN + r, kk = kb + q * 8;
+        const int nb = bsplit ? r >> 6 : 0;
+        const int nn = bsplit ? (r & 63) : tn * BN + r, kk = kb + q * 8;
+        const int g = nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3];
+        const uint16_t* bb = nb == 0 ? bpv[0] : nb == 1 ? bpv[1] : nb == 2 ? bpv[2] : bpv[3];
         uint32_t w[4] = {0, 0, 0, 0};
-        if (nn < p.n) {
+        if (nn < p.n && g >= 0) {
 #pragma unroll
           for (int e = 0; e < 8; ++e)
-            if (kk + e < p.k) w[e >> 1] |= ld16(bp + (long long)nn * p.ldb + kk + e) << (16 * (e & 1));
+            if (kk + e < p.k) w[e >> 1] |= ld16(bb + (long long)nn * p.ldb + kk + e) << (16 * (e & 1));
         }
         sts16(sB + (r >> 3) * 1024 + (r & 7) * 128 + ((q ^ (r & 7)) << 4), make_uint4(w[0], w[1], w[2], w[3]));
       }
@@ -309,12 +378,14 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         for (int c = t; c < 64 * CPR; c += kProd) {
           const int kk = c / CPR, ch = c % CPR;
           const int j = ch >> 3, cc = ch & 7;
-          const int mrow = tm * BM + ch * 8, kg = kb + kk;
+          const int r = ch * 8, ma = asplit ? r >> 6 : 0;
+          const int mrow = asplit ? (r & 63) : tm * BM + r, kg = kb + kk;
+          const uint16_t* ab = ma ? apv[1] : apv[0];
           uint32_t w[4] = {0, 0, 0, 0};
-          if (kg < p.k) {
+          if (kg < p.k && (ma ? ga[1] : ga[0]) >= 0) {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              if (mrow + e < p.m) w[e >> 1] |= ld16(ap + mrow + e + (long long)kg * p.lda) << (16 * (e & 1));
+              if (mrow + e < p.m) w[e >> 1] |= ld16(ab + mrow + e + (long long)kg * p.lda) << (16 * (e & 1));
           }
           sts16(sA + j * 8192 + (kk >> 3) * 1024 + (kk & 7) * 128 + ((cc ^ (kk & 7)) << 4),
                 make_uint4(w[0], w[1], w[2], w[3]));
@@ -323,15 +394,19 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         const uint32_t sRaw = sB + S::B_BYTES;
         for (int unit = t; unit < NUNITS; unit += kProd) {
           const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+          const int r = mq * 4, ma = asplit ? r >> 6 : 0;
+          const int r0 = asplit ? (r & 63) : tm * BM + r;
+          const uint16_t* ab = ma ? apv[1] : apv[0];
+          const bool gok = (ma ? ga[1] : ga[0]) >= 0;
 #pragma unroll
           for (int pp = 0; pp < 4; ++pp) {
             const int ke = kb + pq * 8 + 2 * pp;   // k of the pair's even element
             uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int mm = 0; mm < 4; ++mm) {
-              const int mrow = tm * BM + mq * 4 + mm;
-              if (mrow < p.m) {
-                const uint16_t* q = ap + (long long)(ke >> 1) * 2 * p.m + 2 * mrow;
+              const int mrow = r0 + mm;
+              if (gok && mrow < p.m) {
+                const uint16_t* q = ab + (long long)(ke >> 1) * 2 * p.m + 2 * mrow;
                 if (ke < p.k) w[mm] |= ld16(q);
                 if (ke + 1 < p.k) w[mm] |= ld16(q + 1) << 16;
               }
@@ -350,18 +425,17 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     while (cur.tile < ntiles) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
-      const uint16_t *ap, *bp;
-      const bool fast = stage_ptrs(cur, ap, bp);
+      const bool fast = stage_ptrs(cur);
       if (p.dbg & 8) mbar_wait_sleep(&empty[s], ph ^ 1); else mbar_wait(&empty[s], ph ^ 1);
       const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
       if (p.dbg & 2) {
         mbar_arrive(&landed[s]);
       } else if (fast) {
-        issue_fast(cur.kc, ap, bp, sA, sB);
-        if (p.vnni) issue_vnni(cur.kc, ap, sB + S::B_BYTES);
+        issue_fast(cur.kc, sA, sB);
+        if (p.vnni) issue_vnni(cur.kc, sB + S::B_BYTES);
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&landed[s])) : "memory");
       } else {
-        issue_generic(cur.kc, ap, bp, sA, sB);
+        issue_generic(cur.kc, sA, sB);
         fence_async_smem();
         mbar_arrive(&landed[s]);
       }
@@ -451,13 +525,32 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     const int lrow = BM == 128 ? q * 32 + lane : q * 16 + lane;
     const bool lane_ok = BM == 128 || lane < 16;
     uint32_t tcount = 0;
+    const bool asplit = p.gang_ma == 2, bsplit = p.gang_nb > 1;
+    const int ma = asplit ? lrow >> 6 : 0;   // this lane's A sub-block (gangs)
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
-      const int per_g = p.tiles_m * p.tiles_n;
-      const int g = tile / per_g;
-      const int rem = tile - g * per_g;
-      const int tm = rem / p.tiles_n, tn = rem - tm * p.tiles_n;
-      float* cg = p.c + (p.c_off ? p.c_off[g] : 0);
-      const int row = tm * BM + lrow;
+      int tm, tn, row;
+      // C blocks of this lane's row: one per B sub-block (gangs) or the group's
+      float* cgs[kGangNB] = {nullptr, nullptr, nullptr, nullptr};
+      if (p.gang_cells) {
+        const int j = tile / p.tiles_n;
+        tn = tile - j * p.tiles_n;
+        tm = 0;
+        row = asplit ? (lrow & 63) : lrow;
+#pragma unroll
+        for (int nb = 0; nb < kGangNB; ++nb) {
+          const int cell = nb < p.gang_nb && ma < p.gang_ma ? __ldg(p.gang_cells + (j * p.gang_ma + ma) * p.gang_nb + nb)
+                                                            : -1;
+          cgs[nb] = cell >= 0 ? p.c + (p.c_off ? p.c_off[cell] : 0) : nullptr;
+        }
+      } else {
+        const int per_g = p.tiles_m * p.tiles_n;
+        const int g = tile / per_g;
+        const int rem = tile - g * per_g;
+        tm = rem / p.tiles_n;
+        tn = rem - tm * p.tiles_n;
+        row = tm * BM + lrow;
+        cgs[0] = p.c + (p.c_off ? p.c_off[g] : 0);
+      }
       const bool row_ok = lane_ok && row < p.m;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       if (p.dbg & 8) mbar_wait_sleep(&tfull[as], aph); else mbar_wait(&tfull[as], aph);
@@ -473,8 +566,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[as]);
         }
-        const int col0 = tn * BN + ch * 32;
-        if (row_ok) {
+        // split B: chunk ch is columns (ch & 1) * 32 .. of B sub-block ch / 2
+        const int nbc = bsplit ? ch >> 1 : 0;
+        float* cg = nbc == 0 ? cgs[0] : nbc == 1 ? cgs[1] : nbc == 2 ? cgs[2] : cgs[3];
+        const int col0 = bsplit ? (ch & 1) * 32 : tn * BN + ch * 32;
+        if (row_ok && cg != nullptr) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = col0 + i;
@@ -504,7 +600,7 @@ static int launch(const GParams& p, cudaStream_t s) {
   auto kern = brgemm_grouped_kernel<BM, BN, STAGES>;
   cudaError_t e = ensure_smem_attr((const void*)kern, S::BYTES);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_grouped_kernel)");
-  const long long ntiles = p.groups * p.tiles_m * p.tiles_n;
+  const long long ntiles = p.gang_cells ? (long long)p.ngangs * p.tiles_n : p.groups * p.tiles_m * p.tiles_n;
   const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -520,7 +616,8 @@ static int launch(const GParams& p, cudaStream_t s) {
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_grouped_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_grouped_kernel");
   set_last_config("brgemm_grouped_kernel<" + std::to_string(BM) + "," + std::to_string(BN) + "," +
-                  std::to_string(STAGES) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(ntiles));
+                  std::to_string(STAGES) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(ntiles) +
+                  (p.gang_cells ? " gang=" + std::to_string(p.gang_ma) + "x" + std::to_string(p.gang_nb) : ""));
   return TPP_OK;
 }
 
@@ -529,10 +626,25 @@ static int launch(const GParams& p, cudaStream_t s) {
 // 1 = not applicable (caller falls back to the ordered engine), else a status
 int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const void* b, int64_t stride_a,
                       int64_t stride_b, const int64_t* a_idx, const int64_t* b_idx, int64_t count, void* c,
-                      const int64_t* c_off, int64_t groups, cudaStream_t s) {
+                      const int64_t* c_off, int64_t groups, cudaStream_t s, const int32_t* gang, int ngangs,
+                      int gang_ma, int gang_nb) {
   using namespace grp;
   if (d->in_dtype != TPP_BF16 || count < 1 || groups < 1) return 1;
   GParams p{};
+  p.gang_ma = 1;
+  p.gang_nb = 1;
+  if (gang != nullptr) {
+    TPP_REQUIRE(ngangs >= 1 && (gang_ma == 1 || gang_ma == 2) && (gang_nb == 1 || gang_nb == 2 || gang_nb == 4),
+                TPP_E_TENSOR, "gangs: 1 or 2 A sub-blocks x 1, 2 or 4 B sub-blocks");
+    TPP_REQUIRE(d->m <= 64 && (gang_nb == 1 || d->n <= 64), TPP_E_UNSUPPORTED,
+                "gangs stack 64-row A blocks (m <= 64) and, for several B sub-blocks, 64-column B blocks (n <= 64)");
+    p.gang_ma = gang_ma;
+    p.gang_nb = gang_nb;
+    p.ngangs = ngangs;
+    p.gang_rows = gang;
+    p.gang_cols = gang + (int64_t)ngangs * gang_ma;
+    p.gang_cells = gang + (int64_t)ngangs * (gang_ma + gang_nb);
+  }
   // fast-path shape condition; block alignment is checked per stage in the kernel
   p.dims_ok = !(d->k % 8 || d->m % 8 || d->ldb % 8 || (!d->a_vnni && d->lda % 8));
   p.m = d->m; p.n = d->n; p.k = d->k;
@@ -553,15 +665,16 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.beta_mode = d->beta == 0.0 ? 0 : d->beta == 1.0 ? 1 : 2;
   static const int dbg = getenv("TPP_GRP_DBG") ? atoi(getenv("TPP_GRP_DBG")) : 0;
   p.dbg = dbg;
-  const int BM = d->m <= 64 ? 64 : 128;
+  const int BM = gang ? 64 * gang_ma : (d->m <= 64 ? 64 : 128);
   // widest N tile that still gives every SM a tile (one C block of a
   // single brgemm() call is otherwise only a handful of work items)
-  const long long tm_all = groups * ((d->m + BM - 1) / BM);
+  const long long tm_all = gang ? ngangs : groups * ((d->m + BM - 1) / BM);
   int BN = d->n <= 64 ? 64 : d->n <= 128 ? 128 : 256;
   while (BN > 64 && tm_all * ((d->n + BN - 1) / BN) < num_sms()) BN /= 2;
-  p.tiles_m = (d->m + BM - 1) / BM;
-  p.tiles_n = (d->n + BN - 1) / BN;
-  TPP_REQUIRE(groups * p.tiles_m * p.tiles_n < (1LL << 31), TPP_E_UNSUPPORTED, "grouped BRGEMM: too many tiles");
+  if (gang && gang_nb > 1) BN = 64 * gang_nb;
+  p.tiles_m = gang ? 1 : (d->m + BM - 1) / BM;
+  p.tiles_n = gang && gang_nb > 1 ? 1 : (d->n + BN - 1) / BN;
+  TPP_REQUIRE(tm_all * p.tiles_m * p.tiles_n < (1LL << 31), TPP_E_UNSUPPORTED, "grouped BRGEMM: too many tiles");
   if (BM == 64) {
     if (BN == 64) return launch<64, 64, 8>(p, s);
     if (BN == 128) return launch<64, 128, 6>(p, s);

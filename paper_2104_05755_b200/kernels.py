@@ -476,6 +476,14 @@ class _OffsetConv:
         self.c_off = torch.from_numpy(np.ascontiguousarray(c_off, dtype=np.int64)).to(device)
         self.planes = n * co_b
         self.acc_elems = n * co_b * p * wp * 64
+        # output-channel blocks share B lists, output rows share A lists: pairs
+        # of channel blocks tile together (M = 128 MMAs) when there are two
+        from .contraction import _gang_table
+        self.gang = None
+        if torch.device(device).type == "cuda":
+            self.gang = _gang_table([int(v) for v in kbg.reshape(-1)],
+                                    [(int(a), int(b)) for a, b in zip(ng.reshape(-1), obg.reshape(-1))],
+                                    64, ncols, device, int(_lib.load().tpp_device_sm_count()))
 
     def run(self, w_vnni: torch.Tensor, xpad: torch.Tensor, out_bf16: torch.Tensor, stream=None) -> None:
         lib = _lib.load()
@@ -483,10 +491,17 @@ class _OffsetConv:
         d = self.spec.c()
         d.engine = _lib.ENGINE_TENSOR
         s = _lib.stream_ptr(stream)
-        _lib.check(lib.tpp_brgemm_grouped(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
-                                          self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
-                                          acc.data_ptr(), self.c_off.data_ptr(), self.groups, s),
-                   "conv (offset BRGEMM)")
+        if self.gang is not None:
+            table, ngangs, gm, gn = self.gang
+            _lib.check(lib.tpp_brgemm_grouped_gang(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
+                                                   self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
+                                                   acc.data_ptr(), self.c_off.data_ptr(), self.groups,
+                                                   table.data_ptr(), ngangs, gm, gn, s), "conv (offset BRGEMM)")
+        else:
+            _lib.check(lib.tpp_brgemm_grouped(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
+                                              self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
+                                              acc.data_ptr(), self.c_off.data_ptr(), self.groups, s),
+                       "conv (offset BRGEMM)")
         # FP32 accumulators -> BF16 RNE (dtypes.py:82-97), dropping the
         # columns past each row's end: rows = Q*64 valid elements of a padded-
         # width row (ld Wp*64), one column per output row

@@ -97,7 +97,8 @@ def test_conv_offset_fixture_grouped_and_single(golden):
                 tpp.brgemm(spec, tpp.BrgemmBatch.offset(wd, xd, ao, bo), cv)
                 assert _lib.last_config().startswith(GROUPED)
     tpp.brgemm_grouped(spec, tpp.GroupedBatch.offset(wd, xd, a_rows, b_rows), out, c_offs)
-    assert _lib.last_config().startswith(GROUPED) and f"tiles={N * Kb * H}" in _lib.last_config()
+    cfg = _lib.last_config()   # output rows (n, oh) x channel blocks: pairs of kb per tile (gangs)
+    assert cfg.startswith(GROUPED) and (f"tiles={N * Kb * H}" in cfg or "gang=2x1" in cfg), cfg
     for res in (out, single):
         got = to_host(res).reshape(N, Kb, H, W, bk)
         assert normwise(got, O.bf16_to_fp32(want)) <= TOL
@@ -131,11 +132,45 @@ def test_cfg2_composition_grouped(variant):
                                       [[(xd, (nb * Cb + i) * blk) for i in range(Cb)] for nb, _ in groups])
     out = torch.empty(Nb * Kb * bn * bk, dtype=torch.float32, device="cuda")
     tpp.brgemm_grouped(spec, gb, out, [(nb * Kb + kb) * bn * bk for nb, kb in groups])
-    assert _lib.last_config().startswith("brgemm_grouped_kernel<64,64,"), _lib.last_config()
+    # the groups form a full cross product (weight block rows x token blocks):
+    # pairs of weight block rows tile together (M = 128 MMAs)
+    assert _lib.last_config().startswith(GROUPED) and "gang=2x1" in _lib.last_config(), _lib.last_config()
     sel = [0, 7, 15]
     _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)   # FP32 pre-narrow
     got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
     assert normwise(got, want) <= TOL
+
+
+@pytest.mark.parametrize("variant", ["stride", "offset"])
+def test_gangs_partial_and_wide(variant):
+    """Gangs of 2 x 4 groups (M = 128 x N = 256 tiles) with partial gangs at
+    both edges (11 weight block rows, 121 token blocks): every C block against
+    the oracle composition."""
+    rng = np.random.default_rng(92)
+    Nb, Cb, bn, bc, Kb, bk = 121, 2, 64, 64, 11, 64
+    x = O.fp32_to_bf16_rne(rng.normal(0, 1, (Nb, Cb, bn, bc)).astype(np.float32))
+    wv = vnni_weights(rng, Kb, Cb, bk, bc, 0.05)
+    xd, wd = to_dev(x), to_dev(wv)
+    blk = bc * bk
+    spec = tpp.GemmSpec(bk, bn, bc, bk, bc, bk, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                        a_layout=tpp.ALayout.VNNI)
+    groups = [(nb, kb) for nb in range(Nb) for kb in range(Kb)]
+    if variant == "stride":
+        gb = tpp.GroupedBatch.stride(wd, xd, blk, blk, Cb, [kb * Cb * blk for _, kb in groups],
+                                     [nb * Cb * blk for nb, _ in groups])
+    else:
+        gb = tpp.GroupedBatch.offset(wd, xd, [[(kb * Cb + i) * blk for i in range(Cb)] for _, kb in groups],
+                                     [[(nb * Cb + i) * blk for i in range(Cb)] for nb, _ in groups])
+    out = torch.full((Nb * Kb * bn * bk,), float("nan"), dtype=torch.float32, device="cuda")
+    tpp.brgemm_grouped(spec, gb, out, [(nb * Kb + kb) * bn * bk for nb, kb in groups])
+    assert "gang=2x4" in _lib.last_config(), _lib.last_config()
+    sel = [0, 1, 59, 118, 119, 120]          # incl. the last (partial) gang column
+    _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)
+    got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
+    assert not np.isnan(got).any()
+    assert normwise(got, want) <= TOL
+    # every block written (the partial gang row / column too)
+    assert not torch.isnan(out).any()
 
 
 @pytest.mark.parametrize("beta", [0.0, 1.0, 0.5])

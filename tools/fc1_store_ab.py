@@ -21,11 +21,15 @@ w1 = (torch.randn(f, h, 64, 64, generator=gen, device=dev) * 0.02).to(torch.bflo
 w2 = (torch.randn(h, f, 64, 64, generator=gen, device=dev) * 0.02).to(torch.bfloat16)
 fc1 = tpp.FcLayer(f, h, 64, 64, bench._vnni_from_logical(w1).reshape(-1), activation=tpp.UnaryKind.GELU)
 fc2 = tpp.FcLayer(h, f, 64, 64, bench._vnni_from_logical(w2).reshape(-1))
+fc1n = tpp.FcLayer(f, h, 64, 64, bench._vnni_from_logical(w1).reshape(-1))            # no activation
+fc1r = tpp.FcLayer(f, h, 64, 64, bench._vnni_from_logical(w1).reshape(-1), activation=tpp.UnaryKind.RELU)
 mid = torch.empty(nb * f * bn * 64, dtype=torch.bfloat16, device=dev)
 o2 = torch.empty(nb * h * bn * 64, dtype=torch.bfloat16, device=dev)
 fl = 2 * 16384 * 1024 * 4096
 mode = "off" if os.environ.get("TPP_NO_TMA_STORE") else "on"
 for name, fn in (("fc1_gelu", lambda: fc1.forward(x, nb, bn, out=mid)),
+                 ("fc1_none", lambda: fc1n.forward(x, nb, bn, out=mid)),
+                 ("fc1_relu", lambda: fc1r.forward(x, nb, bn, out=mid)),
                  ("fc2_residual", lambda: fc2.forward(mid, nb, bn, out=o2, residual=x))):
     g = bench.graph_of(torch, [fn] * 10)
     ms = statistics.median(bench.time_graph(torch, None, g, reps_min=10, min_seconds=0.5)) / 10
