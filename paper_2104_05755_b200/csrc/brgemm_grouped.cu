@@ -27,13 +27,16 @@
 //
 // Persistent CTAs walk work items (group, row tile, column tile).
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 
 #include <mutex>
 
 #include "common.cuh"
 #include "sm100.cuh"
+#include "launch.h"
 
 namespace tpp {
 using namespace sm100;
@@ -77,10 +80,19 @@ struct GParams {
   const int* gang_rows;
   const int* gang_cols;
   const int* gang_cells;
+  long long* trace;   // TPP_GRP_TRACE: CTA 0's clock64 stamps per stage (probe only)
+  // TMA staging (STRIDE / OFFSET batches, power-of-two row pitches): a stage
+  // whose blocks all start on a row of the tensor maps' 2-D views is loaded
+  // by one thread's TMA boxes instead of 12+ cp.async per producer thread
+  int tma;
+  int a_shift, b_shift;   // log2 of the A row pitch (VNNI: 2m, PLAIN: lda) and of ldb, in elements
+  int b_box;              // B rows per box (a B sub-block or the whole BN tile)
 };
+constexpr int kTrace = 128;   // stages traced
 constexpr int kGangMA = 2, kGangNB = 4;
 
-constexpr int kIdxChunk = 256;   // batch entries whose indices sit in smem at a time
+constexpr int kIdxChunk = 256;
+constexpr int kTmaRowBits = 30;  // rows of the TMA maps' 2-D views of a / b   // batch entries whose indices sit in smem at a time
 
 template <int BM, int BN, int STAGES>
 struct GSmem {
@@ -109,9 +121,32 @@ __device__ __forceinline__ uint4 ldg_nc16(const void* p) {
                : "l"(p));
   return v;
 }
+// explicit shared-space accesses: the aligned dynamic smem pointer is an
+// integer round trip, so plain C++ accesses through it compile to GENERIC
+// loads -- six dependent ones per stage cost the producers ~700 cycles
+__device__ __forceinline__ long long lds64(uint32_t a) {
+  long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, long long v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
 __device__ __forceinline__ void sts16(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+__device__ __forceinline__ uint32_t selp32(uint32_t a, uint32_t b, int c) {   // c ? a : b, no branch
+  uint32_t r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.b32 %0, %1, %2, q;\n\t}" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+  return r;
+}
+// v rotated left by rot (0..3) words: result word j = v word (j + rot) & 3
+__device__ __forceinline__ uint4 rot4(uint4 v, int rot) {
+  const int r1 = rot & 1, r2 = rot & 2;
+  uint4 t = make_uint4(selp32(v.y, v.x, r1), selp32(v.z, v.y, r1), selp32(v.w, v.z, r1), selp32(v.x, v.w, r1));
+  return make_uint4(selp32(t.z, t.x, r2), selp32(t.w, t.y, r2), selp32(t.x, t.z, r2), selp32(t.y, t.w, r2));
 }
 
 // the producer's walk over (work item, batch entry, k chunk)
@@ -122,7 +157,9 @@ struct StageIt {
 };
 
 template <int BM, int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GParams p) {
+__global__ void __launch_bounds__(kThreads, 1)
+    brgemm_grouped_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                          const GParams p) {
   using S = GSmem<BM, BN, STAGES>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -142,7 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kFinWarps);   // one arrival per finisher warp
       mbar_init(&empty[s], 1);
-      mbar_init(&landed[s], kProd);
+      mbar_init(&landed[s], p.tma ? 1 : kProd);   // TMA mode: one arrival per stage (its issuing lane)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -150,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     }
     fence_mbar_init();
   }
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[7 * kTrace] = clock64();
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, S::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
@@ -175,6 +213,12 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     // A VNNI: units (k-pair quad pq, row quad mq) = t + u * 128
     constexpr int AU = (BM * 2 + kProd - 1) / kProd;   // units of 4 k-pairs x 4 rows: 8 * BM / 4 in all
     constexpr int NUNITS = BM * 2;
+    // raw VNNI A in smem, the TMA boxes' layout: [sub-block][k-pair 0..31][row]
+    // of 32-bit words, a sub-block = 64 rows (gangs) or the whole tile
+    const int bmsub = p.gang_ma == 2 ? 64 : BM;
+    auto raw_off = [&](int kp, int r) -> uint32_t {
+      return (uint32_t)((r / bmsub) * (32 * bmsub * 4) + kp * bmsub * 4 + (r % bmsub) * 4);
+    };
     // ---- per-tile state, refreshed when the walk reaches a new tile ----
     // A row r of the tile: sub-block ma = r / 64 of a gang (gang_ma == 2) or
     // row tm*BM + r of the one group; B row r: sub-block nb = r / 64 of a gang
@@ -251,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     // a stage then reads them from smem.  A global load per stage whose result
     // the same stage consumes was the producers' critical path -- one L2 round
     // trip per stage, ~0.5 us, with the copies, MMAs and transposes all off.
-    long long* sidx = reinterpret_cast<long long*>(smem + S::IDX_OFF);   // [kGangMA + kGangNB][kIdxChunk]
+    const uint32_t sidx = smem_u32(smem + S::IDX_OFF);   // long long [kGangMA + kGangNB][kIdxChunk]
     auto refill = [&](const StageIt& st) {
       named_bar_sync(2, kProd);   // every producer is done with the previous chunk
 #pragma unroll
@@ -261,12 +305,12 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
                            : (sl == 2 ? gb[0] : sl == 3 ? gb[1] : sl == 4 ? gb[2] : gb[3]);
         if (g < 0) continue;
         const long long* idx = is_a ? p.a_idx : p.b_idx;
-        long long* dst = sidx + sl * kIdxChunk;
+        const uint32_t dst = sidx + sl * kIdxChunk * 8;
         if (p.kind == 0) {
-          if (t == 0) dst[0] = idx ? __ldg(idx + g) : 0;
+          if (t == 0) sts64(dst, idx ? __ldg(idx + g) : 0);
         } else {
           const long long base = (long long)g * p.count + st.i;
-          for (int e = t; e < kIdxChunk && st.i + e < p.count; e += kProd) dst[e] = __ldg(idx + base + e);
+          for (int e = t; e < kIdxChunk && st.i + e < p.count; e += kProd) sts64(dst + e * 8, __ldg(idx + base + e));
         }
       }
       named_bar_sync(2, kProd);
@@ -281,6 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       const int e = p.kind == 0 ? 0 : (int)(st.i % kIdxChunk);
       uintptr_t ormask = 0;
       const uint16_t* any = nullptr;   // a real block address: the source of zero-size (masked) copies
+      long long vs[kGangMA + kGangNB];  // all index loads first: one smem latency per stage
+#pragma unroll
+      for (int sl = 0; sl < kGangMA + kGangNB; ++sl) {
+        const int g = sl < kGangMA ? (sl == 0 ? ga[0] : ga[1])
+                                   : (sl == 2 ? gb[0] : sl == 3 ? gb[1] : sl == 4 ? gb[2] : gb[3]);
+        vs[sl] = g >= 0 ? lds64(sidx + (sl * kIdxChunk + e) * 8) : 0;
+      }
 #pragma unroll
       for (int sl = 0; sl < kGangMA + kGangNB; ++sl) {
         const bool is_a = sl < kGangMA;
@@ -289,7 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         const uint16_t* ptr = nullptr;
         if (g >= 0) {
           const uint16_t* base = is_a ? p.a : p.b;
-          const long long v = sidx[sl * kIdxChunk + e];
+          const long long v = vs[sl];
           if (p.kind == 0) ptr = base + v + st.i * (is_a ? p.stride_a : p.stride_b);
           else if (p.kind == 1) ptr = base + v;
           else ptr = reinterpret_cast<const uint16_t*>(v);
@@ -319,9 +370,10 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         const bool ok = ((v_rows_ok >> u) & 1u) && k0 < p.k;
         const uint16_t* ab = ((v_ma >> u) & 1u) ? apv[1] : apv[0];
         const uint16_t* src = ab + (long long)(k0 >> 1) * 2 * p.m + 2 * v_row[u];
+        const uint32_t dst = sRaw + raw_off(pq * 4, (unit % (BM / 4)) * 4);
 #pragma unroll
         for (int pp = 0; pp < 4; ++pp)
-          cp_async16(sRaw + (unit * 4 + pp) * 16, ok ? (const void*)(src + (long long)pp * 2 * p.m) : (const void*)ab,
+          cp_async16(dst + pp * bmsub * 4, ok ? (const void*)(src + (long long)pp * 2 * p.m) : (const void*)ab,
                      ok ? 16 : 0);
       }
     };
@@ -357,9 +409,9 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       }
     };
     // generic path: every chunk from 2-byte loads, bounds per element
-    auto issue_generic = [&](int kc, uint32_t sA, uint32_t sB) {
+    auto issue_generic = [&](int kc, uint32_t sA, uint32_t sB, int tid, int nthr) {
       const int kb = kc * 64;
-      for (int c = t; c < BN * 8; c += kProd) {  // B: column nn, k = kk .. kk+7
+      for (int c = tid; c < BN * 8; c += nthr) {  // B: column nn, k = kk .. kk+7
         const int r = c >> 3, q = c & 7;
         const int nb = bsplit ? r >> 6 : 0;
         const int nn = bsplit ? (r & 63) : tn * BN + r, kk = kb + q * 8;
@@ -375,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       }
       if (!p.vnni) {  // A PLAIN, MN-major chunks: 8 rows at one k
         constexpr int CPR = BM / 8;
-        for (int c = t; c < 64 * CPR; c += kProd) {
+        for (int c = tid; c < 64 * CPR; c += nthr) {
           const int kk = c / CPR, ch = c % CPR;
           const int j = ch >> 3, cc = ch & 7;
           const int r = ch * 8, ma = asplit ? r >> 6 : 0;
@@ -392,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         }
       } else {  // A VNNI: the raw unit layout of the fast path (the finisher transposes)
         const uint32_t sRaw = sB + S::B_BYTES;
-        for (int unit = t; unit < NUNITS; unit += kProd) {
+        for (int unit = tid; unit < NUNITS; unit += nthr) {
           const int pq = unit / (BM / 4), mq = unit % (BM / 4);
           const int r = mq * 4, ma = asplit ? r >> 6 : 0;
           const int r0 = asplit ? (r & 63) : tm * BM + r;
@@ -411,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
                 if (ke + 1 < p.k) w[mm] |= ld16(q + 1) << 16;
               }
             }
-            sts16(sRaw + (unit * 4 + pp) * 16, make_uint4(w[0], w[1], w[2], w[3]));
+            sts16(sRaw + raw_off(pq * 4 + pp, r), make_uint4(w[0], w[1], w[2], w[3]));
           }
         }
       }
@@ -422,11 +474,131 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     // flight, bounded only by the MMA consuming slots.
     StageIt cur{(int)blockIdx.x, 0, 0};
     uint32_t it = 0;
-    while (cur.tile < ntiles) {
+    const bool tr = p.trace && blockIdx.x == 0 && t == 0;
+    if (p.tma) {
+      // ---- TMA mode: the four producer warps take the stages round-robin
+      // (a stage's control code is a serial chain of ~200 instructions; one
+      // warp per stage runs four of them at once).  A stage whose blocks do
+      // not all start on a row of the maps' views is written element-wise by
+      // its warp instead.
+      // (at most STAGES warps: a warp's next stage is then never two ring
+      // revolutions ahead of the MMA, where the parity wait is ambiguous)
+      constexpr int kRR = kProdWarps < STAGES ? kProdWarps : STAGES;
+      const int w = warp - kProdWarp0;
+      if (w >= kRR) cur.tile = ntiles;
+      for (int j = 0; j < w && cur.tile < ntiles; ++j) { advance(cur); ++it; }
+      const int asub = p.gang_ma == 2 ? 2 : 1, bsub = bsplit ? p.gang_nb : 1;
+      long long abase[kGangMA] = {0, 0}, bbase[kGangNB] = {0, 0, 0, 0};   // STRIDE: the groups' offsets
+      const bool trw = p.trace && blockIdx.x == 0 && lane == 0;
+      while (cur.tile < ntiles) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        if ((int)cur.tile != cur_tile) {
+          set_tile((int)cur.tile);
+          if (p.kind == 0) {
+#pragma unroll
+            for (int ma = 0; ma < kGangMA; ++ma) {
+              const int g = ma == 0 ? ga[0] : ga[1];
+              abase[ma] = g >= 0 && p.a_idx ? __ldg(p.a_idx + g) : 0;
+            }
+#pragma unroll
+            for (int nb = 0; nb < kGangNB; ++nb) {
+              const int g = nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3];
+              bbase[nb] = g >= 0 && p.b_idx ? __ldg(p.b_idx + g) : 0;
+            }
+          }
+        }
+        // element offsets of the live blocks
+        long long aoff[kGangMA], boff[kGangNB];
+        long long am = 0, bm = 0;
+        const uint16_t* any = nullptr;
+#pragma unroll
+        for (int ma = 0; ma < kGangMA; ++ma) {
+          const int g = ma == 0 ? ga[0] : ga[1];
+          aoff[ma] = 0;
+          if (g >= 0) {
+            aoff[ma] = p.kind == 0 ? abase[ma] + cur.i * p.stride_a : __ldg(p.a_idx + (long long)g * p.count + cur.i);
+            am |= aoff[ma];
+            any = p.a + aoff[ma];
+          }
+        }
+#pragma unroll
+        for (int nb = 0; nb < kGangNB; ++nb) {
+          const int g = nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3];
+          boff[nb] = 0;
+          if (g >= 0) {
+            boff[nb] = p.kind == 0 ? bbase[nb] + cur.i * p.stride_b : __ldg(p.b_idx + (long long)g * p.count + cur.i);
+            bm |= boff[nb];
+          }
+        }
+        // A blocks start on a row of the A view; B blocks on a 64-element
+        // chunk of a row of the B view [rows][ldb / 64][64], with the k
+        // chunks inside the row
+        long long bchunk = 0;
+#pragma unroll
+        for (int nb = 0; nb < kGangNB; ++nb) bchunk = max(bchunk, ((boff[nb] & ((1LL << p.b_shift) - 1)) >> 6) + p.kchunks);
+        const bool rows_ok = ((am & ((1LL << p.a_shift) - 1)) | (bm & 63)) == 0 && bchunk <= (1LL << (p.b_shift - 6)) &&
+                             (am >> (p.a_shift + kTmaRowBits)) == 0 && (bm >> (p.b_shift + kTmaRowBits)) == 0;
+        if (trw && it < kTrace) p.trace[0 * kTrace + it] = clock64();
+        mbar_wait(&empty[s], ph ^ 1);
+        if (trw && it < kTrace) p.trace[1 * kTrace + it] = clock64();
+        uint8_t* stage = smem + s * S::STAGE;
+        if (rows_ok) {
+          if (lane == 0) {
+            uint32_t bytes = 0;
+#pragma unroll
+            for (int ma = 0; ma < kGangMA; ++ma)
+              if (ma < asub && (ma == 0 ? ga[0] : ga[1]) >= 0) bytes += 128 * bmsub;   // 64 k x bmsub rows
+#pragma unroll
+            for (int nb = 0; nb < kGangNB; ++nb)
+              if (nb < bsub && (nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3]) >= 0) bytes += 128 * p.b_box;
+            mbar_arrive_expect_tx(&landed[s], bytes);
+            const int m0 = asplit ? 0 : tm * BM;
+#pragma unroll
+            for (int ma = 0; ma < kGangMA; ++ma) {
+              if (ma >= asub || (ma == 0 ? ga[0] : ga[1]) < 0) continue;
+              const int row0 = (int)(aoff[ma] >> p.a_shift);
+              if (p.vnni) {   // raw k-pair rows: box {2 bmsub, 32}
+                tma_load_5d(stage + S::A_BYTES + S::B_BYTES + ma * 32 * bmsub * 4, &tmA, &landed[s], 2 * m0,
+                            row0 + cur.kc * 32, 0, 0, 0);
+              } else {        // MN-major 64 x 64 boxes, SW128
+                for (int j = 0; j < bmsub / 64; ++j)
+                  tma_load_5d(stage + (ma * (bmsub / 64) + j) * 8192, &tmA, &landed[s], m0 + 64 * j,
+                              row0 + cur.kc * 64, 0, 0, 0);
+              }
+            }
+#pragma unroll
+            for (int nb = 0; nb < kGangNB; ++nb) {
+              if (nb >= bsub || (nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3]) < 0) continue;
+              const int row0 = (int)(boff[nb] >> p.b_shift) + (bsplit ? 0 : tn * BN);
+              const int ch0 = (int)((boff[nb] & ((1LL << p.b_shift) - 1)) >> 6);
+              tma_load_5d(stage + S::A_BYTES + nb * 64 * 128, &tmB, &landed[s], 0, ch0 + cur.kc, row0, 0, 0);
+            }
+          }
+        } else {
+          // element-wise by this warp, then its one arrival
+#pragma unroll
+          for (int ma = 0; ma < kGangMA; ++ma) apv[ma] = (ma == 0 ? ga[0] : ga[1]) >= 0 ? p.a + aoff[ma] : any;
+#pragma unroll
+          for (int nb = 0; nb < kGangNB; ++nb)
+            bpv[nb] = (nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3]) >= 0 ? p.b + boff[nb] : any;
+          const uint32_t sA = smem_u32(stage);
+          issue_generic(cur.kc, sA, sA + S::A_BYTES, lane, 32);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&landed[s]);
+        }
+        if (trw && it < kTrace) p.trace[2 * kTrace + it] = clock64();
+        for (int j = 0; j < kRR && cur.tile < ntiles; ++j) { advance(cur); ++it; }
+      }
+    }
+    while (!p.tma && cur.tile < ntiles) {
       const int s = it % STAGES;
       const uint32_t ph = (it / STAGES) & 1;
       const bool fast = stage_ptrs(cur);
+      if (tr && it < kTrace) p.trace[0 * kTrace + it] = clock64();
       if (p.dbg & 8) mbar_wait_sleep(&empty[s], ph ^ 1); else mbar_wait(&empty[s], ph ^ 1);
+      if (tr && it < kTrace) p.trace[1 * kTrace + it] = clock64();
       const uint32_t sA = smem_u32(smem + s * S::STAGE), sB = sA + S::A_BYTES;
       if (p.dbg & 2) {
         mbar_arrive(&landed[s]);
@@ -435,10 +607,11 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
         if (p.vnni) issue_vnni(cur.kc, sB + S::B_BYTES);
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&landed[s])) : "memory");
       } else {
-        issue_generic(cur.kc, sA, sB);
+        issue_generic(cur.kc, sA, sB, t, kProd);
         fence_async_smem();
         mbar_arrive(&landed[s]);
       }
+      if (tr && it < kTrace) p.trace[2 * kTrace + it] = clock64();
       advance(cur);
       ++it;
     }
@@ -448,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     // the generic -> async proxy fence the tensor core's operand reads need,
     // then full[s] for the MMA warp
     const int t = threadIdx.x - kFinWarp0 * 32;
+    const int bmsub = p.gang_ma == 2 ? 64 : BM;
     constexpr int AU = (BM * 2 + 32 * kFinWarps - 1) / (32 * kFinWarps);
     constexpr int NUNITS = BM * 2;
     const int per_tile = (int)(p.count * p.kchunks);
@@ -456,6 +630,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
     for (long long it = 0; it < nst; ++it) {
       const int s = (int)(it % STAGES);
       if (p.dbg & 8) mbar_wait_sleep(&landed[s], (uint32_t)((it / STAGES) & 1)); else mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
+      if (p.trace && blockIdx.x == 0 && t == 0 && it < kTrace) p.trace[3 * kTrace + it] = clock64();
       if (p.vnni && !(p.dbg & 4)) {
         const uint32_t sA = smem_u32(smem + s * S::STAGE), sRaw = sA + S::A_BYTES + S::B_BYTES;
 #pragma unroll
@@ -463,19 +638,30 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           const int unit = t + u * 32 * kFinWarps;
           if (unit >= NUNITS) break;
           const int pq = unit / (BM / 4), mq = unit % (BM / 4);
+          // raw [sub-block][k-pair][row] words: consecutive lanes read
+          // consecutive 16 B (no bank conflicts)
+          const int r0 = mq * 4;
+          const uint32_t src = sRaw + (uint32_t)((r0 / bmsub) * (32 * bmsub * 4) + pq * 4 * bmsub * 4 + (r0 % bmsub) * 4);
           uint4 r[4];
 #pragma unroll
           for (int pp = 0; pp < 4; ++pp)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(r[pp].x), "=r"(r[pp].y), "=r"(r[pp].z), "=r"(r[pp].w)
-                         : "r"(sRaw + (unit * 4 + pp) * 16));
+                         : "r"(src + pp * bmsub * 4));
+          // write j: row mq*4 + (j + rot) & 3, rotated by lane so that any 8
+          // consecutive lanes hit 8 different 16-byte bank groups (the same
+          // row offset for all lanes puts a warp's 32 chunks on 2 of them);
+          // the words are rotated once with predicated selects (no branches)
+          const int rot = (lane >> 1) & 3;
 #pragma unroll
-          for (int mm = 0; mm < 4; ++mm) {
-            const int row = mq * 4 + mm;
-            const uint32_t w0 = mm == 0 ? r[0].x : mm == 1 ? r[0].y : mm == 2 ? r[0].z : r[0].w;
-            const uint32_t w1 = mm == 0 ? r[1].x : mm == 1 ? r[1].y : mm == 2 ? r[1].z : r[1].w;
-            const uint32_t w2 = mm == 0 ? r[2].x : mm == 1 ? r[2].y : mm == 2 ? r[2].z : r[2].w;
-            const uint32_t w3 = mm == 0 ? r[3].x : mm == 1 ? r[3].y : mm == 2 ? r[3].z : r[3].w;
+          for (int pp = 0; pp < 4; ++pp) r[pp] = rot4(r[pp], rot);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int row = mq * 4 + ((j + rot) & 3);
+            const uint32_t w0 = j == 0 ? r[0].x : j == 1 ? r[0].y : j == 2 ? r[0].z : r[0].w;
+            const uint32_t w1 = j == 0 ? r[1].x : j == 1 ? r[1].y : j == 2 ? r[1].z : r[1].w;
+            const uint32_t w2 = j == 0 ? r[2].x : j == 1 ? r[2].y : j == 2 ? r[2].z : r[2].w;
+            const uint32_t w3 = j == 0 ? r[3].x : j == 1 ? r[3].y : j == 2 ? r[3].z : r[3].w;
             sts16(sA + (row >> 3) * 1024 + (row & 7) * 128 + ((pq ^ (row & 7)) << 4), make_uint4(w0, w1, w2, w3));
           }
         }
@@ -486,6 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       if (!(p.dbg & 32)) fence_async_smem();
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&full[s]);
+      if (p.trace && blockIdx.x == 0 && t == 0 && it < kTrace) p.trace[4 * kTrace + it] = clock64();
     }
   } else if (warp == kMmaWarp) {
     // ============================ MMA issue ============================
@@ -502,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       for (long long j = 0; j < per_tile; ++j, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
+        if (p.trace && blockIdx.x == 0 && lane == 0 && it < kTrace) p.trace[5 * kTrace + it] = clock64();
         tc_fence_after();
         const uint64_t soff = (uint64_t)((s * S::STAGE) >> 4);
 #pragma unroll
@@ -554,6 +742,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
       const bool row_ok = lane_ok && row < p.m;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
       if (p.dbg & 8) mbar_wait_sleep(&tfull[as], aph); else mbar_wait(&tfull[as], aph);
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && tcount < 8) p.trace[6 * kTrace + 2 * tcount] = clock64();
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN;
       uint32_t v[32];
@@ -583,6 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
           }
         }
       }
+      if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && tcount < 8) p.trace[6 * kTrace + 2 * tcount + 1] = clock64();
     }
   }
   tc_fence_before();
@@ -594,8 +784,27 @@ __global__ void __launch_bounds__(kThreads, 1) brgemm_grouped_kernel(const GPara
 }
 
 template <int BM, int BN, int STAGES>
-static int launch(const GParams& p, cudaStream_t s) {
+static int launch(GParams p, cudaStream_t s) {
   using S = GSmem<BM, BN, STAGES>;
+  CUtensorMap ma, mb;
+  memset(&ma, 0, sizeof(ma));
+  memset(&mb, 0, sizeof(mb));
+  if (p.tma) {
+    const int bmsub = p.gang_ma == 2 ? 64 : BM;
+    const uint64_t R = 1ull << kTmaRowBits;
+    uint64_t da[5] = {(uint64_t)(p.vnni ? 2 * p.m : p.m), R, 1, 1, 1};
+    uint64_t sa[4] = {(uint64_t)(p.vnni ? 4 * p.m : 2 * p.lda), 0, 0, 0};
+    uint32_t ba[5] = {(uint32_t)(p.vnni ? 2 * bmsub : 64), (uint32_t)(p.vnni ? 32 : 64), 1, 1, 1};
+    sa[1] = sa[0] * R; sa[2] = sa[1]; sa[3] = sa[1];
+    int rc = make_tma_map_5d(&ma, p.a, da, sa, ba, p.vnni ? 0 : 128);
+    // B view [rows][ldb / 64][64]: a block may start on any 64-element chunk
+    uint64_t db[5] = {64, (uint64_t)(p.ldb / 64), R, 1, 1};
+    uint64_t sb[4] = {128, (uint64_t)(2 * p.ldb), 0, 0};
+    sb[2] = sb[1] * R; sb[3] = sb[2];
+    uint32_t bb[5] = {64, 1, (uint32_t)p.b_box, 1, 1};
+    if (rc == TPP_OK) rc = make_tma_map_5d(&mb, p.b, db, sb, bb, 128);
+    if (rc != TPP_OK) p.tma = 0;   // (a map the driver rejects: the cp.async path)
+  }
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   auto kern = brgemm_grouped_kernel<BM, BN, STAGES>;
   cudaError_t e = ensure_smem_attr((const void*)kern, S::BYTES);
@@ -612,12 +821,27 @@ static int launch(const GParams& p, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = pdl_allowed();
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, p);
+  e = cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
   if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(brgemm_grouped_kernel)");
   TPP_CUDA_LAUNCH_CHECK("brgemm_grouped_kernel");
+  if (p.trace) {   // probe: dump CTA 0's stamps (cycles from kernel entry)
+    long long h[8 * kTrace];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost);
+    const long long t0 = h[7 * kTrace];
+    fprintf(stderr, "grp trace <%d,%d,%d>: it  prod_ready empty_ok issued | landed full_arr | mma_full\n", BM, BN, STAGES);
+    for (int i = 0; i < kTrace; ++i) {
+      if (h[5 * kTrace + i] == 0) break;
+      fprintf(stderr, "  %3d %7lld %7lld %7lld | %7lld %7lld | %7lld\n", i, h[i] - t0, h[kTrace + i] - t0,
+              h[2 * kTrace + i] - t0, h[3 * kTrace + i] - t0, h[4 * kTrace + i] - t0, h[5 * kTrace + i] - t0);
+    }
+    for (int j = 0; j < 8 && h[6 * kTrace + 2 * j]; ++j)
+      fprintf(stderr, "  tile %d: tfull %lld epi_done %lld\n", j, h[6 * kTrace + 2 * j] - t0, h[6 * kTrace + 2 * j + 1] - t0);
+  }
   set_last_config("brgemm_grouped_kernel<" + std::to_string(BM) + "," + std::to_string(BN) + "," +
                   std::to_string(STAGES) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(ntiles) +
-                  (p.gang_cells ? " gang=" + std::to_string(p.gang_ma) + "x" + std::to_string(p.gang_nb) : ""));
+                  (p.gang_cells ? " gang=" + std::to_string(p.gang_ma) + "x" + std::to_string(p.gang_nb) : "") +
+                  (p.tma ? " tma" : ""));
   return TPP_OK;
 }
 
@@ -665,6 +889,12 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.beta_mode = d->beta == 0.0 ? 0 : d->beta == 1.0 ? 1 : 2;
   static const int dbg = getenv("TPP_GRP_DBG") ? atoi(getenv("TPP_GRP_DBG")) : 0;
   p.dbg = dbg;
+  if (getenv("TPP_GRP_TRACE")) {
+    static long long* tbuf = nullptr;
+    if (!tbuf) cudaMalloc(&tbuf, 8 * kTrace * sizeof(long long));
+    cudaMemsetAsync(tbuf, 0, 8 * kTrace * sizeof(long long), s);
+    p.trace = tbuf;
+  }
   const int BM = gang ? 64 * gang_ma : (d->m <= 64 ? 64 : 128);
   // widest N tile that still gives every SM a tile (one C block of a
   // single brgemm() call is otherwise only a handful of work items)
@@ -675,6 +905,24 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.tiles_m = gang ? 1 : (d->m + BM - 1) / BM;
   p.tiles_n = gang && gang_nb > 1 ? 1 : (d->n + BN - 1) / BN;
   TPP_REQUIRE(tm_all * p.tiles_m * p.tiles_n < (1LL << 31), TPP_E_UNSUPPORTED, "grouped BRGEMM: too many tiles");
+  {
+    // TMA staging: power-of-two row pitches (a block's first row is then a
+    // shift of its offset, checked per stage), whole 64-k chunks, B tiles
+    // that are whole boxes; ADDRESS batches keep the cp.async path
+    static const bool no_tma = getenv("TPP_GRP_NO_TMA") != nullptr;
+    auto pow2 = [](long long v) { return v > 0 && (v & (v - 1)) == 0; };
+    auto lg2 = [](long long v) { int r = 0; while ((1LL << r) < v) ++r; return r; };
+    const long long pa = d->a_vnni ? 2LL * d->m : d->lda;
+    const int bn_sub = gang && gang_nb > 1 ? 64 : BN;
+    const int b_box = d->n < bn_sub ? d->n : bn_sub;
+    const bool ok = !no_tma && kind != 2 && d->k % 64 == 0 && pow2(pa) && pa >= 8 && pow2(d->ldb) && d->ldb >= 64 &&
+                    d->n % 8 == 0 && d->n % b_box == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0 &&
+                    reinterpret_cast<uintptr_t>(b) % 16 == 0;
+    p.tma = ok ? 1 : 0;
+    p.a_shift = lg2(pa);
+    p.b_shift = lg2(d->ldb);
+    p.b_box = b_box;
+  }
   if (BM == 64) {
     if (BN == 64) return launch<64, 64, 8>(p, s);
     if (BN == 128) return launch<64, 128, 6>(p, s);

@@ -429,12 +429,12 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
     const uint32_t slot = i % kTQ, par = (i / kTQ) & 1;
     if (q_remote) mbar_wait_cluster(&tqf[slot], par);
     else mbar_wait(&tqf[slot], par);
-    return *reinterpret_cast<volatile int*>(&tq_ids[slot]);
+    return ld_shared_volatile_s32(smem_u32(&tq_ids[slot]));
   };
   // the leader's producer: publish item i to both CTAs
   auto tq_push = [&](uint32_t i, int t) {
     const uint32_t slot = i % kTQ;
-    *reinterpret_cast<volatile int*>(&tq_ids[slot]) = t;
+    st_shared_volatile_s32(smem_u32(&tq_ids[slot]), t);
     if (PAIR) {
       st_shared_cluster_s32(mapa_shared(smem_u32(&tq_ids[slot]), 1), t);
       mbar_arrive_cluster(mapa_shared(smem_u32(&tqf[slot]), 1));
@@ -1008,7 +1008,7 @@ brgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
           // row `lane`, 16-byte chunk c lands at chunk c ^ ((lane >> 1) & 3) (SWIZZLE_64B)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            *reinterpret_cast<uint4*>(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) = val[c];
+            st_shared_v4(smem_u32(stg + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)), val[c]);
           fence_async_smem();
           __syncwarp();
           ++nstore;
