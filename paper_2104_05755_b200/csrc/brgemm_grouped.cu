@@ -87,6 +87,11 @@ struct GParams {
   int tma;
   int a_shift, b_shift;   // log2 of the A row pitch (VNNI: 2m, PLAIN: lda) and of ldb, in elements
   int b_box;              // B rows per box (a B sub-block or the whole BN tile)
+  // VNNI A through tensor memory (M = 128, TMA mode): a VNNI word (row m,
+  // k pair) is exactly a TMEM cell of the MMA's A operand (lane m, one column
+  // per k pair), so the finisher copies raw words smem -> TMEM (tcgen05.st)
+  // instead of transposing them into a K-major smem tile
+  int tmem_a;
 };
 constexpr int kTrace = 128;   // stages traced
 constexpr int kGangMA = 2, kGangNB = 4;
@@ -188,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[7 * kTrace] = clock64();
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, S::TMEM_COLS);
+  const uint32_t tcols = p.tmem_a ? 512u : (uint32_t)S::TMEM_COLS;   // + STAGES x 32 A columns
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -631,6 +637,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = (int)(it % STAGES);
       if (p.dbg & 8) mbar_wait_sleep(&landed[s], (uint32_t)((it / STAGES) & 1)); else mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
       if (p.trace && blockIdx.x == 0 && t == 0 && it < kTrace) p.trace[3 * kTrace + it] = clock64();
+      if (p.tmem_a) {
+        // row q*32 + lane of the A tile: its 32 k-pair words -> TMEM columns
+        // 2 BN + 32 s .. (lane quarter q = warp % 4)
+        tc_fence_after();
+        const int q = warp & 3, r = q * 32 + lane;
+        const uint32_t sRaw = smem_u32(smem + s * S::STAGE) + S::A_BYTES + S::B_BYTES +
+                              (uint32_t)((r / bmsub) * (32 * bmsub * 4) + (r % bmsub) * 4);
+        uint32_t w[32];
+#pragma unroll
+        for (int kp = 0; kp < 32; ++kp)
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[kp]) : "r"(sRaw + kp * bmsub * 4));
+        tmem_st32(tmem_base + ((uint32_t)(q * 32) << 16) + 2 * BN + s * 32, w);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+        if (p.trace && blockIdx.x == 0 && t == 0 && it < kTrace) p.trace[4 * kTrace + it] = clock64();
+        continue;
+      }
       if (p.vnni && !(p.dbg & 4)) {
         const uint32_t sA = smem_u32(smem + s * S::STAGE), sRaw = sA + S::A_BYTES + S::B_BYTES;
 #pragma unroll
@@ -692,10 +717,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.trace && blockIdx.x == 0 && lane == 0 && it < kTrace) p.trace[5 * kTrace + it] = clock64();
         tc_fence_after();
         const uint64_t soff = (uint64_t)((s * S::STAGE) >> 4);
+        if (p.tmem_a) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (!(p.dbg & 1))
-            umma_f16_warp(tmem_d, a0 + soff + astep * kk, b0 + soff + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_tmem_a_warp(tmem_d, tmem_base + 2 * BN + s * 32 + kk * 8, b0 + soff + 2 * kk, idesc,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            if (!(p.dbg & 1))
+              umma_f16_warp(tmem_d, a0 + soff + astep * kk, b0 + soff + 2 * kk, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+        }
         if (p.dbg & 16) {
           if (lane == 0) mbar_arrive(&empty[s]);
         } else {
@@ -779,13 +811,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, S::TMEM_COLS);
+    tmem_dealloc(tmem_base, tcols);
   }
 }
 
 template <int BM, int BN, int STAGES>
 static int launch(GParams p, cudaStream_t s) {
   using S = GSmem<BM, BN, STAGES>;
+  static const bool no_tmem_a = getenv("TPP_GRP_NO_TMEM_A") != nullptr;
+  p.tmem_a = p.tma && p.vnni && BM == 128 && 2 * BN + STAGES * 32 <= 512 && !no_tmem_a;
   CUtensorMap ma, mb;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
@@ -803,7 +837,7 @@ static int launch(GParams p, cudaStream_t s) {
     sb[2] = sb[1] * R; sb[3] = sb[2];
     uint32_t bb[5] = {64, 1, (uint32_t)p.b_box, 1, 1};
     if (rc == TPP_OK) rc = make_tma_map_5d(&mb, p.b, db, sb, bb, 128);
-    if (rc != TPP_OK) p.tma = 0;   // (a map the driver rejects: the cp.async path)
+    if (rc != TPP_OK) p.tma = p.tmem_a = 0;   // (a map the driver rejects: the cp.async path)
   }
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
   auto kern = brgemm_grouped_kernel<BM, BN, STAGES>;
@@ -841,7 +875,7 @@ static int launch(GParams p, cudaStream_t s) {
   set_last_config("brgemm_grouped_kernel<" + std::to_string(BM) + "," + std::to_string(BN) + "," +
                   std::to_string(STAGES) + "> grid=" + std::to_string(grid) + " tiles=" + std::to_string(ntiles) +
                   (p.gang_cells ? " gang=" + std::to_string(p.gang_ma) + "x" + std::to_string(p.gang_nb) : "") +
-                  (p.tma ? " tma" : ""));
+                  (p.tma ? " tma" : "") + (p.tmem_a ? " tmem_a" : ""));
   return TPP_OK;
 }
 

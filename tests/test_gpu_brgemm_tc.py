@@ -134,7 +134,10 @@ def test_cfg2_composition_grouped(variant):
     tpp.brgemm_grouped(spec, gb, out, [(nb * Kb + kb) * bn * bk for nb, kb in groups])
     # the groups form a full cross product (weight block rows x token blocks):
     # pairs of weight block rows tile together (M = 128 MMAs)
-    assert _lib.last_config().startswith(GROUPED) and "gang=2x1" in _lib.last_config(), _lib.last_config()
+    cfg = _lib.last_config()
+    assert cfg.startswith(GROUPED) and "gang=2x1" in cfg, cfg
+    # STRIDE / OFFSET: TMA staging, VNNI A through tensor memory; ADDRESS: cp.async
+    assert (" tma" in cfg and " tmem_a" in cfg) == (variant != "address"), cfg
     sel = [0, 7, 15]
     _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)   # FP32 pre-narrow
     got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
@@ -171,6 +174,56 @@ def test_gangs_partial_and_wide(variant):
     assert normwise(got, want) <= TOL
     # every block written (the partial gang row / column too)
     assert not torch.isnan(out).any()
+
+
+@pytest.mark.parametrize("case", ["gang_partial", "m128", "plain", "misaligned_stages"])
+def test_tma_staging_modes(case):
+    """The TMA staging paths of the grouped kernel against the oracle:
+    a partial gang (an empty A sub-block) with VNNI A in tensor memory, one
+    M = 128 VNNI block per group (TMEM A, one sub-block), PLAIN A boxes, and
+    an OFFSET batch whose blocks start off a row of the TMA views in some
+    entries (those stages are staged element-wise by their producer warp)
+    while B blocks start mid-row (64-element chunk coordinates, ldb = 256)."""
+    rng = np.random.default_rng(93)
+    vnni = case != "plain"
+    m = 128 if case in ("m128", "plain") else 64
+    n, k, ldb = 64, 128, (256 if case == "misaligned_stages" else 128)
+    groups, cnt = (5, 3) if case == "gang_partial" else (6, 4)
+    lda = m
+    ablk = k * m                       # VNNI [k/2][m][2] or PLAIN [k][lda]
+    bblk = ldb * n
+    a = O.fp32_to_bf16_rne(rng.standard_normal(ablk * (groups * cnt + 2) + 256).astype(np.float32))
+    b = O.fp32_to_bf16_rne(rng.standard_normal(bblk * (groups * cnt + 2) + 256).astype(np.float32))
+    spec = tpp.GemmSpec(m, n, k, lda, ldb, m, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                        a_layout=tpp.ALayout.VNNI if vnni else tpp.ALayout.PLAIN)
+    ad, bd = to_dev(a), to_dev(b)
+    rng2 = np.random.default_rng(94)
+    if case == "gang_partial":
+        # weight block rows kb x token blocks nb (a 5 x 1 cross product of A / B lists -> 3 gangs, the last partial)
+        a_lists = [[(g * cnt + i) * ablk for i in range(cnt)] for g in range(groups)]
+        b_lists = [[i * bblk for i in range(cnt)] for _ in range(groups)]
+    else:
+        a_lists = [[int(rng2.integers(0, groups * cnt)) * ablk for _ in range(cnt)] for _ in range(groups)]
+        b_lists = [[int(rng2.integers(0, groups * cnt)) * bblk for _ in range(cnt)] for _ in range(groups)]
+        if case == "misaligned_stages":
+            a_lists[1][2] += 2          # off the 2m-element rows of the A view
+            b_lists[3][0] += 64         # mid-row B block: chunk coordinate 1
+            b_lists[4][1] += 70         # off any 64-element chunk
+    gb = tpp.GroupedBatch.offset(ad, bd, a_lists, b_lists)
+    out = torch.full((groups * m * n,), float("nan"), dtype=torch.float32, device="cuda")
+    tpp.brgemm_grouped(spec, gb, out, [g * m * n for g in range(groups)])
+    cfg = _lib.last_config()
+    assert cfg.startswith(GROUPED) and " tma" in cfg, cfg
+    if vnni and case != "misaligned_stages":
+        assert " tmem_a" in cfg, cfg
+    if case == "gang_partial":
+        assert "gang=2x1" in cfg, cfg
+    got = to_host(out).reshape(groups, n, m)
+    for g in range(groups):
+        ab = [O.load_a(a, off, m, k, lda, "bf16", vnni=vnni) for off in a_lists[g]]
+        bb = [O.load_b(b, off, k, n, ldb, "bf16") for off in b_lists[g]]
+        want = O.brgemm(ab, bb, np.zeros((m, n), np.float32), 0.0, "bf16")
+        assert normwise(got[g].T, want) <= TOL, (case, g)
 
 
 @pytest.mark.parametrize("beta", [0.0, 1.0, 0.5])
