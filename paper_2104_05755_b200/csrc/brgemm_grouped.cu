@@ -96,12 +96,14 @@ struct GParams {
 constexpr int kTrace = 128;   // stages traced
 constexpr int kGangMA = 2, kGangNB = 4;
 
-constexpr int kIdxChunk = 256;
-constexpr int kTmaRowBits = 30;  // rows of the TMA maps' 2-D views of a / b   // batch entries whose indices sit in smem at a time
+constexpr int kIdxChunk = 256;  // batch entries whose indices sit in smem at a time
+constexpr int kTmaRowBits = 30;  // rows of the TMA maps' 2-D views of a / b
 
-template <int BM, int BN, int STAGES>
+// TA: VNNI A through tensor memory -- no K-major A tile in the stage, so
+// deeper rings fit
+template <int BM, int BN, int STAGES, bool TA = false>
 struct GSmem {
-  static constexpr int A_BYTES = BM * 128;  // BM rows x 64 k (bf16)
+  static constexpr int A_BYTES = TA ? 0 : BM * 128;  // BM rows x 64 k (bf16)
   static constexpr int B_BYTES = BN * 128;
   static constexpr int RAW_BYTES = BM * 128;  // VNNI A as loaded, before the word transpose
   static constexpr int STAGE = A_BYTES + B_BYTES + RAW_BYTES;
@@ -161,11 +163,11 @@ struct StageIt {
   int kc;
 };
 
-template <int BM, int BN, int STAGES>
+template <int BM, int BN, int STAGES, bool TA>
 __global__ void __launch_bounds__(kThreads, 1)
     brgemm_grouped_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           const GParams p) {
-  using S = GSmem<BM, BN, STAGES>;
+  using S = GSmem<BM, BN, STAGES, TA>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -193,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_mbar_init();
   }
   if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[7 * kTrace] = clock64();
-  const uint32_t tcols = p.tmem_a ? 512u : (uint32_t)S::TMEM_COLS;   // + STAGES x 32 A columns
+  const uint32_t tcols = TA ? 512u : (uint32_t)S::TMEM_COLS;   // + STAGES x 32 A columns
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
@@ -491,6 +493,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       // revolutions ahead of the MMA, where the parity wait is ambiguous)
       constexpr int kRR = kProdWarps < STAGES ? kProdWarps : STAGES;
       const int w = warp - kProdWarp0;
+      if (lane == 0) {
+        prefetch_tmap(&tmA);
+        prefetch_tmap(&tmB);
+      }
       if (w >= kRR) cur.tile = ntiles;
       for (int j = 0; j < w && cur.tile < ntiles; ++j) { advance(cur); ++it; }
       const int asub = p.gang_ma == 2 ? 2 : 1, bsub = bsplit ? p.gang_nb : 1;
@@ -637,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int s = (int)(it % STAGES);
       if (p.dbg & 8) mbar_wait_sleep(&landed[s], (uint32_t)((it / STAGES) & 1)); else mbar_wait(&landed[s], (uint32_t)((it / STAGES) & 1));
       if (p.trace && blockIdx.x == 0 && t == 0 && it < kTrace) p.trace[3 * kTrace + it] = clock64();
-      if (p.tmem_a) {
+      if (TA) {
         // row q*32 + lane of the A tile: its 32 k-pair words -> TMEM columns
         // 2 BN + 32 s .. (lane quarter q = warp % 4)
         tc_fence_after();
@@ -717,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (p.trace && blockIdx.x == 0 && lane == 0 && it < kTrace) p.trace[5 * kTrace + it] = clock64();
         tc_fence_after();
         const uint64_t soff = (uint64_t)((s * S::STAGE) >> 4);
-        if (p.tmem_a) {
+        if (TA) {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             umma_f16_tmem_a_warp(tmem_d, tmem_base + 2 * BN + s * 32 + kk * 8, b0 + soff + 2 * kk, idesc,
@@ -782,6 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ch = 0; ch < BN / 32; ++ch) {
         tmem_ld32(tacc + ch * 32, v);
         tmem_ld_wait();
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && tcount == 0 && ch < 8) p.trace[6 * kTrace + 32 + ch] = clock64();
         if (ch == BN / 32 - 1) {
           tc_fence_before();
           __syncwarp();
@@ -791,7 +798,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nbc = bsplit ? ch >> 1 : 0;
         float* cg = nbc == 0 ? cgs[0] : nbc == 1 ? cgs[1] : nbc == 2 ? cgs[2] : cgs[3];
         const int col0 = bsplit ? (ch & 1) * 32 : tn * BN + ch * 32;
-        if (row_ok && cg != nullptr) {
+        if (row_ok && cg != nullptr && p.beta_mode == 0 && col0 + 32 <= p.n) {
+          // whole chunk, beta = 0: 32 independent stores (one basic block;
+          // a per-store beta / bounds branch serialised them, ~45 cycles each)
+          float* dst = cg + row + (long long)col0 * p.ldc;
+          const long long ld = p.ldc;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dst[i * ld] = __uint_as_float(v[i]);
+        } else if (row_ok && cg != nullptr) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = col0 + i;
@@ -815,11 +829,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BM, int BN, int STAGES>
+template <int BM, int BN, int STAGES, bool TA = false>
 static int launch(GParams p, cudaStream_t s) {
-  using S = GSmem<BM, BN, STAGES>;
-  static const bool no_tmem_a = getenv("TPP_GRP_NO_TMEM_A") != nullptr;
-  p.tmem_a = p.tma && p.vnni && BM == 128 && 2 * BN + STAGES * 32 <= 512 && !no_tmem_a;
+  using S = GSmem<BM, BN, STAGES, TA>;
+  static_assert(!TA || (BM == 128 && 2 * BN + STAGES * 32 <= 512), "TMEM: accumulators + A stages");
+  p.tmem_a = TA;
   CUtensorMap ma, mb;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
@@ -837,10 +851,10 @@ static int launch(GParams p, cudaStream_t s) {
     sb[2] = sb[1] * R; sb[3] = sb[2];
     uint32_t bb[5] = {64, 1, (uint32_t)p.b_box, 1, 1};
     if (rc == TPP_OK) rc = make_tma_map_5d(&mb, p.b, db, sb, bb, 128);
-    if (rc != TPP_OK) p.tma = p.tmem_a = 0;   // (a map the driver rejects: the cp.async path)
+    if (rc != TPP_OK) p.tma = 0;   // (a map the driver rejects: the cp.async path)
   }
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
-  auto kern = brgemm_grouped_kernel<BM, BN, STAGES>;
+  auto kern = brgemm_grouped_kernel<BM, BN, STAGES, TA>;
   cudaError_t e = ensure_smem_attr((const void*)kern, S::BYTES);
   if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(brgemm_grouped_kernel)");
   const long long ntiles = p.gang_cells ? (long long)p.ngangs * p.tiles_n : p.groups * p.tiles_m * p.tiles_n;
@@ -869,6 +883,7 @@ static int launch(GParams p, cudaStream_t s) {
       fprintf(stderr, "  %3d %7lld %7lld %7lld | %7lld %7lld | %7lld\n", i, h[i] - t0, h[kTrace + i] - t0,
               h[2 * kTrace + i] - t0, h[3 * kTrace + i] - t0, h[4 * kTrace + i] - t0, h[5 * kTrace + i] - t0);
     }
+    for (int c = 0; c < 8 && h[6 * kTrace + 32 + c]; ++c) fprintf(stderr, "  tile 0 chunk %d loaded %lld\n", c, h[6 * kTrace + 32 + c] - t0);
     for (int j = 0; j < 8 && h[6 * kTrace + 2 * j]; ++j)
       fprintf(stderr, "  tile %d: tfull %lld epi_done %lld\n", j, h[6 * kTrace + 2 * j] - t0, h[6 * kTrace + 2 * j + 1] - t0);
   }
@@ -961,6 +976,11 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
     if (BN == 64) return launch<64, 64, 8>(p, s);
     if (BN == 128) return launch<64, 128, 6>(p, s);
     return launch<64, 256, 4>(p, s);
+  }
+  static const bool no_tmem_a = getenv("TPP_GRP_NO_TMEM_A") != nullptr;
+  if (p.vnni && BN <= 128 && !no_tmem_a) {   // VNNI A through tensor memory, deeper rings
+    if (BN == 64) return launch<128, 64, 8, true>(p, s);
+    return launch<128, 128, 6, true>(p, s);
   }
   if (BN == 64) return launch<128, 64, 5>(p, s);
   if (BN == 128) return launch<128, 128, 4>(p, s);

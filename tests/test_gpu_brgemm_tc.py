@@ -136,8 +136,8 @@ def test_cfg2_composition_grouped(variant):
     # pairs of weight block rows tile together (M = 128 MMAs)
     cfg = _lib.last_config()
     assert cfg.startswith(GROUPED) and "gang=2x1" in cfg, cfg
-    # STRIDE / OFFSET: TMA staging, VNNI A through tensor memory; ADDRESS: cp.async
-    assert (" tma" in cfg and " tmem_a" in cfg) == (variant != "address"), cfg
+    # VNNI A through tensor memory; STRIDE / OFFSET: TMA staging, ADDRESS: cp.async
+    assert " tmem_a" in cfg and (" tma" in cfg) == (variant != "address"), cfg
     sel = [0, 7, 15]
     _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)   # FP32 pre-narrow
     got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
