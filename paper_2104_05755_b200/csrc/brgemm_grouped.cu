@@ -87,6 +87,7 @@ struct GParams {
   int tma;
   int a_shift, b_shift;   // log2 of the A row pitch (VNNI: 2m, PLAIN: lda) and of ldb, in elements
   int b_box;              // B rows per box (a B sub-block or the whole BN tile)
+  int a_rbits, b_rbits;   // log2 of the views' row counts
   // VNNI A through tensor memory (M = 128, TMA mode): a VNNI word (row m,
   // k pair) is exactly a TMEM cell of the MMA's A operand (lane m, one column
   // per k pair), so the finisher copies raw words smem -> TMEM (tcgen05.st)
@@ -97,7 +98,7 @@ constexpr int kTrace = 128;   // stages traced
 constexpr int kGangMA = 2, kGangNB = 4;
 
 constexpr int kIdxChunk = 256;  // batch entries whose indices sit in smem at a time
-constexpr int kTmaRowBits = 30;  // rows of the TMA maps' 2-D views of a / b
+constexpr int kTmaRowBits = 30;  // rows of the TMA maps' 2-D views of a / b (at most; strides stay < 2^39 B)
 
 // TA: VNNI A through tensor memory -- no K-major A tile in the stage, so
 // deeper rings fit
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int nb = 0; nb < kGangNB; ++nb) bchunk = max(bchunk, ((boff[nb] & ((1LL << p.b_shift) - 1)) >> 6) + p.kchunks);
         const bool rows_ok = ((am & ((1LL << p.a_shift) - 1)) | (bm & 63)) == 0 && bchunk <= (1LL << (p.b_shift - 6)) &&
-                             (am >> (p.a_shift + kTmaRowBits)) == 0 && (bm >> (p.b_shift + kTmaRowBits)) == 0;
+                             (am >> (p.a_shift + p.a_rbits)) == 0 && (bm >> (p.b_shift + p.b_rbits)) == 0;
         if (trw && it < kTrace) p.trace[0 * kTrace + it] = clock64();
         mbar_wait(&empty[s], ph ^ 1);
         if (trw && it < kTrace) p.trace[1 * kTrace + it] = clock64();
@@ -839,16 +840,22 @@ static int launch(GParams p, cudaStream_t s) {
   memset(&mb, 0, sizeof(mb));
   if (p.tma) {
     const int bmsub = p.gang_ma == 2 ? 64 : BM;
-    const uint64_t R = 1ull << kTmaRowBits;
+    // row counts: 2^30 at most, and the outer strides (rows x pitch) < 2^39 B
+    auto rbits = [](uint64_t pitch) { int b = kTmaRowBits; while (b > 0 && (pitch << b) >= (1ull << 39)) --b; return b; };
+    const uint64_t pa = (uint64_t)(p.vnni ? 4 * p.m : 2 * p.lda), pb = (uint64_t)(2 * p.ldb);
+    p.a_rbits = rbits(pa);
+    p.b_rbits = rbits(pb);
+    const uint64_t R = 1ull << p.a_rbits;
     uint64_t da[5] = {(uint64_t)(p.vnni ? 2 * p.m : p.m), R, 1, 1, 1};
-    uint64_t sa[4] = {(uint64_t)(p.vnni ? 4 * p.m : 2 * p.lda), 0, 0, 0};
+    uint64_t sa[4] = {pa, 0, 0, 0};
     uint32_t ba[5] = {(uint32_t)(p.vnni ? 2 * bmsub : 64), (uint32_t)(p.vnni ? 32 : 64), 1, 1, 1};
     sa[1] = sa[0] * R; sa[2] = sa[1]; sa[3] = sa[1];
     int rc = make_tma_map_5d(&ma, p.a, da, sa, ba, p.vnni ? 0 : 128);
     // B view [rows][ldb / 64][64]: a block may start on any 64-element chunk
-    uint64_t db[5] = {64, (uint64_t)(p.ldb / 64), R, 1, 1};
-    uint64_t sb[4] = {128, (uint64_t)(2 * p.ldb), 0, 0};
-    sb[2] = sb[1] * R; sb[3] = sb[2];
+    const uint64_t RB = 1ull << p.b_rbits;
+    uint64_t db[5] = {64, (uint64_t)(p.ldb / 64), RB, 1, 1};
+    uint64_t sb[4] = {128, pb, 0, 0};
+    sb[2] = sb[1] * RB; sb[3] = sb[2];
     uint32_t bb[5] = {64, 1, (uint32_t)p.b_box, 1, 1};
     if (rc == TPP_OK) rc = make_tma_map_5d(&mb, p.b, db, sb, bb, 128);
     if (rc != TPP_OK) p.tma = 0;   // (a map the driver rejects: the cp.async path)
