@@ -360,6 +360,12 @@ class GroupedBatch:
         count = len(a[0]) if a else 0
         if any(len(x) != count for x in a):
             raise TensorError("every group needs the same batch length")
+        # every A block in one buffer and every B block in one buffer: the
+        # same blocks as offsets from those bases (the kernel's TMA staging
+        # needs a base to build its views on; raw pointers get cp.async)
+        if count and all(r[0] is a[0][0][0] for row in a for r in row) and \
+                all(r[0] is b[0][0][0] for row in b for r in row):
+            return GroupedBatch(BatchKind.OFFSET, a, b, count)
         return GroupedBatch(BatchKind.ADDRESS, a, b, count)
 
     @staticmethod

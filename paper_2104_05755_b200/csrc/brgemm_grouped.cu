@@ -521,29 +521,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // element offsets of the live blocks
+        // element offsets of the live blocks (OFFSET: loads issued before
+        // the slot wait, used after it)
         long long aoff[kGangMA], boff[kGangNB];
-        long long am = 0, bm = 0;
-        const uint16_t* any = nullptr;
 #pragma unroll
         for (int ma = 0; ma < kGangMA; ++ma) {
           const int g = ma == 0 ? ga[0] : ga[1];
-          aoff[ma] = 0;
-          if (g >= 0) {
-            aoff[ma] = p.kind == 0 ? abase[ma] + cur.i * p.stride_a : __ldg(p.a_idx + (long long)g * p.count + cur.i);
-            am |= aoff[ma];
-            any = p.a + aoff[ma];
-          }
+          aoff[ma] = g < 0 ? 0
+                     : p.kind == 0 ? abase[ma] + cur.i * p.stride_a
+                                   : __ldg(p.a_idx + (long long)g * p.count + cur.i);
         }
 #pragma unroll
         for (int nb = 0; nb < kGangNB; ++nb) {
           const int g = nb == 0 ? gb[0] : nb == 1 ? gb[1] : nb == 2 ? gb[2] : gb[3];
-          boff[nb] = 0;
-          if (g >= 0) {
-            boff[nb] = p.kind == 0 ? bbase[nb] + cur.i * p.stride_b : __ldg(p.b_idx + (long long)g * p.count + cur.i);
-            bm |= boff[nb];
-          }
+          boff[nb] = g < 0 ? 0
+                     : p.kind == 0 ? bbase[nb] + cur.i * p.stride_b
+                                   : __ldg(p.b_idx + (long long)g * p.count + cur.i);
         }
+        if (trw && it < kTrace) p.trace[0 * kTrace + it] = clock64();
+        mbar_wait(&empty[s], ph ^ 1);
+        if (trw && it < kTrace) p.trace[1 * kTrace + it] = clock64();
+        long long am = 0, bm = 0;
+        const uint16_t* any = nullptr;
+#pragma unroll
+        for (int ma = 0; ma < kGangMA; ++ma)
+          if ((ma == 0 ? ga[0] : ga[1]) >= 0) {
+            am |= aoff[ma];
+            any = p.a + aoff[ma];
+          }
+#pragma unroll
+        for (int nb = 0; nb < kGangNB; ++nb) bm |= boff[nb];
         // A blocks start on a row of the A view; B blocks on a 64-element
         // chunk of a row of the B view [rows][ldb / 64][64], with the k
         // chunks inside the row
@@ -552,9 +559,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int nb = 0; nb < kGangNB; ++nb) bchunk = max(bchunk, ((boff[nb] & ((1LL << p.b_shift) - 1)) >> 6) + p.kchunks);
         const bool rows_ok = ((am & ((1LL << p.a_shift) - 1)) | (bm & 63)) == 0 && bchunk <= (1LL << (p.b_shift - 6)) &&
                              (am >> (p.a_shift + p.a_rbits)) == 0 && (bm >> (p.b_shift + p.b_rbits)) == 0;
-        if (trw && it < kTrace) p.trace[0 * kTrace + it] = clock64();
-        mbar_wait(&empty[s], ph ^ 1);
-        if (trw && it < kTrace) p.trace[1 * kTrace + it] = clock64();
         uint8_t* stage = smem + s * S::STAGE;
         if (rows_ok) {
           if (lane == 0) {

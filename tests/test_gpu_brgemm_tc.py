@@ -106,7 +106,7 @@ def test_conv_offset_fixture_grouped_and_single(golden):
     assert torch.equal(out, single)   # same kernel, same per-tile order
 
 
-@pytest.mark.parametrize("variant", ["stride", "offset", "address"])
+@pytest.mark.parametrize("variant", ["stride", "offset", "address", "address_two_buffers"])
 def test_cfg2_composition_grouped(variant):
     """BASELINE cfg 2 composed from the BRGEMM TPP the way the reference's
     fc_forward does (kernels.py:312-329): 256 C blocks (token block nb x
@@ -127,17 +127,23 @@ def test_cfg2_composition_grouped(variant):
     elif variant == "offset":
         gb = tpp.GroupedBatch.offset(wd, xd, [[(kb * Cb + i) * blk for i in range(Cb)] for _, kb in groups],
                                      [[(nb * Cb + i) * blk for i in range(Cb)] for nb, _ in groups])
-    else:
+    elif variant == "address":
         gb = tpp.GroupedBatch.address([[(wd, (kb * Cb + i) * blk) for i in range(Cb)] for _, kb in groups],
                                       [[(xd, (nb * Cb + i) * blk) for i in range(Cb)] for nb, _ in groups])
+    else:   # B blocks from two buffers: raw pointers (cp.async staging)
+        xd2 = xd.clone()
+        gb = tpp.GroupedBatch.address([[(wd, (kb * Cb + i) * blk) for i in range(Cb)] for _, kb in groups],
+                                      [[(xd2 if (nb + i) % 2 else xd, (nb * Cb + i) * blk) for i in range(Cb)]
+                                       for nb, _ in groups])
     out = torch.empty(Nb * Kb * bn * bk, dtype=torch.float32, device="cuda")
     tpp.brgemm_grouped(spec, gb, out, [(nb * Kb + kb) * bn * bk for nb, kb in groups])
     # the groups form a full cross product (weight block rows x token blocks):
     # pairs of weight block rows tile together (M = 128 MMAs)
     cfg = _lib.last_config()
     assert cfg.startswith(GROUPED) and "gang=2x1" in cfg, cfg
-    # VNNI A through tensor memory; STRIDE / OFFSET: TMA staging, ADDRESS: cp.async
-    assert " tmem_a" in cfg and (" tma" in cfg) == (variant != "address"), cfg
+    # VNNI A through tensor memory, TMA staging (ADDRESS blocks all in one
+    # buffer per operand run as offsets from it)
+    assert " tmem_a" in cfg and (" tma" in cfg) == (variant != "address_two_buffers"), cfg
     sel = [0, 7, 15]
     _, _, want = O.fc_forward_bf16(x, wv, None, activation=None, nb_sel=sel)   # FP32 pre-narrow
     got = to_host(out).reshape(Nb, Kb, bn, bk)[sel]
