@@ -133,6 +133,20 @@ int tpp_brgemm_grouped_gang(const tpp_gemm_desc* d, int32_t kind, const void* a,
                             const int64_t* b_index, int64_t count, void* c, const int64_t* c_offsets,
                             int64_t groups, const int32_t* gang, int32_t ngangs, int32_t gang_m,
                             int32_t gang_n, void* stream);
+/* tpp_brgemm_grouped(_gang) with the C blocks emitted in BF16 (beta = 0): the
+ * FP32 accumulator of each element is narrowed RNE with the reference's NaN
+ * rule (dtypes.py:82-97) -- the same bits as an FP32 call followed by
+ * tpp_convert -- and block column v goes to column (v / col_period) *
+ * col_keep + v % col_period of the output block at c_bf16 + c_offsets[g]
+ * (column stride ldc), dropped when v % col_period >= col_keep.  This is the
+ * conv composition's tail (kernels.py conv: padded-width rows of Wp virtual
+ * columns, Q kept) fused into the BRGEMM epilogue; col_period = col_keep =
+ * n keeps every column.  gang may be null (ungrouped tiling). */
+int tpp_brgemm_grouped_bf16(const tpp_gemm_desc* d, int32_t kind, const void* a, const void* b,
+                            int64_t stride_a, int64_t stride_b, const int64_t* a_index,
+                            const int64_t* b_index, int64_t count, void* c_bf16, const int64_t* c_offsets,
+                            int64_t groups, const int32_t* gang, int32_t ngangs, int32_t gang_m,
+                            int32_t gang_n, int32_t col_period, int32_t col_keep, void* stream);
 /* Many independent stride-BRGEMMs in one launch (the GPU form of the
  * reference's `threads=` job loop over disjoint C tiles, contraction.py:317-322
  * and kernels.py:323-329): instance j uses a + j*inst_a, b + j*inst_b,

@@ -70,6 +70,8 @@ _SIGS = {
                                      _I64, _P]),
     "tpp_brgemm_grouped_gang": (C.c_int, [C.POINTER(GemmDescC), _I32, _P, _P, _I64, _I64, _P, _P, _I64, _P, _P,
                                           _I64, _P, _I32, _I32, _I32, _P]),
+    "tpp_brgemm_grouped_bf16": (C.c_int, [C.POINTER(GemmDescC), _I32, _P, _P, _I64, _I64, _P, _P, _I64, _P, _P,
+                                          _I64, _P, _I32, _I32, _I32, _I32, _I32, _P]),
     "tpp_brgemm_stride_batched": (C.c_int, [C.POINTER(GemmDescC), _P, _P, _I64, _I64, _I64, _P,
                                             _I64, _I64, _I64, _I64, _P]),
     "tpp_fc_packed_weight_bytes": (C.c_int64, [C.POINTER(FcDescC)]),

@@ -88,6 +88,13 @@ struct GParams {
   int a_shift, b_shift;   // log2 of the A row pitch (VNNI: 2m, PLAIN: lda) and of ldb, in elements
   int b_box;              // B rows per box (a B sub-block or the whole BN tile)
   int a_rbits, b_rbits;   // log2 of the views' row counts
+  // BF16 output (beta = 0): C emitted RNE-narrowed (dtypes.py:82-97) at
+  // c16 + c_off, block column v -> column (v / col_period) * col_keep +
+  // v % col_period, dropped when v % col_period >= col_keep (the conv
+  // composition's padded-width rows; col_period = n keeps all)
+  uint16_t* c16;
+  int col_period, col_keep;
+  unsigned col_magic;   // ceil(2^32 / col_period): v / col_period = umulhi(v, magic) for the block's columns
   // VNNI A through tensor memory (M = 128, TMA mode): a VNNI word (row m,
   // k pair) is exactly a TMEM cell of the MMA's A operand (lane m, one column
   // per k pair), so the finisher copies raw words smem -> TMEM (tcgen05.st)
@@ -762,6 +769,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int tm, tn, row;
       // C blocks of this lane's row: one per B sub-block (gangs) or the group's
       float* cgs[kGangNB] = {nullptr, nullptr, nullptr, nullptr};
+      // (BF16 output: the same pointers carry uint16_t element offsets)
+      auto cptr = [&](long long off) -> float* {
+        return p.c16 ? reinterpret_cast<float*>(p.c16 + off) : p.c + off;
+      };
       if (p.gang_cells) {
         const int j = tile / p.tiles_n;
         tn = tile - j * p.tiles_n;
@@ -771,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int nb = 0; nb < kGangNB; ++nb) {
           const int cell = nb < p.gang_nb && ma < p.gang_ma ? __ldg(p.gang_cells + (j * p.gang_ma + ma) * p.gang_nb + nb)
                                                             : -1;
-          cgs[nb] = cell >= 0 ? p.c + (p.c_off ? p.c_off[cell] : 0) : nullptr;
+          cgs[nb] = cell >= 0 ? cptr(p.c_off ? p.c_off[cell] : 0) : nullptr;
         }
       } else {
         const int per_g = p.tiles_m * p.tiles_n;
@@ -780,7 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tm = rem / p.tiles_n;
         tn = rem - tm * p.tiles_n;
         row = tm * BM + lrow;
-        cgs[0] = p.c + (p.c_off ? p.c_off[g] : 0);
+        cgs[0] = cptr(p.c_off ? p.c_off[g] : 0);
       }
       const bool row_ok = lane_ok && row < p.m;
       const uint32_t as = tcount & 1, aph = (tcount >> 1) & 1;
@@ -803,7 +814,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nbc = bsplit ? ch >> 1 : 0;
         float* cg = nbc == 0 ? cgs[0] : nbc == 1 ? cgs[1] : nbc == 2 ? cgs[2] : cgs[3];
         const int col0 = bsplit ? (ch & 1) * 32 : tn * BN + ch * 32;
-        if (row_ok && cg != nullptr && p.beta_mode == 0 && col0 + 32 <= p.n) {
+        if (p.c16) {
+          if (row_ok && cg != nullptr) {
+            // straight-line: per column a multiply-high division and a
+            // predicated 2-byte store (a branch per column serialised them)
+            uint16_t* cb = reinterpret_cast<uint16_t*>(cg) + row;
+            const unsigned per = (unsigned)p.col_period, keep = (unsigned)p.col_keep, nn = (unsigned)p.n;
+            const unsigned r0 = __umulhi((unsigned)col0, p.col_magic), c0 = (unsigned)col0 - r0 * per;
+            if (c0 + 32 <= keep && (unsigned)col0 + 32 <= nn) {
+              // the chunk inside one kept row segment: columns map linearly
+              uint16_t* dst = cb + (long long)(r0 * keep + c0) * p.ldc;
+              const long long ld = p.ldc;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) dst[i * ld] = f32_to_bf16(__uint_as_float(v[i]));
+            } else
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const unsigned vc = (unsigned)col0 + i;
+              const unsigned orow = __umulhi(vc, p.col_magic);
+              const unsigned ocol = vc - orow * per;
+              const int ok = vc < nn && ocol < keep;
+              uint16_t* dst = cb + (long long)(orow * keep + ocol) * p.ldc;
+              const uint16_t hv = f32_to_bf16(__uint_as_float(v[i]));
+              asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, 0;\n\t@q st.global.u16 [%0], %1;\n\t}"
+                           ::"l"(dst), "h"(hv), "r"(ok) : "memory");
+            }
+          }
+        } else if (row_ok && cg != nullptr && p.beta_mode == 0 && col0 + 32 <= p.n) {
           // whole chunk, beta = 0: 32 independent stores (one basic block;
           // a per-store beta / bounds branch serialised them, ~45 cycles each)
           float* dst = cg + row + (long long)col0 * p.ldc;
@@ -911,7 +948,7 @@ static int launch(GParams p, cudaStream_t s) {
 int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const void* b, int64_t stride_a,
                       int64_t stride_b, const int64_t* a_idx, const int64_t* b_idx, int64_t count, void* c,
                       const int64_t* c_off, int64_t groups, cudaStream_t s, const int32_t* gang, int ngangs,
-                      int gang_ma, int gang_nb) {
+                      int gang_ma, int gang_nb, void* c_bf16, int col_period, int col_keep) {
   using namespace grp;
   if (d->in_dtype != TPP_BF16 || count < 1 || groups < 1) return 1;
   GParams p{};
@@ -942,6 +979,13 @@ int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const voi
   p.b_idx = reinterpret_cast<const long long*>(b_idx);
   p.count = count;
   p.c = reinterpret_cast<float*>(c);
+  p.c16 = reinterpret_cast<uint16_t*>(c_bf16);
+  p.col_period = col_period > 0 ? col_period : d->n;
+  p.col_keep = col_keep > 0 ? col_keep : p.col_period;
+  p.col_magic = (unsigned)((0x100000000ull + (unsigned long long)p.col_period - 1) / (unsigned long long)p.col_period);
+  TPP_REQUIRE(!c_bf16 || (long long)d->n * p.col_period < (1LL << 31), TPP_E_UNSUPPORTED,
+              "BF16 output column map: n x col_period < 2^31");
+  TPP_REQUIRE(!c_bf16 || d->beta == 0.0, TPP_E_TENSOR, "BF16 output needs beta = 0");
   p.c_off = reinterpret_cast<const long long*>(c_off);
   p.groups = groups;
   p.kchunks = (d->k + 63) / 64;

@@ -211,6 +211,30 @@ int tpp_brgemm_grouped_gang(const tpp_gemm_desc* d, int32_t kind, const void* a,
   return fail(TPP_E_UNSUPPORTED, "grouped BRGEMM: BF16 inputs and count >= 1");
 }
 
+int tpp_brgemm_grouped_bf16(const tpp_gemm_desc* d, int32_t kind, const void* a, const void* b, int64_t stride_a,
+                            int64_t stride_b, const int64_t* a_index, const int64_t* b_index, int64_t count,
+                            void* c_bf16, const int64_t* c_offsets, int64_t groups, const int32_t* gang,
+                            int32_t ngangs, int32_t gang_m, int32_t gang_n, int32_t col_period, int32_t col_keep,
+                            void* stream) {
+  int rc = check_gemm(d);
+  if (rc) return rc;
+  TPP_REQUIRE(kind >= 0 && kind <= 2, TPP_E_TENSOR, "batch kind must be 0 STRIDE, 1 OFFSET or 2 ADDRESS");
+  TPP_REQUIRE(count >= 1 && groups >= 1 && c_bf16 && (groups == 1 || c_offsets), TPP_E_TENSOR,
+              "grouped BRGEMM (BF16 out) needs count >= 1, an output and per-group C offsets");
+  TPP_REQUIRE(kind == 0 || (a_index && b_index), TPP_E_TENSOR, "null offset / pointer arrays");
+  TPP_REQUIRE(!gang || ngangs >= 1, TPP_E_TENSOR, "empty gang table");
+  TPP_REQUIRE(col_period >= 1 && col_keep >= 1 && col_keep <= col_period, TPP_E_TENSOR,
+              "column map: 1 <= col_keep <= col_period");
+  TPP_REQUIRE(d->beta == 0.0, TPP_E_TENSOR, "BF16 output needs beta = 0");
+  TPP_REQUIRE(d->engine != TPP_ENGINE_ORDERED && d->in_dtype == TPP_BF16, TPP_E_UNSUPPORTED,
+              "grouped BRGEMM runs the BF16 tensor-core engine");
+  const int r = brgemm_grouped_tc(d, kind, a, b, stride_a, stride_b, a_index, b_index, count, nullptr, c_offsets,
+                                  groups, as_stream(stream), gang, gang ? ngangs : 0, gang ? gang_m : 1,
+                                  gang ? gang_n : 1, c_bf16, col_period, col_keep);
+  if (r != 1) return r;
+  return fail(TPP_E_UNSUPPORTED, "grouped BRGEMM: BF16 inputs and count >= 1");
+}
+
 int tpp_brgemm_stride_batched(const tpp_gemm_desc* d, const void* a, const void* b,
                               int64_t stride_a, int64_t stride_b, int64_t count, void* c,
                               int64_t instances, int64_t inst_a, int64_t inst_b, int64_t inst_c,

@@ -72,7 +72,8 @@ unsigned long long* debug_timestamps();
 int brgemm_grouped_tc(const tpp_gemm_desc* d, int kind, const void* a, const void* b, int64_t stride_a,
                       int64_t stride_b, const int64_t* a_idx, const int64_t* b_idx, int64_t count, void* c,
                       const int64_t* c_off, int64_t groups, cudaStream_t s, const int32_t* gang = nullptr,
-                      int ngangs = 0, int gang_ma = 1, int gang_nb = 1);
+                      int ngangs = 0, int gang_ma = 1, int gang_nb = 1, void* c_bf16 = nullptr,
+                      int col_period = 0, int col_keep = 0);
 // brgemm_i8.cu (K10): INT8 STRIDE BRGEMM on tcgen05 kind::i8; 1 = not applicable
 int brgemm_i8_stride_tc(int m, int n, int k, const int8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
                         int64_t stride_a, int64_t stride_b, int64_t count, int32_t* c, int64_t ldc, double beta,

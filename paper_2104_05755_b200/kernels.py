@@ -19,6 +19,7 @@ plus the B200 layer objects the paper's drivers become on a GPU:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 import math
 from typing import Optional
@@ -431,6 +432,11 @@ class ConvSpec:
         return 2 * self.n * self.p * self.q * self.c_b * self.bc * self.k_b * self.bk * self.r * self.s
 
 
+# TPP_CONV_FP32_TAIL=1: the generic conv writes FP32 accumulators and narrows
+# them in a separate tpp_convert pass (the reference's two steps; A/B)
+_CONV_FP32_TAIL = bool(os.environ.get("TPP_CONV_FP32_TAIL"))
+
+
 class _OffsetConv:
     """One offset-BRGEMM convolution (the reference composition) on the
     tensor cores.  Batch entries = taps (r, s) x input channel blocks cb, in
@@ -474,6 +480,9 @@ class _OffsetConv:
         self.a_idx = torch.from_numpy(np.ascontiguousarray(a_off.reshape(-1), dtype=np.int64)).to(device)
         self.b_idx = torch.from_numpy(np.ascontiguousarray(b_off.reshape(-1), dtype=np.int64)).to(device)
         self.c_off = torch.from_numpy(np.ascontiguousarray(c_off, dtype=np.int64)).to(device)
+        # the same blocks in the BF16 output [planes][P][Q*64] (the fused
+        # epilogue drops the Wp - Q columns past each row's end)
+        self.c_off16 = torch.from_numpy(np.ascontiguousarray(c_off // wp * q, dtype=np.int64)).to(device)
         self.planes = n * co_b
         self.acc_elems = n * co_b * p * wp * 64
         # output-channel blocks share B lists, output rows share A lists: pairs
@@ -487,10 +496,20 @@ class _OffsetConv:
 
     def run(self, w_vnni: torch.Tensor, xpad: torch.Tensor, out_bf16: torch.Tensor, stream=None) -> None:
         lib = _lib.load()
-        acc = torch.empty(self.acc_elems, dtype=torch.float32, device=xpad.device)
         d = self.spec.c()
         d.engine = _lib.ENGINE_TENSOR
         s = _lib.stream_ptr(stream)
+        if not _CONV_FP32_TAIL:
+            # FP32 accumulators narrowed RNE in the BRGEMM epilogue, straight
+            # into the BF16 output (the same bits as the FP32 call + convert)
+            table, ngangs, gm, gn = self.gang if self.gang is not None else (None, 0, 1, 1)
+            _lib.check(lib.tpp_brgemm_grouped_bf16(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
+                                                   self.a_idx.data_ptr(), self.b_idx.data_ptr(), self.count,
+                                                   out_bf16.data_ptr(), self.c_off16.data_ptr(), self.groups,
+                                                   table.data_ptr() if table is not None else None, ngangs, gm, gn,
+                                                   self.wp, self.q, s), "conv (offset BRGEMM, BF16 out)")
+            return
+        acc = torch.empty(self.acc_elems, dtype=torch.float32, device=xpad.device)
         if self.gang is not None:
             table, ngangs, gm, gn = self.gang
             _lib.check(lib.tpp_brgemm_grouped_gang(C.byref(d), 1, w_vnni.data_ptr(), xpad.data_ptr(), 0, 0,
