@@ -325,3 +325,54 @@ def test_grouped_fallback_other_dtypes_matches_single_calls():
     with pytest.raises(NotImplementedError):
         tpp.brgemm_grouped(tpp.GemmSpec(m, n, k, m, k, m, engine=tpp.Engine.TENSOR), gb, out,
                            [g * m * n for g in range(G)])
+
+
+@pytest.mark.parametrize("gang", [False, True])
+def test_grouped_bf16_output_column_map(gang):
+    """tpp_brgemm_grouped_bf16: the BF16 epilogue (RNE with the reference's
+    NaN rule) with a column map (period 10, keep 7) gives the same bits as
+    the FP32 grouped call narrowed by the oracle's RNE and remapped -- on a
+    ganged (2 x 1, TMEM A) and an ungrouped tiling, with NaN / Inf / tie
+    inputs in A."""
+    import ctypes as C
+    rng = np.random.default_rng(95)
+    groups, cnt, m, n, k = 6, 3, 64, 40, 64
+    blk = m * k
+    a = O.fp32_to_bf16_rne(rng.standard_normal(blk * groups * cnt).astype(np.float32))
+    a[5] = 0x7FC1            # NaN
+    a[blk + 7] = 0x7F80      # +Inf
+    b = O.fp32_to_bf16_rne(rng.standard_normal(k * n * cnt).astype(np.float32))
+    ad, bd = to_dev(a), to_dev(b)
+    spec = tpp.GemmSpec(m, n, k, m, k, m, in_dtype=tpp.DType.BF16, out_dtype=tpp.DType.FP32,
+                        a_layout=tpp.ALayout.VNNI)
+    a_off = torch.tensor([(g * cnt + i) * blk for g in range(groups) for i in range(cnt)], dtype=torch.int64).cuda()
+    b_off = torch.tensor([i * k * n for _ in range(groups) for i in range(cnt)], dtype=torch.int64).cuda()
+    acc = torch.empty(groups * m * n, dtype=torch.float32, device="cuda")
+    lib = _lib.load()
+    d = spec.c()
+    d.engine = _lib.ENGINE_TENSOR
+    c_off = torch.tensor([g * m * n for g in range(groups)], dtype=torch.int64).cuda()
+    _lib.check(lib.tpp_brgemm_grouped(C.byref(d), 1, ad.data_ptr(), bd.data_ptr(), 0, 0, a_off.data_ptr(),
+                                      b_off.data_ptr(), cnt, acc.data_ptr(), c_off.data_ptr(), groups, None), "fp32")
+    per, keep = 10, 7
+    ncols = n // per * keep
+    out = torch.full((groups * m * ncols,), -1, dtype=torch.int16, device="cuda")
+    c16 = torch.tensor([g * m * ncols for g in range(groups)], dtype=torch.int64).cuda()
+    table, ng, gm, gn = None, 0, 1, 1
+    if gang:   # rows: groups 2j, 2j+1 (distinct A lists); one B list; cells
+        ng, gm, gn = groups // 2, 2, 1
+        rows = [g for g in range(groups)]
+        cols = [2 * j for j in range(ng)]
+        cells = [g for g in range(groups)]
+        table = torch.tensor(rows + cols + cells, dtype=torch.int32).cuda()
+    _lib.check(lib.tpp_brgemm_grouped_bf16(C.byref(d), 1, ad.data_ptr(), bd.data_ptr(), 0, 0, a_off.data_ptr(),
+                                           b_off.data_ptr(), cnt, out.data_ptr(), c16.data_ptr(), groups,
+                                           table.data_ptr() if table is not None else None, ng, gm, gn, per, keep,
+                                           None), "bf16")
+    cfg = _lib.last_config()
+    assert cfg.startswith(GROUPED) and (("gang=2x1" in cfg and " tmem_a" in cfg) if gang else True), cfg
+    want_full = O.fp32_to_bf16_rne(to_host(acc)).reshape(groups, n, m)       # [g][column][row]
+    keep_cols = [v for v in range(n) if v % per < keep]
+    want = want_full[:, keep_cols, :]
+    got = to_host(out).view(np.uint16).reshape(groups, ncols, m)
+    assert np.array_equal(got, want)
