@@ -58,7 +58,15 @@ namespace tc {
 
 constexpr int BM = 128;          // tokens per tile (UMMA M, TMEM lanes)
 constexpr int BK = 64;           // bf16 per reduce block = one 128B swizzle row
-constexpr int kEpiGroups = 2;    // epilogue warps per TMEM lane quarter (split the columns)
+// Experiment switch (-DTPP_EPI_GROUPS=3|4 via TPP_NVCC_EXTRA): more epilogue
+// warps.  The staging for TMA stores then no longer fits beside the operand
+// ring of the big tiles (STG_BUFS = 0), so such builds run with
+// TPP_NO_TMA_STORE=1.  Measured on the cfg-5 K=1024 GEMMs (DESIGN 4c): 3
+// groups no faster, 4 groups 20 % slower; the product build uses 2.
+#ifndef TPP_EPI_GROUPS
+#define TPP_EPI_GROUPS 2
+#endif
+constexpr int kEpiGroups = TPP_EPI_GROUPS;  // epilogue warps per TMEM lane quarter (split the columns)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
@@ -221,7 +229,9 @@ struct Smem {
   // when the smem budget allows (a chunk's store need not have left the
   // buffer before the next chunk is staged)
   static constexpr int STG_OFF = (BIAS_OFF + (RES >= 2 ? 0 : 2 * 256 * 4) + 1023) & ~1023;
-  static constexpr int STG_BUFS = ConvTile<RES>::STRIP ? 0 : (STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2 : 1);
+  static constexpr int STG_BUFS = ConvTile<RES>::STRIP ? 0
+                                  : STG_OFF + kEpiWarps * 2048 * 2 + 1024 <= 227 * 1024 ? 2
+                                  : STG_OFF + kEpiWarps * 2048 + 1024 <= 227 * 1024 ? 1 : 0;
   static constexpr int BYTES = STG_OFF + kEpiWarps * 2048 * STG_BUFS + 1024;
 };
 
@@ -1274,6 +1284,9 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
                       const Params& p, cudaStream_t stream) {
   using S = Smem<BN, STAGES, KPS, RES, CG>;
   static_assert(S::BYTES <= 227 * 1024, "shared memory budget");
+  static_assert(TPP_EPI_GROUPS != 2 || ConvTile<RES>::STRIP || S::STG_BUFS > 0, "product build: TMA-store staging must fit");
+  if (S::STG_BUFS == 0 && p.tma_store && !ConvTile<RES>::STRIP)  // experiment builds only
+    return fail(TPP_E_UNSUPPORTED, "no TMA-store staging in this build: set TPP_NO_TMA_STORE=1");
   auto kern = brgemm_tc_kernel<BN, STAGES, KPS, RES, CG, MC>;
   constexpr int CL = CG * MC;  // cluster size (one of CG, MC is 1)
   {

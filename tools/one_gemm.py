@@ -15,9 +15,10 @@ dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev)
 g.manual_seed(0)
 D, TOK = 4096, 8192
-w = T.pack_logical_weight((torch.randn(D, D, generator=g, device=dev) * 0.02).to(torch.bfloat16))
-layer = tpp.FcLayer(D // 64, D // 64, 64, 64, None, activation=tpp.UnaryKind.RELU, w_packed=w)
-x = torch.randn(TOK * D, generator=g, device=dev).to(torch.bfloat16)
+C = int(os.environ.get("K_IN", "4096"))  # reduce width: 1024 = the cfg5 fwd0 shape
+w = T.pack_logical_weight((torch.randn(D, C, generator=g, device=dev) * 0.02).to(torch.bfloat16))
+layer = tpp.FcLayer(D // 64, C // 64, 64, 64, None, activation=tpp.UnaryKind.RELU, w_packed=w)
+x = torch.randn(TOK * C, generator=g, device=dev).to(torch.bfloat16)
 out = torch.empty(TOK * D, dtype=torch.bfloat16, device=dev)
 mask = torch.empty(TOK * D // 8, dtype=torch.uint8, device=dev)
 for _ in range(int(os.environ.get("REPS", "5"))):
